@@ -1,0 +1,117 @@
+/* edl_b200.h — C-ABI of the B200 (sm_100a) EDL-Dist distillation hot path.
+ *
+ * The reference (EDL-Dist, pkg/src/edl) is pure Python + numpy float64 and has
+ * no FFI layer; its boundary is the Python API of edl.nnkit / edl.teacher_node /
+ * edl.student_node. Each entry point below replaces the numpy arithmetic behind
+ * one of those calls (cited per function); the Python mirror
+ * paper_2207_06667_b200/nnkit.py binds them with ctypes, keeping the reference
+ * names, argument meaning and error classes.
+ *
+ * Conventions
+ *   - All pointers are device pointers owned by the caller; nothing allocates.
+ *   - Matrices are row-major with an explicit leading dimension in ELEMENTS.
+ *     bf16 operands of the tensor-core paths need a 16-byte aligned base and
+ *     ld % 8 == 0 (TMA row pitch). Padding columns must hold zeros.
+ *   - `stream` is a cudaStream_t (passed as void*); every call is asynchronous
+ *     on it and reentrant per (device, stream).
+ *   - Return 0 on success or a negative EDL_ERR_* code; edl_last_error() holds
+ *     the message (thread-local). Device-detected errors (bad label / class id,
+ *     non-finite loss) are reported through the `status` word of the loss call.
+ */
+#ifndef EDL_B200_H
+#define EDL_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EDL_B200_ABI_VERSION 1
+
+/* status codes: mirror edl.nnkit's exception classes (edl/nnkit.py:31-40) */
+#define EDL_OK 0
+#define EDL_ERR_SHAPE (-1)   /* ShapeError(ValueError)                    */
+#define EDL_ERR_NUMERIC (-2) /* NumericError: non-finite loss (nnkit:296) */
+#define EDL_ERR_PARAM (-3)   /* ValueError: T <= 0, bad k / alpha / beta  */
+#define EDL_ERR_CUDA (-4)    /* launch / driver failure                   */
+
+#define EDL_ACT_NONE 0 /* z = x W^T + b, fp32 out (logit layer)           */
+#define EDL_ACT_TANH 1 /* h = tanh(x W^T + b), bf16 out (hidden layers)   */
+
+int edl_version(void);
+const char* edl_last_error(void);
+int edl_device_sms(void);
+
+/* One dense layer of edl.nnkit.forward (edl/nnkit.py:223-234, `z = h @ w.T + b`
+ * at :232, tanh at :233). X: bf16 [M][ldx] (K used), W: bf16 [N][ldw], bias:
+ * fp32 [N]. act=EDL_ACT_TANH writes bf16 Y [M][ldy]; EDL_ACT_NONE writes fp32.
+ * tcgen05 GEMM, TMA-fed, fused bias/activation epilogue. */
+int edl_linear_fwd(const void* X, long long ldx, const void* W, long long ldw, const float* bias,
+                   void* Y, long long ldy, int M, int N, int K, int act, void* stream);
+
+/* Backprop through one tanh layer, edl/nnkit.py:308:
+ *   dX[M][K] = (dY[M][N] @ W[N][K]) * (1 - H[M][K]^2)      (all bf16) */
+int edl_linear_bwd_data(const void* dY, long long lddy, const void* W, long long ldw,
+                        const void* H, long long ldh, void* dX, long long lddx, int M, int N,
+                        int K, void* stream);
+
+/* Weight/bias gradients, edl/nnkit.py:305-306:
+ *   dW[N][K] = scale * dY[M][N]^T @ X[M][K]   (fp32 out)
+ *   db[N]    = scale * sum_m dY[m][:]         (fp32, optional; needs workspace of
+ *              edl_colsum_workspace_floats(M, N) floats)                        */
+int edl_linear_bwd_weight(const void* dY, long long lddy, const void* X, long long ldx, float* dW,
+                          long long lddw, float* db, float* workspace, int M, int N, int K,
+                          float scale, void* stream);
+long long edl_colsum_workspace_floats(int M, int N);
+
+/* Teacher head = soft_label_reply's math (edl/teacher_node.py:54:
+ * tempered_softmax(forward(model, inputs), T), edl/nnkit.py:193-208,232) fused
+ * with the top-k soft-label extraction EDL-Dist ships to students:
+ *   p = softmax((H W^T + b) / T);  (vals[M][k], idx[M][k]) = top-k of p per row,
+ *   ordered by probability desc, ties -> lower class index (edl/nnkit.py:333).
+ * Logits stay on chip (TMEM -> registers -> DSMEM merge across a cluster).
+ * N = number of classes (<= 2048), 1 <= k <= min(N, 32). */
+int edl_teacher_head_softmax_topk(const void* H, long long ldh, const void* W, long long ldw,
+                                  const float* bias, int M, int N, int K, float T, int k,
+                                  float* vals, int* idx, void* stream);
+
+/* Dense tempered softmax, edl/nnkit.py:193-208 (fp32 logits -> fp32 probs). */
+int edl_tempered_softmax(const float* logits, long long ld, float* probs, long long ldp, int B,
+                         int K, float T, void* stream);
+
+/* Fused distillation loss forward + backward, edl/nnkit.py:283-295:
+ *   loss = mean_rows[ alpha*CE(onehot(y), softmax z) + beta*T^2*CE(q, softmax(z/T)) ]
+ *   dz   = alpha/B*(softmax z - onehot y) + beta*T/B*(softmax(z/T) - q)
+ * q = (q_vals, q_idx)[B][k] renormalised to sum 1 per row (k = K: dense).
+ * logits fp32 [B][ldz]; labels int64 [B]; dlogits bf16 [B][lddz] (padding
+ * columns zeroed); row_loss fp32 [B] scratch; loss_out fp32 scalar (batch mean,
+ * deterministic order); ticket: one zero-initialised uint (self-resetting);
+ * status: int, set to EDL_ERR_SHAPE / EDL_ERR_NUMERIC by the device. */
+int edl_kd_loss_fwd_bwd(const float* logits, long long ldz, const long long* labels,
+                        const float* q_vals, const int* q_idx, int B, int K, int k, float alpha,
+                        float beta, float T, float* row_loss, float* loss_out, unsigned* ticket,
+                        void* dlogits, long long lddz, int* status, void* stream);
+
+/* SGD, edl/nnkit.py:312-322 (`w - eta * gw`), on fp32 masters in place; the
+ * optional bf16 copy (same element offsets) is refreshed in the same pass.
+ * scale = eta / world_size folds the all-reduce mean (edl/allreduce.py:119). */
+int edl_sgd_step(float* p, void* p_bf16, const float* g, long long n, float scale, void* stream);
+
+/* Batch gather from an HBM-resident shard, edl/student_node.py:150-151:
+ * dst[b][:D] = src[idx[b]][:D] (bf16, idx int64). */
+int edl_gather_rows(const void* src, long long ld_src, const long long* idx, void* dst,
+                    long long ld_dst, int B, int D, void* stream);
+
+/* Top-k accuracy counter, edl/nnkit.py:325-335: hits += #rows whose label
+ * ranks < k under (logit desc, class asc). */
+int edl_topk_hits(const float* logits, long long ld, const long long* labels, int B, int K, int k,
+                  unsigned* hits, void* stream);
+
+/* fp32 -> bf16 matrix cast (parameter / input staging). */
+int edl_cast_bf16(const float* src, long long ld_src, void* dst, long long ld_dst, int rows,
+                  int cols, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EDL_B200_H */

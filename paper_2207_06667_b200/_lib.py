@@ -1,0 +1,98 @@
+"""ctypes binding of libedl_b200.so (include/edl_b200.h).
+
+There is no CPU fallback: if the library is missing or the process has no
+CUDA device, every compute entry point raises. ctypes drops the GIL around
+each foreign call, so teacher and student threads launch concurrently.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libedl_b200.so")
+
+_lock = threading.Lock()
+_lib: ctypes.CDLL | None = None
+
+c_int, c_ll, c_float, c_void_p, c_char_p = (ctypes.c_int, ctypes.c_longlong, ctypes.c_float,
+                                            ctypes.c_void_p, ctypes.c_char_p)
+
+# name -> argtypes (all return int unless listed in _RESTYPES)
+_SIGNATURES = {
+    "edl_version": [],
+    "edl_last_error": [],
+    "edl_device_sms": [],
+    "edl_linear_fwd": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_void_p, c_ll, c_int, c_int,
+                       c_int, c_int, c_void_p],
+    "edl_linear_bwd_data": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_ll,
+                            c_int, c_int, c_int, c_void_p],
+    "edl_linear_bwd_weight": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_ll, c_void_p,
+                              c_void_p, c_int, c_int, c_int, c_float, c_void_p],
+    "edl_colsum_workspace_floats": [c_int, c_int],
+    "edl_teacher_head_softmax_topk": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_int, c_int,
+                                      c_int, c_float, c_int, c_void_p, c_void_p, c_void_p],
+    "edl_tempered_softmax": [c_void_p, c_ll, c_void_p, c_ll, c_int, c_int, c_float, c_void_p],
+    "edl_kd_loss_fwd_bwd": [c_void_p, c_ll, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int,
+                            c_float, c_float, c_float, c_void_p, c_void_p, c_void_p, c_void_p,
+                            c_ll, c_void_p, c_void_p],
+    "edl_sgd_step": [c_void_p, c_void_p, c_void_p, c_ll, c_float, c_void_p],
+    "edl_gather_rows": [c_void_p, c_ll, c_void_p, c_void_p, c_ll, c_int, c_int, c_void_p],
+    "edl_topk_hits": [c_void_p, c_ll, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p],
+    "edl_cast_bf16": [c_void_p, c_ll, c_void_p, c_ll, c_int, c_int, c_void_p],
+}
+_RESTYPES = {"edl_last_error": c_char_p, "edl_colsum_workspace_floats": c_ll}
+
+EDL_ERR_SHAPE, EDL_ERR_NUMERIC, EDL_ERR_PARAM, EDL_ERR_CUDA = -1, -2, -3, -4
+EDL_ACT_NONE, EDL_ACT_TANH = 0, 1
+ABI_VERSION = 1
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGNATURES)
+
+
+def load() -> ctypes.CDLL:
+    """Load and type the shared library (no GPU needed for loading)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2207_06667_b200.build` "
+                "(the B200 path has no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, args in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = _RESTYPES.get(name, c_int)
+        if lib.edl_version() != ABI_VERSION:
+            raise RuntimeError("libedl_b200.so ABI version mismatch; rebuild")
+        _lib = lib
+        return lib
+
+
+def last_error() -> str:
+    return load().edl_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str) -> None:
+    """Map C status codes onto the reference's exception classes."""
+    if rc == 0:
+        return
+    from .nnkit import NumericError, ShapeError
+    msg = f"{what}: {last_error()}"
+    if rc == EDL_ERR_SHAPE:
+        raise ShapeError(msg)
+    if rc == EDL_ERR_NUMERIC:
+        raise NumericError(msg)
+    if rc == EDL_ERR_PARAM:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)

@@ -1,0 +1,277 @@
+// capi.cu — the C-ABI boundary (include/edl_b200.h). Plain pointers, sizes and
+// a cudaStream_t; the caller owns all device memory and nothing here allocates
+// on the step path. TMA tensor maps are encoded on first use and cached by
+// (pointer, shape, box), so steady-state calls are a cache lookup + launch.
+#include "../../include/edl_b200.h"
+#include "internal.h"
+
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+using namespace edl;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(EDL_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+struct MapKey {
+  const void* ptr;
+  long long rows, cols, ld;
+  int box0, box1;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && rows == o.rows && cols == o.cols && ld == o.ld && box0 == o.box0 &&
+           box1 == o.box1;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    size_t h = std::hash<const void*>()(k.ptr);
+    h ^= std::hash<long long>()(k.rows * 1000003LL + k.cols) + 0x9e3779b9 + (h << 6) + (h >> 2);
+    h ^= std::hash<long long>()(k.ld * 131 + k.box0 * 7 + k.box1) + 0x9e3779b9 + (h << 6) + (h >> 2);
+    return h;
+  }
+};
+
+std::mutex g_map_mu;
+std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+// 2-D bf16 row-major matrix [rows][cols] with leading dimension ld (elements),
+// box {box0 along cols, box1 along rows}, 128-byte swizzle, zero OOB fill.
+int tensor_map(const void* ptr, long long rows, long long cols, long long ld, int box0, int box1,
+               CUtensorMap* out) {
+  MapKey key{ptr, rows, cols, ld, box0, box1};
+  {
+    std::lock_guard<std::mutex> g(g_map_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) { *out = it->second; return 0; }
+  }
+  auto fn = encode_fn();
+  if (!fn) return fail(EDL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * 2) % 16)
+    return fail(EDL_ERR_SHAPE, "TMA operand needs 16-byte aligned base and row pitch (ld=%lld)", ld);
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box0), static_cast<cuuint32_t>(box1)};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMap m;
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(EDL_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+  {
+    std::lock_guard<std::mutex> g(g_map_mu);
+    if (g_maps.size() > 4096) g_maps.clear();
+    g_maps.emplace(key, m);
+  }
+  *out = m;
+  return 0;
+}
+
+int num_sms() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+// Pick the N tile: fewest waves, then the widest tile (best operand reuse).
+int pick_bn(int M, int N) {
+  const int sms = num_sms();
+  int best = 256;
+  long long best_cost = -1;
+  for (int bn : {256, 128, 64}) {
+    if (bn > 64 && N <= bn / 2) continue;
+    const long long tiles = static_cast<long long>((M + 127) / 128) * ((N + bn - 1) / bn);
+    const long long waves = (tiles + sms - 1) / sms;
+    const long long cost = waves * (bn + 48);
+    if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = bn; }
+  }
+  return best;
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+extern "C" {
+
+int edl_version(void) { return EDL_B200_ABI_VERSION; }
+
+const char* edl_last_error(void) { return g_err.c_str(); }
+
+int edl_device_sms(void) { return num_sms(); }
+
+int edl_linear_fwd(const void* X, long long ldx, const void* W, long long ldw, const float* bias,
+                   void* Y, long long ldy, int M, int N, int K, int act, void* stream) {
+  if (M < 1 || N < 1 || K < 1 || ldx < K || ldw < K || ldy < N)
+    return fail(EDL_ERR_SHAPE, "linear_fwd: bad shape M=%d N=%d K=%d", M, N, K);
+  if (act != EDL_ACT_TANH && act != EDL_ACT_NONE) return fail(EDL_ERR_SHAPE, "linear_fwd: bad act %d", act);
+  const int bn = pick_bn(M, N);
+  CUtensorMap ta, tb;
+  int rc;
+  if ((rc = tensor_map(X, M, K, ldx, 64, 128, &ta))) return rc;
+  if ((rc = tensor_map(W, N, K, ldw, 64, bn, &tb))) return rc;
+  EpiArgs ep{Y, ldy, bias, nullptr, 0, 1.0f};
+  cudaError_t e = launch_gemm(act == EDL_ACT_TANH ? GemmKind::FwdTanh : GemmKind::FwdLinear, bn, ta,
+                              tb, M, N, K, ep, num_sms(), as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "linear_fwd");
+}
+
+int edl_linear_bwd_data(const void* dY, long long lddy, const void* W, long long ldw,
+                        const void* H, long long ldh, void* dX, long long lddx, int M, int N,
+                        int K, void* stream) {
+  if (M < 1 || N < 1 || K < 1 || lddy < N || ldw < K || ldh < K || lddx < K)
+    return fail(EDL_ERR_SHAPE, "linear_bwd_data: bad shape M=%d N=%d K=%d", M, N, K);
+  const int bn = pick_bn(M, K);
+  CUtensorMap ta, tb;
+  int rc;
+  // A = dY [M][N] (reduction N contiguous: K-major); B = W [N][K] read as [red][MN].
+  if ((rc = tensor_map(dY, M, N, lddy, 64, 128, &ta))) return rc;
+  if ((rc = tensor_map(W, N, K, ldw, 64, 64, &tb))) return rc;
+  EpiArgs ep{dX, lddx, nullptr, reinterpret_cast<const __nv_bfloat16*>(H), ldh, 1.0f};
+  cudaError_t e = launch_gemm(GemmKind::BwdData, bn, ta, tb, M, K, N, ep, num_sms(), as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "linear_bwd_data");
+}
+
+int edl_linear_bwd_weight(const void* dY, long long lddy, const void* X, long long ldx, float* dW,
+                          long long lddw, float* db, float* workspace, int M, int N, int K,
+                          float scale, void* stream) {
+  if (M < 1 || N < 1 || K < 1 || lddy < N || ldx < K || lddw < K)
+    return fail(EDL_ERR_SHAPE, "linear_bwd_weight: bad shape M=%d N=%d K=%d", M, N, K);
+  const int bn = pick_bn(N, K);
+  CUtensorMap ta, tb;
+  int rc;
+  // A = dY^T: dY [M][N] read as [red=M][MN=N]; B = X^T: X [M][K] read as [red=M][MN=K].
+  if ((rc = tensor_map(dY, M, N, lddy, 64, 64, &ta))) return rc;
+  if ((rc = tensor_map(X, M, K, ldx, 64, 64, &tb))) return rc;
+  EpiArgs ep{dW, lddw, nullptr, nullptr, 0, scale};
+  cudaError_t e = launch_gemm(GemmKind::BwdWeight, bn, ta, tb, N, K, M, ep, num_sms(), as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "linear_bwd_weight");
+  if (db) {
+    if (!workspace) return fail(EDL_ERR_SHAPE, "linear_bwd_weight: db needs a workspace");
+    e = launch_colsum(reinterpret_cast<const __nv_bfloat16*>(dY), lddy, M, N, workspace, db, scale,
+                      as_stream(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "colsum");
+  }
+  return 0;
+}
+
+long long edl_colsum_workspace_floats(int M, int N) {
+  return static_cast<long long>((M + 127) / 128) * N;
+}
+
+int edl_teacher_head_softmax_topk(const void* H, long long ldh, const void* W, long long ldw,
+                                  const float* bias, int M, int N, int K, float T, int k,
+                                  float* vals, int* idx, void* stream) {
+  if (M < 1 || N < 1 || K < 1 || ldh < K || ldw < K)
+    return fail(EDL_ERR_SHAPE, "teacher_head: bad shape M=%d N=%d K=%d", M, N, K);
+  if (!(T > 0.f) || !std::isfinite(T)) return fail(EDL_ERR_PARAM, "teacher_head: temperature %g", T);
+  if (k < 1 || k > N || k > 32) return fail(EDL_ERR_PARAM, "teacher_head: k=%d (1..min(N,32))", k);
+  const int kmax = k <= 4 ? 4 : k <= 8 ? 8 : k <= 16 ? 16 : 32;
+  const int bn = N <= 64 ? 64 : N <= 128 ? 128 : 256;
+  if ((N + bn - 1) / bn > 8) return fail(EDL_ERR_SHAPE, "teacher_head: N=%d exceeds 8 x 256 classes", N);
+  CUtensorMap ta, tb;
+  int rc;
+  if ((rc = tensor_map(H, M, K, ldh, 64, 128, &ta))) return rc;
+  if ((rc = tensor_map(W, N, K, ldw, 64, bn, &tb))) return rc;
+  HeadArgs hp{bias, 1.0f / T, k, vals, idx};
+  cudaError_t e = launch_teacher_head(bn, kmax, ta, tb, M, N, K, hp, as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "teacher_head");
+}
+
+int edl_tempered_softmax(const float* logits, long long ld, float* probs, long long ldp, int B,
+                         int K, float T, void* stream) {
+  if (B < 1 || K < 1 || ld < K || ldp < K) return fail(EDL_ERR_SHAPE, "tempered_softmax: bad shape");
+  if (!(T > 0.f) || !std::isfinite(T)) return fail(EDL_ERR_PARAM, "tempered_softmax: temperature %g", T);
+  cudaError_t e = launch_tempered_softmax(logits, ld, probs, ldp, B, K, T, as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "tempered_softmax");
+}
+
+int edl_kd_loss_fwd_bwd(const float* logits, long long ldz, const long long* labels,
+                        const float* q_vals, const int* q_idx, int B, int K, int k, float alpha,
+                        float beta, float T, float* row_loss, float* loss_out, unsigned* ticket,
+                        void* dlogits, long long lddz, int* status, void* stream) {
+  if (B < 1 || K < 1 || ldz < K || lddz < K) return fail(EDL_ERR_SHAPE, "kd_loss: bad shape B=%d K=%d", B, K);
+  if (!(T > 0.f) || !std::isfinite(T)) return fail(EDL_ERR_PARAM, "kd_loss: temperature %g", T);
+  if (alpha < 0.f || beta < 0.f || !(alpha + beta > 0.f)) return fail(EDL_ERR_PARAM, "kd_loss: alpha/beta");
+  if (beta > 0.f && (k < 1 || k > K || !q_vals || !q_idx))
+    return fail(EDL_ERR_SHAPE, "kd_loss: beta > 0 requires soft labels (k=%d)", k);
+  cudaError_t e = launch_kd_loss(logits, ldz, reinterpret_cast<const int64_t*>(labels), q_vals, q_idx,
+                                 B, K, beta > 0.f ? k : 0, alpha, beta, T, row_loss, loss_out, ticket,
+                                 reinterpret_cast<__nv_bfloat16*>(dlogits), lddz, status,
+                                 as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "kd_loss");
+}
+
+int edl_sgd_step(float* p, void* p_bf16, const float* g, long long n, float scale, void* stream) {
+  if (n < 0) return fail(EDL_ERR_SHAPE, "sgd_step: n=%lld", n);
+  if ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(g)) & 15)
+    return fail(EDL_ERR_SHAPE, "sgd_step: buffers must be 16-byte aligned");
+  if (n == 0) return 0;
+  cudaError_t e = launch_sgd(p, reinterpret_cast<__nv_bfloat16*>(p_bf16), g, n, scale, as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "sgd_step");
+}
+
+int edl_gather_rows(const void* src, long long ld_src, const long long* idx, void* dst,
+                    long long ld_dst, int B, int D, void* stream) {
+  if (B < 1 || D < 1 || ld_src < D || ld_dst < D || (ld_src % 8) || (ld_dst % 8))
+    return fail(EDL_ERR_SHAPE, "gather_rows: bad shape B=%d D=%d", B, D);
+  cudaError_t e = launch_gather_rows(reinterpret_cast<const __nv_bfloat16*>(src), ld_src,
+                                     reinterpret_cast<const int64_t*>(idx),
+                                     reinterpret_cast<__nv_bfloat16*>(dst), ld_dst, B, D,
+                                     as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "gather_rows");
+}
+
+int edl_topk_hits(const float* logits, long long ld, const long long* labels, int B, int K, int k,
+                  unsigned* hits, void* stream) {
+  if (B < 1 || K < 1 || ld < K) return fail(EDL_ERR_SHAPE, "topk_hits: bad shape");
+  if (k < 1 || k > K) return fail(EDL_ERR_PARAM, "topk_hits: k=%d", k);
+  cudaError_t e = launch_topk_hits(logits, ld, reinterpret_cast<const int64_t*>(labels), B, K, k,
+                                   hits, as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "topk_hits");
+}
+
+int edl_cast_bf16(const float* src, long long ld_src, void* dst, long long ld_dst, int rows,
+                  int cols, void* stream) {
+  if (rows < 0 || cols < 0 || ld_src < cols || ld_dst < cols) return fail(EDL_ERR_SHAPE, "cast_bf16: bad shape");
+  if (rows == 0 || cols == 0) return 0;
+  cudaError_t e = launch_cast_bf16(src, ld_src, reinterpret_cast<__nv_bfloat16*>(dst), ld_dst, rows,
+                                   cols, as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "cast_bf16");
+}
+
+}  // extern "C"

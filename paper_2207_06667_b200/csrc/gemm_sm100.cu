@@ -1,0 +1,521 @@
+// gemm_sm100.cu — the tensor-core kernels of the EDL-Dist hot path (sm_100a).
+//
+//   C[M,N] = sum_k A[m,k] * B[n,k]      bf16 x bf16 -> fp32 accumulate in TMEM
+//
+// One warp-specialised, persistent kernel template covers every dense layer the
+// reference runs through numpy `@` (edl/nnkit.py:232,243,305,308):
+//   forward hidden  h = tanh(x W^T + b)        A=x  (K-major)  B=W (K-major)   EPI_TANH_BF16
+//   student logits  z = h W^T + b              A=h  (K-major)  B=W (K-major)   EPI_BIAS_F32
+//   backprop data   d = (dY W) * (1 - a^2)     A=dY (K-major)  B=W (MN-major)  EPI_DTANH_BF16
+//   backprop weight dW = dY^T a                A=dY (MN-major) B=a (MN-major)  EPI_F32
+// and a cluster kernel for the teacher head (edl/nnkit.py:193-208 + top-k, see
+// teacher_head_kernel below) whose epilogue never writes logits to HBM.
+//
+// Roles (256 threads, 1 CTA/SM): warp0 lane0 = TMA producer, warp1 lane0 =
+// tcgen05.mma issuer, warp2 = TMEM allocator, warps4-7 = epilogue (each owns the
+// 32 TMEM lanes = 32 accumulator rows its warp-in-warpgroup index selects).
+// Pipelines: STAGES-deep smem ring (full/empty mbarriers) and a 2-deep TMEM
+// accumulator ring (tmem_full/tmem_empty) so tile i's epilogue overlaps tile
+// i+1's MMAs. Operand tiles are 128-byte-swizzled TMA boxes of 64 bf16 along
+// the contiguous dimension.
+#include "internal.h"
+#include "sm100.cuh"
+
+namespace edl {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;
+constexpr int kThreads = 256;
+
+__host__ __device__ constexpr uint32_t tmem_cols_for(int cols) {
+  return cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
+}
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int kStages = BN >= 256 ? 4 : BN >= 128 ? 6 : 8;
+  static constexpr uint32_t kABytes = kBM * kBK * 2;
+  static constexpr uint32_t kBBytes = BN * kBK * 2;
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr uint32_t kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+// Issue the TMA loads of one (A,B) k-block into stage buffers.
+template <int BN, bool A_MN, bool B_MN>
+__device__ __forceinline__ void load_kblock(const CUtensorMap* tmA, const CUtensorMap* tmB,
+                                            uint8_t* sa, uint8_t* sb, uint64_t* bar, int m0,
+                                            int n0, int k0) {
+  mbar_arrive_expect_tx(bar, GemmCfg<BN>::kStageBytes);
+  if constexpr (!A_MN) {
+    tma_load_2d(sa, tmA, bar, k0, m0);
+  } else {
+#pragma unroll
+    for (int j = 0; j < kBM / 64; ++j) tma_load_2d(sa + j * 8192, tmA, bar, m0 + 64 * j, k0);
+  }
+  if constexpr (!B_MN) {
+    tma_load_2d(sb, tmB, bar, k0, n0);
+  } else {
+#pragma unroll
+    for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, tmB, bar, n0 + 64 * j, k0);
+  }
+}
+
+// Four 128xBNx16 MMAs consume one 64-deep k-block.
+template <int BN, bool A_MN, bool B_MN>
+__device__ __forceinline__ void mma_kblock(uint32_t d_tmem, uint32_t a_base, uint32_t b_base,
+                                           bool first) {
+  constexpr uint32_t idesc = idesc_bf16_f32(kBM, BN, A_MN, B_MN);
+#pragma unroll
+  for (int k = 0; k < kBK / 16; ++k) {
+    // K-major: a 16-element K slice is 32 bytes further along each swizzled row.
+    // MN-major: a 16-row K slice is 16 * 128 bytes further; LBO = one 64-wide box.
+    uint64_t ad = A_MN ? smem_desc_sw128(a_base + k * 2048, 8192, 1024)
+                       : smem_desc_sw128(a_base + k * 32, 16, 1024);
+    uint64_t bd = B_MN ? smem_desc_sw128(b_base + k * 2048, 8192, 1024)
+                       : smem_desc_sw128(b_base + k * 32, 16, 1024);
+    umma_bf16(d_tmem, ad, bd, idesc, (first && k == 0) ? 0u : 1u);
+  }
+}
+
+// ------------------------------------------------------------------ epilogues
+template <int EPI>
+__device__ __forceinline__ void epilogue_store(const EpiArgs& ep, int row, int M, int col0,
+                                               int N, float (&v)[32]) {
+  if (row >= M) return;
+  const bool full = (col0 + 32 <= N);
+  if constexpr (EPI == EPI_TANH_BF16 || EPI == EPI_BIAS_F32) {
+    if (ep.bias != nullptr) {
+      if (full) {
+        const float4* b4 = reinterpret_cast<const float4*>(ep.bias + col0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float4 b = __ldg(b4 + i);
+          v[4 * i] += b.x; v[4 * i + 1] += b.y; v[4 * i + 2] += b.z; v[4 * i + 3] += b.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (col0 + i < N) v[i] += __ldg(ep.bias + col0 + i);
+      }
+    }
+  }
+  if constexpr (EPI == EPI_TANH_BF16) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = tanh_fast(v[i]);
+  }
+  if constexpr (EPI == EPI_DTANH_BF16) {
+    const __nv_bfloat16* h = ep.aux + static_cast<size_t>(row) * ep.ld_aux + col0;
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint4 q = __ldg(reinterpret_cast<const uint4*>(h) + i);
+        const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&q);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float a = __bfloat162float(hb[j]);
+          v[8 * i + j] *= (1.0f - a * a);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < N) {
+          float a = __bfloat162float(h[i]);
+          v[i] *= (1.0f - a * a);
+        }
+    }
+  }
+  if constexpr (EPI == EPI_F32) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] *= ep.scale;
+  }
+  if constexpr (EPI == EPI_TANH_BF16 || EPI == EPI_DTANH_BF16) {
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(ep.out) + static_cast<size_t>(row) * ep.ld_out + col0;
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint4 q;
+        q.x = pack_bf16x2(v[8 * i + 0], v[8 * i + 1]);
+        q.y = pack_bf16x2(v[8 * i + 2], v[8 * i + 3]);
+        q.z = pack_bf16x2(v[8 * i + 4], v[8 * i + 5]);
+        q.w = pack_bf16x2(v[8 * i + 6], v[8 * i + 7]);
+        reinterpret_cast<uint4*>(o)[i] = q;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < N) o[i] = __float2bfloat16_rn(v[i]);
+    }
+  } else {
+    float* o = reinterpret_cast<float*>(ep.out) + static_cast<size_t>(row) * ep.ld_out + col0;
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        reinterpret_cast<float4*>(o)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < N) o[i] = v[i];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ GEMM
+template <int BN, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                int M, int N, int K, EpiArgs ep) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int S = Cfg::kStages;
+  constexpr uint32_t kTmemCols = tmem_cols_for(2 * BN);
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * Cfg::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kBBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_m = (M + kBM - 1) / kBM;
+  const int num_n = (N + BN - 1) / BN;
+  const int tiles = num_m * num_n;
+  const int nk = (K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    uint32_t g = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int m0 = (t % num_m) * kBM, n0 = (t / num_m) * BN;
+      for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int s = g % S;
+        mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
+        load_kblock<BN, A_MN, B_MN>(&tmA, &tmB, sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes,
+                                    &full[s], m0, n0, kb * kBK);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    uint32_t g = 0, i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      const uint32_t as = i & 1;
+      mbar_wait(&tempty[as], ((i >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + as * BN;
+      for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int s = g % S;
+        mbar_wait(&full[s], (g / S) & 1);
+        tc_fence_after();
+        mma_kblock<BN, A_MN, B_MN>(d, smem_u32(sA + s * Cfg::kABytes),
+                                   smem_u32(sB + s * Cfg::kBBytes), kb == 0);
+        umma_commit(&empty[s]);
+      }
+      umma_commit(&tfull[as]);
+    }
+  } else if (warp >= 4) {
+    const int e = warp - 4;
+    uint32_t i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      const int m0 = (t % num_m) * kBM, n0 = (t / num_m) * BN;
+      const uint32_t as = i & 1;
+      mbar_wait(&tfull[as], (i >> 1) & 1);
+      tc_fence_after();
+      const int row = m0 + 32 * e + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN + c, v);
+        if (n0 + c < N) epilogue_store<EPI>(ep, row, M, n0 + c, N, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[as]);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ teacher head
+// Logits z = H W^T + b for a 128-row block, scaled s = z / T, and per row: the
+// running max / rescaled sum of exp(s) (online softmax) plus a register top-k
+// list ordered by (value desc, class index asc) — the tie rule of
+// edl/nnkit.py:333. The class dimension is split across a cluster of CS CTAs
+// (256 classes each); rank 0 merges the CS partial states through distributed
+// shared memory and writes only (prob, class) pairs: logits never reach HBM.
+template <int KMAX>
+struct TopK {
+  float v[KMAX];
+  int i[KMAX];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) { v[j] = -INFINITY; i[j] = 0x7fffffff; }
+  }
+  __device__ __forceinline__ static bool better(float a, int ia, float b, int ib) {
+    return a > b || (a == b && ia < ib);
+  }
+  __device__ __forceinline__ void push(float x, int ix) {
+    if (!better(x, ix, v[KMAX - 1], i[KMAX - 1])) return;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+      if (better(x, ix, v[j], i[j])) {
+        float tv = v[j]; int ti = i[j];
+        v[j] = x; i[j] = ix;
+        x = tv; ix = ti;
+      }
+    }
+  }
+};
+
+template <int BN, int KMAX>
+__global__ void __launch_bounds__(kThreads, 1)
+    teacher_head_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+                        HeadArgs hp) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int S = Cfg::kStages;
+  constexpr uint32_t kTmemCols = tmem_cols_for(BN);
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * Cfg::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kBBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  // merge scratch reuses the (drained) operand ring: [2 + 2*KMAX][128] words
+  float* st_m = reinterpret_cast<float*>(smem);
+  float* st_l = st_m + kBM;
+  float* st_v = st_l + kBM;
+  int* st_i = reinterpret_cast<int*>(st_v + KMAX * kBM);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int cs = static_cast<int>(gridDim.x);            // cluster spans the class chunks
+  const int rank = static_cast<int>(blockIdx.x);         // == %cluster_ctarank
+  const int m0 = blockIdx.y * kBM;
+  const int n0 = rank * BN;
+  const int nk = (K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(&tfull[0], 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % S;
+      mbar_wait(&empty[s], ((kb / S) & 1) ^ 1);
+      load_kblock<BN, false, false>(&tmA, &tmB, sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes,
+                                    &full[s], m0, n0, kb * kBK);
+    }
+  } else if (warp == 1 && lane == 0) {
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % S;
+      mbar_wait(&full[s], (kb / S) & 1);
+      tc_fence_after();
+      mma_kblock<BN, false, false>(tmem_base, smem_u32(sA + s * Cfg::kABytes),
+                                   smem_u32(sB + s * Cfg::kBBytes), kb == 0);
+      umma_commit(&empty[s]);
+    }
+    umma_commit(&tfull[0]);
+  }
+
+  const int e = warp - 4;
+  const int rl = 32 * e + lane;  // local row
+  TopK<KMAX> top;
+  float run_m = -INFINITY, run_l = 0.f;
+  if (warp >= 4) {
+    mbar_wait(&tfull[0], 0);
+    tc_fence_after();
+    top.init();
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      float v[32];
+      tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * e) << 16) + c, v);
+      const int col0 = n0 + c;
+      if (col0 >= N) continue;
+      float cmax = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int n = col0 + j;
+        float s = (n < N) ? (v[j] + __ldg(hp.bias + n)) * hp.inv_t : -INFINITY;
+        v[j] = s;
+        cmax = fmaxf(cmax, s);
+      }
+      const float nm = fmaxf(run_m, cmax);
+      float acc = 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc += __expf(v[j] - nm);
+      run_l = run_l * __expf(run_m - nm) + acc;
+      run_m = nm;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < N) top.push(v[j], col0 + j);
+    }
+    tc_fence_before();
+  }
+  __syncthreads();  // every CTA: MMAs drained, operand ring free for scratch
+  if (warp >= 4) {
+    st_m[rl] = run_m;
+    st_l[rl] = run_l;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) { st_v[j * kBM + rl] = top.v[j]; st_i[j * kBM + rl] = top.i[j]; }
+  }
+  if (cs > 1) cluster_sync(); else __syncthreads();
+  if (rank == 0 && warp >= 4) {
+    for (int r = 1; r < cs; ++r) {
+      const uint32_t bm = mapa(smem_u32(st_m + rl), r);
+      const uint32_t bl = mapa(smem_u32(st_l + rl), r);
+      const float om = ld_dsmem_f32(bm), ol = ld_dsmem_f32(bl);
+      const float nm = fmaxf(run_m, om);
+      run_l = run_l * __expf(run_m - nm) + ol * __expf(om - nm);
+      run_m = nm;
+      for (int j = 0; j < hp.k; ++j) {
+        const float ov = ld_dsmem_f32(mapa(smem_u32(st_v + j * kBM + rl), r));
+        const int oi = ld_dsmem_s32(mapa(smem_u32(st_i + j * kBM + rl), r));
+        top.push(ov, oi);
+      }
+    }
+    const int row = m0 + rl;
+    if (row < M) {
+      const float inv_l = 1.0f / run_l;
+      float* ov = hp.vals + static_cast<size_t>(row) * hp.k;
+      int* oi = hp.idx + static_cast<size_t>(row) * hp.k;
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j)
+        if (j < hp.k) { ov[j] = __expf(top.v[j] - run_m) * inv_l; oi[j] = top.i[j]; }
+    }
+  }
+  if (cs > 1) cluster_sync(); else __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+template <int BN, bool A_MN, bool B_MN, int EPI>
+static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N,
+                                 int K, const EpiArgs& ep, int num_sms, cudaStream_t stream) {
+  auto kern = gemm_kernel<BN, A_MN, B_MN, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         GemmCfg<BN>::kSmem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
+  const int grid = tiles < num_sms ? tiles : num_sms;
+  kern<<<grid, kThreads, GemmCfg<BN>::kSmem, stream>>>(ta, tb, M, N, K, ep);
+  return cudaGetLastError();
+}
+
+template <bool A_MN, bool B_MN, int EPI>
+static cudaError_t launch_gemm_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb, int M,
+                                  int N, int K, const EpiArgs& ep, int num_sms,
+                                  cudaStream_t stream) {
+  switch (bn) {
+    case 64: return launch_gemm_t<64, A_MN, B_MN, EPI>(ta, tb, M, N, K, ep, num_sms, stream);
+    case 128: return launch_gemm_t<128, A_MN, B_MN, EPI>(ta, tb, M, N, K, ep, num_sms, stream);
+    case 256: return launch_gemm_t<256, A_MN, B_MN, EPI>(ta, tb, M, N, K, ep, num_sms, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
+                        int M, int N, int K, const EpiArgs& ep, int num_sms,
+                        cudaStream_t stream) {
+  switch (kind) {
+    case GemmKind::FwdTanh:
+      return launch_gemm_bn<false, false, EPI_TANH_BF16>(bn, ta, tb, M, N, K, ep, num_sms, stream);
+    case GemmKind::FwdLinear:
+      return launch_gemm_bn<false, false, EPI_BIAS_F32>(bn, ta, tb, M, N, K, ep, num_sms, stream);
+    case GemmKind::BwdData:
+      return launch_gemm_bn<false, true, EPI_DTANH_BF16>(bn, ta, tb, M, N, K, ep, num_sms, stream);
+    case GemmKind::BwdWeight:
+      return launch_gemm_bn<true, true, EPI_F32>(bn, ta, tb, M, N, K, ep, num_sms, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int BN, int KMAX>
+static cudaError_t launch_head_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N,
+                                 int K, const HeadArgs& hp, cudaStream_t stream) {
+  auto kern = teacher_head_kernel<BN, KMAX>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         GemmCfg<BN>::kSmem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int cs = (N + BN - 1) / BN;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs, (M + kBM - 1) / kBM, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = GemmCfg<BN>::kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, hp);
+}
+
+template <int BN>
+static cudaError_t launch_head_k(int kmax, const CUtensorMap& ta, const CUtensorMap& tb, int M,
+                                 int N, int K, const HeadArgs& hp, cudaStream_t stream) {
+  switch (kmax) {
+    case 4: return launch_head_t<BN, 4>(ta, tb, M, N, K, hp, stream);
+    case 8: return launch_head_t<BN, 8>(ta, tb, M, N, K, hp, stream);
+    case 16: return launch_head_t<BN, 16>(ta, tb, M, N, K, hp, stream);
+    case 32: return launch_head_t<BN, 32>(ta, tb, M, N, K, hp, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_teacher_head(int bn, int kmax, const CUtensorMap& ta, const CUtensorMap& tb,
+                                int M, int N, int K, const HeadArgs& hp, cudaStream_t stream) {
+  switch (bn) {
+    case 64: return launch_head_k<64>(kmax, ta, tb, M, N, K, hp, stream);
+    case 128: return launch_head_k<128>(kmax, ta, tb, M, N, K, hp, stream);
+    case 256: return launch_head_k<256>(kmax, ta, tb, M, N, K, hp, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace edl

@@ -1,0 +1,62 @@
+// internal.h — launcher interfaces shared by the .cu files behind the C-ABI.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace edl {
+
+enum EpiMode : int {
+  EPI_TANH_BF16 = 0,   // out(bf16) = tanh(acc + bias)
+  EPI_BIAS_F32 = 1,    // out(f32)  = acc + bias
+  EPI_DTANH_BF16 = 2,  // out(bf16) = acc * (1 - aux^2)
+  EPI_F32 = 3,         // out(f32)  = acc * scale
+};
+
+struct EpiArgs {
+  void* out;
+  long long ld_out;
+  const float* bias;
+  const __nv_bfloat16* aux;
+  long long ld_aux;
+  float scale;
+};
+
+struct HeadArgs {
+  const float* bias;
+  float inv_t;
+  int k;
+  float* vals;
+  int* idx;
+};
+
+enum class GemmKind { FwdTanh, FwdLinear, BwdData, BwdWeight };
+
+cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
+                        int M, int N, int K, const EpiArgs& ep, int num_sms,
+                        cudaStream_t stream);
+cudaError_t launch_teacher_head(int bn, int kmax, const CUtensorMap& ta, const CUtensorMap& tb,
+                                int M, int N, int K, const HeadArgs& hp, cudaStream_t stream);
+
+// SIMT kernels (kernels.cu)
+cudaError_t launch_kd_loss(const float* logits, long long ld_z, const int64_t* labels,
+                           const float* q_vals, const int* q_idx, int B, int K, int k,
+                           float alpha, float beta, float T, float* row_loss, float* loss_out,
+                           unsigned* ticket, __nv_bfloat16* dlogits, long long ld_dz,
+                           int* status, cudaStream_t stream);
+cudaError_t launch_tempered_softmax(const float* logits, long long ld, float* probs,
+                                    long long ld_p, int B, int K, float T, cudaStream_t stream);
+cudaError_t launch_sgd(float* p, __nv_bfloat16* p_bf16, const float* g, long long n,
+                       float scale, cudaStream_t stream);
+cudaError_t launch_gather_rows(const __nv_bfloat16* src, long long ld_src, const int64_t* idx,
+                               __nv_bfloat16* dst, long long ld_dst, int B, int D,
+                               cudaStream_t stream);
+cudaError_t launch_colsum(const __nv_bfloat16* x, long long ld, int M, int N, float* partial,
+                          float* out, float scale, cudaStream_t stream);
+cudaError_t launch_topk_hits(const float* logits, long long ld, const int64_t* labels, int B,
+                             int K, int k, unsigned* hits, cudaStream_t stream);
+cudaError_t launch_cast_bf16(const float* src, long long ld_src, __nv_bfloat16* dst,
+                             long long ld_dst, int rows, int cols, cudaStream_t stream);
+
+}  // namespace edl

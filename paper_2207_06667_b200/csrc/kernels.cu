@@ -1,0 +1,340 @@
+// kernels.cu — the HBM-bound (SIMT) kernels of the EDL-Dist hot path.
+//
+//   kd_loss_kernel        edl/nnkit.py:283-295  fused hard+soft loss and dlogits,
+//                         one warp per row, both log-sum-exps in one HBM pass
+//   tempered_softmax      edl/nnkit.py:193-208  dense probabilities (reference API)
+//   sgd_kernel            edl/nnkit.py:312-322  p -= scale * g on fp32 masters,
+//                         refreshes the bf16 operand copy in the same pass
+//   gather_rows           edl/student_node.py:145-151  batch = shard[rows]
+//   colsum                edl/nnkit.py:306      db = sum over the batch of delta
+//   topk_hits             edl/nnkit.py:325-335  top-k accuracy, lower-index ties
+#include "internal.h"
+
+#include <cfloat>
+
+namespace edl {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ void set_status(int* status, int code) {
+  if (status) atomicCAS(status, 0, code);
+}
+
+// ------------------------------------------------------------------ KD loss
+// loss_row = alpha * (lse(z) - z_y) + beta * T^2 * (-sum_j q_j (z_{i_j}/T - lse(z/T)))
+// dz       = alpha/B (softmax(z) - onehot(y)) + beta*T/B (softmax(z/T) - q)
+// q is the teacher's top-k (prob, class) list renormalised to sum 1 (k = K is
+// the dense reference case). The row lives in shared memory (fp32) between the
+// passes, so HBM sees one read of z and one bf16 write of dz.
+constexpr int kKdWarps = 8;
+
+__global__ void __launch_bounds__(kKdWarps * 32)
+    kd_loss_kernel(const float* __restrict__ z, long long ld_z, const int64_t* __restrict__ labels,
+                   const float* __restrict__ qv, const int* __restrict__ qi, int B, int K,
+                   int Kw, int k, float alpha, float beta, float T, float* __restrict__ row_loss,
+                   float* __restrict__ loss_out, unsigned* __restrict__ ticket,
+                   __nv_bfloat16* __restrict__ dz, long long ld_dz, int* __restrict__ status) {
+  extern __shared__ float sm[];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int kp = (Kw + 3) & ~3;
+  float* zs = sm + warp * 2 * kp;
+  float* ds = zs + kp;
+  const float inv_t = 1.0f / T;
+  const float ch = alpha / static_cast<float>(B);
+  const float cs = beta * T / static_cast<float>(B);
+  const bool use_soft = beta > 0.f && k > 0;
+
+  for (int row = blockIdx.x * kKdWarps + warp; row < B; row += gridDim.x * kKdWarps) {
+    const float* zr = z + static_cast<size_t>(row) * ld_z;
+    float m = -INFINITY;
+    for (int c = lane; c < K; c += 32) {
+      const float v = __ldg(zr + c);
+      zs[c] = v;
+      m = fmaxf(m, v);
+    }
+    m = warp_max(m);
+    float s1 = 0.f, st = 0.f;
+    for (int c = lane; c < K; c += 32) {
+      const float d = zs[c] - m;
+      s1 += __expf(d);
+      st += __expf(d * inv_t);
+    }
+    s1 = warp_sum(s1);
+    st = warp_sum(st);
+    const float lse1 = m + __logf(s1);
+    const float lset = m * inv_t + __logf(st);
+    const int64_t y = labels[row];
+    const bool y_ok = (y >= 0 && y < K);
+    if (!y_ok && lane == 0) set_status(status, -1);
+    float qsum = 0.f;
+    if (use_soft) {
+      for (int j = lane; j < k; j += 32) qsum += __ldg(qv + static_cast<size_t>(row) * k + j);
+      qsum = warp_sum(qsum);
+    }
+    for (int c = lane; c < K; c += 32) {
+      const float v = zs[c];
+      float d = 0.f;
+      if (alpha > 0.f) d += ch * (__expf(v - lse1) - (c == y ? 1.f : 0.f));
+      if (use_soft) d += cs * __expf(v * inv_t - lset);
+      ds[c] = d;
+    }
+    __syncwarp();
+    float lsoft = 0.f;
+    if (use_soft) {
+      const float inv_q = 1.0f / qsum;
+      for (int j = lane; j < k; j += 32) {
+        const float q = __ldg(qv + static_cast<size_t>(row) * k + j) * inv_q;
+        const int id = __ldg(qi + static_cast<size_t>(row) * k + j);
+        if (id < 0 || id >= K) { set_status(status, -1); continue; }
+        ds[id] -= cs * q;
+        lsoft += q * (zs[id] * inv_t - lset);
+      }
+      lsoft = -warp_sum(lsoft);
+    }
+    __syncwarp();
+    __nv_bfloat16* dr = dz + static_cast<size_t>(row) * ld_dz;
+    for (int c = lane; c < Kw; c += 32) dr[c] = __float2bfloat16_rn(c < K ? ds[c] : 0.f);
+    if (lane == 0) {
+      float l = 0.f;
+      if (alpha > 0.f) l += alpha * (y_ok ? (lse1 - zs[y]) : 0.f);
+      if (use_soft) l += beta * T * T * lsoft;
+      row_loss[row] = l;
+    }
+    __syncwarp();
+  }
+
+  // Deterministic batch mean: the last block to finish sums row losses in a
+  // fixed order (independent of the grid), so every rank computes the same bits.
+  __shared__ bool is_last;
+  __shared__ double red[kKdWarps * 32];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!is_last) return;
+  double acc = 0.0;
+  for (int r = threadIdx.x; r < B; r += blockDim.x) acc += static_cast<double>(__ldcg(row_loss + r));
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const float loss = static_cast<float>(red[0] / static_cast<double>(B));
+    *loss_out = loss;
+    if (!isfinite(loss)) set_status(status, -2);
+    *ticket = 0u;
+  }
+}
+
+cudaError_t launch_kd_loss(const float* logits, long long ld_z, const int64_t* labels,
+                           const float* q_vals, const int* q_idx, int B, int K, int k,
+                           float alpha, float beta, float T, float* row_loss, float* loss_out,
+                           unsigned* ticket, __nv_bfloat16* dlogits, long long ld_dz,
+                           int* status, cudaStream_t stream) {
+  const int Kw = static_cast<int>(ld_dz < (((K + 15) / 16) * 16) ? ld_dz : ((K + 15) / 16) * 16);
+  const int kp = (Kw + 3) & ~3;
+  const size_t smem = static_cast<size_t>(kKdWarps) * 2 * kp * sizeof(float);
+  static size_t smem_set = 48 * 1024;
+  if (smem > smem_set) {
+    cudaError_t e = cudaFuncSetAttribute(kd_loss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    smem_set = smem;
+  }
+  int blocks = (B + kKdWarps - 1) / kKdWarps;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  kd_loss_kernel<<<blocks, kKdWarps * 32, smem, stream>>>(logits, ld_z, labels, q_vals, q_idx, B, K,
+                                                         Kw, k, alpha, beta, T, row_loss, loss_out,
+                                                         ticket, dlogits, ld_dz, status);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ tempered softmax
+__global__ void tempered_softmax_kernel(const float* __restrict__ z, long long ld,
+                                        float* __restrict__ p, long long ld_p, int B, int K,
+                                        float inv_t) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+  if (warp >= B) return;
+  const float* zr = z + static_cast<size_t>(warp) * ld;
+  float m = -INFINITY;
+  for (int c = lane; c < K; c += 32) m = fmaxf(m, zr[c]);
+  m = warp_max(m);
+  float s = 0.f;
+  for (int c = lane; c < K; c += 32) s += __expf((zr[c] - m) * inv_t);
+  s = warp_sum(s);
+  const float inv_s = 1.0f / s;
+  float* pr = p + static_cast<size_t>(warp) * ld_p;
+  for (int c = lane; c < K; c += 32) pr[c] = __expf((zr[c] - m) * inv_t) * inv_s;
+}
+
+cudaError_t launch_tempered_softmax(const float* logits, long long ld, float* probs,
+                                    long long ld_p, int B, int K, float T, cudaStream_t stream) {
+  const int threads = 256;
+  const int blocks = (B * 32 + threads - 1) / threads;
+  tempered_softmax_kernel<<<blocks, threads, 0, stream>>>(logits, ld, probs, ld_p, B, K, 1.0f / T);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ SGD
+__global__ void sgd_kernel(float* __restrict__ p, __nv_bfloat16* __restrict__ pb,
+                           const float* __restrict__ g, long long n, float scale) {
+  const long long n4 = n / 4;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+    float4 pv = reinterpret_cast<float4*>(p)[i];
+    const float4 gv = __ldg(reinterpret_cast<const float4*>(g) + i);
+    pv.x -= scale * gv.x; pv.y -= scale * gv.y; pv.z -= scale * gv.z; pv.w -= scale * gv.w;
+    reinterpret_cast<float4*>(p)[i] = pv;
+    if (pb) {
+      uint2 q;
+      __nv_bfloat162 a = __floats2bfloat162_rn(pv.x, pv.y), b = __floats2bfloat162_rn(pv.z, pv.w);
+      q.x = *reinterpret_cast<uint32_t*>(&a);
+      q.y = *reinterpret_cast<uint32_t*>(&b);
+      reinterpret_cast<uint2*>(pb)[i] = q;
+    }
+  }
+  for (long long i = n4 * 4 + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    p[i] -= scale * g[i];
+    if (pb) pb[i] = __float2bfloat16_rn(p[i]);
+  }
+}
+
+cudaError_t launch_sgd(float* p, __nv_bfloat16* p_bf16, const float* g, long long n, float scale,
+                       cudaStream_t stream) {
+  const int threads = 256;
+  long long blocks = (n / 4 + threads - 1) / threads;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  sgd_kernel<<<static_cast<int>(blocks), threads, 0, stream>>>(p, p_bf16, g, n, scale);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ gather
+__global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, long long ld_src,
+                                   const int64_t* __restrict__ idx, __nv_bfloat16* __restrict__ dst,
+                                   long long ld_dst, int B, int D) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+  if (warp >= B) return;
+  const int64_t r = idx[warp];
+  const __nv_bfloat16* s = src + static_cast<size_t>(r) * ld_src;
+  __nv_bfloat16* d = dst + static_cast<size_t>(warp) * ld_dst;
+  const int v = D / 8;
+  for (int c = lane; c < v; c += 32) reinterpret_cast<uint4*>(d)[c] = __ldg(reinterpret_cast<const uint4*>(s) + c);
+  for (int c = v * 8 + lane; c < D; c += 32) d[c] = s[c];
+}
+
+cudaError_t launch_gather_rows(const __nv_bfloat16* src, long long ld_src, const int64_t* idx,
+                               __nv_bfloat16* dst, long long ld_dst, int B, int D,
+                               cudaStream_t stream) {
+  const int threads = 256;
+  const int blocks = (B * 32 + threads - 1) / threads;
+  gather_rows_kernel<<<blocks, threads, 0, stream>>>(src, ld_src, idx, dst, ld_dst, B, D);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ column sum
+// Two fixed-order passes: 128-row chunks -> partial[chunk][n], then chunks summed
+// in order (deterministic, no atomics).
+constexpr int kColRows = 128;
+
+__global__ void colsum_partial_kernel(const __nv_bfloat16* __restrict__ x, long long ld, int M,
+                                      int N, float* __restrict__ partial) {
+  __shared__ float2 red[8][32];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int n = blockIdx.x * 64 + 2 * lane;
+  const int r0 = blockIdx.y * kColRows;
+  float2 acc = make_float2(0.f, 0.f);
+  if (n < N) {
+    for (int r = r0 + warp; r < r0 + kColRows && r < M; r += 8) {
+      const __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(x + static_cast<size_t>(r) * ld + n);
+      acc.x += __bfloat162float(v.x);
+      acc.y += __bfloat162float(v.y);
+    }
+  }
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && n < N) {
+    float2 s = red[0][lane];
+    for (int w = 1; w < 8; ++w) { s.x += red[w][lane].x; s.y += red[w][lane].y; }
+    partial[static_cast<size_t>(blockIdx.y) * N + n] = s.x;
+    if (n + 1 < N) partial[static_cast<size_t>(blockIdx.y) * N + n + 1] = s.y;
+  }
+}
+
+__global__ void colsum_final_kernel(const float* __restrict__ partial, int chunks, int N,
+                                    float* __restrict__ out, float scale) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  float s = 0.f;
+  for (int c = 0; c < chunks; ++c) s += partial[static_cast<size_t>(c) * N + n];
+  out[n] = s * scale;
+}
+
+cudaError_t launch_colsum(const __nv_bfloat16* x, long long ld, int M, int N, float* partial,
+                          float* out, float scale, cudaStream_t stream) {
+  const int chunks = (M + kColRows - 1) / kColRows;
+  dim3 grid((N + 63) / 64, chunks);
+  colsum_partial_kernel<<<grid, 256, 0, stream>>>(x, ld, M, N, partial);
+  colsum_final_kernel<<<(N + 255) / 256, 256, 0, stream>>>(partial, chunks, N, out, scale);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ top-k accuracy
+__global__ void topk_hits_kernel(const float* __restrict__ z, long long ld,
+                                 const int64_t* __restrict__ labels, int B, int K, int k,
+                                 unsigned* __restrict__ hits) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+  if (warp >= B) return;
+  const float* zr = z + static_cast<size_t>(warp) * ld;
+  const int64_t y = labels[warp];
+  const float zy = zr[y];
+  int cnt = 0;
+  for (int c = lane; c < K; c += 32) {
+    const float v = zr[c];
+    cnt += (v > zy || (v == zy && c < y)) ? 1 : 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if (lane == 0 && cnt < k) atomicAdd(hits, 1u);
+}
+
+cudaError_t launch_topk_hits(const float* logits, long long ld, const int64_t* labels, int B,
+                             int K, int k, unsigned* hits, cudaStream_t stream) {
+  const int threads = 256;
+  topk_hits_kernel<<<(B * 32 + threads - 1) / threads, threads, 0, stream>>>(logits, ld, labels, B, K, k, hits);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ fp32 -> bf16
+__global__ void cast_bf16_kernel(const float* __restrict__ src, long long ld_src,
+                                 __nv_bfloat16* __restrict__ dst, long long ld_dst, int rows,
+                                 int cols) {
+  const long long total = static_cast<long long>(rows) * cols;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / cols, c = i % cols;
+    dst[r * ld_dst + c] = __float2bfloat16_rn(src[r * ld_src + c]);
+  }
+}
+
+cudaError_t launch_cast_bf16(const float* src, long long ld_src, __nv_bfloat16* dst,
+                             long long ld_dst, int rows, int cols, cudaStream_t stream) {
+  long long total = static_cast<long long>(rows) * cols;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (blocks < 1) blocks = 1;
+  cast_bf16_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(src, ld_src, dst, ld_dst, rows, cols);
+  return cudaGetLastError();
+}
+
+}  // namespace edl

@@ -1,0 +1,193 @@
+"""Kernel-level parity on the B200: each sm_100a kernel against a plain torch
+fp32 computation over the SAME bf16 operands (so the comparison isolates the
+kernel's accumulation / epilogue error from bf16 input rounding)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2207_06667_b200 import _lib
+    return _lib
+
+
+def _s():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _bf(x):
+    return x.to(torch.bfloat16)
+
+
+def _rand(*shape, scale=1.0, seed=0):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    return (torch.randn(*shape, generator=g) * scale).cuda()
+
+
+def _padded(t, rows, cols, dtype=torch.bfloat16):
+    out = torch.zeros(rows, cols, dtype=dtype, device=t.device)
+    out[:t.shape[0], :t.shape[1]] = t.to(dtype)
+    return out
+
+
+GEMM_SHAPES = [(37, 16, 16), (128, 64, 64), (300, 208, 112), (513, 320, 1000), (1024, 1024, 2048),
+               (256, 2304, 512)]
+
+
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+@pytest.mark.parametrize("act", [0, 1])
+def test_linear_fwd(lib, M, N, K, act):
+    Kp, Np = (K + 15) // 16 * 16, (N + 15) // 16 * 16
+    x = _padded(_rand(M, K, seed=1), M, Kp)
+    w = _padded(_rand(N, K, scale=K ** -0.5, seed=2), Np, Kp)
+    b = torch.zeros(Np, device="cuda")
+    b[:N] = _rand(N, seed=3) * 0.1
+    ref = x.float() @ w.float().T + b
+    if act == 1:
+        y = torch.empty(M, Np, dtype=torch.bfloat16, device="cuda")
+        ref = torch.tanh(ref)
+    else:
+        y = torch.empty(M, Np, dtype=torch.float32, device="cuda")
+    lib.call("edl_linear_fwd", x.data_ptr(), Kp, w.data_ptr(), Kp, b.data_ptr(), y.data_ptr(), Np,
+             M, Np, Kp, act, _s())
+    torch.cuda.synchronize()
+    err = (y.float() - ref).abs().max().item()
+    tol = 2e-2 if act == 1 else 1e-3 * max(1.0, ref.abs().max().item())
+    assert err < tol, (err, tol)
+
+
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+def test_linear_bwd_data(lib, M, N, K):
+    # dX[M,K] = (dY[M,N] @ W[N,K]) * (1 - H^2)
+    Kp, Np = (K + 15) // 16 * 16, (N + 15) // 16 * 16
+    dy = _padded(_rand(M, N, seed=4), M, Np)
+    w = _padded(_rand(N, K, scale=N ** -0.5, seed=5), Np, Kp)
+    h = _padded(torch.tanh(_rand(M, K, seed=6)), M, Kp)
+    dx = torch.empty(M, Kp, dtype=torch.bfloat16, device="cuda")
+    lib.call("edl_linear_bwd_data", dy.data_ptr(), Np, w.data_ptr(), Kp, h.data_ptr(), Kp,
+             dx.data_ptr(), Kp, M, Np, Kp, _s())
+    torch.cuda.synchronize()
+    ref = (dy.float() @ w.float()) * (1 - h.float() ** 2)
+    err = (dx.float() - ref).abs().max().item()
+    assert err < 2e-2 * max(1.0, ref.abs().max().item()), err
+
+
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+def test_linear_bwd_weight(lib, M, N, K):
+    # dW[N,K] = s * dY[M,N]^T @ X[M,K];  db = s * colsum(dY)
+    Kp, Np = (K + 15) // 16 * 16, (N + 15) // 16 * 16
+    dy = _padded(_rand(M, N, seed=7), M, Np)
+    x = _padded(_rand(M, K, seed=8), M, Kp)
+    dw = torch.full((Np, Kp), float("nan"), device="cuda")
+    db = torch.full((Np,), float("nan"), device="cuda")
+    ws = torch.empty(int(lib.load().edl_colsum_workspace_floats(M, Np)), device="cuda")
+    lib.call("edl_linear_bwd_weight", dy.data_ptr(), Np, x.data_ptr(), Kp, dw.data_ptr(), Kp,
+             db.data_ptr(), ws.data_ptr(), M, Np, Kp, 0.5, _s())
+    torch.cuda.synchronize()
+    ref = 0.5 * dy.float().T @ x.float()
+    refb = 0.5 * dy.float().sum(0)
+    scale = max(1.0, ref.abs().max().item())
+    assert (dw - ref).abs().max().item() < 1e-3 * scale
+    assert (db - refb).abs().max().item() < 1e-3 * max(1.0, refb.abs().max().item())
+
+
+@pytest.mark.parametrize("B,H,K,k", [(32, 256, 10, 10), (32, 256, 10, 4), (200, 512, 100, 16),
+                                     (256, 1024, 1000, 16), (130, 2048, 1000, 32),
+                                     (64, 256, 2000, 8)])
+def test_teacher_head_softmax_topk(lib, B, H, K, k):
+    T = 2.0
+    Hp, Kp = (H + 15) // 16 * 16, (K + 15) // 16 * 16
+    h = _padded(torch.tanh(_rand(B, H, seed=9)), B, Hp)
+    w = _padded(_rand(K, H, scale=3 * H ** -0.5, seed=10), Kp, Hp)
+    b = torch.zeros(Kp, device="cuda")
+    b[:K] = _rand(K, seed=11) * 0.1
+    vals = torch.empty(B, k, device="cuda")
+    idx = torch.empty(B, k, dtype=torch.int32, device="cuda")
+    lib.call("edl_teacher_head_softmax_topk", h.data_ptr(), Hp, w.data_ptr(), Hp, b.data_ptr(), B, K,
+             Hp, T, k, vals.data_ptr(), idx.data_ptr(), _s())
+    torch.cuda.synchronize()
+    z = (h.double() @ w.double().T + b.double())[:, :K]
+    p = torch.softmax(z / T, dim=1)
+    order = torch.from_numpy(np.argsort(-p.cpu().numpy(), axis=1, kind="stable")[:, :k]).cuda()
+    # index parity where the k-th / (k+1)-th gap exceeds fp32 accumulation noise
+    sp = torch.sort(z, dim=1, descending=True).values
+    gap = (sp[:, k - 1] - sp[:, k]) if k < K else torch.full((B,), 1e9, device="cuda", dtype=sp.dtype)
+    safe = gap > 1e-3
+    assert safe.float().mean() > 0.5
+    assert torch.equal(idx[safe].long(), order[safe])
+    pv = torch.gather(p, 1, idx.long())
+    assert (vals.double() - pv).abs().max().item() < 1e-5
+
+
+@pytest.mark.parametrize("B,K,k,alpha,beta,T", [(32, 10, 10, 0.5, 0.5, 2.0), (32, 10, 4, 1.0, 0.0, 2.0),
+                                                (300, 1000, 16, 0.5, 0.5, 2.0), (64, 100, 100, 0.0, 1.0, 3.0),
+                                                (4096, 1000, 16, 0.7, 0.3, 0.5)])
+def test_kd_loss(lib, B, K, k, alpha, beta, T):
+    Kp = (K + 15) // 16 * 16
+    z = torch.zeros(B, Kp, device="cuda")
+    z[:, :K] = _rand(B, K, scale=3.0, seed=12)
+    y = torch.randint(0, K, (B,), generator=torch.Generator().manual_seed(1)).cuda()
+    q = torch.rand(B, K, generator=torch.Generator().manual_seed(2)).cuda() + 0.05
+    qv, qi = torch.topk(q, k, dim=1)
+    qi = qi.int()
+    qv = qv.contiguous()
+    row = torch.empty(B, device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    ticket = torch.zeros(1, dtype=torch.int32, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    dz = torch.full((B, Kp), 7.0, dtype=torch.bfloat16, device="cuda")
+    lib.call("edl_kd_loss_fwd_bwd", z.data_ptr(), Kp, y.data_ptr(), qv.data_ptr(), qi.data_ptr(), B, K, k,
+             alpha, beta, T, row.data_ptr(), loss.data_ptr(), ticket.data_ptr(), dz.data_ptr(), Kp,
+             status.data_ptr(), _s())
+    torch.cuda.synchronize()
+    zz = z[:, :K].double()
+    qd = torch.zeros(B, K, device="cuda", dtype=torch.float64).scatter_(1, qi.long(), qv.double())
+    qd = qd / qd.sum(1, keepdim=True)
+    logp = torch.log_softmax(zz, 1)
+    logpt = torch.log_softmax(zz / T, 1)
+    ref = 0.0
+    dref = torch.zeros_like(zz)
+    if alpha > 0:
+        ref += alpha * (-logp[torch.arange(B), y]).mean()
+        dref += alpha / B * (logp.exp() - torch.nn.functional.one_hot(y, K))
+    if beta > 0:
+        ref += beta * T * T * (-(qd * logpt).sum(1)).mean()
+        dref += beta * T / B * (logpt.exp() - qd)
+    assert status.item() == 0 and ticket.item() == 0
+    assert abs(loss.item() - float(ref)) < 1e-4 * max(1.0, abs(float(ref)))
+    assert (dz[:, :K].double() - dref).abs().max().item() < 1e-2 * dref.abs().max().item() + 1e-6
+    assert (dz[:, K:] == 0).all()
+
+
+def test_sgd_and_cast(lib):
+    n = 1003
+    p = _rand(n, seed=13)
+    g = _rand(n, seed=14)
+    pb = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    ref = p - 0.25 * g
+    lib.call("edl_sgd_step", p.data_ptr(), pb.data_ptr(), g.data_ptr(), n, 0.25, _s())
+    torch.cuda.synchronize()
+    assert torch.equal(p, ref)
+    assert torch.equal(pb, ref.to(torch.bfloat16))
+
+
+def test_gather_rows(lib):
+    src = _bf(_rand(100, 48, seed=15))
+    idx = torch.tensor([5, 99, 0, 5, 42], dtype=torch.int64, device="cuda")
+    dst = torch.empty(5, 48, dtype=torch.bfloat16, device="cuda")
+    lib.call("edl_gather_rows", src.data_ptr(), 48, idx.data_ptr(), dst.data_ptr(), 48, 5, 48, _s())
+    torch.cuda.synchronize()
+    assert torch.equal(dst, src[idx])
+
+
+def test_topk_hits_tie_rule(lib):
+    z = torch.zeros(4, 16, device="cuda")
+    y = torch.tensor([0, 1, 3, 2], dtype=torch.int64, device="cuda")
+    hits = torch.zeros(1, dtype=torch.int32, device="cuda")
+    lib.call("edl_topk_hits", z.data_ptr(), 16, y.data_ptr(), 4, 10, 1, hits.data_ptr(), _s())
+    torch.cuda.synchronize()
+    assert hits.item() == 1   # constant logits: only class 0 ranks first
