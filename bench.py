@@ -1,0 +1,458 @@
+#!/usr/bin/env python
+"""EDL-Dist hot path on B200: student-train samples/s with the teacher in the loop.
+
+Workload (default, --config cfg3): BASELINE.json configs[2]'s wide MLP pair —
+teacher [3072, 8192, 8192, 1000] (100.5 M params, bf16), student
+[3072, 2048, 1024, 1000] (9.4 M params, fp32 master + bf16), synthetic
+1000-class blobs (make_blobs seed 0), T=2, alpha=beta=0.5, eta=0.05, top-k=16,
+per-GPU student batch 4096. One "step" = one student training step (gather ->
+fwd GEMMs -> fused KD loss -> bwd GEMMs -> [NCCL all-reduce] -> SGD) whose soft
+labels were produced by the teacher pool inside the timed region
+(teacher: gather -> 2 tanh GEMMs -> head GEMM with fused softmax/top-k).
+
+Placement (--placement): `colocated` (default) runs a teacher worker on each
+GPU next to that GPU's student shard (its own CUDA stream, decoupled through
+the DistilReader ring), with the student gradient all-reduced over NCCL.
+`online` is the reference's synchronous online-KD baseline with the same
+kernels (teacher then student on one stream). Both are measured; `value` is
+the EDL-Dist (decoupled) number.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "cfg3": dict(workload="cfg3 wide-MLP distillation (teacher 100.5M -> student 9.4M, 1000 classes)",
+                 dim=3072, classes=1000, teacher=(3072, 8192, 8192, 1000), student=(3072, 2048, 1024, 1000),
+                 topk=16, T=2.0, alpha=0.5, beta=0.5, eta=0.05, batch=4096, n_data=32768, ref_batch=256),
+    "cfg2": dict(workload="cfg2 small-MLP distillation (teacher [16,256,256,10] -> student [16,64,10])",
+                 dim=16, classes=10, teacher=(16, 256, 256, 10), student=(16, 64, 10),
+                 topk=10, T=2.0, alpha=0.5, beta=0.5, eta=0.05, batch=4096, n_data=65536, ref_batch=4096),
+}
+
+
+def flops_per_sample(cfg) -> tuple[float, float]:
+    t = cfg["teacher"]
+    s = cfg["student"]
+    tf = 2.0 * sum(t[i] * t[i + 1] for i in range(len(t) - 1))
+    fwd = 2.0 * sum(s[i] * s[i + 1] for i in range(len(s) - 1))
+    dx = 2.0 * sum(s[i] * s[i + 1] for i in range(1, len(s) - 1))
+    return tf, 2 * fwd + dx
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p["hbm_gbs"], p["bf16_tflops"], p["bf16_tflops_sustained"], "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except (OSError, subprocess.SubprocessError):
+                return
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [int(r[1]) for r in self.rows if r[1].isdigit()]
+        mx = [int(r[2]) for r in self.rows if r[2].isdigit()]
+        reasons = set()
+        for r in self.rows:
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"),
+                               r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": int(statistics.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU arms (the oracle is only ever the baseline here)
+
+
+def cpu_reference_rate(cfg, teacher_h, student_h, samples, labels, budget_s: float, max_batches: int):
+    """Reference CPU path (oracle port of edl/nnkit.py, numpy fp64, all host
+    threads): teacher tempered_softmax(forward()) + top-k, then kd_loss +
+    sgd_step on the student — one bounded batch per step."""
+    from oracle import nnkit_ref as ref
+    tw, tb = list(teacher_h.weights), list(teacher_h.biases)
+    sw, sb = list(student_h.weights), list(student_h.biases)
+    B = cfg["ref_batch"]
+    n = 0
+    t0 = time.perf_counter()
+    times = []
+    while n < max_batches and (time.perf_counter() - t0 < budget_s or n < 2):
+        lo = (n * B) % (samples.shape[0] - B)
+        x, y = samples[lo:lo + B], labels[lo:lo + B]
+        s = time.perf_counter()
+        p = ref.tempered_softmax(ref.forward(tw, tb, x), cfg["T"])
+        q = ref.topk_dense(*ref.topk(p, cfg["topk"]), p.shape[1])
+        _, gw, gb = ref.kd_loss(sw, sb, x, y, q, cfg["alpha"], cfg["beta"], cfg["T"])
+        sw, sb = ref.sgd_step(sw, sb, gw, gb, cfg["eta"])
+        times.append(time.perf_counter() - s)
+        n += 1
+    return B / statistics.median(times), n, B
+
+
+def run_reference_arm(args, cfg):
+    from paper_2207_06667_b200 import formats
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    samples, labels = _host_data(cfg, rows=max(cfg["ref_batch"] * 8, 4096))
+    teacher_h = formats.init_model(cfg["teacher"], 1)
+    student_h = formats.init_model(cfg["student"], 0)
+    total = args.warmup + args.steps
+    rate, n, B = cpu_reference_rate(cfg, teacher_h, student_h, samples, labels, budget_s=1e9, max_batches=total)
+    cores = os.cpu_count()
+    line = {"metric": "student_train_samples_per_s_teacher_in_loop", "value": round(rate, 3),
+            "unit": "samples/s", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "batch_per_step": B},
+            "cpu_baseline": {"value": round(rate, 3), "unit": "samples/s", "cores": cores, "kind": "port",
+                             "sample": f"{n} batches of {B} rows (median step), numpy fp64 oracle of "
+                                       f"edl/nnkit.py, OpenBLAS threads={os.environ.get('OPENBLAS_NUM_THREADS', cores)}"},
+            "e2e": {"value": round(rate, 3), "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _host_data(cfg, rows=None):
+    from paper_2207_06667_b200 import formats
+    n = rows or cfg["n_data"]
+    d = formats.make_blobs(0, n, cfg["dim"], cfg["classes"], 1.0)
+    return d.samples, d.labels
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-online", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.batch:
+        cfg["batch"] = args.batch
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2207_06667_b200 import _lib, formats, nnkit
+    from paper_2207_06667_b200.data import DeviceDataset, DeviceShardSampler
+    from paper_2207_06667_b200.nnkit import Model, SoftLabels, TrainConfig
+    from paper_2207_06667_b200.reader import DistilReader, EventLog, SchedulerConfig, TeacherPool
+    from paper_2207_06667_b200.student import StudentStep
+    from paper_2207_06667_b200.teacher import TeacherConfig, TeacherWorker
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (the B200 path has no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _lib.load()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    B = cfg["batch"]
+    samples, labels = _host_data(cfg)
+    data = formats.Dataset(samples, labels)
+    ddata = DeviceDataset(data, dev)
+    teacher_h = formats.init_model(cfg["teacher"], 1)
+    student_h = formats.init_model(cfg["student"], 0)
+    teacher = Model.from_host(teacher_h, dev)
+    tcfg = TrainConfig(eta=cfg["eta"], alpha=cfg["alpha"], beta=cfg["beta"], temperature=cfg["T"], batch_size=B)
+    sampler = DeviceShardSampler(ddata, world, rank, B, seed=0)
+    W, K = args.warmup, args.steps
+    tflop_t, tflop_s = flops_per_sample(cfg)
+    hbm, peak_burst, peak_sust, peak_kind = load_peaks()
+
+    # ---------------- EDL-Dist (decoupled, co-located teacher worker per GPU)
+    student = Model.from_host(student_h, dev)
+    engine = StudentStep(student, tcfg, B, world, max_steps=W + K + 8)
+    pool = TeacherPool()
+    worker = TeacherWorker(TeacherConfig("t1", cfg["T"], cfg["topk"]), teacher, ddata)
+    pool.register(worker)
+    sched = SchedulerConfig(lt=2, ut=8, pipeline_depth=2, acquire_cooldown=1e9)
+
+    def edl_run(start, count, timed):
+        reader = DistilReader(f"student-{rank}", pool, sched, sampler, start, start + count, 1, EventLog(),
+                              cfg["T"], cfg["topk"])
+        reader.acquire(1)
+        probe = (1, []) if timed and len(cfg["teacher"]) > 3 else None
+        worker.probe = probe
+        barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        launches0 = _lib.launch_count
+        s.record()
+        for it in range(start, start + count):
+            batch = sampler.batch_for(it, out=engine.batch)
+            soft = reader.consume(it)
+            engine.step(batch, soft)
+        e.record()
+        barrier()
+        launches = _lib.launch_count - launches0
+        ledger = reader.ledger()
+        reader.close()
+        worker.probe = None
+        return s.elapsed_time(e) / 1e3, launches, ledger, probe
+
+    edl_run(0, W, False)
+    with ClockSampler(local) as clk:
+        t_edl, launches, ledger, probe = edl_run(W, K, True)
+    clocks = clk.summary()
+    t_edl_max = _max_over_ranks(t_edl, world, dev)
+    value = world * B * K / t_edl_max
+
+    # dominant kernel (teacher hidden layer 2, M=B N=8192 K=8192): CUDA events on
+    # the teacher worker's stream around each launch inside the timed region
+    roof = None
+    if probe and probe[1]:
+        durs = [a.elapsed_time(b) / 1e3 for a, b in probe[1]]
+        avg = sum(durs) / len(durs)
+        t = cfg["teacher"]
+        flop = 2.0 * B * t[1] * t[2]
+        achieved = flop / avg / 1e12
+        roof = {"kernel": "gemm_kernel<256,K-major,K-major,EPI_TANH_BF16> (teacher layer 2)",
+                "bound": "tensor", "achieved": round(achieved, 1), "peak": peak_sust,
+                "peak_kind": f"{peak_kind} bf16_tflops_sustained", "unit": "TFLOP/s",
+                "frac": round(achieved / peak_sust, 4), "avg_us": round(avg * 1e6, 2),
+                "algorithmic_flop_per_launch": flop, "traffic": _traffic_from_profiles()}
+
+    # ---------------- synchronous online-KD baseline (same kernels, one stream)
+    online = None
+    if not args.no_online:
+        student2 = Model.from_host(student_h, dev)
+        eng2 = StudentStep(student2, tcfg, B, world, max_steps=W + K + 8)
+        tws = nnkit.Workspace(teacher, B)
+        out = SoftLabels(torch.empty(B, cfg["topk"], device=dev),
+                         torch.empty(B, cfg["topk"], dtype=torch.int32, device=dev), cfg["T"])
+
+        def online_run(start, count):
+            barrier()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            for it in range(start, start + count):
+                batch = sampler.batch_for(it, out=eng2.batch)
+                soft = nnkit.teacher_soft_labels(teacher, batch.inputs, cfg["T"], cfg["topk"], out=out, ws=tws)
+                eng2.step(batch, soft)
+            e.record()
+            barrier()
+            return s.elapsed_time(e) / 1e3
+
+        online_run(0, W)
+        t_on = _max_over_ranks(online_run(W, K), world, dev)
+        online = {"value": round(world * B * K / t_on, 1), "unit": "samples/s",
+                  "ms_per_step": round(t_on / K * 1e3, 4),
+                  "edl_over_online": round((world * B * K / t_edl_max) / (world * B * K / t_on), 4)}
+
+    # ---------------- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = _e2e(cfg, samples, labels, teacher, student_h, tcfg, B, W, K, world, rank, dev, barrier)
+
+    # ---------------- CPU baseline (oracle port, rank 0 only, bounded sample)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, n, rb = cpu_reference_rate(cfg, teacher_h, student_h, samples, labels, budget_s=12.0, max_batches=40)
+        cpu = {"value": round(rate, 2), "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"{n} batches of {rb} rows of the same workload (median), numpy fp64 oracle of "
+                         "edl/nnkit.py teacher fwd+softmax+top-k and kd_loss+sgd_step"}
+
+    if rank == 0:
+        line = {
+            "metric": "student_train_samples_per_s_teacher_in_loop", "value": round(value, 1),
+            "unit": "samples/s", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": round(t_edl_max / K * 1e3, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (make_blobs seed 0, random-init teacher seed 1 / student seed 0)",
+            "config": {"workload": cfg["workload"], "placement": "colocated teacher worker + student per GPU",
+                       "mode": "edl (decoupled)", "global_batch": B * world, "per_gpu_batch": B,
+                       "topk": cfg["topk"], "temperature": cfg["T"], "parallelism": f"dp{world}",
+                       "l2": "inputs > L2 (dataset 200 MB, teacher weights 201 MB streamed every step)"},
+            "teacher_infer_samples_per_s": None,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "online": online,
+            "gpu_launches": launches, "clocks": clocks, "ledger_ok": ledger["ok"],
+            "algorithmic_flop_per_sample": {"teacher_fwd": tflop_t, "student_train": tflop_s},
+        }
+        line["tensor_roofline_samples_per_s"] = round(world * peak_sust * 1e12 / (tflop_t + tflop_s), 1)
+        line["frac_of_step_roofline"] = round(value / line["tensor_roofline_samples_per_s"], 4)
+        line["teacher_infer_samples_per_s"] = _teacher_rate(teacher, sampler, cfg, B, dev)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _teacher_rate(teacher, sampler, cfg, B, dev):
+    import torch
+
+    from paper_2207_06667_b200 import nnkit
+    x = sampler.batch_for(0).inputs
+    ws = nnkit.Workspace(teacher, B)
+    for _ in range(3):
+        nnkit.teacher_soft_labels(teacher, x, cfg["T"], cfg["topk"], ws=ws)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = 10
+    s.record()
+    for _ in range(n):
+        nnkit.teacher_soft_labels(teacher, x, cfg["T"], cfg["topk"], ws=ws)
+    e.record()
+    torch.cuda.synchronize()
+    return round(B * n / (s.elapsed_time(e) / 1e3), 1)
+
+
+def _e2e(cfg, samples, labels, teacher, student_h, tcfg, B, W, K, world, rank, dev, barrier):
+    """Same metric through the public API (nnkit.teacher_soft_labels / kd_loss /
+    sgd_step) with every step's inputs copied host->device from pinned memory
+    (double-buffered on a copy stream) and the step's loss read back to pinned
+    host memory."""
+    import torch
+
+    from paper_2207_06667_b200 import nnkit
+    from paper_2207_06667_b200.nnkit import Batch, Model, SoftLabels
+    from paper_2207_06667_b200.student import StudentStep
+    Dp = nnkit.pad(cfg["dim"])
+    nb = 4
+    host_x = torch.zeros(nb, B, Dp, dtype=torch.bfloat16).pin_memory()
+    host_y = torch.zeros(nb, B, dtype=torch.int64).pin_memory()
+    n = samples.shape[0]
+    for j in range(nb):
+        lo = (j * B * world + rank * B) % (n - B)
+        host_x[j, :, :cfg["dim"]] = torch.from_numpy(samples[lo:lo + B].astype(np.float32)).to(torch.bfloat16)
+        host_y[j] = torch.from_numpy(labels[lo:lo + B])
+    loss_host = torch.zeros(W + K, dtype=torch.float32).pin_memory()
+    student = Model.from_host(student_h, dev)
+    eng = StudentStep(student, tcfg, B, world, max_steps=W + K + 8)
+    tws = nnkit.Workspace(teacher, B)
+    bufs = [Batch(torch.empty(B, Dp, dtype=torch.bfloat16, device=dev), torch.empty(B, dtype=torch.int64, device=dev),
+                  cfg["dim"]) for _ in range(2)]
+    out = SoftLabels(torch.empty(B, cfg["topk"], device=dev),
+                     torch.empty(B, cfg["topk"], dtype=torch.int32, device=dev), cfg["T"])
+    copy = torch.cuda.Stream(dev)
+    main = torch.cuda.current_stream(dev)
+    up = [torch.cuda.Event() for _ in range(2)]
+    used = [None, None]
+
+    def upload(i):
+        j = i % 2
+        with torch.cuda.stream(copy):
+            if used[j] is not None:
+                copy.wait_event(used[j])
+            bufs[j].inputs.copy_(host_x[i % nb], non_blocking=True)
+            bufs[j].hard_labels.copy_(host_y[i % nb], non_blocking=True)
+            up[j].record(copy)
+
+    def run(start, count):
+        barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        upload(start)
+        for i in range(start, start + count):
+            if i + 1 < start + count:
+                upload(i + 1)
+            j = i % 2
+            main.wait_event(up[j])
+            soft = nnkit.teacher_soft_labels(teacher, bufs[j].inputs, cfg["T"], cfg["topk"], out=out, ws=tws)
+            eng.step(bufs[j], soft)
+            loss_host[i:i + 1].copy_(eng.losses[(eng._n - 1) % eng.losses.shape[0]:][:1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(main)
+            used[j] = ev
+        e.record()
+        barrier()
+        return s.elapsed_time(e) / 1e3
+
+    run(0, W)
+    t = _max_over_ranks(run(W, K), world, dev)
+    assert np.isfinite(loss_host[W:W + K].numpy()).all()
+    return {"value": round(world * B * K / t, 1), "unit": "samples/s", "h2d_bytes_per_step": B * (Dp * 2 + 8),
+            "d2h_bytes_per_step": 4, "mode": "online pipeline through nnkit public API, H2D double-buffered"}
+
+
+def _max_over_ranks(x: float, world: int, dev) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _traffic_from_profiles():
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh).get("teacher_layer2_dram_bytes")
+    except (OSError, ValueError):
+        return None
+
+
+if __name__ == "__main__":
+    main()

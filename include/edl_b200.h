@@ -97,9 +97,11 @@ int edl_kd_loss_fwd_bwd(const float* logits, long long ldz, const long long* lab
 int edl_sgd_step(float* p, void* p_bf16, const float* g, long long n, float scale, void* stream);
 
 /* Batch gather from an HBM-resident shard, edl/student_node.py:150-151:
- * dst[b][:D] = src[idx[b]][:D] (bf16, idx int64). */
+ * dst[b][:D] = src[idx[b]][:D] (bf16, idx int64) and, when both label
+ * pointers are given, dst_labels[b] = src_labels[idx[b]] (int64). */
 int edl_gather_rows(const void* src, long long ld_src, const long long* idx, void* dst,
-                    long long ld_dst, int B, int D, void* stream);
+                    long long ld_dst, int B, int D, const long long* src_labels,
+                    long long* dst_labels, void* stream);
 
 /* Top-k accuracy counter, edl/nnkit.py:325-335: hits += #rows whose label
  * ranks < k under (logit desc, class asc). */

@@ -257,3 +257,63 @@ def dp_distill_trajectory(student, teacher, samples, labels, students, batch_siz
         gw, gb = unflatten(avg, dims)
         ws, bs = sgd_step(ws, bs, gw, gb, eta)
     return (ws, bs), losses
+
+
+# ---------------------------------------------------------------- bf16-storage emulation
+def bf16(a):
+    """Round-to-nearest-even to bfloat16, returned as float64 (emulates the
+    device's bf16 storage points; arithmetic stays fp64)."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return r.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def kd_loss_bf16_storage(weights, biases, x, labels, soft_probs, alpha, beta, temperature):
+    """kd_loss (edl/nnkit.py:254-309) with the device path's storage points
+    rounded to bf16: inputs, weight copies, hidden activations, dlogits and
+    hidden deltas. Isolates the kernels' accumulation error in the parity
+    tests."""
+    wq = [bf16(w) for w in weights]
+    b = x.shape[0]
+    acts = [bf16(x)]
+    h = acts[0]
+    last = len(weights) - 1
+    for l, (w, bb) in enumerate(zip(wq, biases)):
+        z = h @ w.T + bb
+        h = z if l == last else bf16(np.tanh(z))
+        acts.append(h)
+    logits = acts[-1]
+    rows = np.arange(b)
+    loss = 0.0
+    dlogits = np.zeros_like(logits)
+    if alpha > 0:
+        logp = log_softmax(logits)
+        loss += alpha * float(-logp[rows, labels].mean())
+        p = np.exp(logp)
+        p[rows, labels] -= 1.0
+        dlogits += (alpha / b) * p
+    if beta > 0:
+        t = temperature
+        logp_t = log_softmax(logits / t)
+        loss += beta * t * t * float(-(soft_probs * logp_t).sum(axis=1).mean())
+        dlogits += (beta * t / b) * (np.exp(logp_t) - soft_probs)
+    gw = [None] * len(weights)
+    gb = [None] * len(biases)
+    delta = bf16(dlogits)
+    for l in range(len(weights) - 1, -1, -1):
+        gw[l] = delta.T @ acts[l]
+        gb[l] = delta.sum(axis=0)
+        if l > 0:
+            delta = bf16((delta @ wq[l]) * (1.0 - acts[l] ** 2))
+    return loss, gw, gb
+
+
+def forward_bf16_storage(weights, biases, x):
+    """forward() with bf16 inputs / weights / hidden activations (device storage)."""
+    h = bf16(x)
+    last = len(weights) - 1
+    for l, (w, b) in enumerate(zip(weights, biases)):
+        z = h @ bf16(w).T + b
+        h = z if l == last else bf16(np.tanh(z))
+    return h

@@ -39,7 +39,8 @@ _SIGNATURES = {
                             c_float, c_float, c_float, c_void_p, c_void_p, c_void_p, c_void_p,
                             c_ll, c_void_p, c_void_p],
     "edl_sgd_step": [c_void_p, c_void_p, c_void_p, c_ll, c_float, c_void_p],
-    "edl_gather_rows": [c_void_p, c_ll, c_void_p, c_void_p, c_ll, c_int, c_int, c_void_p],
+    "edl_gather_rows": [c_void_p, c_ll, c_void_p, c_void_p, c_ll, c_int, c_int, c_void_p, c_void_p,
+                        c_void_p],
     "edl_topk_hits": [c_void_p, c_ll, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p],
     "edl_cast_bf16": [c_void_p, c_ll, c_void_p, c_ll, c_int, c_int, c_void_p],
 }
@@ -94,5 +95,12 @@ def check(rc: int, what: str) -> None:
     raise RuntimeError(msg)
 
 
+# kernel launches per C entry point (bench.py reports launches in its timed region)
+_LAUNCHES = {"edl_linear_bwd_weight": 3}   # GEMM + two column-sum passes when db is requested
+launch_count = 0
+
+
 def call(name: str, *args) -> None:
+    global launch_count
     check(getattr(load(), name)(*args), name)
+    launch_count += _LAUNCHES.get(name, 1)

@@ -246,13 +246,15 @@ int edl_sgd_step(float* p, void* p_bf16, const float* g, long long n, float scal
 }
 
 int edl_gather_rows(const void* src, long long ld_src, const long long* idx, void* dst,
-                    long long ld_dst, int B, int D, void* stream) {
+                    long long ld_dst, int B, int D, const long long* src_labels,
+                    long long* dst_labels, void* stream) {
   if (B < 1 || D < 1 || ld_src < D || ld_dst < D || (ld_src % 8) || (ld_dst % 8))
     return fail(EDL_ERR_SHAPE, "gather_rows: bad shape B=%d D=%d", B, D);
   cudaError_t e = launch_gather_rows(reinterpret_cast<const __nv_bfloat16*>(src), ld_src,
                                      reinterpret_cast<const int64_t*>(idx),
                                      reinterpret_cast<__nv_bfloat16*>(dst), ld_dst, B, D,
-                                     as_stream(stream));
+                                     reinterpret_cast<const int64_t*>(src_labels),
+                                     reinterpret_cast<int64_t*>(dst_labels), as_stream(stream));
   return e == cudaSuccess ? 0 : cuda_fail(e, "gather_rows");
 }
 

@@ -257,31 +257,51 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ------------------------------------------------------------------ teacher head
 // Logits z = H W^T + b for a 128-row block, scaled s = z / T, and per row: the
 // running max / rescaled sum of exp(s) (online softmax) plus a register top-k
-// list ordered by (value desc, class index asc) — the tie rule of
+// buffer ordered by (value desc, class index asc) — the tie rule of
 // edl/nnkit.py:333. The class dimension is split across a cluster of CS CTAs
-// (256 classes each); rank 0 merges the CS partial states through distributed
+// (BN classes each); rank 0 merges the CS partial states through distributed
 // shared memory and writes only (prob, class) pairs: logits never reach HBM.
+//
+// The buffer is UNSORTED with a tracked worst entry: a candidate that beats it
+// replaces it (KMAX independent selects) and the worst is recomputed by a
+// depth-log2(KMAX) tree, so an insertion is short and ILP-rich instead of a
+// KMAX-long dependent compare-swap chain. The list is rank-sorted once at the
+// end. All 8 warps run the epilogue (warps w and w+4 share TMEM lanes and
+// split the 32-column chunks), halving the per-thread serial work.
 template <int KMAX>
 struct TopK {
   float v[KMAX];
   int i[KMAX];
-  __device__ __forceinline__ void init() {
-#pragma unroll
-    for (int j = 0; j < KMAX; ++j) { v[j] = -INFINITY; i[j] = 0x7fffffff; }
-  }
+  float wv;
+  int wi, wp;  // current worst entry (value, class, slot)
   __device__ __forceinline__ static bool better(float a, int ia, float b, int ib) {
     return a > b || (a == b && ia < ib);
   }
-  __device__ __forceinline__ void push(float x, int ix) {
-    if (!better(x, ix, v[KMAX - 1], i[KMAX - 1])) return;
+  __device__ __forceinline__ void init() {
 #pragma unroll
-    for (int j = 0; j < KMAX; ++j) {
-      if (better(x, ix, v[j], i[j])) {
-        float tv = v[j]; int ti = i[j];
-        v[j] = x; i[j] = ix;
-        x = tv; ix = ti;
+    for (int j = 0; j < KMAX; ++j) { v[j] = -INFINITY; i[j] = 0x7fffffff; }
+    wv = -INFINITY; wi = 0x7fffffff; wp = 0;
+  }
+  __device__ __forceinline__ void refresh_worst() {
+    float tv[KMAX];
+    int ti[KMAX], tp[KMAX];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) { tv[j] = v[j]; ti[j] = i[j]; tp[j] = j; }
+#pragma unroll
+    for (int st = 1; st < KMAX; st <<= 1) {
+#pragma unroll
+      for (int j = 0; j + st < KMAX; j += 2 * st) {
+        if (better(tv[j], ti[j], tv[j + st], ti[j + st])) { tv[j] = tv[j + st]; ti[j] = ti[j + st]; tp[j] = tp[j + st]; }
       }
     }
+    wv = tv[0]; wi = ti[0]; wp = tp[0];
+  }
+  __device__ __forceinline__ void push(float x, int ix) {
+    if (!better(x, ix, wv, wi)) return;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j)
+      if (j == wp) { v[j] = x; i[j] = ix; }
+    refresh_worst();
   }
 };
 
@@ -293,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::kStages;
   constexpr uint32_t kTmemCols = tmem_cols_for(BN);
+  constexpr int kState = 2 + 2 * KMAX;  // words per row: m, l, v[KMAX], i[KMAX]
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
@@ -302,11 +323,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
-  // merge scratch reuses the (drained) operand ring: [2 + 2*KMAX][128] words
-  float* st_m = reinterpret_cast<float*>(smem);
-  float* st_l = st_m + kBM;
-  float* st_v = st_l + kBM;
-  int* st_i = reinterpret_cast<int*>(st_v + KMAX * kBM);
+  // Epilogue scratch reuses the drained operand ring (word-interleaved by
+  // thread so every access is bank-conflict free):
+  float* stage = reinterpret_cast<float*>(smem);                    // [32][256] candidates
+  float* hx = stage + 32 * kThreads;                                 // [kState][128] half merge
+  float* st = hx + kState * kBM;                                     // [kState][128] cluster merge
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -347,71 +368,113 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     umma_commit(&tfull[0]);
   }
+  __syncwarp();
 
-  const int e = warp - 4;
-  const int rl = 32 * e + lane;  // local row
+  const int q = warp & 3;       // TMEM lane quarter == row block of this warp
+  const int half = warp >> 2;   // which interleaved 32-column chunks this warp takes
+  const int rl = 32 * q + lane; // local row
+  const int tid = threadIdx.x;
   TopK<KMAX> top;
+  top.init();
   float run_m = -INFINITY, run_l = 0.f;
-  if (warp >= 4) {
-    mbar_wait(&tfull[0], 0);
-    tc_fence_after();
-    top.init();
+  mbar_wait(&tfull[0], 0);
+  tc_fence_after();
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      float v[32];
-      tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * e) << 16) + c, v);
-      const int col0 = n0 + c;
-      if (col0 >= N) continue;
-      float cmax = -INFINITY;
+  for (int c = 32 * half; c < BN; c += 64) {
+    float v[32];
+    tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + c, v);
+    const int col0 = n0 + c;
+    if (col0 >= N) continue;
+    float cmax = -INFINITY;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int n = col0 + j;
-        float s = (n < N) ? (v[j] + __ldg(hp.bias + n)) * hp.inv_t : -INFINITY;
-        v[j] = s;
-        cmax = fmaxf(cmax, s);
-      }
-      const float nm = fmaxf(run_m, cmax);
-      float acc = 0.f;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) acc += __expf(v[j] - nm);
-      run_l = run_l * __expf(run_m - nm) + acc;
-      run_m = nm;
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (col0 + j < N) top.push(v[j], col0 + j);
+    for (int j = 0; j < 32; ++j) {
+      const int n = col0 + j;
+      const float s = (n < N) ? (v[j] + __ldg(hp.bias + n)) * hp.inv_t : -INFINITY;
+      v[j] = s;
+      cmax = fmaxf(cmax, s);
     }
-    tc_fence_before();
-  }
-  __syncthreads();  // every CTA: MMAs drained, operand ring free for scratch
-  if (warp >= 4) {
-    st_m[rl] = run_m;
-    st_l[rl] = run_l;
+    const float nm = fmaxf(run_m, cmax);
+    float acc = 0.f;
 #pragma unroll
-    for (int j = 0; j < KMAX; ++j) { st_v[j * kBM + rl] = top.v[j]; st_i[j * kBM + rl] = top.i[j]; }
+    for (int j = 0; j < 32; ++j) acc += __expf(v[j] - nm);
+    run_l = run_l * __expf(run_m - nm) + acc;
+    run_m = nm;
+    // Candidates vs. the current worst entry as a 32-bit mask (compact
+    // straight-line code); insertions run in ONE rolled loop over values staged
+    // in shared memory, so the insertion body exists once in the binary.
+    uint32_t mask = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      mask |= (TopK<KMAX>::better(v[j], col0 + j, top.wv, top.wi) ? 1u : 0u) << j;
+    if (mask) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) stage[j * kThreads + tid] = v[j];
+      while (mask) {
+        const int j = __ffs(mask) - 1;
+        mask &= mask - 1;
+        top.push(stage[j * kThreads + tid], col0 + j);
+      }
+    }
+  }
+  tc_fence_before();
+  // halves -> one state per row (half 1 hands over through shared memory)
+  if (half == 1) {
+    hx[0 * kBM + rl] = run_m;
+    hx[1 * kBM + rl] = run_l;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+      hx[(2 + j) * kBM + rl] = top.v[j];
+      hx[(2 + KMAX + j) * kBM + rl] = __int_as_float(top.i[j]);
+    }
+  }
+  __syncthreads();
+  if (half == 0) {
+    const float om = hx[0 * kBM + rl], ol = hx[1 * kBM + rl];
+    const float nm = fmaxf(run_m, om);
+    run_l = (run_l > 0.f ? run_l * __expf(run_m - nm) : 0.f) + (ol > 0.f ? ol * __expf(om - nm) : 0.f);
+    run_m = nm;
+#pragma unroll 1
+    for (int j = 0; j < KMAX; ++j)
+      top.push(hx[(2 + j) * kBM + rl], __float_as_int(hx[(2 + KMAX + j) * kBM + rl]));
+    st[0 * kBM + rl] = run_m;
+    st[1 * kBM + rl] = run_l;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+      st[(2 + j) * kBM + rl] = top.v[j];
+      st[(2 + KMAX + j) * kBM + rl] = __int_as_float(top.i[j]);
+    }
   }
   if (cs > 1) cluster_sync(); else __syncthreads();
-  if (rank == 0 && warp >= 4) {
+  if (rank == 0 && half == 0) {
     for (int r = 1; r < cs; ++r) {
-      const uint32_t bm = mapa(smem_u32(st_m + rl), r);
-      const uint32_t bl = mapa(smem_u32(st_l + rl), r);
-      const float om = ld_dsmem_f32(bm), ol = ld_dsmem_f32(bl);
-      const float nm = fmaxf(run_m, om);
-      run_l = run_l * __expf(run_m - nm) + ol * __expf(om - nm);
+      // batch the remote reads (independent loads in flight), then merge
+      float rv[kState];
+#pragma unroll
+      for (int w = 0; w < kState; ++w) rv[w] = ld_dsmem_f32(mapa(smem_u32(st + w * kBM + rl), r));
+      const float nm = fmaxf(run_m, rv[0]);
+      run_l = run_l * __expf(run_m - nm) + rv[1] * __expf(rv[0] - nm);
       run_m = nm;
-      for (int j = 0; j < hp.k; ++j) {
-        const float ov = ld_dsmem_f32(mapa(smem_u32(st_v + j * kBM + rl), r));
-        const int oi = ld_dsmem_s32(mapa(smem_u32(st_i + j * kBM + rl), r));
-        top.push(ov, oi);
-      }
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j) stage[j * kThreads + tid] = rv[2 + j];
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j) stage[(j + KMAX) * kThreads + tid] = rv[2 + KMAX + j];
+#pragma unroll 1
+      for (int j = 0; j < KMAX; ++j)
+        top.push(stage[j * kThreads + tid], __float_as_int(stage[(j + KMAX) * kThreads + tid]));
     }
     const int row = m0 + rl;
     if (row < M) {
       const float inv_l = 1.0f / run_l;
       float* ov = hp.vals + static_cast<size_t>(row) * hp.k;
       int* oi = hp.idx + static_cast<size_t>(row) * hp.k;
+      // rank sort: entry j goes to position #{entries better than j}
 #pragma unroll
-      for (int j = 0; j < KMAX; ++j)
-        if (j < hp.k) { ov[j] = __expf(top.v[j] - run_m) * inv_l; oi[j] = top.i[j]; }
+      for (int j = 0; j < KMAX; ++j) {
+        int r = 0;
+#pragma unroll
+        for (int m = 0; m < KMAX; ++m) r += TopK<KMAX>::better(top.v[m], top.i[m], top.v[j], top.i[j]) ? 1 : 0;
+        if (r < hp.k) { ov[r] = __expf(top.v[j] - run_m) * inv_l; oi[r] = top.i[j]; }
+      }
     }
   }
   if (cs > 1) cluster_sync(); else __syncthreads();

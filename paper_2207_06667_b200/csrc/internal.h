@@ -51,7 +51,7 @@ cudaError_t launch_sgd(float* p, __nv_bfloat16* p_bf16, const float* g, long lon
                        float scale, cudaStream_t stream);
 cudaError_t launch_gather_rows(const __nv_bfloat16* src, long long ld_src, const int64_t* idx,
                                __nv_bfloat16* dst, long long ld_dst, int B, int D,
-                               cudaStream_t stream);
+                               const int64_t* src_labels, int64_t* dst_labels, cudaStream_t stream);
 cudaError_t launch_colsum(const __nv_bfloat16* x, long long ld, int M, int N, float* partial,
                           float* out, float scale, cudaStream_t stream);
 cudaError_t launch_topk_hits(const float* logits, long long ld, const int64_t* labels, int B,

@@ -222,10 +222,12 @@ cudaError_t launch_sgd(float* p, __nv_bfloat16* p_bf16, const float* g, long lon
 // ------------------------------------------------------------------ gather
 __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, long long ld_src,
                                    const int64_t* __restrict__ idx, __nv_bfloat16* __restrict__ dst,
-                                   long long ld_dst, int B, int D) {
+                                   long long ld_dst, int B, int D, const int64_t* __restrict__ src_lab,
+                                   int64_t* __restrict__ dst_lab) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
   if (warp >= B) return;
   const int64_t r = idx[warp];
+  if (dst_lab && lane == 0) dst_lab[warp] = src_lab[r];
   const __nv_bfloat16* s = src + static_cast<size_t>(r) * ld_src;
   __nv_bfloat16* d = dst + static_cast<size_t>(warp) * ld_dst;
   const int v = D / 8;
@@ -235,10 +237,11 @@ __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, long l
 
 cudaError_t launch_gather_rows(const __nv_bfloat16* src, long long ld_src, const int64_t* idx,
                                __nv_bfloat16* dst, long long ld_dst, int B, int D,
-                               cudaStream_t stream) {
+                               const int64_t* src_labels, int64_t* dst_labels, cudaStream_t stream) {
   const int threads = 256;
   const int blocks = (B * 32 + threads - 1) / threads;
-  gather_rows_kernel<<<blocks, threads, 0, stream>>>(src, ld_src, idx, dst, ld_dst, B, D);
+  gather_rows_kernel<<<blocks, threads, 0, stream>>>(src, ld_src, idx, dst, ld_dst, B, D, src_labels,
+                                                     dst_labels);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,84 @@
+"""HBM-resident dataset and the device ShardSampler.
+
+The reference ships every batch's B x D inputs through JSON (INFER_REQUEST,
+edl/student_node.py:369-372), which caps B. Here the dataset is
+uploaded once as bf16 rows padded to a multiple of 16 and both the student and
+its teachers read batches by row index (the paper's own future-work item).
+
+DeviceShardSampler mirrors ShardSampler (edl/student_node.py:125-151): the
+same contiguous shard (edl/nnkit.py:391-399), the same per-epoch permutation
+(edl/nnkit.py:402-405) and the same equal batches-per-epoch across ranks, so
+batch_for(it) selects exactly the rows the reference would.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .formats import Dataset, epoch_order
+from .nnkit import Batch, pad
+
+
+class DeviceDataset:
+    def __init__(self, data: Dataset, device=None, chunk_rows: int = 65536):
+        self.id = data.id
+        self.size = data.size
+        self.dim = data.dim
+        self.classes = int(data.labels.max()) + 1
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.samples = torch.zeros(self.size, pad(self.dim), dtype=torch.bfloat16, device=self.device)
+        for lo in range(0, self.size, chunk_rows):
+            hi = min(lo + chunk_rows, self.size)
+            blk = torch.from_numpy(np.ascontiguousarray(data.samples[lo:hi], dtype=np.float32))
+            self.samples[lo:hi, :self.dim] = blk.to(self.device).to(torch.bfloat16)
+        self.labels = torch.from_numpy(np.ascontiguousarray(data.labels, dtype=np.int64)).to(self.device)
+
+
+class DeviceShardSampler:
+    """batch_for(iteration) -> Batch gathered on the device from the shard."""
+
+    def __init__(self, data: DeviceDataset, world_size: int, rank: int, batch_size: int, seed: int):
+        if world_size < 1 or not 0 <= rank < world_size:
+            raise ValueError(f"bad world_size={world_size} rank={rank}")
+        n = data.size
+        self.data = data
+        self.lo, self.hi = (n * rank) // world_size, (n * (rank + 1)) // world_size
+        self.batch_size = batch_size
+        self.seed = seed
+        self.rank = rank
+        self.batches_per_epoch = (n // world_size) // batch_size
+        if self.batches_per_epoch < 1:
+            raise ValueError("shard smaller than one batch")
+        self._orders: dict[int, torch.Tensor] = {}
+
+    def rows_for(self, iteration: int) -> torch.Tensor:
+        """Global dataset row indices (device int64 [B]) of batch `iteration`."""
+        epoch, i = divmod(iteration, self.batches_per_epoch)
+        order = self._orders.get(epoch)
+        if order is None:
+            host = epoch_order(self.seed, epoch, self.rank, self.hi - self.lo) + self.lo
+            order = torch.from_numpy(host.astype(np.int64)).to(self.data.device)
+            # keep a few epochs alive: in-flight teacher / student work may
+            # still read the previous epoch's permutation on other streams
+            if len(self._orders) >= 3:
+                self._orders.pop(min(self._orders))
+            self._orders[epoch] = order
+        return order[i * self.batch_size:(i + 1) * self.batch_size]
+
+    def batch_for(self, iteration: int, out: Batch | None = None, stream=None) -> Batch:
+        rows = self.rows_for(iteration)
+        return gather_batch(self.data, rows, out, stream)
+
+
+def gather_batch(data: DeviceDataset, rows: torch.Tensor, out: Batch | None = None, stream=None) -> Batch:
+    B = rows.shape[0]
+    if out is None:
+        out = Batch(torch.empty(B, data.samples.shape[1], dtype=torch.bfloat16, device=data.device),
+                    torch.empty(B, dtype=torch.int64, device=data.device), data.dim)
+    s = (stream or torch.cuda.current_stream()).cuda_stream
+    _lib.call("edl_gather_rows", data.samples.data_ptr(), data.samples.stride(0), rows.data_ptr(),
+              out.inputs.data_ptr(), out.inputs.stride(0), B, data.samples.shape[1],
+              data.labels.data_ptr(), out.hard_labels.data_ptr(), s)
+    return out

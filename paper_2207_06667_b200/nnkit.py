@@ -338,7 +338,7 @@ def tempered_softmax(logits: torch.Tensor, temperature: float, stream=None) -> t
 
 
 def teacher_soft_labels(model: Model, inputs, temperature: float, k: int, out: SoftLabels | None = None,
-                        stream=None) -> SoftLabels:
+                        stream=None, probe: tuple | None = None, ws: Workspace | None = None) -> SoftLabels:
     """Fused teacher inference: hidden tanh layers, then the head GEMM with the
     tempered-softmax + top-k epilogue (edl/teacher_node.py:54 + top-k)."""
     x = inputs.inputs if isinstance(inputs, Batch) else inputs
@@ -350,13 +350,21 @@ def teacher_soft_labels(model: Model, inputs, temperature: float, k: int, out: S
         raise ValueError(f"k must be in [1, {min(K, 32)}], got {k}")
     L = model.layout
     B = x.shape[0]
-    ws = workspace_for(model, B)
+    ws = ws or workspace_for(model, B)
     s = _stream(stream)
     h = x
     for l in range(L.layers - 1):
+        # probe = (layer, list): CUDA events bracketing that layer's GEMM (bench timing)
+        timed = probe is not None and probe[0] == l
+        if timed:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record(stream or torch.cuda.current_stream())
         _lib.call("edl_linear_fwd", h.data_ptr(), h.stride(0), model.w_bf16(l).data_ptr(), L.dims_p[l],
                   model.b(l).data_ptr(), ws.acts[l + 1].data_ptr(), ws.acts[l + 1].stride(0), B,
                   L.dims_p[l + 1], L.dims_p[l], _lib.EDL_ACT_TANH, s)
+        if timed:
+            ev[1].record(stream or torch.cuda.current_stream())
+            probe[1].append(ev)
         h = ws.acts[l + 1]
     if out is None:
         out = SoftLabels(torch.empty(B, k, dtype=torch.float32, device=x.device),
@@ -369,7 +377,8 @@ def teacher_soft_labels(model: Model, inputs, temperature: float, k: int, out: S
 
 
 def kd_loss(model: Model, batch: Batch, soft: SoftLabels | None, cfg: TrainConfig,
-            stream=None, ws: Workspace | None = None) -> tuple[DeviceLoss, Gradients]:
+            stream=None, ws: Workspace | None = None,
+            loss_slot: torch.Tensor | None = None) -> tuple[DeviceLoss, Gradients]:
     """Combined distillation loss and analytic gradients (edl/nnkit.py:254-309):
     forward GEMMs -> fused loss/dlogits kernel -> backward GEMMs."""
     if cfg.beta > 0:
@@ -392,13 +401,13 @@ def kd_loss(model: Model, batch: Batch, soft: SoftLabels | None, cfg: TrainConfi
     q_vals = soft.probs if (soft is not None and cfg.beta > 0) else None
     q_idx = soft.classes if (soft is not None and cfg.beta > 0) else None
     k = soft.k if q_vals is not None else 0
-    ws.status.zero_()
+    loss = ws.loss if loss_slot is None else loss_slot
     _lib.call("edl_kd_loss_fwd_bwd", ws.logits.data_ptr(), ws.logits.stride(0), batch.hard_labels.data_ptr(),
               _ptr(q_vals), _ptr(q_idx), B, model.num_classes, k, float(cfg.alpha), float(cfg.beta),
-              float(cfg.temperature), ws.row_loss.data_ptr(), ws.loss.data_ptr(), ws.ticket.data_ptr(),
+              float(cfg.temperature), ws.row_loss.data_ptr(), loss.data_ptr(), ws.ticket.data_ptr(),
               dz.data_ptr(), dz.stride(0), ws.status.data_ptr(), s)
     backward_into(model, x, ws, stream)
-    return DeviceLoss(ws.loss, ws.status), ws.grads
+    return DeviceLoss(loss, ws.status), ws.grads
 
 
 def backward_into(model: Model, x: torch.Tensor, ws: Workspace, stream=None) -> None:

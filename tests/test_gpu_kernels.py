@@ -179,9 +179,16 @@ def test_gather_rows(lib):
     src = _bf(_rand(100, 48, seed=15))
     idx = torch.tensor([5, 99, 0, 5, 42], dtype=torch.int64, device="cuda")
     dst = torch.empty(5, 48, dtype=torch.bfloat16, device="cuda")
-    lib.call("edl_gather_rows", src.data_ptr(), 48, idx.data_ptr(), dst.data_ptr(), 48, 5, 48, _s())
+    lab = torch.arange(100, dtype=torch.int64, device="cuda") * 3
+    dlab = torch.empty(5, dtype=torch.int64, device="cuda")
+    lib.call("edl_gather_rows", src.data_ptr(), 48, idx.data_ptr(), dst.data_ptr(), 48, 5, 48, None, None, _s())
     torch.cuda.synchronize()
     assert torch.equal(dst, src[idx])
+    dst.zero_()
+    lib.call("edl_gather_rows", src.data_ptr(), 48, idx.data_ptr(), dst.data_ptr(), 48, 5, 48, lab.data_ptr(),
+             dlab.data_ptr(), _s())
+    torch.cuda.synchronize()
+    assert torch.equal(dst, src[idx]) and torch.equal(dlab, lab[idx])
 
 
 def test_topk_hits_tie_rule(lib):
