@@ -31,6 +31,8 @@ _SIGNATURES = {
                             c_int, c_int, c_int, c_void_p],
     "edl_linear_bwd_weight": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_ll, c_void_p,
                               c_void_p, c_int, c_int, c_int, c_float, c_void_p],
+    "edl_linear_bwd_weight_grouped": [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                      c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_float, c_void_p],
     "edl_colsum_workspace_floats": [c_int, c_int],
     "edl_teacher_head_softmax_topk": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_int, c_int,
                                       c_int, c_float, c_int, c_void_p, c_void_p, c_void_p],
@@ -104,3 +106,18 @@ def call(name: str, *args) -> None:
     global launch_count
     check(getattr(load(), name)(*args), name)
     launch_count += _LAUNCHES.get(name, 1)
+
+
+def bwd_weight_grouped(dys, xs, dws, dbs, workspace, Ms, Ns, Ks, scale, stream) -> None:
+    """edl_linear_bwd_weight_grouped with Python lists of tensors / sizes."""
+    global launch_count
+    n = len(dys)
+    P = c_void_p * n
+    L = c_ll * n
+    I = c_int * n
+    args = (n, P(*[t.data_ptr() for t in dys]), L(*[t.stride(0) for t in dys]),
+            P(*[t.data_ptr() for t in xs]), L(*[t.stride(0) for t in xs]),
+            P(*[t.data_ptr() for t in dws]), L(*Ks), P(*[t.data_ptr() for t in dbs]),
+            workspace.data_ptr(), I(*Ms), I(*Ns), I(*Ks), scale, stream)
+    check(load().edl_linear_bwd_weight_grouped(*args), "edl_linear_bwd_weight_grouped")
+    launch_count += 1 + 2 * n

@@ -189,6 +189,45 @@ int edl_linear_bwd_weight(const void* dY, long long lddy, const void* X, long lo
   return 0;
 }
 
+int edl_linear_bwd_weight_grouped(int count, const void* const* dY, const long long* lddy,
+                                  const void* const* X, const long long* ldx, float* const* dW,
+                                  const long long* lddw, float* const* db, float* workspace,
+                                  const int* M, const int* N, const int* K, float scale, void* stream) {
+  if (count < 1 || count > kMaxGroup)
+    return fail(EDL_ERR_SHAPE, "linear_bwd_weight_grouped: count=%d (1..%d)", count, kMaxGroup);
+  GroupMaps maps;
+  GroupArgs ga;
+  std::memset(&ga, 0, sizeof(ga));
+  ga.count = count;
+  const int bn = grouped_tile_bn();
+  int tiles = 0;
+  for (int p = 0; p < count; ++p) {
+    if (M[p] < 1 || N[p] < 1 || K[p] < 1 || lddy[p] < N[p] || ldx[p] < K[p] || lddw[p] < K[p])
+      return fail(EDL_ERR_SHAPE, "linear_bwd_weight_grouped[%d]: bad shape M=%d N=%d K=%d", p, M[p], N[p], K[p]);
+    int rc;
+    // same operand views as edl_linear_bwd_weight: GEMM M=N[p], N=K[p], K=M[p]
+    if ((rc = tensor_map(dY[p], M[p], N[p], lddy[p], 64, 64, &maps.a[p]))) return rc;
+    if ((rc = tensor_map(X[p], M[p], K[p], ldx[p], 64, 64, &maps.b[p]))) return rc;
+    ga.M[p] = N[p];
+    ga.N[p] = K[p];
+    ga.K[p] = M[p];
+    ga.ep[p] = EpiArgs{dW[p], lddw[p], nullptr, nullptr, 0, scale};
+    ga.tile_start[p] = tiles;
+    tiles += ((N[p] + 127) / 128) * ((K[p] + bn - 1) / bn);
+  }
+  ga.tile_start[count] = tiles;
+  cudaError_t e = launch_gemm_grouped_bwd_weight(maps, ga, num_sms(), as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "linear_bwd_weight_grouped");
+  for (int p = 0; p < count; ++p) {
+    if (!db || !db[p]) continue;
+    if (!workspace) return fail(EDL_ERR_SHAPE, "linear_bwd_weight_grouped: db needs a workspace");
+    e = launch_colsum(reinterpret_cast<const __nv_bfloat16*>(dY[p]), lddy[p], M[p], N[p], workspace, db[p],
+                      scale, as_stream(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "colsum");
+  }
+  return 0;
+}
+
 long long edl_colsum_workspace_floats(int M, int N) {
   return static_cast<long long>((M + 127) / 128) * N;
 }

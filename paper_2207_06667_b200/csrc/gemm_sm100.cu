@@ -254,54 +254,204 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------------------------------ grouped GEMM
+// Several independent problems in ONE persistent launch (the student's dW_l
+// for every layer: each alone has 32-192 output tiles, too few for 148 SMs;
+// together they fill ~2 waves). Tile t maps to (problem, m-block, n-block)
+// through the prefix sums in GroupArgs; the pipelines are the same as above.
+template <int BN, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_grouped_kernel(const __grid_constant__ GroupMaps maps, GroupArgs ga) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int S = Cfg::kStages;
+  constexpr uint32_t kTmemCols = tmem_cols_for(2 * BN);
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * Cfg::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kBBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (warp == 0 && lane == 0) {
+    for (int p = 0; p < ga.count; ++p) { prefetch_tmap(&maps.a[p]); prefetch_tmap(&maps.b[p]); }
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int tiles = ga.tile_start[ga.count];
+
+  // tile -> (problem, m0, n0)
+  auto locate = [&](int t, int& p, int& m0, int& n0) {
+    p = 0;
+    while (p + 1 < ga.count && t >= ga.tile_start[p + 1]) ++p;
+    const int local = t - ga.tile_start[p];
+    const int num_m = (ga.M[p] + kBM - 1) / kBM;
+    m0 = (local % num_m) * kBM;
+    n0 = (local / num_m) * BN;
+  };
+
+  if (warp == 0 && lane == 0) {
+    uint32_t g = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      int p, m0, n0;
+      locate(t, p, m0, n0);
+      const int nk = (ga.K[p] + kBK - 1) / kBK;
+      for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int s = g % S;
+        mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
+        load_kblock<BN, A_MN, B_MN>(&maps.a[p], &maps.b[p], sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes,
+                                    &full[s], m0, n0, kb * kBK);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    uint32_t g = 0, i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      int p, m0, n0;
+      locate(t, p, m0, n0);
+      const int nk = (ga.K[p] + kBK - 1) / kBK;
+      const uint32_t as = i & 1;
+      mbar_wait(&tempty[as], ((i >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + as * BN;
+      for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int s = g % S;
+        mbar_wait(&full[s], (g / S) & 1);
+        tc_fence_after();
+        mma_kblock<BN, A_MN, B_MN>(d, smem_u32(sA + s * Cfg::kABytes), smem_u32(sB + s * Cfg::kBBytes), kb == 0);
+        umma_commit(&empty[s]);
+      }
+      umma_commit(&tfull[as]);
+    }
+  } else if (warp >= 4) {
+    const int e = warp - 4;
+    uint32_t i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      int p, m0, n0;
+      locate(t, p, m0, n0);
+      const uint32_t as = i & 1;
+      mbar_wait(&tfull[as], (i >> 1) & 1);
+      tc_fence_after();
+      const int row = m0 + 32 * e + lane;
+      const int M = ga.M[p], N = ga.N[p];
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN + c, v);
+        if (n0 + c < N) epilogue_store<EPI>(ga.ep[p], row, M, n0 + c, N, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[as]);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
 // ------------------------------------------------------------------ teacher head
 // Logits z = H W^T + b for a 128-row block, scaled s = z / T, and per row: the
 // running max / rescaled sum of exp(s) (online softmax) plus a register top-k
-// buffer ordered by (value desc, class index asc) — the tie rule of
+// list kept SORTED by (value desc, class index asc) — the tie rule of
 // edl/nnkit.py:333. The class dimension is split across a cluster of CS CTAs
 // (BN classes each); rank 0 merges the CS partial states through distributed
 // shared memory and writes only (prob, class) pairs: logits never reach HBM.
 //
-// The buffer is UNSORTED with a tracked worst entry: a candidate that beats it
-// replaces it (KMAX independent selects) and the worst is recomputed by a
-// depth-log2(KMAX) tree, so an insertion is short and ILP-rich instead of a
-// KMAX-long dependent compare-swap chain. The list is rank-sorted once at the
-// end. All 8 warps run the epilogue (warps w and w+4 share TMEM lanes and
-// split the 32-column chunks), halving the per-thread serial work.
-template <int KMAX>
-struct TopK {
-  float v[KMAX];
-  int i[KMAX];
-  float wv;
-  int wi, wp;  // current worst entry (value, class, slot)
+// Selection is built from data-independent sorting networks (no divergence,
+// all-static register indexing, high ILP): the first 32-column chunk is
+// bitonic-sorted and its best KMAX kept; later chunks only insert the rare
+// columns that beat the current k-th entry; partial lists (the two warp halves,
+// then the cluster ranks) are combined with a bitonic merge-split + clean.
+struct Key {
   __device__ __forceinline__ static bool better(float a, int ia, float b, int ib) {
     return a > b || (a == b && ia < ib);
   }
+};
+
+// compare-exchange so that slot j holds the better entry
+__device__ __forceinline__ void cex(float& va, int& ia, float& vb, int& ib) {
+  if (Key::better(vb, ib, va, ia)) {
+    const float tv = va; va = vb; vb = tv;
+    const int ti = ia; ia = ib; ib = ti;
+  }
+}
+
+// bitonic sort of N entries, descending by Key
+template <int N>
+__device__ __forceinline__ void bitonic_sort(float (&v)[N], int (&ix)[N]) {
+#pragma unroll
+  for (int size = 2; size <= N; size <<= 1) {
+#pragma unroll
+    for (int stride = size / 2; stride > 0; stride >>= 1) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        const int p = j ^ stride;
+        if (p > j) {
+          if ((j & size) == 0) cex(v[j], ix[j], v[p], ix[p]);
+          else cex(v[p], ix[p], v[j], ix[j]);
+        }
+      }
+    }
+  }
+}
+
+// sort a bitonic sequence of N entries descending (the "clean" half of a merge)
+template <int N>
+__device__ __forceinline__ void bitonic_clean(float (&v)[N], int (&ix)[N]) {
+#pragma unroll
+  for (int stride = N / 2; stride > 0; stride >>= 1) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      const int p = j ^ stride;
+      if (p > j) cex(v[j], ix[j], v[p], ix[p]);
+    }
+  }
+}
+
+template <int KMAX>
+struct TopK {
+  float v[KMAX];  // sorted: v[0] best
+  int i[KMAX];
   __device__ __forceinline__ void init() {
 #pragma unroll
     for (int j = 0; j < KMAX; ++j) { v[j] = -INFINITY; i[j] = 0x7fffffff; }
-    wv = -INFINITY; wi = 0x7fffffff; wp = 0;
   }
-  __device__ __forceinline__ void refresh_worst() {
-    float tv[KMAX];
-    int ti[KMAX], tp[KMAX];
+  // keep the best KMAX of (this) U (o), both sorted
+  __device__ __forceinline__ void merge(const float (&ov)[KMAX], const int (&oi)[KMAX]) {
 #pragma unroll
-    for (int j = 0; j < KMAX; ++j) { tv[j] = v[j]; ti[j] = i[j]; tp[j] = j; }
+    for (int j = 0; j < KMAX; ++j) {
+      const float bv = ov[KMAX - 1 - j];
+      const int bi = oi[KMAX - 1 - j];
+      if (Key::better(bv, bi, v[j], i[j])) { v[j] = bv; i[j] = bi; }
+    }
+    bitonic_clean<KMAX>(v, i);
+  }
+  // insert one candidate that beats the current last entry
+  __device__ __forceinline__ void insert(float x, int ix) {
+    bool b[KMAX];
 #pragma unroll
-    for (int st = 1; st < KMAX; st <<= 1) {
+    for (int j = 0; j < KMAX; ++j) b[j] = Key::better(v[j], i[j], x, ix);
 #pragma unroll
-      for (int j = 0; j + st < KMAX; j += 2 * st) {
-        if (better(tv[j], ti[j], tv[j + st], ti[j + st])) { tv[j] = tv[j + st]; ti[j] = ti[j + st]; tp[j] = tp[j + st]; }
+    for (int j = KMAX - 1; j > 0; --j) {
+      if (!b[j]) {
+        v[j] = b[j - 1] ? x : v[j - 1];
+        i[j] = b[j - 1] ? ix : i[j - 1];
       }
     }
-    wv = tv[0]; wi = ti[0]; wp = tp[0];
-  }
-  __device__ __forceinline__ void push(float x, int ix) {
-    if (!better(x, ix, wv, wi)) return;
-#pragma unroll
-    for (int j = 0; j < KMAX; ++j)
-      if (j == wp) { v[j] = x; i[j] = ix; }
-    refresh_worst();
+    if (!b[0]) { v[0] = x; i[0] = ix; }
   }
 };
 
@@ -324,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + S;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
   // Epilogue scratch reuses the drained operand ring (word-interleaved by
-  // thread so every access is bank-conflict free):
+  // thread / row so every access is bank-conflict free):
   float* stage = reinterpret_cast<float*>(smem);                    // [32][256] candidates
   float* hx = stage + 32 * kThreads;                                 // [kState][128] half merge
   float* st = hx + kState * kBM;                                     // [kState][128] cluster merge
@@ -379,6 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   float run_m = -INFINITY, run_l = 0.f;
   mbar_wait(&tfull[0], 0);
   tc_fence_after();
+  bool first = true;
 #pragma unroll 1
   for (int c = 32 * half; c < BN; c += 64) {
     float v[32];
@@ -399,20 +550,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < 32; ++j) acc += __expf(v[j] - nm);
     run_l = run_l * __expf(run_m - nm) + acc;
     run_m = nm;
-    // Candidates vs. the current worst entry as a 32-bit mask (compact
-    // straight-line code); insertions run in ONE rolled loop over values staged
-    // in shared memory, so the insertion body exists once in the binary.
+    if (first) {
+      // the first chunk seeds the list: bitonic-sort all 32, keep the best KMAX
+      first = false;
+      int ix[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) ix[j] = (col0 + j < N) ? col0 + j : 0x7fffffff;
+      bitonic_sort<32>(v, ix);
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j) { top.v[j] = v[j]; top.i[j] = ix[j]; }
+      continue;
+    }
+    // later chunks: only columns beating the current k-th entry (rare), each
+    // inserted by a branch-free shift; the values are staged in smem so the
+    // rolled loop can address them
     uint32_t mask = 0;
 #pragma unroll
     for (int j = 0; j < 32; ++j)
-      mask |= (TopK<KMAX>::better(v[j], col0 + j, top.wv, top.wi) ? 1u : 0u) << j;
+      mask |= (Key::better(v[j], col0 + j, top.v[KMAX - 1], top.i[KMAX - 1]) ? 1u : 0u) << j;
     if (mask) {
 #pragma unroll
       for (int j = 0; j < 32; ++j) stage[j * kThreads + tid] = v[j];
       while (mask) {
         const int j = __ffs(mask) - 1;
         mask &= mask - 1;
-        top.push(stage[j * kThreads + tid], col0 + j);
+        const float x = stage[j * kThreads + tid];
+        if (Key::better(x, col0 + j, top.v[KMAX - 1], top.i[KMAX - 1])) top.insert(x, col0 + j);
       }
     }
   }
@@ -433,9 +596,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float nm = fmaxf(run_m, om);
     run_l = (run_l > 0.f ? run_l * __expf(run_m - nm) : 0.f) + (ol > 0.f ? ol * __expf(om - nm) : 0.f);
     run_m = nm;
-#pragma unroll 1
-    for (int j = 0; j < KMAX; ++j)
-      top.push(hx[(2 + j) * kBM + rl], __float_as_int(hx[(2 + KMAX + j) * kBM + rl]));
+    float ov[KMAX];
+    int oi[KMAX];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+      ov[j] = hx[(2 + j) * kBM + rl];
+      oi[j] = __float_as_int(hx[(2 + KMAX + j) * kBM + rl]);
+    }
+    top.merge(ov, oi);
     st[0 * kBM + rl] = run_m;
     st[1 * kBM + rl] = run_l;
 #pragma unroll
@@ -446,35 +614,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (cs > 1) cluster_sync(); else __syncthreads();
   if (rank == 0 && half == 0) {
+#pragma unroll 1
     for (int r = 1; r < cs; ++r) {
-      // batch the remote reads (independent loads in flight), then merge
+      // all remote words in flight at once, then a register bitonic merge
       float rv[kState];
 #pragma unroll
       for (int w = 0; w < kState; ++w) rv[w] = ld_dsmem_f32(mapa(smem_u32(st + w * kBM + rl), r));
       const float nm = fmaxf(run_m, rv[0]);
       run_l = run_l * __expf(run_m - nm) + rv[1] * __expf(rv[0] - nm);
       run_m = nm;
+      float ov[KMAX];
+      int oi[KMAX];
 #pragma unroll
-      for (int j = 0; j < KMAX; ++j) stage[j * kThreads + tid] = rv[2 + j];
-#pragma unroll
-      for (int j = 0; j < KMAX; ++j) stage[(j + KMAX) * kThreads + tid] = rv[2 + KMAX + j];
-#pragma unroll 1
-      for (int j = 0; j < KMAX; ++j)
-        top.push(stage[j * kThreads + tid], __float_as_int(stage[(j + KMAX) * kThreads + tid]));
+      for (int j = 0; j < KMAX; ++j) { ov[j] = rv[2 + j]; oi[j] = __float_as_int(rv[2 + KMAX + j]); }
+      top.merge(ov, oi);
     }
     const int row = m0 + rl;
     if (row < M) {
       const float inv_l = 1.0f / run_l;
       float* ov = hp.vals + static_cast<size_t>(row) * hp.k;
       int* oi = hp.idx + static_cast<size_t>(row) * hp.k;
-      // rank sort: entry j goes to position #{entries better than j}
 #pragma unroll
-      for (int j = 0; j < KMAX; ++j) {
-        int r = 0;
-#pragma unroll
-        for (int m = 0; m < KMAX; ++m) r += TopK<KMAX>::better(top.v[m], top.i[m], top.v[j], top.i[j]) ? 1 : 0;
-        if (r < hp.k) { ov[r] = __expf(top.v[j] - run_m) * inv_l; oi[r] = top.i[j]; }
-      }
+      for (int j = 0; j < KMAX; ++j)
+        if (j < hp.k) { ov[j] = __expf(top.v[j] - run_m) * inv_l; oi[j] = top.i[j]; }
     }
   }
   if (cs > 1) cluster_sync(); else __syncthreads();
@@ -529,6 +691,25 @@ cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUte
   }
   return cudaErrorInvalidValue;
 }
+
+cudaError_t launch_gemm_grouped_bwd_weight(const GroupMaps& maps, const GroupArgs& ga, int num_sms,
+                                           cudaStream_t stream) {
+  constexpr int BN = 256;
+  auto kern = gemm_grouped_kernel<BN, true, true, EPI_F32>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         GemmCfg<BN>::kSmem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = ga.tile_start[ga.count];
+  const int grid = tiles < num_sms ? tiles : num_sms;
+  kern<<<grid, kThreads, GemmCfg<BN>::kSmem, stream>>>(maps, ga);
+  return cudaGetLastError();
+}
+
+int grouped_tile_bn() { return 256; }
 
 template <int BN, int KMAX>
 static cudaError_t launch_head_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N,

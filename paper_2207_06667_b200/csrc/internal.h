@@ -33,6 +33,21 @@ struct HeadArgs {
 
 enum class GemmKind { FwdTanh, FwdLinear, BwdData, BwdWeight };
 
+constexpr int kMaxGroup = 4;
+struct GroupMaps {
+  CUtensorMap a[kMaxGroup];
+  CUtensorMap b[kMaxGroup];
+};
+struct GroupArgs {
+  int count;
+  int M[kMaxGroup], N[kMaxGroup], K[kMaxGroup];
+  int tile_start[kMaxGroup + 1];
+  EpiArgs ep[kMaxGroup];
+};
+cudaError_t launch_gemm_grouped_bwd_weight(const GroupMaps& maps, const GroupArgs& ga, int num_sms,
+                                           cudaStream_t stream);
+int grouped_tile_bn();
+
 cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
                         int M, int N, int K, const EpiArgs& ep, int num_sms,
                         cudaStream_t stream);

@@ -32,10 +32,14 @@ __device__ __forceinline__ void set_status(int* status, int code) {
 // loss_row = alpha * (lse(z) - z_y) + beta * T^2 * (-sum_j q_j (z_{i_j}/T - lse(z/T)))
 // dz       = alpha/B (softmax(z) - onehot(y)) + beta*T/B (softmax(z/T) - q)
 // q is the teacher's top-k (prob, class) list renormalised to sum 1 (k = K is
-// the dense reference case). The row lives in shared memory (fp32) between the
-// passes, so HBM sees one read of z and one bf16 write of dz.
+// the dense reference case). One warp per row: the row is loaded into
+// registers up front (KPL independent loads per lane -> full memory-level
+// parallelism), both log-sum-exps come from registers, and only dz is staged
+// in shared memory (fp32) so the k sparse corrections can land before the
+// coalesced bf16 store. HBM sees one read of z and one write of dz.
 constexpr int kKdWarps = 8;
 
+template <int KPL>
 __global__ void __launch_bounds__(kKdWarps * 32)
     kd_loss_kernel(const float* __restrict__ z, long long ld_z, const int64_t* __restrict__ labels,
                    const float* __restrict__ qv, const int* __restrict__ qi, int B, int K,
@@ -44,9 +48,7 @@ __global__ void __launch_bounds__(kKdWarps * 32)
                    __nv_bfloat16* __restrict__ dz, long long ld_dz, int* __restrict__ status) {
   extern __shared__ float sm[];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int kp = (Kw + 3) & ~3;
-  float* zs = sm + warp * 2 * kp;
-  float* ds = zs + kp;
+  float* ds = sm + warp * (32 * KPL);
   const float inv_t = 1.0f / T;
   const float ch = alpha / static_cast<float>(B);
   const float cs = beta * T / static_cast<float>(B);
@@ -54,16 +56,27 @@ __global__ void __launch_bounds__(kKdWarps * 32)
 
   for (int row = blockIdx.x * kKdWarps + warp; row < B; row += gridDim.x * kKdWarps) {
     const float* zr = z + static_cast<size_t>(row) * ld_z;
+    float v[KPL];
     float m = -INFINITY;
-    for (int c = lane; c < K; c += 32) {
-      const float v = __ldg(zr + c);
-      zs[c] = v;
-      m = fmaxf(m, v);
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      const int c = lane + 32 * i;
+      v[i] = c < K ? __ldg(zr + c) : -INFINITY;
     }
+    const int64_t y = labels[row];
+    float qsum = 0.f, qv_l = 0.f;
+    int qi_l = -1;
+    if (use_soft && lane < k) {
+      qv_l = __ldg(qv + static_cast<size_t>(row) * k + lane);
+      qi_l = __ldg(qi + static_cast<size_t>(row) * k + lane);
+    }
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) m = fmaxf(m, v[i]);
     m = warp_max(m);
     float s1 = 0.f, st = 0.f;
-    for (int c = lane; c < K; c += 32) {
-      const float d = zs[c] - m;
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      const float d = v[i] - m;
       s1 += __expf(d);
       st += __expf(d * inv_t);
     }
@@ -71,19 +84,19 @@ __global__ void __launch_bounds__(kKdWarps * 32)
     st = warp_sum(st);
     const float lse1 = m + __logf(s1);
     const float lset = m * inv_t + __logf(st);
-    const int64_t y = labels[row];
     const bool y_ok = (y >= 0 && y < K);
     if (!y_ok && lane == 0) set_status(status, -1);
-    float qsum = 0.f;
     if (use_soft) {
-      for (int j = lane; j < k; j += 32) qsum += __ldg(qv + static_cast<size_t>(row) * k + j);
-      qsum = warp_sum(qsum);
+      float part = qv_l;
+      for (int j = lane + 32; j < k; j += 32) part += __ldg(qv + static_cast<size_t>(row) * k + j);
+      qsum = warp_sum(part);
     }
-    for (int c = lane; c < K; c += 32) {
-      const float v = zs[c];
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      const int c = lane + 32 * i;
       float d = 0.f;
-      if (alpha > 0.f) d += ch * (__expf(v - lse1) - (c == y ? 1.f : 0.f));
-      if (use_soft) d += cs * __expf(v * inv_t - lset);
+      if (alpha > 0.f) d += ch * (__expf(v[i] - lse1) - (c == y ? 1.f : 0.f));
+      if (use_soft) d += cs * __expf(v[i] * inv_t - lset);
       ds[c] = d;
     }
     __syncwarp();
@@ -91,20 +104,24 @@ __global__ void __launch_bounds__(kKdWarps * 32)
     if (use_soft) {
       const float inv_q = 1.0f / qsum;
       for (int j = lane; j < k; j += 32) {
-        const float q = __ldg(qv + static_cast<size_t>(row) * k + j) * inv_q;
-        const int id = __ldg(qi + static_cast<size_t>(row) * k + j);
+        const float q = (j == lane ? qv_l : __ldg(qv + static_cast<size_t>(row) * k + j)) * inv_q;
+        const int id = (j == lane ? qi_l : __ldg(qi + static_cast<size_t>(row) * k + j));
         if (id < 0 || id >= K) { set_status(status, -1); continue; }
         ds[id] -= cs * q;
-        lsoft += q * (zs[id] * inv_t - lset);
+        lsoft += q * (__ldg(zr + id) * inv_t - lset);
       }
       lsoft = -warp_sum(lsoft);
     }
     __syncwarp();
     __nv_bfloat16* dr = dz + static_cast<size_t>(row) * ld_dz;
-    for (int c = lane; c < Kw; c += 32) dr[c] = __float2bfloat16_rn(c < K ? ds[c] : 0.f);
+    for (int c = 2 * lane; c < Kw; c += 64) {
+      const float a = c < K ? ds[c] : 0.f;
+      const float b = c + 1 < K ? ds[c + 1] : 0.f;
+      *reinterpret_cast<__nv_bfloat162*>(dr + c) = __floats2bfloat162_rn(a, b);
+    }
     if (lane == 0) {
       float l = 0.f;
-      if (alpha > 0.f) l += alpha * (y_ok ? (lse1 - zs[y]) : 0.f);
+      if (alpha > 0.f) l += alpha * (y_ok ? (lse1 - __ldg(zr + y)) : 0.f);
       if (use_soft) l += beta * T * T * lsoft;
       row_loss[row] = l;
     }
@@ -136,27 +153,49 @@ __global__ void __launch_bounds__(kKdWarps * 32)
   }
 }
 
+template <int KPL>
+static cudaError_t launch_kd_t(const float* logits, long long ld_z, const int64_t* labels,
+                               const float* q_vals, const int* q_idx, int B, int K, int Kw, int k,
+                               float alpha, float beta, float T, float* row_loss, float* loss_out,
+                               unsigned* ticket, __nv_bfloat16* dlogits, long long ld_dz, int* status,
+                               cudaStream_t stream) {
+  const size_t smem = static_cast<size_t>(kKdWarps) * 32 * KPL * sizeof(float);
+  static bool set = false;
+  if (!set && smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kd_loss_kernel<KPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  set = true;
+  int blocks = (B + kKdWarps - 1) / kKdWarps;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  kd_loss_kernel<KPL><<<blocks, kKdWarps * 32, smem, stream>>>(logits, ld_z, labels, q_vals, q_idx, B, K, Kw,
+                                                              k, alpha, beta, T, row_loss, loss_out, ticket,
+                                                              dlogits, ld_dz, status);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_kd_loss(const float* logits, long long ld_z, const int64_t* labels,
                            const float* q_vals, const int* q_idx, int B, int K, int k,
                            float alpha, float beta, float T, float* row_loss, float* loss_out,
                            unsigned* ticket, __nv_bfloat16* dlogits, long long ld_dz,
                            int* status, cudaStream_t stream) {
-  const int Kw = static_cast<int>(ld_dz < (((K + 15) / 16) * 16) ? ld_dz : ((K + 15) / 16) * 16);
-  const int kp = (Kw + 3) & ~3;
-  const size_t smem = static_cast<size_t>(kKdWarps) * 2 * kp * sizeof(float);
-  static size_t smem_set = 48 * 1024;
-  if (smem > smem_set) {
-    cudaError_t e = cudaFuncSetAttribute(kd_loss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    smem_set = smem;
-  }
-  int blocks = (B + kKdWarps - 1) / kKdWarps;
-  if (blocks > 148 * 8) blocks = 148 * 8;
-  kd_loss_kernel<<<blocks, kKdWarps * 32, smem, stream>>>(logits, ld_z, labels, q_vals, q_idx, B, K,
-                                                         Kw, k, alpha, beta, T, row_loss, loss_out,
-                                                         ticket, dlogits, ld_dz, status);
-  return cudaGetLastError();
+  // columns written: the padded width (multiple of 16), capped by the row pitch
+  const int Kp = ((K + 15) / 16) * 16;
+  const int Kw = static_cast<int>(ld_dz < Kp ? ld_dz : Kp);
+  const int need = (Kw + 31) / 32;  // columns per lane
+#define EDL_KD(KPL)                                                                                  \
+  return launch_kd_t<KPL>(logits, ld_z, labels, q_vals, q_idx, B, K, Kw, k, alpha, beta, T, row_loss, \
+                          loss_out, ticket, dlogits, ld_dz, status, stream)
+  if (need <= 1) EDL_KD(1);
+  if (need <= 2) EDL_KD(2);
+  if (need <= 4) EDL_KD(4);
+  if (need <= 8) EDL_KD(8);
+  if (need <= 16) EDL_KD(16);
+  if (need <= 32) EDL_KD(32);
+  if (need <= 64) EDL_KD(64);
+#undef EDL_KD
+  return cudaErrorInvalidValue;  // > 2048 classes
 }
 
 // ------------------------------------------------------------------ tempered softmax

@@ -417,18 +417,23 @@ def backward_into(model: Model, x: torch.Tensor, ws: Workspace, stream=None) -> 
     B = x.shape[0]
     s = _stream(stream)
     g = ws.grads.flat
-    for l in range(L.layers - 1, -1, -1):
+    # the delta chain first (each step needs the previous one) ...
+    for l in range(L.layers - 1, 0, -1):
         d = ws.deltas[l + 1]
-        a = x if l == 0 else ws.acts[l]
-        dw = g[L.w_off[l]:L.w_off[l] + L.dims_p[l + 1] * L.dims_p[l]]
-        db = g[L.b_off[l]:L.b_off[l] + L.dims_p[l + 1]]
-        _lib.call("edl_linear_bwd_weight", d.data_ptr(), d.stride(0), a.data_ptr(), a.stride(0),
-                  dw.data_ptr(), L.dims_p[l], db.data_ptr(), ws.colsum.data_ptr(), B, L.dims_p[l + 1],
-                  L.dims_p[l], 1.0, s)
-        if l > 0:
-            _lib.call("edl_linear_bwd_data", d.data_ptr(), d.stride(0), model.w_bf16(l).data_ptr(),
-                      L.dims_p[l], a.data_ptr(), a.stride(0), ws.deltas[l].data_ptr(),
-                      ws.deltas[l].stride(0), B, L.dims_p[l + 1], L.dims_p[l], s)
+        a = ws.acts[l]
+        _lib.call("edl_linear_bwd_data", d.data_ptr(), d.stride(0), model.w_bf16(l).data_ptr(),
+                  L.dims_p[l], a.data_ptr(), a.stride(0), ws.deltas[l].data_ptr(),
+                  ws.deltas[l].stride(0), B, L.dims_p[l + 1], L.dims_p[l], s)
+    # ... then every layer's dW / db: independent, so one grouped launch
+    # (chunks of 4 layers for deeper nets)
+    layers = list(range(L.layers - 1, -1, -1))
+    for c in range(0, len(layers), 4):
+        part = layers[c:c + 4]
+        _lib.bwd_weight_grouped(
+            [ws.deltas[l + 1] for l in part], [x if l == 0 else ws.acts[l] for l in part],
+            [g[L.w_off[l]:L.w_off[l] + L.dims_p[l + 1] * L.dims_p[l]] for l in part],
+            [g[L.b_off[l]:L.b_off[l] + L.dims_p[l + 1]] for l in part], ws.colsum,
+            [B] * len(part), [L.dims_p[l + 1] for l in part], [L.dims_p[l] for l in part], 1.0, s)
 
 
 def sgd_step(model: Model, grads: Gradients, eta: float, world_size: int = 1, stream=None) -> Model:

@@ -198,3 +198,21 @@ def test_topk_hits_tie_rule(lib):
     lib.call("edl_topk_hits", z.data_ptr(), 16, y.data_ptr(), 4, 10, 1, hits.data_ptr(), _s())
     torch.cuda.synchronize()
     assert hits.item() == 1   # constant logits: only class 0 ranks first
+
+
+def test_linear_bwd_weight_grouped_matches_reference(lib):
+    # three student-like layers of different shapes in one launch
+    B = 300
+    shapes = [(208, 112), (64, 208), (16, 64)]    # (N_out, K_in), padded
+    dys = [_padded(_rand(B, n, seed=20 + i), B, n) for i, (n, k) in enumerate(shapes)]
+    xs = [_padded(_rand(B, k, seed=30 + i), B, k) for i, (n, k) in enumerate(shapes)]
+    dws = [torch.full((n, k), float("nan"), device="cuda") for n, k in shapes]
+    dbs = [torch.full((n,), float("nan"), device="cuda") for n, k in shapes]
+    ws = torch.empty(max(int(lib.load().edl_colsum_workspace_floats(B, n)) for n, _ in shapes), device="cuda")
+    lib.bwd_weight_grouped(dys, xs, dws, dbs, ws, [B] * 3, [n for n, _ in shapes], [k for _, k in shapes], 1.0,
+                           _s())
+    torch.cuda.synchronize()
+    for dy, x, dw, db in zip(dys, xs, dws, dbs):
+        ref = dy.float().T @ x.float()
+        assert (dw - ref).abs().max().item() < 1e-3 * max(1.0, ref.abs().max().item())
+        assert (db - dy.float().sum(0)).abs().max().item() < 1e-3 * max(1.0, db.abs().max().item())
