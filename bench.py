@@ -203,6 +203,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-online", action="store_true")
+    ap.add_argument("--placement", default="colocated", choices=["colocated", "split"],
+                    help="colocated: teacher worker + student on every GPU; split: teacher GPUs feed "
+                         "student GPUs over NVLink (EDL-Dist teacher pool)")
+    ap.add_argument("--teachers", type=int, default=0, help="teacher GPUs for --placement split")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.batch:
@@ -245,6 +249,12 @@ def main():
     student_h = formats.init_model(cfg["student"], 0)
     teacher = Model.from_host(teacher_h, dev)
     tcfg = TrainConfig(eta=cfg["eta"], alpha=cfg["alpha"], beta=cfg["beta"], temperature=cfg["T"], batch_size=B)
+    if args.placement == "split":
+        if world < 2:
+            raise SystemExit("--placement split needs >= 2 GPUs")
+        _split_main(args, cfg, world, rank, local, dev, ddata, teacher, student_h, tcfg, barrier)
+        dist.destroy_process_group()
+        return
     sampler = DeviceShardSampler(ddata, world, rank, B, seed=0)
     W, K = args.warmup, args.steps
     tflop_t, tflop_s = flops_per_sample(cfg)
@@ -364,6 +374,67 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _split_main(args, cfg, world, rank, local, dev, ddata, teacher, student_h, tcfg, barrier):
+    """EDL-Dist teacher pool: n_teachers GPUs infer, the others train; soft
+    labels cross NVLink as NCCL point-to-point transfers; students all-reduce
+    among themselves only."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2207_06667_b200 import _lib
+    from paper_2207_06667_b200.data import DeviceShardSampler
+    from paper_2207_06667_b200.nnkit import Model
+    from paper_2207_06667_b200.pool import Placement, RemoteSoftLabels, teacher_serve
+    from paper_2207_06667_b200.student import StudentStep
+    B, W, K = cfg["batch"], args.warmup, args.steps
+    nt = args.teachers or max(1, round(world * 0.75))
+    pl = Placement(world, min(nt, world - 1))
+    students = list(range(pl.n_students))
+    sgroup = dist.new_group(students)
+    is_student = pl.is_student(rank)
+    if is_student:
+        sampler = DeviceShardSampler(ddata, pl.n_students, rank, B, seed=0)
+        engine = StudentStep(Model.from_host(student_h, dev), tcfg, B, pl.n_students, process_group=sgroup,
+                             max_steps=W + K + 8)
+
+    def run(start, count):
+        barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = _lib.launch_count
+        s.record()
+        if is_student:
+            rx = RemoteSoftLabels(pl, rank, B, cfg["topk"], cfg["T"], dev, start, start + count)
+            for it in range(start, start + count):
+                batch = sampler.batch_for(it, out=engine.batch)
+                soft = rx.consume(it)
+                engine.step(batch, soft)
+                rx.released(it)
+        else:
+            teacher_serve(pl, rank, teacher, ddata, B, 0, cfg["T"], cfg["topk"], start, start + count)
+        e.record()
+        barrier()
+        return s.elapsed_time(e) / 1e3, _lib.launch_count - l0
+
+    run(0, W)
+    with ClockSampler(local) as clk:
+        t, launches = run(W, K)
+    tmax = _max_over_ranks(t, world, dev)
+    losses = engine.loss_values() if is_student else []
+    ok = bool(np.isfinite(losses).all()) if is_student else True
+    if rank == 0:
+        value = pl.n_students * B * K / tmax
+        print(json.dumps({
+            "metric": "student_train_samples_per_s_teacher_in_loop", "value": round(value, 1), "unit": "samples/s",
+            "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": round(tmax / K * 1e3, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (make_blobs seed 0, random-init teacher seed 1 / student seed 0)",
+            "config": {"workload": cfg["workload"], "placement": f"split {pl.n_teachers}T+{pl.n_students}S "
+                       "(teacher pool -> students over NVLink P2P, NCCL student all-reduce)",
+                       "mode": "edl (decoupled)", "global_batch": B * pl.n_students, "per_gpu_batch": B,
+                       "topk": cfg["topk"], "parallelism": f"dp{pl.n_students}"},
+            "gpu_launches": launches, "clocks": clk.summary(), "losses_finite": ok}), flush=True)
 
 
 def _teacher_rate(teacher, sampler, cfg, B, dev):

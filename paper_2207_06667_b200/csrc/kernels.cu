@@ -137,8 +137,19 @@ __global__ void __launch_bounds__(kKdWarps * 32)
   if (threadIdx.x == 0) is_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
   __syncthreads();
   if (!is_last) return;
+  // 8 independent loads in flight per thread (a dependent strided loop would
+  // serialise on L2 latency); fixed association order -> deterministic
   double acc = 0.0;
-  for (int r = threadIdx.x; r < B; r += blockDim.x) acc += static_cast<double>(__ldcg(row_loss + r));
+  for (int r0 = threadIdx.x; r0 < B; r0 += 8 * blockDim.x) {
+    float f[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int r = r0 + u * blockDim.x;
+      f[u] = r < B ? __ldcg(row_loss + r) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += static_cast<double>(f[u]);
+  }
   red[threadIdx.x] = acc;
   __syncthreads();
   for (int s = blockDim.x / 2; s > 0; s >>= 1) {

@@ -67,6 +67,25 @@ def main():
         t = timeit(lambda i: _lib.call("edl_linear_bwd_weight", dy.data_ptr(), N, x.data_ptr(), K, dw.data_ptr(), K,
                                        db.data_ptr(), ws.data_ptr(), B, N, K, 1.0, st), a.iters)
         res[name] = dict(us=t * 1e6, tflops=2 * B * N * K / t / 1e12)
+    # operand-major experiment: the dW1 problem (M=2048, N=3072, K=4096) with
+    # K-major operands through the forward kernel, vs. MN-major (s_bwd_w1)
+    xa = torch.randn(2048, B, device="cuda").to(bf)
+    xb = torch.randn(3072, B, device="cuda").to(bf)
+    yo = torch.empty(2048, 3072, device="cuda")
+    t = timeit(lambda i: _lib.call("edl_linear_fwd", xa.data_ptr(), B, xb.data_ptr(), B, None, yo.data_ptr(), 3072,
+                                   2048, 3072, B, 0, st), a.iters)
+    res["dw1_shape_kmajor"] = dict(us=t * 1e6, tflops=2 * B * 2048 * 3072 / t / 1e12)
+    # the three student dW in one grouped launch (what the backward pass issues)
+    shapes = [(2048, 3072), (1024, 2048), (1008, 1024)]
+    dys = [torch.randn(B, n, device="cuda").to(bf) for n, _ in shapes]
+    xs = [torch.randn(B, kk, device="cuda").to(bf) for _, kk in shapes]
+    dws = [torch.empty(n, kk, device="cuda") for n, kk in shapes]
+    dbs = [torch.empty(n, device="cuda") for n, _ in shapes]
+    ws = torch.empty(max(int(_lib.load().edl_colsum_workspace_floats(B, n)) for n, _ in shapes), device="cuda")
+    t = timeit(lambda i: _lib.bwd_weight_grouped(dys, xs, dws, dbs, ws, [B] * 3, [n for n, _ in shapes],
+                                                 [kk for _, kk in shapes], 1.0, st), a.iters)
+    fl = sum(2 * B * n * kk for n, kk in shapes)
+    res["s_bwd_w_grouped"] = dict(us=t * 1e6, tflops=fl / t / 1e12)
     # teacher head
     H, C, k = 8192, 1000, 16
     hs = [torch.randn(B, H, device="cuda").to(bf) for _ in range(2)]
