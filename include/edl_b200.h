@@ -67,11 +67,13 @@ long long edl_colsum_workspace_floats(int M, int N);
  * (host arrays of per-layer pointers / sizes). The backward pass issues every
  * dW of the student this way once the delta chain (edl_linear_bwd_data) is
  * done: each layer alone has too few output tiles to fill 148 SMs.
- * workspace: max over layers of edl_colsum_workspace_floats(M[p], N[p]). */
+ * workspace: edl_colsum_group_workspace_floats(count, M, N) floats (all the
+ * layers' column sums run as one deterministic two-pass launch pair). */
 int edl_linear_bwd_weight_grouped(int count, const void* const* dY, const long long* lddy,
                                   const void* const* X, const long long* ldx, float* const* dW,
                                   const long long* lddw, float* const* db, float* workspace,
                                   const int* M, const int* N, const int* K, float scale, void* stream);
+long long edl_colsum_group_workspace_floats(int count, const int* M, const int* N);
 
 /* Teacher head = soft_label_reply's math (edl/teacher_node.py:54:
  * tempered_softmax(forward(model, inputs), T), edl/nnkit.py:193-208,232) fused

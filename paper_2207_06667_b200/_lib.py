@@ -34,6 +34,7 @@ _SIGNATURES = {
     "edl_linear_bwd_weight_grouped": [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                       c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_float, c_void_p],
     "edl_colsum_workspace_floats": [c_int, c_int],
+    "edl_colsum_group_workspace_floats": [c_int, c_void_p, c_void_p],
     "edl_teacher_head_softmax_topk": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_int, c_int,
                                       c_int, c_float, c_int, c_void_p, c_void_p, c_void_p],
     "edl_tempered_softmax": [c_void_p, c_ll, c_void_p, c_ll, c_int, c_int, c_float, c_void_p],
@@ -46,7 +47,8 @@ _SIGNATURES = {
     "edl_topk_hits": [c_void_p, c_ll, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p],
     "edl_cast_bf16": [c_void_p, c_ll, c_void_p, c_ll, c_int, c_int, c_void_p],
 }
-_RESTYPES = {"edl_last_error": c_char_p, "edl_colsum_workspace_floats": c_ll}
+_RESTYPES = {"edl_last_error": c_char_p, "edl_colsum_workspace_floats": c_ll,
+             "edl_colsum_group_workspace_floats": c_ll}
 
 EDL_ERR_SHAPE, EDL_ERR_NUMERIC, EDL_ERR_PARAM, EDL_ERR_CUDA = -1, -2, -3, -4
 EDL_ACT_NONE, EDL_ACT_TANH = 0, 1
@@ -120,4 +122,9 @@ def bwd_weight_grouped(dys, xs, dws, dbs, workspace, Ms, Ns, Ks, scale, stream) 
             P(*[t.data_ptr() for t in dws]), L(*Ks), P(*[t.data_ptr() for t in dbs]),
             workspace.data_ptr(), I(*Ms), I(*Ns), I(*Ks), scale, stream)
     check(load().edl_linear_bwd_weight_grouped(*args), "edl_linear_bwd_weight_grouped")
-    launch_count += 1 + 2 * n
+    launch_count += 3   # grouped GEMM + one column-sum launch pair for all layers
+
+
+def colsum_group_workspace_floats(Ms, Ns) -> int:
+    n = len(Ms)
+    return int(load().edl_colsum_group_workspace_floats(n, (c_int * n)(*Ms), (c_int * n)(*Ns)))

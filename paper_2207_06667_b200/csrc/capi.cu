@@ -218,18 +218,33 @@ int edl_linear_bwd_weight_grouped(int count, const void* const* dY, const long l
   ga.tile_start[count] = tiles;
   cudaError_t e = launch_gemm_grouped_bwd_weight(maps, ga, num_sms(), as_stream(stream));
   if (e != cudaSuccess) return cuda_fail(e, "linear_bwd_weight_grouped");
-  for (int p = 0; p < count; ++p) {
-    if (!db || !db[p]) continue;
-    if (!workspace) return fail(EDL_ERR_SHAPE, "linear_bwd_weight_grouped: db needs a workspace");
-    e = launch_colsum(reinterpret_cast<const __nv_bfloat16*>(dY[p]), lddy[p], M[p], N[p], workspace, db[p],
-                      scale, as_stream(stream));
-    if (e != cudaSuccess) return cuda_fail(e, "colsum");
+  if (db) {
+    ColsumGroup g = {};
+    for (int p = 0; p < count; ++p) {
+      if (!db[p]) continue;
+      g.x[g.count] = reinterpret_cast<const __nv_bfloat16*>(dY[p]);
+      g.ld[g.count] = lddy[p];
+      g.M[g.count] = M[p];
+      g.N[g.count] = N[p];
+      g.out[g.count] = db[p];
+      ++g.count;
+    }
+    if (g.count > 0) {
+      if (!workspace) return fail(EDL_ERR_SHAPE, "linear_bwd_weight_grouped: db needs a workspace");
+      g.scale = scale;
+      g.partial = workspace;
+      e = launch_colsum_group(g, as_stream(stream));
+      if (e != cudaSuccess) return cuda_fail(e, "colsum");
+    }
   }
   return 0;
 }
 
-long long edl_colsum_workspace_floats(int M, int N) {
-  return static_cast<long long>((M + 127) / 128) * N;
+long long edl_colsum_workspace_floats(int M, int N) { return colsum_workspace_floats(1, &M, &N); }
+
+long long edl_colsum_group_workspace_floats(int count, const int* M, const int* N) {
+  if (count < 1 || count > kMaxGroup) return -1;
+  return colsum_workspace_floats(count, M, N);
 }
 
 int edl_teacher_head_softmax_topk(const void* H, long long ldh, const void* W, long long ldw,

@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();  // PDL: everything above overlapped the previous kernel's tail
 
   const int num_m = (M + kBM - 1) / kBM;
   const int num_n = (N + BN - 1) / BN;
@@ -289,6 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();  // PDL: everything above overlapped the previous kernel's tail
   const int tiles = ga.tile_start[ga.count];
 
   // tile -> (problem, m0, n0)
@@ -499,6 +501,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();  // PDL: everything above overlapped the previous kernel's tail
 
   if (warp == 0 && lane == 0) {
     for (int kb = 0; kb < nk; ++kb) {
@@ -660,8 +663,7 @@ static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, i
   }
   const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms ? tiles : num_sms;
-  kern<<<grid, kThreads, GemmCfg<BN>::kSmem, stream>>>(ta, tb, M, N, K, ep);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(grid), dim3(kThreads), GemmCfg<BN>::kSmem, stream, 1, ta, tb, M, N, K, ep);
 }
 
 template <bool A_MN, bool B_MN, int EPI>
@@ -705,8 +707,7 @@ cudaError_t launch_gemm_grouped_bwd_weight(const GroupMaps& maps, const GroupArg
   }
   const int tiles = ga.tile_start[ga.count];
   const int grid = tiles < num_sms ? tiles : num_sms;
-  kern<<<grid, kThreads, GemmCfg<BN>::kSmem, stream>>>(maps, ga);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(grid), dim3(kThreads), GemmCfg<BN>::kSmem, stream, 1, maps, ga);
 }
 
 int grouped_tile_bn() { return 256; }
@@ -725,19 +726,8 @@ static cudaError_t launch_head_t(const CUtensorMap& ta, const CUtensorMap& tb, i
     attr_set = true;
   }
   const int cs = (N + BN - 1) / BN;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(cs, (M + kBM - 1) / kBM, 1);
-  cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = GemmCfg<BN>::kSmem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cs;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, hp);
+  return launch_pdl(kern, dim3(cs, (M + kBM - 1) / kBM, 1), dim3(kThreads), GemmCfg<BN>::kSmem, stream, cs,
+                    ta, tb, M, N, K, hp);
 }
 
 template <int BN>

@@ -4,8 +4,37 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <utility>
 
 namespace edl {
+
+// Launch with programmatic stream serialization (PDL) and an optional
+// cluster shape; every kernel of the library calls griddep_wait() before its
+// first global access, so early launch is always safe.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, int cluster_x, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[n].val.programmaticStreamSerializationAllowed = 1;
+  ++n;
+  if (cluster_x > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = cluster_x;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 enum EpiMode : int {
   EPI_TANH_BF16 = 0,   // out(bf16) = tanh(acc + bias)
@@ -69,6 +98,19 @@ cudaError_t launch_gather_rows(const __nv_bfloat16* src, long long ld_src, const
                                const int64_t* src_labels, int64_t* dst_labels, cudaStream_t stream);
 cudaError_t launch_colsum(const __nv_bfloat16* x, long long ld, int M, int N, float* partial,
                           float* out, float scale, cudaStream_t stream);
+struct ColsumGroup {
+  int count;
+  const __nv_bfloat16* x[kMaxGroup];
+  long long ld[kMaxGroup];
+  int M[kMaxGroup], N[kMaxGroup];
+  float* out[kMaxGroup];
+  float scale;
+  float* partial;
+  long long part_off[kMaxGroup];
+  int blk_start[kMaxGroup + 1];
+};
+cudaError_t launch_colsum_group(ColsumGroup g, cudaStream_t stream);
+long long colsum_workspace_floats(int count, const int* M, const int* N);
 cudaError_t launch_topk_hits(const float* logits, long long ld, const int64_t* labels, int B,
                              int K, int k, unsigned* hits, cudaStream_t stream);
 cudaError_t launch_cast_bf16(const float* src, long long ld_src, __nv_bfloat16* dst,

@@ -9,6 +9,7 @@
 //   colsum                edl/nnkit.py:306      db = sum over the batch of delta
 //   topk_hits             edl/nnkit.py:325-335  top-k accuracy, lower-index ties
 #include "internal.h"
+#include "sm100.cuh"
 
 #include <cfloat>
 
@@ -46,6 +47,7 @@ __global__ void __launch_bounds__(kKdWarps * 32)
                    int Kw, int k, float alpha, float beta, float T, float* __restrict__ row_loss,
                    float* __restrict__ loss_out, unsigned* __restrict__ ticket,
                    __nv_bfloat16* __restrict__ dz, long long ld_dz, int* __restrict__ status) {
+  griddep_wait();
   extern __shared__ float sm[];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   float* ds = sm + warp * (32 * KPL);
@@ -180,10 +182,8 @@ static cudaError_t launch_kd_t(const float* logits, long long ld_z, const int64_
   set = true;
   int blocks = (B + kKdWarps - 1) / kKdWarps;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  kd_loss_kernel<KPL><<<blocks, kKdWarps * 32, smem, stream>>>(logits, ld_z, labels, q_vals, q_idx, B, K, Kw,
-                                                              k, alpha, beta, T, row_loss, loss_out, ticket,
-                                                              dlogits, ld_dz, status);
-  return cudaGetLastError();
+  return launch_pdl(kd_loss_kernel<KPL>, dim3(blocks), dim3(kKdWarps * 32), smem, stream, 1, logits, ld_z, labels,
+                    q_vals, q_idx, B, K, Kw, k, alpha, beta, T, row_loss, loss_out, ticket, dlogits, ld_dz, status);
 }
 
 cudaError_t launch_kd_loss(const float* logits, long long ld_z, const int64_t* labels,
@@ -213,6 +213,7 @@ cudaError_t launch_kd_loss(const float* logits, long long ld_z, const int64_t* l
 __global__ void tempered_softmax_kernel(const float* __restrict__ z, long long ld,
                                         float* __restrict__ p, long long ld_p, int B, int K,
                                         float inv_t) {
+  griddep_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
   if (warp >= B) return;
   const float* zr = z + static_cast<size_t>(warp) * ld;
@@ -231,13 +232,14 @@ cudaError_t launch_tempered_softmax(const float* logits, long long ld, float* pr
                                     long long ld_p, int B, int K, float T, cudaStream_t stream) {
   const int threads = 256;
   const int blocks = (B * 32 + threads - 1) / threads;
-  tempered_softmax_kernel<<<blocks, threads, 0, stream>>>(logits, ld, probs, ld_p, B, K, 1.0f / T);
-  return cudaGetLastError();
+  return launch_pdl(tempered_softmax_kernel, dim3(blocks), dim3(threads), 0, stream, 1, logits, ld, probs, ld_p, B, K,
+                    1.0f / T);
 }
 
 // ------------------------------------------------------------------ SGD
 __global__ void sgd_kernel(float* __restrict__ p, __nv_bfloat16* __restrict__ pb,
                            const float* __restrict__ g, long long n, float scale) {
+  griddep_wait();
   const long long n4 = n / 4;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
@@ -265,8 +267,7 @@ cudaError_t launch_sgd(float* p, __nv_bfloat16* p_bf16, const float* g, long lon
   long long blocks = (n / 4 + threads - 1) / threads;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  sgd_kernel<<<static_cast<int>(blocks), threads, 0, stream>>>(p, p_bf16, g, n, scale);
-  return cudaGetLastError();
+  return launch_pdl(sgd_kernel, dim3(static_cast<int>(blocks)), dim3(threads), 0, stream, 1, p, p_bf16, g, n, scale);
 }
 
 // ------------------------------------------------------------------ gather
@@ -274,6 +275,7 @@ __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, long l
                                    const int64_t* __restrict__ idx, __nv_bfloat16* __restrict__ dst,
                                    long long ld_dst, int B, int D, const int64_t* __restrict__ src_lab,
                                    int64_t* __restrict__ dst_lab) {
+  griddep_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
   if (warp >= B) return;
   const int64_t r = idx[warp];
@@ -290,62 +292,118 @@ cudaError_t launch_gather_rows(const __nv_bfloat16* src, long long ld_src, const
                                const int64_t* src_labels, int64_t* dst_labels, cudaStream_t stream) {
   const int threads = 256;
   const int blocks = (B * 32 + threads - 1) / threads;
-  gather_rows_kernel<<<blocks, threads, 0, stream>>>(src, ld_src, idx, dst, ld_dst, B, D, src_labels,
-                                                     dst_labels);
-  return cudaGetLastError();
+  return launch_pdl(gather_rows_kernel, dim3(blocks), dim3(threads), 0, stream, 1, src, ld_src, idx, dst, ld_dst, B, D,
+                    src_labels, dst_labels);
 }
 
 // ------------------------------------------------------------------ column sum
-// Two fixed-order passes: 128-row chunks -> partial[chunk][n], then chunks summed
-// in order (deterministic, no atomics).
-constexpr int kColRows = 128;
+// db_l = scale * sum over the batch of delta_l, for up to kMaxGroup layers in
+// ONE pair of launches. Pass 1: a block owns 256 rows x 256 columns of one
+// layer; a lane reads 16 bytes (8 bf16 columns) per row with 8 rows in flight,
+// the 8 warps combine in a fixed order -> partial[row chunk][n]. Pass 2: row
+// chunks summed in order. Deterministic, no atomics.
+constexpr int kColRows = 256;
+constexpr int kColCols = 256;
 
-__global__ void colsum_partial_kernel(const __nv_bfloat16* __restrict__ x, long long ld, int M,
-                                      int N, float* __restrict__ partial) {
-  __shared__ float2 red[8][32];
+__global__ void __launch_bounds__(256) colsum_partial_kernel(ColsumGroup g) {
+  griddep_wait();
+  __shared__ float red[8][kColCols];
+  int p = 0;
+  while (p + 1 < g.count && static_cast<int>(blockIdx.x) >= g.blk_start[p + 1]) ++p;
+  const int local = blockIdx.x - g.blk_start[p];
+  const int cgs = (g.N[p] + kColCols - 1) / kColCols;
+  const int cg = local % cgs, rc = local / cgs;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int n = blockIdx.x * 64 + 2 * lane;
-  const int r0 = blockIdx.y * kColRows;
-  float2 acc = make_float2(0.f, 0.f);
-  if (n < N) {
-    for (int r = r0 + warp; r < r0 + kColRows && r < M; r += 8) {
-      const __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(x + static_cast<size_t>(r) * ld + n);
-      acc.x += __bfloat162float(v.x);
-      acc.y += __bfloat162float(v.y);
+  const int n0 = cg * kColCols + lane * 8;
+  const int r0 = rc * kColRows + warp * 32;
+  const int M = g.M[p], N = g.N[p];
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (n0 < N) {
+    const __nv_bfloat16* base = g.x[p] + n0;
+#pragma unroll
+    for (int rr = 0; rr < 32; rr += 8) {
+      uint4 q[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int r = r0 + rr + u;
+        q[u] = r < M ? __ldg(reinterpret_cast<const uint4*>(base + static_cast<size_t>(r) * g.ld[p]))
+                     : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&q[u]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(h[j]);
+      }
     }
   }
-  red[warp][lane] = acc;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) red[warp][lane * 8 + j] = acc[j];
   __syncthreads();
-  if (warp == 0 && n < N) {
-    float2 s = red[0][lane];
-    for (int w = 1; w < 8; ++w) { s.x += red[w][lane].x; s.y += red[w][lane].y; }
-    partial[static_cast<size_t>(blockIdx.y) * N + n] = s.x;
-    if (n + 1 < N) partial[static_cast<size_t>(blockIdx.y) * N + n + 1] = s.y;
+  const int n = cg * kColCols + threadIdx.x;
+  if (n < N) {
+    float s = red[0][threadIdx.x];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) s += red[w][threadIdx.x];
+    g.partial[g.part_off[p] + static_cast<long long>(rc) * N + n] = s;
   }
 }
 
-__global__ void colsum_final_kernel(const float* __restrict__ partial, int chunks, int N,
-                                    float* __restrict__ out, float scale) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= N) return;
+__global__ void colsum_final_kernel(ColsumGroup g) {
+  griddep_wait();
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  int p = 0;
+  while (p < g.count && t >= g.N[p]) { t -= g.N[p]; ++p; }
+  if (p >= g.count) return;
+  const int chunks = (g.M[p] + kColRows - 1) / kColRows;
+  const float* part = g.partial + g.part_off[p];
   float s = 0.f;
-  for (int c = 0; c < chunks; ++c) s += partial[static_cast<size_t>(c) * N + n];
-  out[n] = s * scale;
+  for (int c = 0; c < chunks; ++c) s += part[static_cast<long long>(c) * g.N[p] + t];
+  g.out[p][t] = s * g.scale;
+}
+
+long long colsum_workspace_floats(int count, const int* M, const int* N) {
+  long long w = 0;
+  for (int p = 0; p < count; ++p) w += static_cast<long long>((M[p] + kColRows - 1) / kColRows) * N[p];
+  return w;
+}
+
+cudaError_t launch_colsum_group(ColsumGroup g, cudaStream_t stream) {
+  int blocks = 0, cols = 0;
+  long long off = 0;
+  for (int p = 0; p < g.count; ++p) {
+    g.blk_start[p] = blocks;
+    g.part_off[p] = off;
+    const int chunks = (g.M[p] + kColRows - 1) / kColRows;
+    blocks += ((g.N[p] + kColCols - 1) / kColCols) * chunks;
+    off += static_cast<long long>(chunks) * g.N[p];
+    cols += g.N[p];
+  }
+  g.blk_start[g.count] = blocks;
+  cudaError_t e = launch_pdl(colsum_partial_kernel, dim3(blocks), dim3(256), 0, stream, 1, g);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(colsum_final_kernel, dim3((cols + 255) / 256), dim3(256), 0, stream, 1, g);
 }
 
 cudaError_t launch_colsum(const __nv_bfloat16* x, long long ld, int M, int N, float* partial,
                           float* out, float scale, cudaStream_t stream) {
-  const int chunks = (M + kColRows - 1) / kColRows;
-  dim3 grid((N + 63) / 64, chunks);
-  colsum_partial_kernel<<<grid, 256, 0, stream>>>(x, ld, M, N, partial);
-  colsum_final_kernel<<<(N + 255) / 256, 256, 0, stream>>>(partial, chunks, N, out, scale);
-  return cudaGetLastError();
+  ColsumGroup g = {};
+  g.count = 1;
+  g.x[0] = x;
+  g.ld[0] = ld;
+  g.M[0] = M;
+  g.N[0] = N;
+  g.out[0] = out;
+  g.scale = scale;
+  g.partial = partial;
+  return launch_colsum_group(g, stream);
 }
 
 // ------------------------------------------------------------------ top-k accuracy
 __global__ void topk_hits_kernel(const float* __restrict__ z, long long ld,
                                  const int64_t* __restrict__ labels, int B, int K, int k,
                                  unsigned* __restrict__ hits) {
+  griddep_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
   if (warp >= B) return;
   const float* zr = z + static_cast<size_t>(warp) * ld;
@@ -372,6 +430,7 @@ cudaError_t launch_topk_hits(const float* logits, long long ld, const int64_t* l
 __global__ void cast_bf16_kernel(const float* __restrict__ src, long long ld_src,
                                  __nv_bfloat16* __restrict__ dst, long long ld_dst, int rows,
                                  int cols) {
+  griddep_wait();
   const long long total = static_cast<long long>(rows) * cols;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {

@@ -185,6 +185,19 @@ __device__ __forceinline__ int ld_dsmem_s32(uint32_t addr) {
   return v;
 }
 
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch: a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// predecessor in the stream drains; it must wait here before touching any
+// global data the predecessor reads or writes.
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+// Let the dependent grid start its prologue (on SMs this grid frees).
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- math
 __device__ __forceinline__ float tanh_fast(float x) {
   float y;

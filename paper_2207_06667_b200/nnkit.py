@@ -267,7 +267,8 @@ class Workspace:
         self.loss = torch.zeros(1, dtype=torch.float32, device=dev)
         self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
-        ws = max(int(_lib.load().edl_colsum_workspace_floats(B, L.dims_p[l + 1])) for l in range(L.layers))
+        ws = max(_lib.colsum_group_workspace_floats([B] * len(part), [L.dims_p[l + 1] for l in part])
+                 for part in (list(range(L.layers))[c:c + 4] for c in range(0, L.layers, 4)))
         self.colsum = torch.empty(max(ws, 1), dtype=torch.float32, device=dev)
         self.grads = Gradients(torch.zeros(L.size, dtype=torch.float32, device=dev), L)
         self.probs = None

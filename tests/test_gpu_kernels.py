@@ -208,7 +208,7 @@ def test_linear_bwd_weight_grouped_matches_reference(lib):
     xs = [_padded(_rand(B, k, seed=30 + i), B, k) for i, (n, k) in enumerate(shapes)]
     dws = [torch.full((n, k), float("nan"), device="cuda") for n, k in shapes]
     dbs = [torch.full((n,), float("nan"), device="cuda") for n, k in shapes]
-    ws = torch.empty(max(int(lib.load().edl_colsum_workspace_floats(B, n)) for n, _ in shapes), device="cuda")
+    ws = torch.empty(lib.colsum_group_workspace_floats([B] * 3, [n for n, _ in shapes]), device="cuda")
     lib.bwd_weight_grouped(dys, xs, dws, dbs, ws, [B] * 3, [n for n, _ in shapes], [k for _, k in shapes], 1.0,
                            _s())
     torch.cuda.synchronize()
