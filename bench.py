@@ -277,12 +277,16 @@ def main():
         barrier()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         launches0 = _lib.launch_count
+        if timed:
+            torch.cuda.nvtx.range_push("edl_timed")   # ncu --nvtx-include edl_timed/
         s.record()
         for it in range(start, start + count):
             batch = sampler.batch_for(it, out=engine.batch)
             soft = reader.consume(it)
             engine.step(batch, soft)
         e.record()
+        if timed:
+            torch.cuda.nvtx.range_pop()
         barrier()
         launches = _lib.launch_count - launches0
         ledger = reader.ledger()

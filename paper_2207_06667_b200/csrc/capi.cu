@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -124,6 +125,33 @@ int pick_bn(int M, int N) {
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Per-(device, stream) tile-scheduler counters for the persistent GEMM
+// ({next tile, CTAs done}, reset by each launch's last CTA). Allocated on a
+// stream's first GEMM only; launches on one stream are ordered (PDL waits),
+// launches on different streams never share a counter.
+std::mutex g_sched_mu;
+std::unordered_map<std::string, unsigned*> g_sched;
+
+unsigned* stream_sched(cudaStream_t s) {
+  static const bool disabled = [] {
+    const char* v = getenv("EDL_STATIC_SCHED");
+    return v && v[0] == '1';
+  }();
+  if (disabled) return nullptr;   // A/B switch: static tile schedule
+  int dev = 0;
+  cudaGetDevice(&dev);
+  char key[64];
+  snprintf(key, sizeof(key), "%d:%p", dev, static_cast<void*>(s));
+  std::lock_guard<std::mutex> g(g_sched_mu);
+  auto it = g_sched.find(key);
+  if (it != g_sched.end()) return it->second;
+  unsigned* p = nullptr;
+  if (cudaMalloc(&p, 2 * sizeof(unsigned)) != cudaSuccess) return nullptr;  // static schedule fallback
+  cudaMemsetAsync(p, 0, 2 * sizeof(unsigned), s);
+  g_sched.emplace(key, p);
+  return p;
+}
+
 }  // namespace
 
 extern "C" {
@@ -144,7 +172,7 @@ int edl_linear_fwd(const void* X, long long ldx, const void* W, long long ldw, c
   int rc;
   if ((rc = tensor_map(X, M, K, ldx, 64, 128, &ta))) return rc;
   if ((rc = tensor_map(W, N, K, ldw, 64, bn, &tb))) return rc;
-  EpiArgs ep{Y, ldy, bias, nullptr, 0, 1.0f};
+  EpiArgs ep{Y, ldy, bias, nullptr, 0, 1.0f, stream_sched(as_stream(stream))};
   cudaError_t e = launch_gemm(act == EDL_ACT_TANH ? GemmKind::FwdTanh : GemmKind::FwdLinear, bn, ta,
                               tb, M, N, K, ep, num_sms(), as_stream(stream));
   return e == cudaSuccess ? 0 : cuda_fail(e, "linear_fwd");
@@ -161,7 +189,8 @@ int edl_linear_bwd_data(const void* dY, long long lddy, const void* W, long long
   // A = dY [M][N] (reduction N contiguous: K-major); B = W [N][K] read as [red][MN].
   if ((rc = tensor_map(dY, M, N, lddy, 64, 128, &ta))) return rc;
   if ((rc = tensor_map(W, N, K, ldw, 64, 64, &tb))) return rc;
-  EpiArgs ep{dX, lddx, nullptr, reinterpret_cast<const __nv_bfloat16*>(H), ldh, 1.0f};
+  EpiArgs ep{dX, lddx, nullptr, reinterpret_cast<const __nv_bfloat16*>(H), ldh, 1.0f,
+             stream_sched(as_stream(stream))};
   cudaError_t e = launch_gemm(GemmKind::BwdData, bn, ta, tb, M, K, N, ep, num_sms(), as_stream(stream));
   return e == cudaSuccess ? 0 : cuda_fail(e, "linear_bwd_data");
 }
@@ -177,7 +206,7 @@ int edl_linear_bwd_weight(const void* dY, long long lddy, const void* X, long lo
   // A = dY^T: dY [M][N] read as [red=M][MN=N]; B = X^T: X [M][K] read as [red=M][MN=K].
   if ((rc = tensor_map(dY, M, N, lddy, 64, 64, &ta))) return rc;
   if ((rc = tensor_map(X, M, K, ldx, 64, 64, &tb))) return rc;
-  EpiArgs ep{dW, lddw, nullptr, nullptr, 0, scale};
+  EpiArgs ep{dW, lddw, nullptr, nullptr, 0, scale, stream_sched(as_stream(stream))};
   cudaError_t e = launch_gemm(GemmKind::BwdWeight, bn, ta, tb, N, K, M, ep, num_sms(), as_stream(stream));
   if (e != cudaSuccess) return cuda_fail(e, "linear_bwd_weight");
   if (db) {

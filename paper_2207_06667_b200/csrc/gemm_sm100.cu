@@ -40,24 +40,35 @@ struct GemmCfg {
   static constexpr uint32_t kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-// Issue the TMA loads of one (A,B) k-block into stage buffers.
+// Issue the TMA loads of one (A,B) k-block into stage buffers, with per-operand
+// L2 eviction policies (pa, pb).
 template <int BN, bool A_MN, bool B_MN>
 __device__ __forceinline__ void load_kblock(const CUtensorMap* tmA, const CUtensorMap* tmB,
                                             uint8_t* sa, uint8_t* sb, uint64_t* bar, int m0,
-                                            int n0, int k0) {
+                                            int n0, int k0, uint64_t pa, uint64_t pb) {
   mbar_arrive_expect_tx(bar, GemmCfg<BN>::kStageBytes);
   if constexpr (!A_MN) {
-    tma_load_2d(sa, tmA, bar, k0, m0);
+    tma_load_2d_hint(sa, tmA, bar, k0, m0, pa);
   } else {
 #pragma unroll
-    for (int j = 0; j < kBM / 64; ++j) tma_load_2d(sa + j * 8192, tmA, bar, m0 + 64 * j, k0);
+    for (int j = 0; j < kBM / 64; ++j) tma_load_2d_hint(sa + j * 8192, tmA, bar, m0 + 64 * j, k0, pa);
   }
   if constexpr (!B_MN) {
-    tma_load_2d(sb, tmB, bar, k0, n0);
+    tma_load_2d_hint(sb, tmB, bar, k0, n0, pb);
   } else {
 #pragma unroll
-    for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, tmB, bar, n0 + 64 * j, k0);
+    for (int j = 0; j < BN / 64; ++j) tma_load_2d_hint(sb + j * 8192, tmB, bar, n0 + 64 * j, k0, pb);
   }
+}
+
+// L2 policy per operand. Measured on B200 (profiles/): evict_last on the
+// re-read activations + evict_first on the streamed weights RAISED teacher
+// layer-2 DRAM reads (619 -> 683 MB/launch) and lowered tensor-pipe activity,
+// so every operand uses the normal policy.
+template <int EPI>
+__device__ __forceinline__ void gemm_policies(uint64_t& pa, uint64_t& pb) {
+  pa = l2_policy_evict_normal();
+  pb = l2_policy_evict_normal();
 }
 
 // Four 128xBNx16 MMAs consume one 64-deep k-block.
@@ -166,6 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 int M, int N, int K, EpiArgs ep) {
   using Cfg = GemmCfg<BN>;
+  unsigned* const sched = ep.sched;
   constexpr int S = Cfg::kStages;
   constexpr uint32_t kTmemCols = tmem_cols_for(2 * BN);
   extern __shared__ uint8_t smem_raw[];
@@ -177,7 +189,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tile_full = tempty + 2;       // [4] tile-index ring
+  uint64_t* tile_empty = tile_full + 4;   // [4]
+  int* tile_ring = reinterpret_cast<int*>(tile_empty + 4);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + 4);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -186,6 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tmB);
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
+    for (int s = 0; s < 4; ++s) { mbar_init(&tile_full[s], 1); mbar_init(&tile_empty[s], 1 + 4); }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
@@ -200,20 +216,43 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tiles = num_m * num_n;
   const int nk = (K + kBK - 1) / kBK;
 
+  // Dynamic tile scheduler: the producer claims tiles from a per-stream
+  // global counter and publishes them to the MMA and epilogue roles through a
+  // 4-deep smem ring. A CTA that starts late (its SM was busy with another
+  // stream's kernel) simply claims fewer tiles, so concurrent teacher and
+  // student kernels share the SMs without a tail; the last CTA to exit
+  // resets the counter for the next launch on the stream (PDL orders it).
+  auto next_tile = [&](int i) -> int {
+    return sched ? static_cast<int>(atomicAdd(sched, 1u)) : static_cast<int>(blockIdx.x + i * gridDim.x);
+  };
+
   if (warp == 0 && lane == 0) {
+    uint64_t pa, pb;
+    gemm_policies<EPI>(pa, pb);
     uint32_t g = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    for (int i = 0;; ++i) {
+      const int slot = i & 3;
+      mbar_wait(&tile_empty[slot], ((i >> 2) & 1) ^ 1);
+      const int t = next_tile(i);
+      tile_ring[slot] = t;
+      mbar_arrive(&tile_full[slot]);
+      if (t >= tiles) break;
       const int m0 = (t % num_m) * kBM, n0 = (t / num_m) * BN;
       for (int kb = 0; kb < nk; ++kb, ++g) {
         const int s = g % S;
         mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
         load_kblock<BN, A_MN, B_MN>(&tmA, &tmB, sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes,
-                                    &full[s], m0, n0, kb * kBK);
+                                    &full[s], m0, n0, kb * kBK, pa, pb);
       }
     }
   } else if (warp == 1 && lane == 0) {
-    uint32_t g = 0, i = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+    uint32_t g = 0;
+    for (uint32_t i = 0;; ++i) {
+      const int slot = i & 3;
+      mbar_wait(&tile_full[slot], (i >> 2) & 1);
+      const int t = tile_ring[slot];
+      mbar_arrive(&tile_empty[slot]);
+      if (t >= tiles) break;
       const uint32_t as = i & 1;
       mbar_wait(&tempty[as], ((i >> 1) & 1) ^ 1);
       tc_fence_after();
@@ -230,8 +269,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     const int e = warp - 4;
-    uint32_t i = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+    for (uint32_t i = 0;; ++i) {
+      const int slot = i & 3;
+      mbar_wait(&tile_full[slot], (i >> 2) & 1);
+      const int t = tile_ring[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tile_empty[slot]);
+      if (t >= tiles) break;
       const int m0 = (t % num_m) * kBM, n0 = (t / num_m) * BN;
       const uint32_t as = i & 1;
       mbar_wait(&tfull[as], (i >> 1) & 1);
@@ -252,6 +296,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem_base);
+  }
+  if (sched && threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(sched + 1, 1u) == gridDim.x - 1) {   // last CTA out: reset for the next launch
+      atomicExch(sched, 0u);
+      atomicExch(sched + 1, 0u);
+    }
   }
 }
 
@@ -304,6 +355,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
 
   if (warp == 0 && lane == 0) {
+    uint64_t pa, pb;
+    gemm_policies<EPI>(pa, pb);
     uint32_t g = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       int p, m0, n0;
@@ -313,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = g % S;
         mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
         load_kblock<BN, A_MN, B_MN>(&maps.a[p], &maps.b[p], sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes,
-                                    &full[s], m0, n0, kb * kBK);
+                                    &full[s], m0, n0, kb * kBK, pa, pb);
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -504,11 +557,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   griddep_wait();  // PDL: everything above overlapped the previous kernel's tail
 
   if (warp == 0 && lane == 0) {
+    const uint64_t pa = l2_policy_evict_normal(), pb = l2_policy_evict_normal();
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % S;
       mbar_wait(&empty[s], ((kb / S) & 1) ^ 1);
       load_kblock<BN, false, false>(&tmA, &tmB, sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes,
-                                    &full[s], m0, n0, kb * kBK);
+                                    &full[s], m0, n0, kb * kBK, pa, pb);
     }
   } else if (warp == 1 && lane == 0) {
     for (int kb = 0; kb < nk; ++kb) {

@@ -50,6 +50,7 @@ struct EpiArgs {
   const __nv_bfloat16* aux;
   long long ld_aux;
   float scale;
+  unsigned* sched = nullptr;  // per-stream {next tile, CTAs done}; null -> static schedule
 };
 
 struct HeadArgs {

@@ -249,7 +249,10 @@ class StudentNode:
                                batch_size=t.batch_size, seed=t.seed)
         return t
 
-    def run(self) -> StudentResult:
+    def run(self, on_iteration=None) -> StudentResult:
+        """Alg. 2 (edl/student_node.py:684-794). `on_iteration(it, reader)` is a
+        fault-injection hook called before each step (kill / add teachers
+        mid-run, like FaultEvent in edl/harness.py:52-69)."""
         cfg = self.cfg
         train_cfg = self._train_config()
         host, start = self.initial_model()
@@ -272,6 +275,8 @@ class StudentNode:
         t0.record()
         trained = 0
         for it in range(start, self.total_steps):
+            if on_iteration is not None:
+                on_iteration(it, reader)
             batch = self.sampler.batch_for(it, out=engine.batch)
             soft = None
             if cfg.mode == MODE_EDL:

@@ -184,3 +184,48 @@ def test_student_modes_and_trajectory():
     dev = ref.flatten(res["ntrain"].model.weights, res["ntrain"].model.biases)
     orc = ref.flatten(ws, bs)
     assert np.linalg.norm(dev - orc) / np.linalg.norm(orc) < 1e-2
+
+
+def _edl_run(faults):
+    from paper_2207_06667_b200 import formats
+    from paper_2207_06667_b200.nnkit import TrainConfig
+    from paper_2207_06667_b200.reader import SchedulerConfig, TeacherPool
+    from paper_2207_06667_b200.student import DataSpec, StudentConfig, StudentNode, spawn_teachers
+    from paper_2207_06667_b200.teacher import TeacherConfig, TeacherWorker
+    spec = DataSpec(seed=1, n=512, dim=8, classes=6, spread=1.0)
+    teacher = formats.init_model((8, 32, 6), 11)
+    train = TrainConfig(eta=0.05, alpha=0.5, beta=0.5, temperature=2.0, batch_size=16, seed=2)
+    cfg = StudentConfig(mode="edl", data=spec, train=train, epochs=2, k=4, teacher_count=2,
+                        sched=SchedulerConfig(lt=2, ut=6, probe_interval=0.0, acquire_cooldown=0.0))
+    pool = TeacherPool()
+    node = StudentNode(cfg, pool=pool)
+    dev = str(node.dataset.device)
+    workers = spawn_teachers(pool, teacher, 3, {dev: node.dataset}, 2.0, 4)
+    events = []
+
+    def hook(it, reader):
+        for kind, at, name in faults:
+            if it == at and kind == "kill":
+                pool.kill(name)
+                events.append(("kill", name))
+            if it == at and kind == "add":
+                w = TeacherWorker(TeacherConfig(name, 2.0, 4), workers[0].model, node.dataset)
+                pool.register(w)
+                events.append(("add", name))
+    return node.run(on_iteration=hook), node, events
+
+
+def test_drop_and_readd_teachers_mid_run_keeps_trajectory():
+    """configs[4] fault test: teachers die with batches in flight and new ones
+    join mid-run; every batch is trained exactly once and the trajectory is
+    bit-identical to the fault-free run (soft labels are deterministic)."""
+    from oracle import nnkit_ref as ref
+    clean, _, _ = _edl_run([])
+    faulty, node, ev = _edl_run([("kill", 5, "t1"), ("kill", 9, "t2"), ("add", 12, "t9"), ("kill", 20, "t3")])
+    assert clean.ledger["ok"] and faulty.ledger["ok"]
+    assert faulty.ledger["consumed"] == clean.ledger["consumed"] == node.total_steps
+    kinds = [e["event"] for e in node.events.entries]
+    assert kinds.count("teacher_failure") >= 2 and "teacher_replaced" in kinds
+    a = ref.flatten(clean.model.weights, clean.model.biases)
+    b = ref.flatten(faulty.model.weights, faulty.model.biases)
+    assert np.array_equal(a, b)
