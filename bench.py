@@ -207,6 +207,9 @@ def main():
                     help="colocated: teacher worker + student on every GPU; split: teacher GPUs feed "
                          "student GPUs over NVLink (EDL-Dist teacher pool)")
     ap.add_argument("--teachers", type=int, default=0, help="teacher GPUs for --placement split")
+    ap.add_argument("--teacher-sm-reserve", type=int, default=-1,
+                    help="SMs the co-located teacher stream leaves free for the student's NCCL "
+                         "all-reduce (-1: 32 when N > 1, else 0)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.batch:
@@ -264,7 +267,10 @@ def main():
     student = Model.from_host(student_h, dev)
     engine = StudentStep(student, tcfg, B, world, max_steps=W + K + 8)
     pool = TeacherPool()
-    worker = TeacherWorker(TeacherConfig("t1", cfg["T"], cfg["topk"]), teacher, ddata)
+    # N=4 sweep on B200 (profiles/README.md): reserve 0/8/16/24/32 SMs ->
+    # EDL 13.5/14.2/14.0/14.3/14.6 M samples/s vs online 13.8-14.5 M
+    reserve = args.teacher_sm_reserve if args.teacher_sm_reserve >= 0 else (32 if world > 1 else 0)
+    worker = TeacherWorker(TeacherConfig("t1", cfg["T"], cfg["topk"]), teacher, ddata, sm_reserve=reserve)
     pool.register(worker)
     sched = SchedulerConfig(lt=2, ut=8, pipeline_depth=2, acquire_cooldown=1e9)
 

@@ -41,6 +41,12 @@ int edl_version(void);
 const char* edl_last_error(void);
 int edl_device_sms(void);
 
+/* Cap the persistent tensor-core kernels launched on `stream` at `max_ctas`
+ * CTAs (<= 0 removes the cap). A co-located teacher stream capped below the
+ * SM count leaves SMs for the student's NCCL all-reduce, which would
+ * otherwise queue behind teacher GEMMs that hold every SM. */
+int edl_set_stream_max_ctas(void* stream, int max_ctas);
+
 /* One dense layer of edl.nnkit.forward (edl/nnkit.py:223-234, `z = h @ w.T + b`
  * at :232, tanh at :233). X: bf16 [M][ldx] (K used), W: bf16 [N][ldw], bias:
  * fp32 [N]. act=EDL_ACT_TANH writes bf16 Y [M][ldy]; EDL_ACT_NONE writes fp32.

@@ -25,6 +25,7 @@ _SIGNATURES = {
     "edl_version": [],
     "edl_last_error": [],
     "edl_device_sms": [],
+    "edl_set_stream_max_ctas": [c_void_p, c_int],
     "edl_linear_fwd": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_void_p, c_ll, c_int, c_int,
                        c_int, c_int, c_void_p],
     "edl_linear_bwd_data": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_ll,

@@ -132,6 +132,20 @@ cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 std::mutex g_sched_mu;
 std::unordered_map<std::string, unsigned*> g_sched;
 
+// Per-stream cap on the persistent GEMM grid (edl_set_stream_max_ctas): a
+// teacher stream capped below the SM count leaves SMs free, so the student's
+// NCCL all-reduce kernels are not blocked behind teacher CTAs that hold
+// every SM for a whole (hundreds of microseconds) GEMM.
+std::mutex g_cap_mu;
+std::unordered_map<cudaStream_t, int> g_cap;
+
+int grid_cap(cudaStream_t s) {
+  const int n = num_sms();
+  std::lock_guard<std::mutex> g(g_cap_mu);
+  auto it = g_cap.find(s);
+  return (it == g_cap.end() || it->second <= 0 || it->second > n) ? n : it->second;
+}
+
 unsigned* stream_sched(cudaStream_t s) {
   static const bool disabled = [] {
     const char* v = getenv("EDL_STATIC_SCHED");
@@ -162,6 +176,13 @@ const char* edl_last_error(void) { return g_err.c_str(); }
 
 int edl_device_sms(void) { return num_sms(); }
 
+int edl_set_stream_max_ctas(void* stream, int max_ctas) {
+  std::lock_guard<std::mutex> g(g_cap_mu);
+  if (max_ctas <= 0) g_cap.erase(as_stream(stream));
+  else g_cap[as_stream(stream)] = max_ctas;
+  return 0;
+}
+
 int edl_linear_fwd(const void* X, long long ldx, const void* W, long long ldw, const float* bias,
                    void* Y, long long ldy, int M, int N, int K, int act, void* stream) {
   if (M < 1 || N < 1 || K < 1 || ldx < K || ldw < K || ldy < N)
@@ -174,7 +195,7 @@ int edl_linear_fwd(const void* X, long long ldx, const void* W, long long ldw, c
   if ((rc = tensor_map(W, N, K, ldw, 64, bn, &tb))) return rc;
   EpiArgs ep{Y, ldy, bias, nullptr, 0, 1.0f, stream_sched(as_stream(stream))};
   cudaError_t e = launch_gemm(act == EDL_ACT_TANH ? GemmKind::FwdTanh : GemmKind::FwdLinear, bn, ta,
-                              tb, M, N, K, ep, num_sms(), as_stream(stream));
+                              tb, M, N, K, ep, grid_cap(as_stream(stream)), as_stream(stream));
   return e == cudaSuccess ? 0 : cuda_fail(e, "linear_fwd");
 }
 
@@ -191,7 +212,8 @@ int edl_linear_bwd_data(const void* dY, long long lddy, const void* W, long long
   if ((rc = tensor_map(W, N, K, ldw, 64, 64, &tb))) return rc;
   EpiArgs ep{dX, lddx, nullptr, reinterpret_cast<const __nv_bfloat16*>(H), ldh, 1.0f,
              stream_sched(as_stream(stream))};
-  cudaError_t e = launch_gemm(GemmKind::BwdData, bn, ta, tb, M, K, N, ep, num_sms(), as_stream(stream));
+  cudaError_t e = launch_gemm(GemmKind::BwdData, bn, ta, tb, M, K, N, ep, grid_cap(as_stream(stream)),
+                              as_stream(stream));
   return e == cudaSuccess ? 0 : cuda_fail(e, "linear_bwd_data");
 }
 
@@ -207,7 +229,8 @@ int edl_linear_bwd_weight(const void* dY, long long lddy, const void* X, long lo
   if ((rc = tensor_map(dY, M, N, lddy, 64, 64, &ta))) return rc;
   if ((rc = tensor_map(X, M, K, ldx, 64, 64, &tb))) return rc;
   EpiArgs ep{dW, lddw, nullptr, nullptr, 0, scale, stream_sched(as_stream(stream))};
-  cudaError_t e = launch_gemm(GemmKind::BwdWeight, bn, ta, tb, N, K, M, ep, num_sms(), as_stream(stream));
+  cudaError_t e = launch_gemm(GemmKind::BwdWeight, bn, ta, tb, N, K, M, ep, grid_cap(as_stream(stream)),
+                              as_stream(stream));
   if (e != cudaSuccess) return cuda_fail(e, "linear_bwd_weight");
   if (db) {
     if (!workspace) return fail(EDL_ERR_SHAPE, "linear_bwd_weight: db needs a workspace");
@@ -245,7 +268,7 @@ int edl_linear_bwd_weight_grouped(int count, const void* const* dY, const long l
     tiles += ((N[p] + 127) / 128) * ((K[p] + bn - 1) / bn);
   }
   ga.tile_start[count] = tiles;
-  cudaError_t e = launch_gemm_grouped_bwd_weight(maps, ga, num_sms(), as_stream(stream));
+  cudaError_t e = launch_gemm_grouped_bwd_weight(maps, ga, grid_cap(as_stream(stream)), as_stream(stream));
   if (e != cudaSuccess) return cuda_fail(e, "linear_bwd_weight_grouped");
   if (db) {
     ColsumGroup g = {};

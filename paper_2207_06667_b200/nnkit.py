@@ -464,6 +464,31 @@ def evaluate(model: Model, samples, labels, k: int = 1, batch: int = 4096) -> fl
 
 
 # ---------------------------------------------------------------------------
+# Model files (edl/nnkit.py:480-487): EDLD v1 in, device model out (fp64 ->
+# fp32 master + bf16 copy, dims padded); device model in, EDLD out (fp32
+# master widened to f64) — the reference's pretrained teachers and
+# checkpoints load unchanged.
+
+
+def load_model(path: str, device=None) -> tuple[Model, int]:
+    from .formats import deserialize_model
+    with open(path, "rb") as fh:
+        host, iteration = deserialize_model(fh.read())
+    return Model.from_host(host, device), iteration
+
+
+def save_model(path: str, model: Model, iteration: int = 0) -> None:
+    import os
+
+    from .formats import serialize_model
+    blob = serialize_model(model.to_host(), iteration)
+    tmp = f"{path}.tmp.{os.getpid()}"
+    with open(tmp, "wb") as fh:
+        fh.write(blob)
+    os.replace(tmp, path)
+
+
+# ---------------------------------------------------------------------------
 # Parameter flattening (edl/nnkit.py:342-364) — host views in reference order
 
 

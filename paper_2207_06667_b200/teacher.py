@@ -78,7 +78,9 @@ def soft_label_reply(model: Model, temperature: float, request: dict, k: int | N
 class TeacherWorker:
     """One teacher (model replica) bound to a device and a CUDA stream."""
 
-    def __init__(self, cfg: TeacherConfig, model: Model, data: DeviceDataset):
+    def __init__(self, cfg: TeacherConfig, model: Model, data: DeviceDataset, sm_reserve: int = 0):
+        """sm_reserve > 0 caps this worker's persistent GEMMs at (SMs - reserve)
+        CTAs, leaving SMs for the co-located student's NCCL collectives."""
         if model.device != data.device:
             raise ValueError("teacher model and its dataset replica must share a device")
         self.cfg = cfg
@@ -87,6 +89,11 @@ class TeacherWorker:
         self.data = data
         self.device = model.device
         self.stream = torch.cuda.Stream(device=self.device)
+        if sm_reserve > 0:
+            from . import _lib
+            with torch.cuda.device(self.device):
+                sms = _lib.load().edl_device_sms()
+            _lib.call("edl_set_stream_max_ctas", self.stream.cuda_stream, max(1, sms - sm_reserve))
         self.alive = True
         self.batches_served = 0
         self._batch: Batch | None = None

@@ -161,6 +161,30 @@ def test_cfg1_distillation_trajectory_and_accuracy(nk):
     assert abs(acc - float(d["holdout_top1_student"])) <= 0.02
 
 
+def test_edld_teacher_ingest_and_checkpoint_write_back(nk, tmp_path):
+    """A reference-written EDLD teacher (the cfg1 pretrained teacher, golden)
+    loads onto the device (f64 -> fp32 master + bf16) and serves the same soft
+    labels; a device model written back is a valid EDLD file whose f64 params
+    are the fp32 masters exactly."""
+    from paper_2207_06667_b200 import formats
+    d = g("cfg1")
+    host = host_model(d["teacher"], (16, 256, 256, 10))
+    p = tmp_path / "teacher.edld"
+    p.write_bytes(formats.serialize_model(host, 7))
+    dev, it = nk.load_model(str(p))
+    assert it == 7 and dev.layer_dims == (16, 256, 256, 10)
+    np.testing.assert_array_equal(nk.flatten_params(dev), d["teacher"].astype(np.float32).astype(np.float64))
+    x = nk.make_batch(d["b0_x"], d["b0_y"]).inputs
+    direct = nk.teacher_soft_labels(nk.Model.from_host(host), x, 2.0, 4)
+    loaded = nk.teacher_soft_labels(dev, x, 2.0, 4)
+    assert torch.equal(direct.probs, loaded.probs) and torch.equal(direct.classes, loaded.classes)
+    q = tmp_path / "ckpt.edld"
+    nk.save_model(str(q), dev, 123)
+    back, it2 = formats.deserialize_model(q.read_bytes())
+    assert it2 == 123
+    np.testing.assert_array_equal(ref.flatten(list(back.weights), list(back.biases)), nk.flatten_params(dev))
+
+
 def test_error_mapping(nk):
     model = nk.Model((8, 16, 4))
     batch = nk.make_batch(np.zeros((3, 8)), np.array([0, 1, 9]))
