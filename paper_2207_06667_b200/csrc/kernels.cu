@@ -298,12 +298,15 @@ cudaError_t launch_gather_rows(const __nv_bfloat16* src, long long ld_src, const
 
 // ------------------------------------------------------------------ column sum
 // db_l = scale * sum over the batch of delta_l, for up to kMaxGroup layers in
-// ONE pair of launches. Pass 1: a block owns 256 rows x 256 columns of one
-// layer; a lane reads 16 bytes (8 bf16 columns) per row with 8 rows in flight,
-// the 8 warps combine in a fixed order -> partial[row chunk][n]. Pass 2: row
-// chunks summed in order. Deterministic, no atomics.
-constexpr int kColRows = 256;
+// ONE pair of launches. Pass 1: a block owns 64 rows x 256 columns of one
+// layer; each warp issues its 8 rows' 16-byte loads (8 bf16 columns per lane)
+// at once, the 8 warps combine in a fixed order -> partial[row chunk][n].
+// Pass 2: row chunks summed in order. Deterministic, no atomics. (256-row
+// chunks ran at 19% of HBM bandwidth: too few blocks, 4 dependent load rounds
+// per warp — profiles/README.md.)
+constexpr int kColRows = 64;
 constexpr int kColCols = 256;
+constexpr int kColRowsPerWarp = kColRows / 8;
 
 __global__ void __launch_bounds__(256) colsum_partial_kernel(ColsumGroup g) {
   griddep_wait();
@@ -315,26 +318,23 @@ __global__ void __launch_bounds__(256) colsum_partial_kernel(ColsumGroup g) {
   const int cg = local % cgs, rc = local / cgs;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int n0 = cg * kColCols + lane * 8;
-  const int r0 = rc * kColRows + warp * 32;
+  const int r0 = rc * kColRows + warp * kColRowsPerWarp;
   const int M = g.M[p], N = g.N[p];
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (n0 < N) {
     const __nv_bfloat16* base = g.x[p] + n0;
+    uint4 q[kColRowsPerWarp];
 #pragma unroll
-    for (int rr = 0; rr < 32; rr += 8) {
-      uint4 q[8];
+    for (int u = 0; u < kColRowsPerWarp; ++u) {
+      const int r = r0 + u;
+      q[u] = r < M ? __ldg(reinterpret_cast<const uint4*>(base + static_cast<size_t>(r) * g.ld[p]))
+                   : make_uint4(0u, 0u, 0u, 0u);
+    }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int r = r0 + rr + u;
-        q[u] = r < M ? __ldg(reinterpret_cast<const uint4*>(base + static_cast<size_t>(r) * g.ld[p]))
-                     : make_uint4(0u, 0u, 0u, 0u);
-      }
+    for (int u = 0; u < kColRowsPerWarp; ++u) {
+      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&q[u]);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&q[u]);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(h[j]);
-      }
+      for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(h[j]);
     }
   }
 #pragma unroll

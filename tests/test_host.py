@@ -133,8 +133,8 @@ def test_library_exports_every_header_symbol():
     assert sorted(_lib.exported_symbols()) == syms
     L = _lib.load()
     assert L.edl_version() == _lib.ABI_VERSION
-    assert L.edl_colsum_workspace_floats(4096, 2048) == 16 * 2048
-    assert _lib.colsum_group_workspace_floats([4096, 4096], [2048, 1008]) == 16 * (2048 + 1008)
+    assert L.edl_colsum_workspace_floats(4096, 2048) == 64 * 2048          # 64-row chunks
+    assert _lib.colsum_group_workspace_floats([4096, 4096], [2048, 1008]) == 64 * (2048 + 1008)
 
 
 def test_product_path_never_imports_oracle():
