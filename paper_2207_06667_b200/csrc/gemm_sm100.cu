@@ -430,18 +430,38 @@ __global__ void __launch_bounds__(kThreads, 1)
 // bitonic-sorted and its best KMAX kept; later chunks only insert the rare
 // columns that beat the current k-th entry; partial lists (the two warp halves,
 // then the cluster ranks) are combined with a bitonic merge-split + clean.
+// Everything below is written branch-free (non-short-circuit predicates +
+// selects): lanes of a warp hold different rows, so a data-dependent branch
+// per compare-exchange diverges and serialises both paths (the first version
+// compiled to 262 reconvergence blocks and ran the epilogue ~3x slower).
 struct Key {
   __device__ __forceinline__ static bool better(float a, int ia, float b, int ib) {
-    return a > b || (a == b && ia < ib);
+    return (a > b) | ((a == b) & (ia < ib));
   }
 };
 
-// compare-exchange so that slot j holds the better entry
+__device__ __forceinline__ float sel(bool p, float a, float b) {
+  float r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\tselp.f32 %0, %1, %2, q;\n\t}"
+      : "=f"(r) : "f"(a), "f"(b), "r"(static_cast<int>(p)));
+  return r;
+}
+__device__ __forceinline__ int sel(bool p, int a, int b) {
+  int r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\tselp.b32 %0, %1, %2, q;\n\t}"
+      : "=r"(r) : "r"(a), "r"(b), "r"(static_cast<int>(p)));
+  return r;
+}
+
+// compare-exchange so that slot a holds the better entry
 __device__ __forceinline__ void cex(float& va, int& ia, float& vb, int& ib) {
-  if (Key::better(vb, ib, va, ia)) {
-    const float tv = va; va = vb; vb = tv;
-    const int ti = ia; ia = ib; ib = ti;
-  }
+  const bool s = Key::better(vb, ib, va, ia);
+  const float x = va, y = vb;
+  const int p = ia, q = ib;
+  va = sel(s, y, x);
+  vb = sel(s, x, y);
+  ia = sel(s, q, p);
+  ib = sel(s, p, q);
 }
 
 // bitonic sort of N entries, descending by Key
@@ -490,23 +510,26 @@ struct TopK {
     for (int j = 0; j < KMAX; ++j) {
       const float bv = ov[KMAX - 1 - j];
       const int bi = oi[KMAX - 1 - j];
-      if (Key::better(bv, bi, v[j], i[j])) { v[j] = bv; i[j] = bi; }
+      const bool s = Key::better(bv, bi, v[j], i[j]);
+      v[j] = sel(s, bv, v[j]);
+      i[j] = sel(s, bi, i[j]);
     }
     bitonic_clean<KMAX>(v, i);
   }
-  // insert one candidate that beats the current last entry
+  // insert one candidate that beats the current last entry (branch-free shift)
   __device__ __forceinline__ void insert(float x, int ix) {
     bool b[KMAX];
 #pragma unroll
     for (int j = 0; j < KMAX; ++j) b[j] = Key::better(v[j], i[j], x, ix);
 #pragma unroll
     for (int j = KMAX - 1; j > 0; --j) {
-      if (!b[j]) {
-        v[j] = b[j - 1] ? x : v[j - 1];
-        i[j] = b[j - 1] ? ix : i[j - 1];
-      }
+      const float nv = sel(b[j - 1], x, v[j - 1]);
+      const int ni = sel(b[j - 1], ix, i[j - 1]);
+      v[j] = sel(b[j], v[j], nv);
+      i[j] = sel(b[j], i[j], ni);
     }
-    if (!b[0]) { v[0] = x; i[0] = ix; }
+    v[0] = sel(b[0], v[0], x);
+    i[0] = sel(b[0], i[0], ix);
   }
 };
 

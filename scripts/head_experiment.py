@@ -11,7 +11,8 @@ def t(fn, it=10):
     for _ in range(it): fn()
     e.record(); torch.cuda.synchronize()
     return s.elapsed_time(e) / it * 1000
-CASES = [(4096, 1000, 8192, 16), (4096, 256, 8192, 16), (4096, 1000, 1024, 16), (4096, 1000, 8192, 4), (1024, 1000, 8192, 16)]
+CASES = [(4096, 1000, 8192, 16), (4096, 256, 8192, 16), (4096, 1000, 1024, 16), (4096, 1000, 8192, 4),
+         (1024, 1000, 8192, 16), (4096, 1000, 64, 16), (4096, 1000, 64, 4), (4096, 256, 64, 16)]
 if len(sys.argv) > 1: CASES = [CASES[int(sys.argv[1])]]
 for (M, N, K, k) in CASES:
     Np = (N + 15) // 16 * 16
