@@ -81,6 +81,17 @@ int edl_linear_bwd_weight_grouped(int count, const void* const* dY, const long l
                                   const int* M, const int* N, const int* K, float scale, void* stream);
 long long edl_colsum_group_workspace_floats(int count, const int* M, const int* N);
 
+/* Single-student step fusion of the above with sgd_step (edl/nnkit.py:320-321):
+ *   W[p] -= eta * dY[p]^T @ X[p];  b[p] -= eta * colsum(dY[p])
+ * on the fp32 masters in place, refreshing the bf16 copies W_bf16 / b_bf16
+ * (b_bf16 may be NULL). The gradients never reach HBM. Only valid when no
+ * gradient all-reduce sits between backward and update (world_size 1). */
+int edl_linear_bwd_weight_grouped_sgd(int count, const void* const* dY, const long long* lddy,
+                                      const void* const* X, const long long* ldx, float* const* W,
+                                      void* const* W_bf16, const long long* ldw, float* const* b,
+                                      void* const* b_bf16, float* workspace, const int* M, const int* N,
+                                      const int* K, float eta, void* stream);
+
 /* Teacher head = soft_label_reply's math (edl/teacher_node.py:54:
  * tempered_softmax(forward(model, inputs), T), edl/nnkit.py:193-208,232) fused
  * with the top-k soft-label extraction EDL-Dist ships to students:

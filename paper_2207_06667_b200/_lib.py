@@ -34,6 +34,9 @@ _SIGNATURES = {
                               c_void_p, c_int, c_int, c_int, c_float, c_void_p],
     "edl_linear_bwd_weight_grouped": [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                       c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_float, c_void_p],
+    "edl_linear_bwd_weight_grouped_sgd": [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                          c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                          c_float, c_void_p],
     "edl_colsum_workspace_floats": [c_int, c_int],
     "edl_colsum_group_workspace_floats": [c_int, c_void_p, c_void_p],
     "edl_teacher_head_softmax_topk": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_int, c_int,
@@ -101,7 +104,8 @@ def check(rc: int, what: str) -> None:
 
 
 # kernel launches per C entry point (bench.py reports launches in its timed region)
-_LAUNCHES = {"edl_linear_bwd_weight": 3}   # GEMM + two column-sum passes when db is requested
+_LAUNCHES = {"edl_linear_bwd_weight": 3,   # GEMM + two column-sum passes when db is requested
+             "edl_kd_loss_fwd_bwd": 2}     # row pass + deterministic batch-mean pass
 launch_count = 0
 
 
@@ -124,6 +128,22 @@ def bwd_weight_grouped(dys, xs, dws, dbs, workspace, Ms, Ns, Ks, scale, stream) 
             workspace.data_ptr(), I(*Ms), I(*Ns), I(*Ks), scale, stream)
     check(load().edl_linear_bwd_weight_grouped(*args), "edl_linear_bwd_weight_grouped")
     launch_count += 3   # grouped GEMM + one column-sum launch pair for all layers
+
+
+def bwd_weight_grouped_sgd(dys, xs, ws32, ws16, bs32, bs16, workspace, Ms, Ns, Ks, eta, stream) -> None:
+    """edl_linear_bwd_weight_grouped_sgd: fused dW/db + SGD on fp32 masters."""
+    global launch_count
+    n = len(dys)
+    P = c_void_p * n
+    L = c_ll * n
+    I = c_int * n
+    args = (n, P(*[t.data_ptr() for t in dys]), L(*[t.stride(0) for t in dys]),
+            P(*[t.data_ptr() for t in xs]), L(*[t.stride(0) for t in xs]),
+            P(*[t.data_ptr() for t in ws32]), P(*[t.data_ptr() for t in ws16]), L(*Ks),
+            P(*[t.data_ptr() for t in bs32]), P(*[t.data_ptr() for t in bs16]),
+            workspace.data_ptr(), I(*Ms), I(*Ns), I(*Ks), eta, stream)
+    check(load().edl_linear_bwd_weight_grouped_sgd(*args), "edl_linear_bwd_weight_grouped_sgd")
+    launch_count += 3
 
 
 def colsum_group_workspace_floats(Ms, Ns) -> int:

@@ -241,10 +241,17 @@ int edl_linear_bwd_weight(const void* dY, long long lddy, const void* X, long lo
   return 0;
 }
 
-int edl_linear_bwd_weight_grouped(int count, const void* const* dY, const long long* lddy,
-                                  const void* const* X, const long long* ldx, float* const* dW,
-                                  const long long* lddw, float* const* db, float* workspace,
-                                  const int* M, const int* N, const int* K, float scale, void* stream) {
+}  // extern "C"
+
+namespace {
+// dW_p = scale * dY_p^T X_p (+ db_p = scale * colsum dY_p) for every p, or with
+// `sgd` the fused update W_p -= scale * dY_p^T X_p, b_p -= scale * colsum dY_p
+// (bf16 copies W16 / b16 refreshed) where the gradients never reach HBM.
+int bwd_weight_grouped_impl(int count, const void* const* dY, const long long* lddy,
+                            const void* const* X, const long long* ldx, float* const* dW,
+                            const long long* lddw, float* const* db, void* const* W16,
+                            void* const* b16, float* workspace, const int* M, const int* N,
+                            const int* K, float scale, void* stream, bool sgd) {
   if (count < 1 || count > kMaxGroup)
     return fail(EDL_ERR_SHAPE, "linear_bwd_weight_grouped: count=%d (1..%d)", count, kMaxGroup);
   GroupMaps maps;
@@ -263,12 +270,14 @@ int edl_linear_bwd_weight_grouped(int count, const void* const* dY, const long l
     ga.M[p] = N[p];
     ga.N[p] = K[p];
     ga.K[p] = M[p];
-    ga.ep[p] = EpiArgs{dW[p], lddw[p], nullptr, nullptr, 0, scale};
+    ga.ep[p] = EpiArgs{dW[p], lddw[p], nullptr, nullptr, 0, scale, nullptr,
+                       sgd ? reinterpret_cast<__nv_bfloat16*>(W16[p]) : nullptr};
+    if (sgd && !W16[p]) return fail(EDL_ERR_SHAPE, "linear_bwd_weight_grouped_sgd[%d]: missing bf16 copy", p);
     ga.tile_start[p] = tiles;
     tiles += ((N[p] + 127) / 128) * ((K[p] + bn - 1) / bn);
   }
   ga.tile_start[count] = tiles;
-  cudaError_t e = launch_gemm_grouped_bwd_weight(maps, ga, grid_cap(as_stream(stream)), as_stream(stream));
+  cudaError_t e = launch_gemm_grouped_bwd_weight(maps, ga, grid_cap(as_stream(stream)), as_stream(stream), sgd);
   if (e != cudaSuccess) return cuda_fail(e, "linear_bwd_weight_grouped");
   if (db) {
     ColsumGroup g = {};
@@ -279,17 +288,39 @@ int edl_linear_bwd_weight_grouped(int count, const void* const* dY, const long l
       g.M[g.count] = M[p];
       g.N[g.count] = N[p];
       g.out[g.count] = db[p];
+      g.out_bf16[g.count] = (sgd && b16) ? reinterpret_cast<__nv_bfloat16*>(b16[p]) : nullptr;
       ++g.count;
     }
     if (g.count > 0) {
       if (!workspace) return fail(EDL_ERR_SHAPE, "linear_bwd_weight_grouped: db needs a workspace");
       g.scale = scale;
+      g.sgd = sgd ? 1 : 0;
       g.partial = workspace;
       e = launch_colsum_group(g, as_stream(stream));
       if (e != cudaSuccess) return cuda_fail(e, "colsum");
     }
   }
   return 0;
+}
+}  // namespace
+
+extern "C" {
+
+int edl_linear_bwd_weight_grouped(int count, const void* const* dY, const long long* lddy,
+                                  const void* const* X, const long long* ldx, float* const* dW,
+                                  const long long* lddw, float* const* db, float* workspace,
+                                  const int* M, const int* N, const int* K, float scale, void* stream) {
+  return bwd_weight_grouped_impl(count, dY, lddy, X, ldx, dW, lddw, db, nullptr, nullptr, workspace, M, N, K,
+                                 scale, stream, false);
+}
+
+int edl_linear_bwd_weight_grouped_sgd(int count, const void* const* dY, const long long* lddy,
+                                      const void* const* X, const long long* ldx, float* const* W,
+                                      void* const* W_bf16, const long long* ldw, float* const* b,
+                                      void* const* b_bf16, float* workspace, const int* M, const int* N,
+                                      const int* K, float eta, void* stream) {
+  return bwd_weight_grouped_impl(count, dY, lddy, X, ldx, W, ldw, b, W_bf16, b_bf16, workspace, M, N, K, eta,
+                                 stream, true);
 }
 
 long long edl_colsum_workspace_floats(int M, int N) { return colsum_workspace_floats(1, &M, &N); }

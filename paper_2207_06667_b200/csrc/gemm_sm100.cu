@@ -140,6 +140,41 @@ __device__ __forceinline__ void epilogue_store(const EpiArgs& ep, int row, int M
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] *= ep.scale;
   }
+  if constexpr (EPI == EPI_SGD_F32) {
+    // fused SGD (edl/nnkit.py:320): the fp32 master row slice is updated in
+    // place, p -= eta * dW, and its bf16 operand copy refreshed; the gradient
+    // itself never reaches HBM
+    float* o = reinterpret_cast<float*>(ep.out) + static_cast<size_t>(row) * ep.ld_out + col0;
+    __nv_bfloat16* ob = ep.out_bf16 + static_cast<size_t>(row) * ep.ld_out + col0;
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float4 p = reinterpret_cast<float4*>(o)[i];
+        p.x -= ep.scale * v[4 * i]; p.y -= ep.scale * v[4 * i + 1];
+        p.z -= ep.scale * v[4 * i + 2]; p.w -= ep.scale * v[4 * i + 3];
+        reinterpret_cast<float4*>(o)[i] = p;
+        v[4 * i] = p.x; v[4 * i + 1] = p.y; v[4 * i + 2] = p.z; v[4 * i + 3] = p.w;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint4 q;
+        q.x = pack_bf16x2(v[8 * i + 0], v[8 * i + 1]);
+        q.y = pack_bf16x2(v[8 * i + 2], v[8 * i + 3]);
+        q.z = pack_bf16x2(v[8 * i + 4], v[8 * i + 5]);
+        q.w = pack_bf16x2(v[8 * i + 6], v[8 * i + 7]);
+        reinterpret_cast<uint4*>(ob)[i] = q;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < N) {
+          const float p = o[i] - ep.scale * v[i];
+          o[i] = p;
+          ob[i] = __float2bfloat16_rn(p);
+        }
+    }
+    return;
+  }
   if constexpr (EPI == EPI_TANH_BF16 || EPI == EPI_DTANH_BF16) {
     __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(ep.out) + static_cast<size_t>(row) * ep.ld_out + col0;
     if (full) {
@@ -771,10 +806,11 @@ cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUte
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_gemm_grouped_bwd_weight(const GroupMaps& maps, const GroupArgs& ga, int num_sms,
-                                           cudaStream_t stream) {
+template <int EPI>
+static cudaError_t launch_grouped_t(const GroupMaps& maps, const GroupArgs& ga, int num_sms,
+                                    cudaStream_t stream) {
   constexpr int BN = 256;
-  auto kern = gemm_grouped_kernel<BN, true, true, EPI_F32>;
+  auto kern = gemm_grouped_kernel<BN, true, true, EPI>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -785,6 +821,12 @@ cudaError_t launch_gemm_grouped_bwd_weight(const GroupMaps& maps, const GroupArg
   const int tiles = ga.tile_start[ga.count];
   const int grid = tiles < num_sms ? tiles : num_sms;
   return launch_pdl(kern, dim3(grid), dim3(kThreads), GemmCfg<BN>::kSmem, stream, 1, maps, ga);
+}
+
+cudaError_t launch_gemm_grouped_bwd_weight(const GroupMaps& maps, const GroupArgs& ga, int num_sms,
+                                           cudaStream_t stream, bool fused_sgd) {
+  return fused_sgd ? launch_grouped_t<EPI_SGD_F32>(maps, ga, num_sms, stream)
+                   : launch_grouped_t<EPI_F32>(maps, ga, num_sms, stream);
 }
 
 int grouped_tile_bn() { return 256; }

@@ -41,6 +41,7 @@ enum EpiMode : int {
   EPI_BIAS_F32 = 1,    // out(f32)  = acc + bias
   EPI_DTANH_BF16 = 2,  // out(bf16) = acc * (1 - aux^2)
   EPI_F32 = 3,         // out(f32)  = acc * scale
+  EPI_SGD_F32 = 4,     // out(f32) -= scale * acc in place; out_bf16 = bf16(out)
 };
 
 struct EpiArgs {
@@ -51,6 +52,7 @@ struct EpiArgs {
   long long ld_aux;
   float scale;
   unsigned* sched = nullptr;  // per-stream {next tile, CTAs done}; null -> static schedule
+  __nv_bfloat16* out_bf16 = nullptr;  // EPI_SGD_F32: bf16 copy of `out` (same ld)
 };
 
 struct HeadArgs {
@@ -75,7 +77,7 @@ struct GroupArgs {
   EpiArgs ep[kMaxGroup];
 };
 cudaError_t launch_gemm_grouped_bwd_weight(const GroupMaps& maps, const GroupArgs& ga, int num_sms,
-                                           cudaStream_t stream);
+                                           cudaStream_t stream, bool fused_sgd = false);
 int grouped_tile_bn();
 
 cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
@@ -105,7 +107,9 @@ struct ColsumGroup {
   long long ld[kMaxGroup];
   int M[kMaxGroup], N[kMaxGroup];
   float* out[kMaxGroup];
+  __nv_bfloat16* out_bf16[kMaxGroup];  // sgd: bf16 copies of the updated biases
   float scale;
+  int sgd;                             // 0: out = scale * colsum; 1: out -= scale * colsum
   float* partial;
   long long part_off[kMaxGroup];
   int blk_start[kMaxGroup + 1];

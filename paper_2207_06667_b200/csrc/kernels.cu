@@ -41,7 +41,7 @@ __device__ __forceinline__ void set_status(int* status, int code) {
 constexpr int kKdWarps = 8;
 
 template <int KPL>
-__global__ void __launch_bounds__(kKdWarps * 32)
+__global__ void __launch_bounds__(kKdWarps * 32, (KPL >= 64) ? 1 : 3)
     kd_loss_kernel(const float* __restrict__ z, long long ld_z, const int64_t* __restrict__ labels,
                    const float* __restrict__ qv, const int* __restrict__ qi, int B, int K,
                    int Kw, int k, float alpha, float beta, float T, float* __restrict__ row_loss,
@@ -129,18 +129,19 @@ __global__ void __launch_bounds__(kKdWarps * 32)
     }
     __syncwarp();
   }
+}
 
-  // Deterministic batch mean: the last block to finish sums row losses in a
-  // fixed order (independent of the grid), so every rank computes the same bits.
-  __shared__ bool is_last;
-  __shared__ double red[kKdWarps * 32];
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) is_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!is_last) return;
+// Deterministic batch mean of the row losses (fixed association order,
+// independent of any grid), a separate tiny launch: a last-block ticket inside
+// kd_loss_kernel needed a gpu-scope fence (membar + L1 invalidate) in every
+// block, which cost more than this PDL-overlapped launch.
+__global__ void __launch_bounds__(256) loss_mean_kernel(const float* __restrict__ row_loss, int B,
+                                                         float* __restrict__ loss_out,
+                                                         int* __restrict__ status) {
+  griddep_wait();
+  __shared__ double red[256];
   // 8 independent loads in flight per thread (a dependent strided loop would
-  // serialise on L2 latency); fixed association order -> deterministic
+  // serialise on L2 latency)
   double acc = 0.0;
   for (int r0 = threadIdx.x; r0 < B; r0 += 8 * blockDim.x) {
     float f[8];
@@ -162,7 +163,6 @@ __global__ void __launch_bounds__(kKdWarps * 32)
     const float loss = static_cast<float>(red[0] / static_cast<double>(B));
     *loss_out = loss;
     if (!isfinite(loss)) set_status(status, -2);
-    *ticket = 0u;
   }
 }
 
@@ -182,8 +182,12 @@ static cudaError_t launch_kd_t(const float* logits, long long ld_z, const int64_
   set = true;
   int blocks = (B + kKdWarps - 1) / kKdWarps;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  return launch_pdl(kd_loss_kernel<KPL>, dim3(blocks), dim3(kKdWarps * 32), smem, stream, 1, logits, ld_z, labels,
-                    q_vals, q_idx, B, K, Kw, k, alpha, beta, T, row_loss, loss_out, ticket, dlogits, ld_dz, status);
+  cudaError_t e = launch_pdl(kd_loss_kernel<KPL>, dim3(blocks), dim3(kKdWarps * 32), smem, stream, 1, logits, ld_z,
+                             labels, q_vals, q_idx, B, K, Kw, k, alpha, beta, T, row_loss, loss_out, ticket,
+                             dlogits, ld_dz, status);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(loss_mean_kernel, dim3(1), dim3(256), 0, stream, 1, static_cast<const float*>(row_loss), B,
+                    loss_out, status);
 }
 
 cudaError_t launch_kd_loss(const float* logits, long long ld_z, const int64_t* labels,
@@ -359,7 +363,13 @@ __global__ void colsum_final_kernel(ColsumGroup g) {
   const float* part = g.partial + g.part_off[p];
   float s = 0.f;
   for (int c = 0; c < chunks; ++c) s += part[static_cast<long long>(c) * g.N[p] + t];
-  g.out[p][t] = s * g.scale;
+  if (g.sgd) {   // fused SGD on the bias (edl/nnkit.py:321): b -= eta * db
+    const float b = g.out[p][t] - g.scale * s;
+    g.out[p][t] = b;
+    if (g.out_bf16[p]) g.out_bf16[p][t] = __float2bfloat16_rn(b);
+  } else {
+    g.out[p][t] = s * g.scale;
+  }
 }
 
 long long colsum_workspace_floats(int count, const int* M, const int* N) {

@@ -379,7 +379,8 @@ def teacher_soft_labels(model: Model, inputs, temperature: float, k: int, out: S
 
 def kd_loss(model: Model, batch: Batch, soft: SoftLabels | None, cfg: TrainConfig,
             stream=None, ws: Workspace | None = None,
-            loss_slot: torch.Tensor | None = None) -> tuple[DeviceLoss, Gradients]:
+            loss_slot: torch.Tensor | None = None,
+            fused_sgd_eta: float | None = None) -> tuple[DeviceLoss, Gradients | None]:
     """Combined distillation loss and analytic gradients (edl/nnkit.py:254-309):
     forward GEMMs -> fused loss/dlogits kernel -> backward GEMMs."""
     if cfg.beta > 0:
@@ -407,13 +408,18 @@ def kd_loss(model: Model, batch: Batch, soft: SoftLabels | None, cfg: TrainConfi
               _ptr(q_vals), _ptr(q_idx), B, model.num_classes, k, float(cfg.alpha), float(cfg.beta),
               float(cfg.temperature), ws.row_loss.data_ptr(), loss.data_ptr(), ws.ticket.data_ptr(),
               dz.data_ptr(), dz.stride(0), ws.status.data_ptr(), s)
-    backward_into(model, x, ws, stream)
-    return DeviceLoss(loss, ws.status), ws.grads
+    backward_into(model, x, ws, stream, sgd_eta=fused_sgd_eta)
+    # fused_sgd_eta: the model was already updated (kd_loss + sgd_step in one
+    # pass, single student); there is no gradient to return
+    return DeviceLoss(loss, ws.status), (None if fused_sgd_eta is not None else ws.grads)
 
 
-def backward_into(model: Model, x: torch.Tensor, ws: Workspace, stream=None) -> None:
+def backward_into(model: Model, x: torch.Tensor, ws: Workspace, stream=None,
+                  sgd_eta: float | None = None) -> None:
     """dW_l = delta^T a_l, db_l = colsum(delta), delta <- (delta W_l)(1 - a_l^2)
-    (edl/nnkit.py:303-308), from ws.deltas[L] = dlogits."""
+    (edl/nnkit.py:303-308), from ws.deltas[L] = dlogits. With `sgd_eta` the
+    update p -= eta * g (edl/nnkit.py:312-322) is fused into the dW / db
+    kernels and no gradient is materialised (single-student step)."""
     L = model.layout
     B = x.shape[0]
     s = _stream(stream)
@@ -430,6 +436,14 @@ def backward_into(model: Model, x: torch.Tensor, ws: Workspace, stream=None) -> 
     layers = list(range(L.layers - 1, -1, -1))
     for c in range(0, len(layers), 4):
         part = layers[c:c + 4]
+        if sgd_eta is not None:
+            _lib.bwd_weight_grouped_sgd(
+                [ws.deltas[l + 1] for l in part], [x if l == 0 else ws.acts[l] for l in part],
+                [model.w(l) for l in part], [model.w_bf16(l) for l in part], [model.b(l) for l in part],
+                [model.flat_bf16[L.b_off[l]:L.b_off[l] + L.dims_p[l + 1]] for l in part], ws.colsum,
+                [B] * len(part), [L.dims_p[l + 1] for l in part], [L.dims_p[l] for l in part],
+                float(sgd_eta), s)
+            continue
         _lib.bwd_weight_grouped(
             [ws.deltas[l + 1] for l in part], [x if l == 0 else ws.acts[l] for l in part],
             [g[L.w_off[l]:L.w_off[l] + L.dims_p[l + 1] * L.dims_p[l]] for l in part],

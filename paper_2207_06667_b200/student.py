@@ -148,10 +148,11 @@ class StudentStep:
     step on the current stream and never allocates or synchronises."""
 
     def __init__(self, model: Model, cfg: TrainConfig, batch_size: int, world_size: int = 1,
-                 process_group=None, max_steps: int = 1 << 16):
+                 process_group=None, max_steps: int = 1 << 16, fuse_sgd: bool = True):
         self.model = model
         self.cfg = cfg
         self.world_size = world_size
+        self.fuse_sgd = fuse_sgd
         self.group = process_group
         self.ws = Workspace(model, batch_size)
         self.batch = Batch(torch.empty(batch_size, nnkit.pad(model.input_dim), dtype=torch.bfloat16,
@@ -162,10 +163,15 @@ class StudentStep:
 
     def step(self, batch: Batch, soft: SoftLabels | None) -> None:
         i = self._n % self.losses.shape[0]
-        nnkit.kd_loss(self.model, batch, soft, self.cfg, ws=self.ws, loss_slot=self.losses[i:i + 1])
-        if self.world_size > 1:
-            torch.distributed.all_reduce(self.ws.grads.flat, group=self.group)
-        nnkit.sgd_step(self.model, self.ws.grads, self.cfg.eta, self.world_size)
+        if self.world_size == 1 and self.fuse_sgd:
+            # single student: the update is fused into the dW / db kernels
+            nnkit.kd_loss(self.model, batch, soft, self.cfg, ws=self.ws, loss_slot=self.losses[i:i + 1],
+                          fused_sgd_eta=self.cfg.eta)
+        else:
+            nnkit.kd_loss(self.model, batch, soft, self.cfg, ws=self.ws, loss_slot=self.losses[i:i + 1])
+            if self.world_size > 1:
+                torch.distributed.all_reduce(self.ws.grads.flat, group=self.group)
+            nnkit.sgd_step(self.model, self.ws.grads, self.cfg.eta, self.world_size)
         self._n += 1
 
     def loss_values(self) -> list[float]:

@@ -1,0 +1,63 @@
+"""Same-process A/B timing of the cfg3 step pieces (box-to-box variance on the
+pool is ~10-15%, so compare variants inside one run only).
+
+    python scripts/stepbench.py [--iters 30]
+"""
+
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2207_06667_b200 import formats, nnkit  # noqa: E402
+from paper_2207_06667_b200.data import DeviceDataset, DeviceShardSampler  # noqa: E402
+from paper_2207_06667_b200.nnkit import Model, SoftLabels, TrainConfig  # noqa: E402
+from paper_2207_06667_b200.student import StudentStep  # noqa: E402
+
+
+def timeit(fn, iters, warm=5):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters * 1e3
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--iters", type=int, default=30)
+    a = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    B = 4096
+    data = DeviceDataset(formats.make_blobs(0, 16384, 3072, 1000, 1.0), dev)
+    sampler = DeviceShardSampler(data, 1, 0, B, seed=0)
+    teacher = Model.from_host(formats.init_model((3072, 8192, 8192, 1000), 1), dev)
+    sh = formats.init_model((3072, 2048, 1024, 1000), 0)
+    cfg = TrainConfig(eta=0.05, alpha=0.5, beta=0.5, temperature=2.0, batch_size=B)
+    batch = sampler.batch_for(0)
+    tws = nnkit.Workspace(teacher, B)
+    soft = SoftLabels(torch.empty(B, 16, device=dev), torch.empty(B, 16, dtype=torch.int32, device=dev), 2.0)
+    nnkit.teacher_soft_labels(teacher, batch.inputs, 2.0, 16, out=soft, ws=tws)
+    res = {}
+    res["teacher_batch_us"] = timeit(lambda: nnkit.teacher_soft_labels(teacher, batch.inputs, 2.0, 16, out=soft,
+                                                                       ws=tws), a.iters)
+    for fused in (False, True):
+        eng = StudentStep(Model.from_host(sh, dev), cfg, B, 1, fuse_sgd=fused)
+        res[f"student_step_{'fused' if fused else 'unfused'}_us"] = timeit(lambda: eng.step(batch, soft), a.iters)
+    eng = StudentStep(Model.from_host(sh, dev), cfg, B, 1)
+    res["online_step_us"] = timeit(lambda: (nnkit.teacher_soft_labels(teacher, batch.inputs, 2.0, 16, out=soft,
+                                                                      ws=tws), eng.step(batch, soft)), a.iters)
+    res["online_samples_per_s"] = B / res["online_step_us"] * 1e6
+    print(json.dumps({k: round(v, 2) for k, v in res.items()}))
+
+
+if __name__ == "__main__":
+    main()

@@ -185,6 +185,29 @@ def test_edld_teacher_ingest_and_checkpoint_write_back(nk, tmp_path):
     np.testing.assert_array_equal(ref.flatten(list(back.weights), list(back.biases)), nk.flatten_params(dev))
 
 
+def test_fused_sgd_step_matches_kd_loss_then_sgd(nk):
+    """kd_loss(..., fused_sgd_eta) (dW/db + SGD in the GEMM / column-sum
+    epilogues) == kd_loss + sgd_step, on the fp32 masters and the bf16 copies."""
+    from paper_2207_06667_b200 import formats
+    host = formats.init_model((40, 96, 48, 30), 4)
+    data = formats.make_blobs(2, 300, 40, 30, 1.0)
+    batch = nk.make_batch(data.samples, data.labels)
+    teacher = nk.Model.from_host(formats.init_model((40, 64, 30), 5))
+    soft = nk.teacher_soft_labels(teacher, batch.inputs, 2.0, 8)
+    cfg = nk.TrainConfig(eta=0.07, alpha=0.6, beta=0.4, temperature=2.0, batch_size=300)
+    a = nk.Model.from_host(host)
+    b = nk.Model.from_host(host)
+    for _ in range(3):
+        la, ga = nk.kd_loss(a, batch, soft, cfg, ws=nk.Workspace(a, 300))
+        nk.sgd_step(a, ga, cfg.eta)
+        lb, gb = nk.kd_loss(b, batch, soft, cfg, ws=nk.Workspace(b, 300), fused_sgd_eta=cfg.eta)
+        assert gb is None
+        assert float(la) == float(lb)
+    torch.cuda.synchronize()
+    assert (a.flat - b.flat).abs().max().item() <= 1e-6 * max(1.0, a.flat.abs().max().item())
+    assert (a.flat_bf16.float() - b.flat_bf16.float()).abs().max().item() <= 1e-2
+
+
 def test_error_mapping(nk):
     model = nk.Model((8, 16, 4))
     batch = nk.make_batch(np.zeros((3, 8)), np.array([0, 1, 9]))
