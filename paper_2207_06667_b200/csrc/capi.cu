@@ -125,6 +125,29 @@ int pick_bn(int M, int N) {
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+std::mutex g_attr_mu;
+std::unordered_map<const void*, unsigned long long> g_attr_done;  // kernel -> device bitmask
+
+}  // namespace
+
+cudaError_t edl::ensure_kernel_attrs(const void* kern, int smem_bytes, bool nonportable_cluster) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  std::lock_guard<std::mutex> g(g_attr_mu);
+  unsigned long long& mask = g_attr_done[kern];
+  if (mask & bit) return cudaSuccess;
+  cudaError_t e = cudaSuccess;
+  if (smem_bytes > 48 * 1024)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  if (e == cudaSuccess && nonportable_cluster)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e == cudaSuccess) mask |= bit;
+  return e;
+}
+
+namespace {
+
 // Per-(device, stream) tile-scheduler counters for the persistent GEMM
 // ({next tile, CTAs done}, reset by each launch's last CTA). Allocated on a
 // stream's first GEMM only; launches on one stream are ordered (PDL waits),

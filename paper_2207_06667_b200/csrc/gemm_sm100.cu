@@ -766,13 +766,8 @@ template <int BN, bool A_MN, bool B_MN, int EPI>
 static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N,
                                  int K, const EpiArgs& ep, int num_sms, cudaStream_t stream) {
   auto kern = gemm_kernel<BN, A_MN, B_MN, EPI>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         GemmCfg<BN>::kSmem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), GemmCfg<BN>::kSmem);
+  if (e != cudaSuccess) return e;
   const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms ? tiles : num_sms;
   return launch_pdl(kern, dim3(grid), dim3(kThreads), GemmCfg<BN>::kSmem, stream, 1, ta, tb, M, N, K, ep);
@@ -811,13 +806,8 @@ static cudaError_t launch_grouped_t(const GroupMaps& maps, const GroupArgs& ga, 
                                     cudaStream_t stream) {
   constexpr int BN = 256;
   auto kern = gemm_grouped_kernel<BN, true, true, EPI>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         GemmCfg<BN>::kSmem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), GemmCfg<BN>::kSmem);
+  if (e != cudaSuccess) return e;
   const int tiles = ga.tile_start[ga.count];
   const int grid = tiles < num_sms ? tiles : num_sms;
   return launch_pdl(kern, dim3(grid), dim3(kThreads), GemmCfg<BN>::kSmem, stream, 1, maps, ga);
@@ -835,15 +825,8 @@ template <int BN, int KMAX>
 static cudaError_t launch_head_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N,
                                  int K, const HeadArgs& hp, cudaStream_t stream) {
   auto kern = teacher_head_kernel<BN, KMAX>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         GemmCfg<BN>::kSmem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), GemmCfg<BN>::kSmem, true);
+  if (e != cudaSuccess) return e;
   const int cs = (N + BN - 1) / BN;
   return launch_pdl(kern, dim3(cs, (M + kBM - 1) / kBM, 1), dim3(kThreads), GemmCfg<BN>::kSmem, stream, cs,
                     ta, tb, M, N, K, hp);

@@ -8,6 +8,12 @@
 
 namespace edl {
 
+// Raise a kernel's dynamic shared-memory limit (and, for clusters wider than
+// 8, allow non-portable sizes) once per (kernel, device): the attribute lives
+// in the device context, so a process driving several GPUs (teacher workers
+// on other devices) must set it on each.
+cudaError_t ensure_kernel_attrs(const void* kern, int smem_bytes, bool nonportable_cluster = false);
+
 // Launch with programmatic stream serialization (PDL) and an optional
 // cluster shape; every kernel of the library calls griddep_wait() before its
 // first global access, so early launch is always safe.

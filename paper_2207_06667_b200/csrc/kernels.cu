@@ -173,16 +173,11 @@ static cudaError_t launch_kd_t(const float* logits, long long ld_z, const int64_
                                unsigned* ticket, __nv_bfloat16* dlogits, long long ld_dz, int* status,
                                cudaStream_t stream) {
   const size_t smem = static_cast<size_t>(kKdWarps) * 32 * KPL * sizeof(float);
-  static bool set = false;
-  if (!set && smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kd_loss_kernel<KPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-  }
-  set = true;
+  cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kd_loss_kernel<KPL>), static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
   int blocks = (B + kKdWarps - 1) / kKdWarps;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  cudaError_t e = launch_pdl(kd_loss_kernel<KPL>, dim3(blocks), dim3(kKdWarps * 32), smem, stream, 1, logits, ld_z,
+  e = launch_pdl(kd_loss_kernel<KPL>, dim3(blocks), dim3(kKdWarps * 32), smem, stream, 1, logits, ld_z,
                              labels, q_vals, q_idx, B, K, Kw, k, alpha, beta, T, row_loss, loss_out, ticket,
                              dlogits, ld_dz, status);
   if (e != cudaSuccess) return e;
