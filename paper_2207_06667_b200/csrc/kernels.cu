@@ -282,8 +282,17 @@ __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, long l
   const __nv_bfloat16* s = src + static_cast<size_t>(r) * ld_src;
   __nv_bfloat16* d = dst + static_cast<size_t>(warp) * ld_dst;
   const int v = D / 8;
-  for (int c = lane; c < v; c += 32) reinterpret_cast<uint4*>(d)[c] = __ldg(reinterpret_cast<const uint4*>(s) + c);
-  for (int c = v * 8 + lane; c < D; c += 32) d[c] = s[c];
+  // 4 independent 16-byte loads in flight per lane before the stores
+  int c = lane;
+  for (; c + 96 < v; c += 128) {
+    uint4 q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) q[u] = __ldg(reinterpret_cast<const uint4*>(s) + c + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) reinterpret_cast<uint4*>(d)[c + 32 * u] = q[u];
+  }
+  for (; c < v; c += 32) reinterpret_cast<uint4*>(d)[c] = __ldg(reinterpret_cast<const uint4*>(s) + c);
+  for (int e = v * 8 + lane; e < D; e += 32) d[e] = s[e];
 }
 
 cudaError_t launch_gather_rows(const __nv_bfloat16* src, long long ld_src, const int64_t* idx,
@@ -348,16 +357,37 @@ __global__ void __launch_bounds__(256) colsum_partial_kernel(ColsumGroup g) {
   }
 }
 
-__global__ void colsum_final_kernel(ColsumGroup g) {
+// Pass 2: a block owns 32 columns; lane = column, the 8 warps stride the row
+// chunks (all loads in flight at once) and combine in a fixed order. (One
+// thread per column walking 64 chunks serially cost 12 us.)
+__global__ void __launch_bounds__(256) colsum_final_kernel(ColsumGroup g) {
   griddep_wait();
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ float red[8][32];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  int t = blockIdx.x * 32 + lane;
   int p = 0;
   while (p < g.count && t >= g.N[p]) { t -= g.N[p]; ++p; }
-  if (p >= g.count) return;
-  const int chunks = (g.M[p] + kColRows - 1) / kColRows;
-  const float* part = g.partial + g.part_off[p];
+  const bool valid = p < g.count;
   float s = 0.f;
-  for (int c = 0; c < chunks; ++c) s += part[static_cast<long long>(c) * g.N[p] + t];
+  if (valid) {
+    const int chunks = (g.M[p] + kColRows - 1) / kColRows;
+    const float* part = g.partial + g.part_off[p];
+    float f[8];
+    for (int c0 = warp; c0 < chunks; c0 += 64) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + 8 * u;
+        f[u] = c < chunks ? __ldcg(part + static_cast<long long>(c) * g.N[p] + t) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += f[u];
+    }
+  }
+  red[warp][lane] = s;
+  __syncthreads();
+  if (warp != 0 || !valid) return;
+#pragma unroll
+  for (int w = 1; w < 8; ++w) s += red[w][lane];
   if (g.sgd) {   // fused SGD on the bias (edl/nnkit.py:321): b -= eta * db
     const float b = g.out[p][t] - g.scale * s;
     g.out[p][t] = b;
@@ -387,7 +417,7 @@ cudaError_t launch_colsum_group(ColsumGroup g, cudaStream_t stream) {
   g.blk_start[g.count] = blocks;
   cudaError_t e = launch_pdl(colsum_partial_kernel, dim3(blocks), dim3(256), 0, stream, 1, g);
   if (e != cudaSuccess) return e;
-  return launch_pdl(colsum_final_kernel, dim3((cols + 255) / 256), dim3(256), 0, stream, 1, g);
+  return launch_pdl(colsum_final_kernel, dim3((cols + 31) / 32), dim3(256), 0, stream, 1, g);
 }
 
 cudaError_t launch_colsum(const __nv_bfloat16* x, long long ld, int M, int N, float* partial,
