@@ -211,7 +211,7 @@ def main():
                     help="CUDA stream priority of the student in the co-located EDL loop")
     ap.add_argument("--teacher-sm-reserve", type=int, default=-1,
                     help="SMs the co-located teacher stream leaves free for the student's NCCL "
-                         "all-reduce (-1: 32 when N > 1, else 0)")
+                         "all-reduce / single-wave kernels (-1: 32 when N > 1, else 16)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.batch:
@@ -269,9 +269,11 @@ def main():
     student = Model.from_host(student_h, dev)
     engine = StudentStep(student, tcfg, B, world, max_steps=W + K + 8)
     pool = TeacherPool()
-    # N=4 sweep on B200 (profiles/README.md): reserve 0/8/16/24/32 SMs ->
-    # EDL 13.5/14.2/14.0/14.3/14.6 M samples/s vs online 13.8-14.5 M
-    reserve = args.teacher_sm_reserve if args.teacher_sm_reserve >= 0 else (32 if world > 1 else 0)
+    # Sweeps on B200 (profiles/README.md): N=4, reserve 0/8/16/24/32 SMs ->
+    # EDL 13.5/14.2/14.0/14.3/14.6 M samples/s (online 13.8-14.5 M); N=1,
+    # reserve 0/16/32/48 -> 4.04/4.16/4.11/2.0 M (online 3.96 M): 16 SMs let
+    # the student's single-wave kernels run beside the teacher's GEMMs.
+    reserve = args.teacher_sm_reserve if args.teacher_sm_reserve >= 0 else (32 if world > 1 else 16)
     worker = TeacherWorker(TeacherConfig("t1", cfg["T"], cfg["topk"]), teacher, ddata, sm_reserve=reserve)
     pool.register(worker)
     sched = SchedulerConfig(lt=2, ut=8, pipeline_depth=2, acquire_cooldown=1e9)
