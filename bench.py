@@ -283,6 +283,8 @@ def main():
     student_stream = (torch.cuda.Stream(dev, priority=-1) if args.student_priority == "high"
                       else torch.cuda.current_stream(dev))
 
+    host_s = [0.0]
+
     def edl_run(start, count, timed):
         reader = DistilReader(f"student-{rank}", pool, sched, sampler, start, start + count, 1, EventLog(),
                               cfg["T"], cfg["topk"])
@@ -296,10 +298,12 @@ def main():
             torch.cuda.nvtx.range_push("edl_timed")   # ncu --nvtx-include edl_timed/
         with torch.cuda.stream(student_stream):
             s.record()
+            h0 = time.perf_counter()
             for it in range(start, start + count):
                 batch = sampler.batch_for(it, out=engine.batch)
                 soft = reader.consume(it)
                 engine.step(batch, soft)
+            host_s[0] = (time.perf_counter() - h0) / count   # host enqueue time per step (incl. waits)
             e.record()
         if timed:
             torch.cuda.nvtx.range_pop()
@@ -394,6 +398,7 @@ def main():
             "teacher_infer_samples_per_s": None,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "online": online,
             "gpu_launches": launches, "clocks": clocks, "ledger_ok": ledger["ok"],
+            "host_ms_per_step": round(host_s[0] * 1e3, 4),
             "algorithmic_flop_per_sample": {"teacher_fwd": tflop_t, "student_train": tflop_s},
         }
         line["tensor_roofline_samples_per_s"] = round(world * peak_sust * 1e12 / (tflop_t + tflop_s), 1)

@@ -56,6 +56,26 @@ def main():
     res["online_step_us"] = timeit(lambda: (nnkit.teacher_soft_labels(teacher, batch.inputs, 2.0, 16, out=soft,
                                                                       ws=tws), eng.step(batch, soft)), a.iters)
     res["online_samples_per_s"] = B / res["online_step_us"] * 1e6
+    # host enqueue cost of one eager step: tiny cfg2 shapes make the device
+    # work negligible, so wall time per step ~ Python + ctypes + launch cost
+    import time
+    t2 = Model.from_host(formats.init_model((16, 256, 256, 10), 1), dev)
+    s2 = StudentStep(Model.from_host(formats.init_model((16, 64, 10), 0), dev),
+                     TrainConfig(eta=0.05, alpha=0.5, beta=0.5, temperature=2.0, batch_size=32), 32, 1)
+    b2 = nnkit.make_batch(formats.make_blobs(0, 32, 16, 10, 1.0).samples, formats.make_blobs(0, 32, 16, 10, 1.0).labels,
+                          dev)
+    ws2 = nnkit.Workspace(t2, 32)
+    o2 = SoftLabels(torch.empty(32, 10, device=dev), torch.empty(32, 10, dtype=torch.int32, device=dev), 2.0)
+    for _ in range(10):
+        nnkit.teacher_soft_labels(t2, b2.inputs, 2.0, 10, out=o2, ws=ws2)
+        s2.step(b2, o2)
+    torch.cuda.synchronize()
+    h0 = time.perf_counter()
+    for _ in range(200):
+        nnkit.teacher_soft_labels(t2, b2.inputs, 2.0, 10, out=o2, ws=ws2)
+        s2.step(b2, o2)
+    torch.cuda.synchronize()
+    res["host_us_per_eager_online_step"] = (time.perf_counter() - h0) / 200 * 1e6
     print(json.dumps({k: round(v, 2) for k, v in res.items()}))
 
 
