@@ -108,19 +108,41 @@ int num_sms() {
   return n;
 }
 
-// Pick the N tile: fewest waves, then the widest tile (best operand reuse).
-int pick_bn(int M, int N) {
-  const int sms = num_sms();
+// Pick the N tile for `cap` CTAs: fewest waves x tile time (one tile's time
+// ~ bn + 48 fixed cost), widest tile on ties (best operand reuse).
+int pick_bn_cap(int M, int N, int cap) {
   int best = 256;
   long long best_cost = -1;
   for (int bn : {256, 128, 64}) {
     if (bn > 64 && N <= bn / 2) continue;
     const long long tiles = static_cast<long long>((M + 127) / 128) * ((N + bn - 1) / bn);
-    const long long waves = (tiles + sms - 1) / sms;
-    const long long cost = waves * (bn + 48);
+    const long long cost = ((tiles + cap - 1) / cap) * (bn + 48);
     if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = bn; }
   }
   return best;
+}
+int pick_bn(int M, int N) { return pick_bn_cap(M, N, num_sms()); }
+
+// CTA-pair 256 x 256 tiles (cta_group::2) do the same per-SM MMA work per
+// tile as a single-CTA 128 x 256 tile with 2/3 of the L2 -> SM operand bytes
+// (measured on B200: teacher layers 437 -> 380 us, student layer 1 49.6 ->
+// 42.5 us), so they win whenever their wave count is no worse. Returns 0 to
+// use the single-CTA kernel. EDL_GEMM_PAIR=0 forces single-CTA (A/B runs).
+int pick_pair_bn(int M, int N, int cap) {
+  static const int mode = [] {
+    const char* v = getenv("EDL_GEMM_PAIR");
+    return v ? atoi(v) : 1;
+  }();
+  if (mode == 0 || cap < 2 || N <= 128) return 0;
+  const int bn = pick_bn_cap(M, N, cap);
+  const long long single = ((static_cast<long long>((M + 127) / 128) * ((N + bn - 1) / bn) + cap - 1) / cap) *
+                           (bn + 48);
+  const long long pair_tiles = static_cast<long long>((M + 255) / 256) * ((N + 255) / 256);
+  const long long pair_waves = (pair_tiles + cap / 2 - 1) / (cap / 2);
+  const long long pair = pair_waves * (256 + 48);
+  // a single wave gains little operand traffic and pays the cluster's
+  // setup (~0.5 us measured on the student's 1-wave layers): ties go single
+  return (pair < single || (pair == single && pair_waves >= 2)) ? 256 : 0;
 }
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -211,14 +233,22 @@ int edl_linear_fwd(const void* X, long long ldx, const void* W, long long ldw, c
   if (M < 1 || N < 1 || K < 1 || ldx < K || ldw < K || ldy < N)
     return fail(EDL_ERR_SHAPE, "linear_fwd: bad shape M=%d N=%d K=%d", M, N, K);
   if (act != EDL_ACT_TANH && act != EDL_ACT_NONE) return fail(EDL_ERR_SHAPE, "linear_fwd: bad act %d", act);
-  const int bn = pick_bn(M, N);
+  const GemmKind kind = act == EDL_ACT_TANH ? GemmKind::FwdTanh : GemmKind::FwdLinear;
+  const int cap = grid_cap(as_stream(stream));
   CUtensorMap ta, tb;
   int rc;
   if ((rc = tensor_map(X, M, K, ldx, 64, 128, &ta))) return rc;
-  if ((rc = tensor_map(W, N, K, ldw, 64, bn, &tb))) return rc;
   EpiArgs ep{Y, ldy, bias, nullptr, 0, 1.0f, stream_sched(as_stream(stream))};
-  cudaError_t e = launch_gemm(act == EDL_ACT_TANH ? GemmKind::FwdTanh : GemmKind::FwdLinear, bn, ta,
-                              tb, M, N, K, ep, grid_cap(as_stream(stream)), as_stream(stream));
+  const int pbn = pick_pair_bn(M, N, cap);
+  cudaError_t e;
+  if (pbn > 0) {
+    if ((rc = tensor_map(W, N, K, ldw, 64, pbn / 2, &tb))) return rc;
+    e = launch_gemm_pair(kind, pbn, ta, tb, M, N, K, ep, cap, as_stream(stream));
+  } else {
+    const int bn = pick_bn_cap(M, N, cap);
+    if ((rc = tensor_map(W, N, K, ldw, 64, bn, &tb))) return rc;
+    e = launch_gemm(kind, bn, ta, tb, M, N, K, ep, cap, as_stream(stream));
+  }
   return e == cudaSuccess ? 0 : cuda_fail(e, "linear_fwd");
 }
 
@@ -227,7 +257,7 @@ int edl_linear_bwd_data(const void* dY, long long lddy, const void* W, long long
                         int K, void* stream) {
   if (M < 1 || N < 1 || K < 1 || lddy < N || ldw < K || ldh < K || lddx < K)
     return fail(EDL_ERR_SHAPE, "linear_bwd_data: bad shape M=%d N=%d K=%d", M, N, K);
-  const int bn = pick_bn(M, K);
+  const int cap = grid_cap(as_stream(stream));
   CUtensorMap ta, tb;
   int rc;
   // A = dY [M][N] (reduction N contiguous: K-major); B = W [N][K] read as [red][MN].
@@ -235,8 +265,10 @@ int edl_linear_bwd_data(const void* dY, long long lddy, const void* W, long long
   if ((rc = tensor_map(W, N, K, ldw, 64, 64, &tb))) return rc;
   EpiArgs ep{dX, lddx, nullptr, reinterpret_cast<const __nv_bfloat16*>(H), ldh, 1.0f,
              stream_sched(as_stream(stream))};
-  cudaError_t e = launch_gemm(GemmKind::BwdData, bn, ta, tb, M, K, N, ep, grid_cap(as_stream(stream)),
-                              as_stream(stream));
+  const int pbn = pick_pair_bn(M, K, cap);
+  cudaError_t e = pbn > 0 ? launch_gemm_pair(GemmKind::BwdData, pbn, ta, tb, M, K, N, ep, cap, as_stream(stream))
+                          : launch_gemm(GemmKind::BwdData, pick_bn_cap(M, K, cap), ta, tb, M, K, N, ep, cap,
+                                        as_stream(stream));
   return e == cudaSuccess ? 0 : cuda_fail(e, "linear_bwd_data");
 }
 

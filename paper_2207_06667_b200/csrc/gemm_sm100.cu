@@ -341,6 +341,205 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------------------------------ CTA-pair GEMM
+// The same contract as gemm_kernel on 256 x BN tiles computed by a CTA pair
+// (cluster of 2, cta_group::2): rank r stages A rows [m0+128r, +128) and B
+// rows [n0 + r*BN/2, +BN/2); rank 0's single MMA thread issues 256 x BN x 16
+// MMAs that read both CTAs' halves, so each SM pulls 2/3 of the operand bytes
+// per FLOP that a 128 x BN single-CTA tile needs (the L2 -> SM TMA stream is
+// what limits the single-CTA kernel on the teacher's big layers).
+// Pipelines: the smem ring's full barriers live in rank 0 (both CTAs' TMA
+// loads complete there); empty / tmem-full barriers are multicast-committed
+// to both CTAs; tmem-empty (rank 0) collects all 8 epilogue warps. Tiles come
+// from the per-stream counter through rank 0's producer, which publishes each
+// tile index into both CTAs' rings.
+template <int BN>
+struct PairCfg {
+  static constexpr int kHalfN = BN / 2;
+  static constexpr uint32_t kABytes = kBM * kBK * 2;
+  static constexpr uint32_t kBBytes = kHalfN * kBK * 2;
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
+  static constexpr uint32_t kSmem = kStages * kStageBytes + 1024 + 256;
+};
+
+template <int BN, bool A_MN, bool B_MN>
+__device__ __forceinline__ void load_kblock_pair(const CUtensorMap* tmA, const CUtensorMap* tmB,
+                                                 uint8_t* sa, uint8_t* sb, uint32_t bar, int m0,
+                                                 int n0, int k0) {
+  if constexpr (!A_MN) {
+    tma_load_2d_pair(sa, tmA, bar, k0, m0);
+  } else {
+#pragma unroll
+    for (int j = 0; j < kBM / 64; ++j) tma_load_2d_pair(sa + j * 8192, tmA, bar, m0 + 64 * j, k0);
+  }
+  if constexpr (!B_MN) {
+    tma_load_2d_pair(sb, tmB, bar, k0, n0);
+  } else {
+#pragma unroll
+    for (int j = 0; j < PairCfg<BN>::kHalfN / 64; ++j)
+      tma_load_2d_pair(sb + j * 8192, tmB, bar, n0 + 64 * j, k0);
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__device__ __forceinline__ void mma_kblock_pair(uint32_t d_tmem, uint32_t a_base, uint32_t b_base,
+                                                bool first) {
+  constexpr uint32_t idesc = idesc_bf16_f32(2 * kBM, BN, A_MN, B_MN);
+#pragma unroll
+  for (int k = 0; k < kBK / 16; ++k) {
+    uint64_t ad = A_MN ? smem_desc_sw128(a_base + k * 2048, 8192, 1024)
+                       : smem_desc_sw128(a_base + k * 32, 16, 1024);
+    uint64_t bd = B_MN ? smem_desc_sw128(b_base + k * 2048, 8192, 1024)
+                       : smem_desc_sw128(b_base + k * 32, 16, 1024);
+    umma_bf16_pair(d_tmem, ad, bd, idesc, (first && k == 0) ? 0u : 1u);
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     int M, int N, int K, EpiArgs ep) {
+  using Cfg = PairCfg<BN>;
+  unsigned* const sched = ep.sched;
+  constexpr int S = Cfg::kStages;
+  constexpr uint32_t kTmemCols = tmem_cols_for(2 * BN);
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * Cfg::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kBBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* tile_full = tempty + 2;       // [4] tile-index ring
+  uint64_t* tile_empty = tile_full + 4;   // [4] (rank 0's is the one used)
+  int* tile_ring = reinterpret_cast<int*>(tile_empty + 4);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + 4);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 8); }
+    // tile ring: rank 0's MMA + 4 epilogue warps, rank 1's producer + 4 epilogue warps
+    for (int s = 0; s < 4; ++s) { mbar_init(&tile_full[s], 1); mbar_init(&tile_empty[s], 10); }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_pair<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();      // barriers of both CTAs initialised before any remote arrive / TMA
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();
+
+  const int num_m = (M + 2 * kBM - 1) / (2 * kBM);
+  const int num_n = (N + BN - 1) / BN;
+  const int tiles = num_m * num_n;
+  const int nk = (K + kBK - 1) / kBK;
+  const int pair = static_cast<int>(blockIdx.x) / 2;
+  const int npairs = static_cast<int>(gridDim.x) / 2;
+  const uint32_t full0 = mapa(smem_u32(full), 0);           // rank 0's full[0]
+  const uint32_t tile_empty0 = mapa(smem_u32(tile_empty), 0);
+  const uint32_t tempty0 = mapa(smem_u32(tempty), 0);
+
+  // every role but rank 0's producer reads tile i from its own ring and
+  // releases the slot on rank 0's tile_empty
+  auto take_tile = [&](uint32_t i) -> int {
+    const int slot = i & 3;
+    mbar_wait_cluster(&tile_full[slot], (i >> 2) & 1);
+    return tile_ring[slot];
+  };
+  auto release_tile = [&](uint32_t i) { mbar_arrive_cluster(tile_empty0 + 8 * (i & 3)); };
+
+  if (warp == 0 && lane == 0) {
+    uint32_t g = 0;
+    for (uint32_t i = 0;; ++i) {
+      int t;
+      if (rank == 0) {
+        const int slot = i & 3;
+        mbar_wait_cluster(&tile_empty[slot], ((i >> 2) & 1) ^ 1);
+        t = sched ? static_cast<int>(atomicAdd(sched, 1u)) : pair + static_cast<int>(i) * npairs;
+        tile_ring[slot] = t;
+        st_dsmem_s32(mapa(smem_u32(&tile_ring[slot]), 1), t);
+        mbar_arrive(&tile_full[slot]);
+        mbar_arrive_cluster(mapa(smem_u32(&tile_full[slot]), 1));
+      } else {
+        t = take_tile(i);
+        release_tile(i);
+      }
+      if (t >= tiles) break;
+      const int m0 = (t % num_m) * 2 * kBM + static_cast<int>(rank) * kBM;
+      const int n0 = (t / num_m) * BN + static_cast<int>(rank) * Cfg::kHalfN;
+      for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int s = g % S;
+        mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
+        if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * Cfg::kStageBytes);
+        load_kblock_pair<BN, A_MN, B_MN>(&tmA, &tmB, sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes,
+                                         full0 + 8 * s, m0, n0, kb * kBK);
+      }
+    }
+  } else if (warp == 1 && lane == 0 && rank == 0) {
+    uint32_t g = 0;
+    for (uint32_t i = 0;; ++i) {
+      const int t = take_tile(i);
+      release_tile(i);
+      if (t >= tiles) break;
+      const uint32_t as = i & 1;
+      mbar_wait_cluster(&tempty[as], ((i >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + as * BN;
+      for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int s = g % S;
+        mbar_wait(&full[s], (g / S) & 1);
+        tc_fence_after();
+        mma_kblock_pair<BN, A_MN, B_MN>(d, smem_u32(sA + s * Cfg::kABytes),
+                                        smem_u32(sB + s * Cfg::kBBytes), kb == 0);
+        umma_commit_pair(&empty[s]);
+      }
+      umma_commit_pair(&tfull[as]);
+    }
+  } else if (warp >= 4) {
+    const int e = warp - 4;
+    for (uint32_t i = 0;; ++i) {
+      const int t = take_tile(i);
+      __syncwarp();
+      if (lane == 0) release_tile(i);
+      if (t >= tiles) break;
+      const int m0 = (t % num_m) * 2 * kBM + static_cast<int>(rank) * kBM;
+      const int n0 = (t / num_m) * BN;
+      const uint32_t as = i & 1;
+      mbar_wait(&tfull[as], (i >> 1) & 1);
+      tc_fence_after();
+      const int row = m0 + 32 * e + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN + c, v);
+        if (n0 + c < N) epilogue_store<EPI>(ep, row, M, n0 + c, N, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty0 + 8 * as);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();      // the peer's TMEM / smem stay live until rank 0's MMAs are done
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair<kTmemCols>(tmem_base);
+  if (sched && threadIdx.x == 0 && rank == 0) {
+    __threadfence();
+    if (atomicAdd(sched + 1, 1u) == gridDim.x / 2 - 1) {   // last pair out: reset for the next launch
+      atomicExch(sched, 0u);
+      atomicExch(sched + 1, 0u);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ grouped GEMM
 // Several independent problems in ONE persistent launch (the student's dW_l
 // for every layer: each alone has 32-192 output tiles, too few for 148 SMs;
@@ -799,6 +998,43 @@ cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUte
       return launch_gemm_bn<true, true, EPI_F32>(bn, ta, tb, M, N, K, ep, num_sms, stream);
   }
   return cudaErrorInvalidValue;
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+static cudaError_t launch_pair_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
+                                 const EpiArgs& ep, int num_sms, cudaStream_t stream) {
+  auto kern = gemm_pair_kernel<BN, A_MN, B_MN, EPI>;
+  cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), PairCfg<BN>::kSmem);
+  if (e != cudaSuccess) return e;
+  const int tiles = ((M + 2 * kBM - 1) / (2 * kBM)) * ((N + BN - 1) / BN);
+  const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
+  if (pairs < 1) return cudaErrorInvalidValue;
+  return launch_pdl(kern, dim3(2 * pairs), dim3(kThreads), PairCfg<BN>::kSmem, stream, 2, ta, tb, M, N, K, ep);
+}
+
+template <bool A_MN, bool B_MN, int EPI>
+static cudaError_t launch_pair_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N,
+                                  int K, const EpiArgs& ep, int num_sms, cudaStream_t stream) {
+  switch (bn) {
+    case 128: return launch_pair_t<128, A_MN, B_MN, EPI>(ta, tb, M, N, K, ep, num_sms, stream);
+    case 256: return launch_pair_t<256, A_MN, B_MN, EPI>(ta, tb, M, N, K, ep, num_sms, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_gemm_pair(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
+                             int M, int N, int K, const EpiArgs& ep, int num_sms,
+                             cudaStream_t stream) {
+  switch (kind) {
+    case GemmKind::FwdTanh:
+      return launch_pair_bn<false, false, EPI_TANH_BF16>(bn, ta, tb, M, N, K, ep, num_sms, stream);
+    case GemmKind::FwdLinear:
+      return launch_pair_bn<false, false, EPI_BIAS_F32>(bn, ta, tb, M, N, K, ep, num_sms, stream);
+    case GemmKind::BwdData:
+      return launch_pair_bn<false, true, EPI_DTANH_BF16>(bn, ta, tb, M, N, K, ep, num_sms, stream);
+    default:
+      return cudaErrorInvalidValue;
+  }
 }
 
 template <int EPI>

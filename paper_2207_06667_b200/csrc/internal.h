@@ -89,6 +89,11 @@ int grouped_tile_bn();
 cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
                         int M, int N, int K, const EpiArgs& ep, int num_sms,
                         cudaStream_t stream);
+// 256 x bn tiles on CTA pairs (cta_group::2); bn in {128, 256}; B's tensor
+// map box covers bn/2 rows (K-major) or bn/2 columns (MN-major).
+cudaError_t launch_gemm_pair(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
+                             int M, int N, int K, const EpiArgs& ep, int num_sms,
+                             cudaStream_t stream);
 cudaError_t launch_teacher_head(int bn, int kmax, const CUtensorMap& ta, const CUtensorMap& tb,
                                 int M, int N, int K, const HeadArgs& hp, cudaStream_t stream);
 

@@ -58,13 +58,19 @@ class DeviceShardSampler:
         epoch, i = divmod(iteration, self.batches_per_epoch)
         order = self._orders.get(epoch)
         if order is None:
-            host = epoch_order(self.seed, epoch, self.rank, self.hi - self.lo) + self.lo
-            order = torch.from_numpy(host.astype(np.int64)).to(self.data.device)
-            # keep a few epochs alive: in-flight teacher / student work may
-            # still read the previous epoch's permutation on other streams
+            host = torch.from_numpy((epoch_order(self.seed, epoch, self.rank, self.hi - self.lo)
+                                     + self.lo).astype(np.int64)).pin_memory()
+            # pinned + non_blocking: a pageable copy would block the host until
+            # the stream drains, a bubble in the enqueue-ahead pipeline every epoch
+            order = host.to(self.data.device, non_blocking=True)
+            # keep a few epochs alive (device tensor + its pinned source, which
+            # must outlive the async copy): in-flight teacher / student work
+            # may still read the previous epoch's permutation on other streams
             if len(self._orders) >= 3:
                 self._orders.pop(min(self._orders))
-            self._orders[epoch] = order
+            self._orders[epoch] = (order, host)
+        else:
+            order = order[0]
         return order[i * self.batch_size:(i + 1) * self.batch_size]
 
     def batch_for(self, iteration: int, out: Batch | None = None, stream=None) -> Batch:

@@ -56,6 +56,51 @@ def main():
     res["online_step_us"] = timeit(lambda: (nnkit.teacher_soft_labels(teacher, batch.inputs, 2.0, 16, out=soft,
                                                                       ws=tws), eng.step(batch, soft)), a.iters)
     res["online_samples_per_s"] = B / res["online_step_us"] * 1e6
+    # the same step with a fresh batch gathered every iteration (epoch
+    # permutations built on demand, as in bench.py) ...
+    ctr = [0]
+
+    def sampled():
+        b = sampler.batch_for(ctr[0], out=eng.batch)
+        ctr[0] += 1
+        nnkit.teacher_soft_labels(teacher, b.inputs, 2.0, 16, out=soft, ws=tws)
+        eng.step(b, soft)
+    res["online_step_sampled_us"] = timeit(sampled, 96)
+    # ... and with the permutations already resident
+    for it in range(ctr[0], ctr[0] + 100, sampler.batches_per_epoch):
+        sampler.rows_for(it)
+    res["online_step_sampled_prewarmed_us"] = timeit(sampled, 16)
+
+    def same_rows():          # gather launched every step, always batch 0's rows
+        b = sampler.batch_for(0, out=eng.batch)
+        nnkit.teacher_soft_labels(teacher, b.inputs, 2.0, 16, out=soft, ws=tws)
+        eng.step(b, soft)
+    res["online_step_gather_same_rows_us"] = timeit(same_rows, 30)
+    bufs = [sampler.batch_for(i) for i in range(8)]
+    ctr[0] = 0
+
+    def rotate():             # 8 pre-gathered batches, no gather launch
+        b = bufs[ctr[0] % 8]
+        ctr[0] += 1
+        nnkit.teacher_soft_labels(teacher, b.inputs, 2.0, 16, out=soft, ws=tws)
+        eng.step(b, soft)
+    res["online_step_rotate8_us"] = timeit(rotate, 32)
+    res["teacher_batch_rotate8_us"] = timeit(
+        lambda: nnkit.teacher_soft_labels(teacher, bufs[(ctr.__setitem__(0, ctr[0] + 1) or ctr[0]) % 8].inputs,
+                                          2.0, 16, out=soft, ws=tws), 32)
+    # order confound check: the fixed-batch variants again, last
+    res["teacher_batch_again_us"] = timeit(lambda: nnkit.teacher_soft_labels(teacher, batch.inputs, 2.0, 16, out=soft,
+                                                                             ws=tws), a.iters)
+    res["online_step_again_us"] = timeit(lambda: (nnkit.teacher_soft_labels(teacher, batch.inputs, 2.0, 16, out=soft,
+                                                                            ws=tws), eng.step(batch, soft)), a.iters)
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+        res["sm_mhz_end"] = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        res["power_w_end"] = pynvml.nvmlDeviceGetPowerUsage(h) / 1e3
+    except Exception:
+        pass
     # host enqueue cost of one eager step: tiny cfg2 shapes make the device
     # work negligible, so wall time per step ~ Python + ctypes + launch cost
     import time

@@ -36,9 +36,14 @@ def _padded(t, rows, cols, dtype=torch.bfloat16):
 
 GEMM_SHAPES = [(37, 16, 16), (128, 64, 64), (300, 208, 112), (513, 320, 1000), (1024, 1024, 2048),
                (256, 2304, 512)]
+# shapes with >= one wave of 256-row tiles take the CTA-pair kernel
+# (capi.cu pick_pair_bn): full tiles, ragged M / N where rank 1's A rows or B
+# columns run off the end (partly or wholly), M < 256, and the bn=128 pair tile
+PAIR_SHAPES = [(4096, 2048, 3072), (3000, 2000, 1000), (1000, 4100, 520), (200, 20000, 64),
+               (300, 19000, 64)]
 
 
-@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES + PAIR_SHAPES)
 @pytest.mark.parametrize("act", [0, 1])
 def test_linear_fwd(lib, M, N, K, act):
     Kp, Np = (K + 15) // 16 * 16, (N + 15) // 16 * 16
