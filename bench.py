@@ -214,6 +214,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-online", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nvls", "nccl"],
+                    help="N>1 student gradient exchange: NCCL all-reduce + SGD, or the fused NVSwitch-multicast "
+                         "all-reduce+SGD kernel (slower on this pool, profiles/r01_exchange_ab.json)")
     ap.add_argument("--placement", default="colocated", choices=["colocated", "split"],
                     help="colocated: teacher worker + student on every GPU; split: teacher GPUs feed "
                          "student GPUs over NVLink (EDL-Dist teacher pool)")
@@ -278,7 +281,7 @@ def main():
 
     # ---------------- EDL-Dist (decoupled, co-located teacher worker per GPU)
     student = Model.from_host(student_h, dev)
-    engine = StudentStep(student, tcfg, B, world, max_steps=W + K + 8)
+    engine = StudentStep(student, tcfg, B, world, max_steps=W + K + 8, exchange=args.exchange)
     pool = TeacherPool()
     # Sweeps on B200 (profiles/README.md): N=4, reserve 0/8/16/24/32 SMs ->
     # EDL 13.5/14.2/14.0/14.3/14.6 M samples/s (online 13.8-14.5 M); N=1,
@@ -340,7 +343,7 @@ def main():
     online_run = None
     if not args.no_online:
         student2 = Model.from_host(student_h, dev)
-        eng2 = StudentStep(student2, tcfg, B, world, max_steps=W + 2 * K + 8)
+        eng2 = StudentStep(student2, tcfg, B, world, max_steps=W + 2 * K + 8, exchange=args.exchange)
         tws = nnkit.Workspace(teacher, B)
         out = SoftLabels(torch.empty(B, cfg["topk"], device=dev),
                          torch.empty(B, cfg["topk"], dtype=torch.int32, device=dev), cfg["T"])
@@ -457,7 +460,7 @@ def _split_main(args, cfg, world, rank, local, dev, ddata, teacher, student_h, t
     if is_student:
         sampler = DeviceShardSampler(ddata, pl.n_students, rank, B, seed=0)
         engine = StudentStep(Model.from_host(student_h, dev), tcfg, B, pl.n_students, process_group=sgroup,
-                             max_steps=W + K + 8)
+                             max_steps=W + K + 8, exchange=args.exchange)
 
     def run(start, count):
         barrier()

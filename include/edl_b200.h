@@ -125,6 +125,27 @@ int edl_kd_loss_fwd_bwd(const float* logits, long long ldz, const long long* lab
  * scale = eta / world_size folds the all-reduce mean (edl/allreduce.py:119). */
 int edl_sgd_step(float* p, void* p_bf16, const float* g, long long n, float scale, void* stream);
 
+/* Data-parallel gradient exchange fused with SGD, over NVSwitch multicast.
+ * Replaces, at world > 1, the ring all-reduce to the mean
+ * (edl/allreduce.py:77-120, called at edl/student_node.py:741) followed by
+ * sgd_step (edl/nnkit.py:312-322, edl/student_node.py:745). Every rank calls
+ * it on its stream after its gradient kernels; rank r sums shard r of the
+ * gradient across ranks in the switch, applies p -= scale * sum and writes
+ * the new fp32 and bf16 parameters into every rank's replica. When the
+ * kernel completes on any rank, all replicas are updated and identical.
+ *   mc_grad, mc_param, mc_param_bf16: multicast addresses of symmetric buffers
+ *       of n elements (fp32, fp32, bf16); n a multiple of 8 * world.
+ *   param: this rank's own fp32 replica (unicast address of mc_param's copy).
+ *   pads: device array of `world` pointers to the ranks' uint32 signal pads of
+ *       pad_bytes each (zero before the first call); counter: one device
+ *       uint32, zero before the first call.
+ *   scale: eta / world (the mean folded into the step).
+ *   epoch: strictly increasing per call, identical on all ranks.
+ * Errors: -1 bad shape, -3 bad rank/world/pad size, -4 CUDA. */
+int edl_nvls_allreduce_sgd(float* mc_grad, float* mc_param, void* mc_param_bf16, const float* param,
+                           unsigned* const* pads, long long pad_bytes, unsigned* counter, int rank, int world,
+                           long long n, float scale, unsigned epoch, void* stream);
+
 /* Batch gather from an HBM-resident shard, edl/student_node.py:150-151:
  * dst[b][:D] = src[idx[b]][:D] (bf16, idx int64) and, when both label
  * pointers are given, dst_labels[b] = src_labels[idx[b]] (int64). */

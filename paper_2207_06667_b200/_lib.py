@@ -19,6 +19,7 @@ _lib: ctypes.CDLL | None = None
 
 c_int, c_ll, c_float, c_void_p, c_char_p = (ctypes.c_int, ctypes.c_longlong, ctypes.c_float,
                                             ctypes.c_void_p, ctypes.c_char_p)
+c_uint = ctypes.c_uint
 
 # name -> argtypes (all return int unless listed in _RESTYPES)
 _SIGNATURES = {
@@ -46,6 +47,8 @@ _SIGNATURES = {
                             c_float, c_float, c_float, c_void_p, c_void_p, c_void_p, c_void_p,
                             c_ll, c_void_p, c_void_p],
     "edl_sgd_step": [c_void_p, c_void_p, c_void_p, c_ll, c_float, c_void_p],
+    "edl_nvls_allreduce_sgd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_ll, c_void_p, c_int, c_int,
+                               c_ll, c_float, c_uint, c_void_p],
     "edl_gather_rows": [c_void_p, c_ll, c_void_p, c_void_p, c_ll, c_int, c_int, c_void_p, c_void_p,
                         c_void_p],
     "edl_topk_hits": [c_void_p, c_ll, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p],

@@ -428,6 +428,35 @@ int edl_kd_loss_fwd_bwd(const float* logits, long long ldz, const long long* lab
   return e == cudaSuccess ? 0 : cuda_fail(e, "kd_loss");
 }
 
+int edl_nvls_allreduce_sgd(float* mc_grad, float* mc_param, void* mc_param_bf16, const float* param,
+                           unsigned* const* pads, long long pad_bytes, unsigned* counter, int rank, int world,
+                           long long n, float scale, unsigned epoch, void* stream) {
+  if (world < 2 || world > 64 || rank < 0 || rank >= world || !pads || !counter)
+    return fail(EDL_ERR_PARAM, "nvls_allreduce_sgd: bad rank %d / world %d", rank, world);
+  if (n < 8 || n % (8LL * world) || !mc_grad || !mc_param || !mc_param_bf16 || !param)
+    return fail(EDL_ERR_SHAPE, "nvls_allreduce_sgd: n=%lld must be a positive multiple of 8*world", n);
+  const int max_blocks = nvls_max_blocks(world, pad_bytes);
+  if (max_blocks < 1) return fail(EDL_ERR_PARAM, "nvls_allreduce_sgd: signal pad of %lld bytes too small", pad_bytes);
+  // A small grid: it runs beside the co-located teacher's persistent GEMMs,
+  // which leave only the stream reserve free (edl_set_stream_max_ctas);
+  // blocks that cannot be resident would wait out a whole teacher GEMM.
+  // EDL_NVLS_BLOCKS overrides (tuning runs).
+  static const int env_blocks = [] {
+    const char* v = getenv("EDL_NVLS_BLOCKS");
+    return v ? atoi(v) : 0;
+  }();
+  const long long items = n / 8 / world;
+  long long blocks = (items + 511) / 512;
+  const long long want = env_blocks > 0 ? env_blocks : 24;
+  if (blocks > want) blocks = want;
+  if (blocks > num_sms()) blocks = num_sms();
+  if (blocks > max_blocks) blocks = max_blocks;
+  cudaError_t e = launch_nvls_allreduce_sgd(mc_grad, mc_param, mc_param_bf16, param,
+                                            reinterpret_cast<uint32_t* const*>(pads), counter, n, scale, epoch,
+                                            rank, world, static_cast<int>(blocks), as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "nvls_allreduce_sgd");
+}
+
 int edl_sgd_step(float* p, void* p_bf16, const float* g, long long n, float scale, void* stream) {
   if (n < 0) return fail(EDL_ERR_SHAPE, "sgd_step: n=%lld", n);
   if ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(g)) & 15)

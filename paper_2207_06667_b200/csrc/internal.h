@@ -89,6 +89,11 @@ int grouped_tile_bn();
 cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
                         int M, int N, int K, const EpiArgs& ep, int num_sms,
                         cudaStream_t stream);
+// Fused gradient exchange + SGD over NVSwitch multicast (exchange.cu).
+int nvls_max_blocks(int world, long long pad_bytes);
+cudaError_t launch_nvls_allreduce_sgd(float* mc_grad, float* mc_param, void* mc_bf16, const float* param,
+                                      uint32_t* const* pads, uint32_t* counter, long long n, float scale,
+                                      uint32_t epoch, int rank, int world, int blocks, cudaStream_t stream);
 // 256 x bn tiles on CTA pairs (cta_group::2); bn in {128, 256}; B's tensor
 // map box covers bn/2 rows (K-major) or bn/2 columns (MN-major).
 cudaError_t launch_gemm_pair(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,

@@ -75,10 +75,13 @@ class StudentConfig:
     max_steps: int = 0
     consume_timeout: float | None = None
     k: int | None = None          # top-k soft labels; None -> min(classes, 32)
+    exchange: str = "nccl"        # world > 1 gradient exchange: "nccl" or "nvls" (fused kernel, exchange.py)
 
     def __post_init__(self):
         if self.mode not in (MODE_EDL, MODE_NTRAIN, MODE_ONLINE):
             raise ValueError(f"unknown mode {self.mode!r}")
+        if self.exchange not in ("nvls", "nccl"):
+            raise ValueError(f"unknown exchange {self.exchange!r}")
 
 
 @dataclass
@@ -148,7 +151,8 @@ class StudentStep:
     step on the current stream and never allocates or synchronises."""
 
     def __init__(self, model: Model, cfg: TrainConfig, batch_size: int, world_size: int = 1,
-                 process_group=None, max_steps: int = 1 << 16, fuse_sgd: bool = True):
+                 process_group=None, max_steps: int = 1 << 16, fuse_sgd: bool = True,
+                 exchange: str = "nccl"):
         self.model = model
         self.cfg = cfg
         self.world_size = world_size
@@ -160,6 +164,18 @@ class StudentStep:
                            torch.empty(batch_size, dtype=torch.int64, device=model.device), model.input_dim)
         self.losses = torch.zeros(max_steps, dtype=torch.float32, device=model.device)
         self._n = 0
+        # world > 1: NCCL all-reduce + SGD (default), or exchange="nvls": the
+        # gradient exchange + SGD in one NVSwitch-multicast kernel (exchange.py;
+        # NCCL if the box has no multicast). Measured on this pool's B200s the
+        # fused kernel is slower than NCCL + SGD (profiles/r01_exchange_ab.json),
+        # so it is opt-in.
+        self.exchange = None
+        if world_size > 1 and exchange == "nvls":
+            from .exchange import ExchangeUnavailable, NvlsGradientExchange
+            try:
+                self.exchange = NvlsGradientExchange(model, self.ws.grads, process_group)
+            except ExchangeUnavailable:
+                self.exchange = None
 
     def step(self, batch: Batch, soft: SoftLabels | None) -> None:
         i = self._n % self.losses.shape[0]
@@ -169,9 +185,12 @@ class StudentStep:
                           fused_sgd_eta=self.cfg.eta)
         else:
             nnkit.kd_loss(self.model, batch, soft, self.cfg, ws=self.ws, loss_slot=self.losses[i:i + 1])
-            if self.world_size > 1:
-                torch.distributed.all_reduce(self.ws.grads.flat, group=self.group)
-            nnkit.sgd_step(self.model, self.ws.grads, self.cfg.eta, self.world_size)
+            if self.exchange is not None:
+                self.exchange.step(self.cfg.eta)
+            else:
+                if self.world_size > 1:
+                    torch.distributed.all_reduce(self.ws.grads.flat, group=self.group)
+                nnkit.sgd_step(self.model, self.ws.grads, self.cfg.eta, self.world_size)
         self._n += 1
 
     def loss_values(self) -> list[float]:
@@ -264,7 +283,7 @@ class StudentNode:
         host, start = self.initial_model()
         model = Model.from_host(host, self.dataset.device)
         engine = StudentStep(model, train_cfg, cfg.train.batch_size, cfg.world_size, self.group,
-                             max_steps=max(self.total_steps, 1))
+                             max_steps=max(self.total_steps, 1), exchange=cfg.exchange)
         engine._n = start
         reader = None
         online_out = None

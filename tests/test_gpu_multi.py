@@ -68,7 +68,7 @@ def _free_port():
     return p
 
 
-def _nccl_student(rank, world, port, q):
+def _nccl_student(rank, world, port, q, exchange="nvls"):
     import torch.distributed as dist
 
     from paper_2207_06667_b200 import formats
@@ -82,7 +82,7 @@ def _nccl_student(rank, world, port, q):
         cfg = StudentConfig(rank=rank, world_size=world, mode="online",
                             data=DataSpec(seed=0, n=2048, dim=16, classes=10, spread=1.0),
                             train=TrainConfig(eta=0.05, alpha=0.5, beta=0.5, temperature=2.0, batch_size=32),
-                            max_steps=int(d["vc_steps"]), k=10)
+                            max_steps=int(d["vc_steps"]), k=10, exchange=exchange)
         node = StudentNode(cfg, teacher_model=_host(d["teacher"], (16, 256, 256, 10)))
         res = node.run()
         q.put((rank, ref.flatten(list(res.model.weights), list(res.model.biases))))
@@ -91,12 +91,13 @@ def _nccl_student(rank, world, port, q):
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-def test_two_students_nccl_vs_virtual_cluster():
+@pytest.mark.parametrize("exchange", ["nvls", "nccl"])
+def test_two_students_nccl_vs_virtual_cluster(exchange):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_nccl_student, args=(r, 2, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=_nccl_student, args=(r, 2, port, q, exchange)) for r in range(2)]
     for p in ps:
         p.start()
     out = dict(q.get(timeout=300) for _ in ps)
@@ -104,9 +105,74 @@ def test_two_students_nccl_vs_virtual_cluster():
         p.join(timeout=120)
         assert p.exitcode == 0
     d = _golden()
-    assert np.array_equal(out[0], out[1])                    # NCCL: bitwise identical across ranks
+    assert np.array_equal(out[0], out[1])                    # bitwise identical replicas across ranks
     rel = np.linalg.norm(out[0] - d["vc_final"]) / np.linalg.norm(d["vc_final"])
     assert rel < 2e-2, rel
+
+
+def _exchange_rank(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2207_06667_b200 import formats
+    from paper_2207_06667_b200.exchange import ExchangeUnavailable, NvlsGradientExchange
+    from paper_2207_06667_b200.nnkit import Model, Workspace
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        dims = (200, 96, 37)                      # padded layout with ragged tails
+        model = Model.from_host(formats.init_model(dims, 3))
+        ws = Workspace(model, 8)
+        try:
+            ex = NvlsGradientExchange(model, ws.grads)
+        except ExchangeUnavailable as e:
+            q.put((rank, "unavailable", str(e)))
+            return
+        n = model.layout.size
+        eta = 0.07
+        p = model.flat.clone()
+        out = []
+        for epoch in range(3):
+            gens = [torch.Generator().manual_seed(100 * epoch + r) for r in range(world)]
+            gs = [torch.randn(n, generator=g) for g in gens]
+            ws.grads.flat.copy_(gs[rank].cuda())
+            ex.step(eta)
+            torch.cuda.synchronize()
+            want = p.cpu() - (eta / world) * torch.stack(gs).sum(0)
+            out.append((model.flat.cpu().numpy().copy(), want.numpy(),
+                        bool(torch.equal(model.flat_bf16.cpu(), model.flat.cpu().to(torch.bfloat16)))))
+            p = model.flat.clone()
+        q.put((rank, "ok", out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_nvls_exchange_sgd_matches_mean_update():
+    """edl_nvls_allreduce_sgd: every replica equals p - eta * mean_r(g_r)
+    (edl/allreduce.py:77-120 + edl/nnkit.py:312-322), bitwise identical across
+    ranks, bf16 copy = bf16(fp32 master), over consecutive epochs."""
+    import torch.multiprocessing as mp
+    world = min(torch.cuda.device_count(), 4)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_exchange_rank, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict((r, (status, payload)) for r, status, payload in (q.get(timeout=300) for _ in ps))
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    if any(st == "unavailable" for st, _ in res.values()):
+        pytest.skip(f"no NVLS multicast: {res[0][1]}")
+    for epoch in range(3):
+        ref0 = res[0][1][epoch][0]
+        for r in range(world):
+            got, want, bf_ok = res[r][1][epoch]
+            assert np.array_equal(got, ref0)                  # identical replicas
+            np.testing.assert_allclose(got, want, rtol=1e-6, atol=1e-6)
+            assert bf_ok
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
