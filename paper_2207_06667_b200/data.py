@@ -51,26 +51,37 @@ class DeviceShardSampler:
         self.batches_per_epoch = (n // world_size) // batch_size
         if self.batches_per_epoch < 1:
             raise ValueError("shard smaller than one batch")
-        self._orders: dict[int, torch.Tensor] = {}
+        self._orders: dict[int, tuple] = {}
+        self._copy_stream = torch.cuda.Stream(data.device)
+
+    # Epoch permutations are uploaded on a private copy stream one epoch
+    # ahead. Their readers are gathers on several streams (the student's, each
+    # teacher worker's), so the upload must be complete before any of them is
+    # enqueued: rows_for waits on the upload's event on the host, which costs
+    # nothing because it was issued an epoch earlier. (An upload on the
+    # caller's stream left teacher-stream gathers racing it.)
+    _KEEP = 4   # epochs kept: the current one, two behind (in-flight readers), one ahead
+
+    def _upload(self, epoch: int) -> None:
+        host = torch.from_numpy((epoch_order(self.seed, epoch, self.rank, self.hi - self.lo)
+                                 + self.lo).astype(np.int64)).pin_memory()
+        with torch.cuda.stream(self._copy_stream):
+            order = host.to(self.data.device, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(self._copy_stream)
+        self._orders[epoch] = (order, host, done)
 
     def rows_for(self, iteration: int) -> torch.Tensor:
         """Global dataset row indices (device int64 [B]) of batch `iteration`."""
         epoch, i = divmod(iteration, self.batches_per_epoch)
-        order = self._orders.get(epoch)
-        if order is None:
-            host = torch.from_numpy((epoch_order(self.seed, epoch, self.rank, self.hi - self.lo)
-                                     + self.lo).astype(np.int64)).pin_memory()
-            # pinned + non_blocking: a pageable copy would block the host until
-            # the stream drains, a bubble in the enqueue-ahead pipeline every epoch
-            order = host.to(self.data.device, non_blocking=True)
-            # keep a few epochs alive (device tensor + its pinned source, which
-            # must outlive the async copy): in-flight teacher / student work
-            # may still read the previous epoch's permutation on other streams
-            if len(self._orders) >= 3:
-                self._orders.pop(min(self._orders))
-            self._orders[epoch] = (order, host)
-        else:
-            order = order[0]
+        if epoch not in self._orders:
+            self._upload(epoch)
+        order, _, done = self._orders[epoch]
+        done.synchronize()
+        if epoch + 1 not in self._orders:
+            self._upload(epoch + 1)
+        while len(self._orders) > self._KEEP:   # drop the epoch farthest from the current one
+            self._orders.pop(max(self._orders, key=lambda e: (abs(e - epoch), e)))
         return order[i * self.batch_size:(i + 1) * self.batch_size]
 
     def batch_for(self, iteration: int, out: Batch | None = None, stream=None) -> Batch:

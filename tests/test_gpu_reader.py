@@ -229,3 +229,28 @@ def test_drop_and_readd_teachers_mid_run_keeps_trajectory():
     a = ref.flatten(clean.model.weights, clean.model.biases)
     b = ref.flatten(faulty.model.weights, faulty.model.biases)
     assert np.array_equal(a, b)
+
+
+def test_epoch_permutation_ready_for_other_streams():
+    """A new epoch's row permutation must be usable by a gather on ANOTHER
+    stream right after rows_for returns, even while the calling stream is
+    still busy (teacher workers gather on their own streams). Regression: the
+    upload used to ride the caller's stream, so a teacher-stream gather could
+    read the index buffer before it landed (illegal address under load)."""
+    from paper_2207_06667_b200 import formats
+    from paper_2207_06667_b200.data import DeviceDataset, DeviceShardSampler, gather_batch
+    from paper_2207_06667_b200.formats import epoch_order
+    host = formats.make_blobs(0, 4096, 48, 10, 1.0)
+    data = DeviceDataset(host)
+    sampler = DeviceShardSampler(data, 1, 0, 256, seed=3)
+    other = torch.cuda.Stream()
+    for epoch in range(6):
+        torch.cuda._sleep(50_000_000)                # the caller's stream stays busy for ~25 ms
+        rows = sampler.rows_for(epoch * sampler.batches_per_epoch + 5)
+        with torch.cuda.stream(other):
+            b = gather_batch(data, rows, stream=other)
+            got = b.hard_labels.clone()
+        other.synchronize()
+        want = epoch_order(3, epoch, 0, 4096)[5 * 256:6 * 256]
+        assert np.array_equal(got.cpu().numpy(), host.labels[want])
+    torch.cuda.synchronize()
