@@ -283,11 +283,13 @@ def main():
     student = Model.from_host(student_h, dev)
     engine = StudentStep(student, tcfg, B, world, max_steps=W + K + 8, exchange=args.exchange)
     pool = TeacherPool()
-    # Sweeps on B200 (profiles/README.md): N=4, reserve 0/8/16/24/32 SMs ->
-    # EDL 13.5/14.2/14.0/14.3/14.6 M samples/s (online 13.8-14.5 M); N=1,
-    # reserve 0/16/32/48 -> 4.04/4.16/4.11/2.0 M (online 3.96 M): 16 SMs let
-    # the student's single-wave kernels run beside the teacher's GEMMs.
-    reserve = args.teacher_sm_reserve if args.teacher_sm_reserve >= 0 else (32 if world > 1 else 16)
+    # Same-box sweeps with the CTA-pair GEMMs (profiles/r01_reserve_sweep.txt):
+    # N=1, reserve 0/8/16/24 -> 4.47-4.70 / 4.40-4.60 / 4.77-5.02 / 4.60-4.81
+    # M samples/s; N=2, 40/48/56 -> 8.70-8.82 / 8.56-8.66 / 8.35 M; N=4,
+    # 40/48/56 -> 17.17-17.35 / 17.19-17.23 / 16.3-16.6 M. The reserved SMs
+    # let the student's one-wave kernels (and at N>1 NCCL's all-reduce) run
+    # beside the teacher's persistent GEMMs.
+    reserve = args.teacher_sm_reserve if args.teacher_sm_reserve >= 0 else (40 if world > 1 else 16)
     worker = TeacherWorker(TeacherConfig("t1", cfg["T"], cfg["topk"]), teacher, ddata, sm_reserve=reserve)
     pool.register(worker)
     sched = SchedulerConfig(lt=2, ut=8, pipeline_depth=2, acquire_cooldown=1e9)
