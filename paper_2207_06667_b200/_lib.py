@@ -12,7 +12,9 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libedl_b200.so")
+# EDL_LIB points at another build of the same library (same-box A/B runs of
+# two kernel versions, scripts/ab_lib.sh); the default is the in-tree build.
+LIB_PATH = os.environ.get("EDL_LIB") or os.path.join(_HERE, "libedl_b200.so")
 
 _lock = threading.Lock()
 _lib: ctypes.CDLL | None = None

@@ -37,7 +37,8 @@ struct GemmCfg {
   static constexpr uint32_t kABytes = kBM * kBK * 2;
   static constexpr uint32_t kBBytes = BN * kBK * 2;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-  static constexpr uint32_t kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t kEpiBytes = 2 * BN * 4;   // double-buffered bias slice
+  static constexpr uint32_t kSmem = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 // Issue the TMA loads of one (A,B) k-block into stage buffers, with per-operand
@@ -90,12 +91,27 @@ __device__ __forceinline__ void mma_kblock(uint32_t d_tmem, uint32_t a_base, uin
 
 // ------------------------------------------------------------------ epilogues
 template <int EPI>
+__host__ __device__ constexpr bool epi_has_bias() {
+  return EPI == EPI_TANH_BF16 || EPI == EPI_BIAS_F32;
+}
+
+// sb: this chunk's 32 bias values staged in shared memory (stage_bias), or
+// null to read ep.bias from global memory.
+template <int EPI>
 __device__ __forceinline__ void epilogue_store(const EpiArgs& ep, int row, int M, int col0,
-                                               int N, float (&v)[32]) {
+                                               int N, float (&v)[32], const float* sb = nullptr,
+                                               const uint4* hpre = nullptr) {
   if (row >= M) return;
   const bool full = (col0 + 32 <= N);
   if constexpr (EPI == EPI_TANH_BF16 || EPI == EPI_BIAS_F32) {
-    if (ep.bias != nullptr) {
+    if (sb != nullptr) {
+      const float4* b4 = reinterpret_cast<const float4*>(sb);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float4 b = b4[i];
+        v[4 * i] += b.x; v[4 * i + 1] += b.y; v[4 * i + 2] += b.z; v[4 * i + 3] += b.w;
+      }
+    } else if (ep.bias != nullptr) {
       if (full) {
         const float4* b4 = reinterpret_cast<const float4*>(ep.bias + col0);
 #pragma unroll
@@ -119,7 +135,7 @@ __device__ __forceinline__ void epilogue_store(const EpiArgs& ep, int row, int M
     if (full) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        uint4 q = __ldg(reinterpret_cast<const uint4*>(h) + i);
+        uint4 q = hpre != nullptr ? hpre[i] : __ldg(reinterpret_cast<const uint4*>(h) + i);
         const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&q);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -206,6 +222,63 @@ __device__ __forceinline__ void epilogue_store(const EpiArgs& ep, int row, int M
   }
 }
 
+// Stage the tile's bias slice [n0, n0 + BN) in shared memory; `et` is the
+// thread's index among the 128 epilogue threads. Done before waiting for the
+// accumulator, so the chunk loop's bias adds never wait on L2.
+template <int BN, int EPI>
+__device__ __forceinline__ void stage_bias(const EpiArgs& ep, float* sb, int n0, int N, int et) {
+  if constexpr (epi_has_bias<EPI>()) {
+    for (int j = et; j < BN; j += 128)
+      sb[j] = (ep.bias != nullptr && n0 + j < N) ? __ldg(ep.bias + n0 + j) : 0.f;
+  }
+}
+
+// One accumulator tile (this warp's 32 rows x BN columns at TMEM address
+// taddr) through the epilogue, the TMEM load of chunk c+1 in flight while
+// chunk c is processed and stored. In one-wave GEMMs nothing hides the
+// epilogue, so its serial load latencies were the kernel's critical path.
+template <int BN, int EPI>
+__device__ __forceinline__ void epilogue_tile(const EpiArgs& ep, uint32_t taddr, int row, int M, int n0,
+                                              int N, const float* sb) {
+  // EPI_DTANH_BF16 reads the layer's activations: the next chunk's 64 bytes
+  // are loaded together with the next TMEM chunk
+  constexpr bool kAux = EPI == EPI_DTANH_BF16;
+  const bool row_ok = row < M;
+  auto aux_ptr = [&](int c) {
+    return reinterpret_cast<const uint4*>(ep.aux + static_cast<size_t>(row) * ep.ld_aux + n0 + c);
+  };
+  uint4 h[4];
+  if constexpr (kAux) {
+    if (row_ok && n0 + 32 <= N) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) h[i] = __ldg(aux_ptr(0) + i);
+    }
+  }
+  uint32_t r[32];
+  tmem_ld32_issue(taddr, r);
+  tmem_ld_wait(r);
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 32) {
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+    uint4 hc[4];
+    if constexpr (kAux) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) hc[i] = h[i];
+      if (row_ok && c + 32 < BN && n0 + c + 64 <= N) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = __ldg(aux_ptr(c + 32) + i);
+      }
+    }
+    if (c + 32 < BN) tmem_ld32_issue(taddr + c + 32, r);
+    if (n0 + c < N)
+      epilogue_store<EPI>(ep, row, M, n0 + c, N, v, sb != nullptr ? sb + c : nullptr,
+                          (kAux && n0 + c + 32 <= N) ? hc : nullptr);
+    if (c + 32 < BN) tmem_ld_wait(r);
+  }
+}
+
 // ------------------------------------------------------------------ GEMM
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -220,7 +293,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kBBytes);
+  float* sbias = reinterpret_cast<float*>(sB + S * Cfg::kBBytes);   // [2][BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kBBytes + Cfg::kEpiBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -312,16 +386,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(&tile_empty[slot]);
       if (t >= tiles) break;
       const int m0 = (t % num_m) * kBM, n0 = (t / num_m) * BN;
+      float* sb = sbias + (i & 1) * BN;
+      stage_bias<BN, EPI>(ep, sb, n0, N, static_cast<int>(threadIdx.x) - 128);
+      if constexpr (epi_has_bias<EPI>()) epi_bar_sync();
       const uint32_t as = i & 1;
       mbar_wait(&tfull[as], (i >> 1) & 1);
       tc_fence_after();
-      const int row = m0 + 32 * e + lane;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        float v[32];
-        tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN + c, v);
-        if (n0 + c < N) epilogue_store<EPI>(ep, row, M, n0 + c, N, v);
-      }
+      epilogue_tile<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e + lane,
+                             M, n0, N, epi_has_bias<EPI>() ? sb : nullptr);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[as]);
@@ -360,7 +432,8 @@ struct PairCfg {
   static constexpr uint32_t kBBytes = kHalfN * kBK * 2;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
-  static constexpr uint32_t kSmem = kStages * kStageBytes + 1024 + 256;
+  static constexpr uint32_t kEpiBytes = 2 * BN * 4;
+  static constexpr uint32_t kSmem = kStages * kStageBytes + kEpiBytes + 1024 + 256;
 };
 
 template <int BN, bool A_MN, bool B_MN>
@@ -409,7 +482,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kBBytes);
+  float* sbias = reinterpret_cast<float*>(sB + S * Cfg::kBBytes);   // [2][BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kBBytes + Cfg::kEpiBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -512,16 +586,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (t >= tiles) break;
       const int m0 = (t % num_m) * 2 * kBM + static_cast<int>(rank) * kBM;
       const int n0 = (t / num_m) * BN;
+      float* sb = sbias + (i & 1) * BN;
+      stage_bias<BN, EPI>(ep, sb, n0, N, static_cast<int>(threadIdx.x) - 128);
+      if constexpr (epi_has_bias<EPI>()) epi_bar_sync();
       const uint32_t as = i & 1;
       mbar_wait(&tfull[as], (i >> 1) & 1);
       tc_fence_after();
-      const int row = m0 + 32 * e + lane;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        float v[32];
-        tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN + c, v);
-        if (n0 + c < N) epilogue_store<EPI>(ep, row, M, n0 + c, N, v);
-      }
+      epilogue_tile<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e + lane,
+                             M, n0, N, epi_has_bias<EPI>() ? sb : nullptr);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty0 + 8 * as);
@@ -556,7 +628,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kBBytes);
+  float* sbias = reinterpret_cast<float*>(sB + S * Cfg::kBBytes);   // [2][BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kBBytes + Cfg::kEpiBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -633,12 +706,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int row = m0 + 32 * e + lane;
       const int M = ga.M[p], N = ga.N[p];
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        float v[32];
-        tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN + c, v);
-        if (n0 + c < N) epilogue_store<EPI>(ga.ep[p], row, M, n0 + c, N, v);
-      }
+      epilogue_tile<BN, EPI>(ga.ep[p], tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, row, M, n0,
+                             N, nullptr);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[as]);
@@ -781,10 +850,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kBBytes);
+  float* sbias = reinterpret_cast<float*>(sB + S * Cfg::kBBytes);   // [2][BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kBBytes + Cfg::kEpiBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  (void)sbias;
   // Epilogue scratch reuses the drained operand ring (word-interleaved by
   // thread / row so every access is bank-conflict free):
   float* stage = reinterpret_cast<float*>(smem);                    // [32][256] candidates
