@@ -855,7 +855,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
-  (void)sbias;
   // Epilogue scratch reuses the drained operand ring (word-interleaved by
   // thread / row so every access is bank-conflict free):
   float* stage = reinterpret_cast<float*>(smem);                    // [32][256] candidates
@@ -912,20 +911,37 @@ __global__ void __launch_bounds__(kThreads, 1)
   TopK<KMAX> top;
   top.init();
   float run_m = -INFINITY, run_l = 0.f;
+  // the class chunk's bias, staged by warps 2-7 while the MMAs run; warps 0/1
+  // join the barrier when their producer / MMA loops are done
+  if (warp >= 2) {
+    for (int j = tid - 64; j < BN; j += kThreads - 64)
+      sbias[j] = (n0 + j < N) ? __ldg(hp.bias + n0 + j) : 0.f;
+  }
+  asm volatile("bar.sync 2, 256;" ::: "memory");
   mbar_wait(&tfull[0], 0);
   tc_fence_after();
   bool first = true;
+  const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * q) << 16);
+  uint32_t r[32];
+  tmem_ld32_issue(taddr + 32 * half, r);
+  tmem_ld_wait(r);
 #pragma unroll 1
   for (int c = 32 * half; c < BN; c += 64) {
     float v[32];
-    tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + c, v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+    const bool more = c + 64 < BN;
+    if (more) tmem_ld32_issue(taddr + c + 64, r);   // next chunk's load overlaps this one's work
     const int col0 = n0 + c;
-    if (col0 >= N) continue;
+    if (col0 >= N) {
+      if (more) tmem_ld_wait(r);
+      continue;
+    }
     float cmax = -INFINITY;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int n = col0 + j;
-      const float s = (n < N) ? (v[j] + __ldg(hp.bias + n)) * hp.inv_t : -INFINITY;
+      const float s = (n < N) ? (v[j] + sbias[c + j]) * hp.inv_t : -INFINITY;
       v[j] = s;
       cmax = fmaxf(cmax, s);
     }
@@ -944,6 +960,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       bitonic_sort<32>(v, ix);
 #pragma unroll
       for (int j = 0; j < KMAX; ++j) { top.v[j] = v[j]; top.i[j] = ix[j]; }
+      if (more) tmem_ld_wait(r);
       continue;
     }
     // later chunks: only columns beating the current k-th entry (rare), each
@@ -963,6 +980,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (Key::better(x, col0 + j, top.v[KMAX - 1], top.i[KMAX - 1])) top.insert(x, col0 + j);
       }
     }
+    __syncwarp();   // the insertions above diverge; tcgen05.wait::ld is .sync.aligned
+    if (more) tmem_ld_wait(r);
   }
   tc_fence_before();
   // halves -> one state per row (half 1 hands over through shared memory)
