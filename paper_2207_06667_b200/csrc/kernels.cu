@@ -41,7 +41,7 @@ __device__ __forceinline__ void set_status(int* status, int code) {
 constexpr int kKdWarps = 8;
 
 template <int KPL>
-__global__ void __launch_bounds__(kKdWarps * 32, (KPL >= 64) ? 1 : 3)
+__global__ void __launch_bounds__(kKdWarps * 32, (KPL >= 64) ? 1 : (KPL >= 32 ? 2 : 3))
     kd_loss_kernel(const float* __restrict__ z, long long ld_z, const int64_t* __restrict__ labels,
                    const float* __restrict__ qv, const int* __restrict__ qi, int B, int K,
                    int Kw, int k, float alpha, float beta, float T, float* __restrict__ row_loss,
@@ -75,17 +75,25 @@ __global__ void __launch_bounds__(kKdWarps * 32, (KPL >= 64) ? 1 : 3)
 #pragma unroll
     for (int i = 0; i < KPL; ++i) m = fmaxf(m, v[i]);
     m = warp_max(m);
+    // the exponentials of both log-sum-exps are kept (v -> exp(z - m), et ->
+    // exp((z - m) / T)) and reused for the softmaxes in dz: two MUFU.EX2 per
+    // element instead of four (z itself is re-read from L2 only at the k soft
+    // classes and at the label)
     float s1 = 0.f, st = 0.f;
+    float et[KPL];
 #pragma unroll
     for (int i = 0; i < KPL; ++i) {
       const float d = v[i] - m;
-      s1 += __expf(d);
-      st += __expf(d * inv_t);
+      v[i] = __expf(d);
+      et[i] = __expf(d * inv_t);
+      s1 += v[i];
+      st += et[i];
     }
     s1 = warp_sum(s1);
     st = warp_sum(st);
     const float lse1 = m + __logf(s1);
     const float lset = m * inv_t + __logf(st);
+    const float inv_s1 = 1.0f / s1, inv_st = 1.0f / st;
     const bool y_ok = (y >= 0 && y < K);
     if (!y_ok && lane == 0) set_status(status, -1);
     if (use_soft) {
@@ -97,8 +105,8 @@ __global__ void __launch_bounds__(kKdWarps * 32, (KPL >= 64) ? 1 : 3)
     for (int i = 0; i < KPL; ++i) {
       const int c = lane + 32 * i;
       float d = 0.f;
-      if (alpha > 0.f) d += ch * (__expf(v[i] - lse1) - (c == y ? 1.f : 0.f));
-      if (use_soft) d += cs * __expf(v[i] * inv_t - lset);
+      if (alpha > 0.f) d += ch * (v[i] * inv_s1 - (c == y ? 1.f : 0.f));
+      if (use_soft) d += cs * (et[i] * inv_st);
       ds[c] = d;
     }
     __syncwarp();
@@ -139,9 +147,10 @@ __global__ void __launch_bounds__(256) loss_mean_kernel(const float* __restrict_
                                                          float* __restrict__ loss_out,
                                                          int* __restrict__ status) {
   griddep_wait();
-  __shared__ double red[256];
+  __shared__ double red[8];
   // 8 independent loads in flight per thread (a dependent strided loop would
-  // serialise on L2 latency)
+  // serialise on L2 latency); fixed-order shuffle + 8-way tree, no grid
+  // dependence, so the mean is bitwise reproducible
   double acc = 0.0;
   for (int r0 = threadIdx.x; r0 < B; r0 += 8 * blockDim.x) {
     float f[8];
@@ -153,14 +162,15 @@ __global__ void __launch_bounds__(256) loss_mean_kernel(const float* __restrict_
 #pragma unroll
     for (int u = 0; u < 8; ++u) acc += static_cast<double>(f[u]);
   }
-  red[threadIdx.x] = acc;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-    __syncthreads();
-  }
   if (threadIdx.x == 0) {
-    const float loss = static_cast<float>(red[0] / static_cast<double>(B));
+    double tot = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) tot += red[w];
+    const float loss = static_cast<float>(tot / static_cast<double>(B));
     *loss_out = loss;
     if (!isfinite(loss)) set_status(status, -2);
   }
