@@ -128,12 +128,16 @@ int pick_bn(int M, int N) { return pick_bn_cap(M, N, num_sms()); }
 // (measured on B200: teacher layers 437 -> 380 us, student layer 1 49.6 ->
 // 42.5 us), so they win whenever their wave count is no worse. Returns 0 to
 // use the single-CTA kernel. EDL_GEMM_PAIR=0 forces single-CTA (A/B runs).
-int pick_pair_bn(int M, int N, int cap) {
+bool pair_mode_enabled() {
   static const int mode = [] {
     const char* v = getenv("EDL_GEMM_PAIR");
     return v ? atoi(v) : 1;
   }();
-  if (mode == 0 || cap < 2 || N <= 128) return 0;
+  return mode != 0;
+}
+
+int pick_pair_bn(int M, int N, int cap) {
+  if (!pair_mode_enabled() || cap < 2 || N <= 128) return 0;
   const int bn = pick_bn_cap(M, N, cap);
   const long long single = ((static_cast<long long>((M + 127) / 128) * ((N + bn - 1) / bn) + cap - 1) / cap) *
                            (bn + 48);
@@ -314,6 +318,18 @@ int bwd_weight_grouped_impl(int count, const void* const* dY, const long long* l
   std::memset(&ga, 0, sizeof(ga));
   ga.count = count;
   const int bn = grouped_tile_bn();
+  const int cap = grid_cap(as_stream(stream));
+  // CTA-pair tiles when their wave-quantised cost is no worse (pick_pair_bn's
+  // rule on the summed tile counts)
+  long long single_tiles = 0, pair_tiles = 0;
+  for (int p = 0; p < count; ++p) {
+    single_tiles += static_cast<long long>((N[p] + 127) / 128) * ((K[p] + bn - 1) / bn);
+    pair_tiles += static_cast<long long>((N[p] + 255) / 256) * ((K[p] + 255) / 256);
+  }
+  const long long single_waves = (single_tiles + cap - 1) / cap;
+  const long long pair_waves = cap >= 2 ? (pair_tiles + cap / 2 - 1) / (cap / 2) : 0;
+  const bool use_pair = cap >= 2 && pair_mode_enabled() &&
+                        (pair_waves < single_waves || (pair_waves == single_waves && pair_waves >= 2));
   int tiles = 0;
   for (int p = 0; p < count; ++p) {
     if (M[p] < 1 || N[p] < 1 || K[p] < 1 || lddy[p] < N[p] || ldx[p] < K[p] || lddw[p] < K[p])
@@ -329,10 +345,11 @@ int bwd_weight_grouped_impl(int count, const void* const* dY, const long long* l
                        sgd ? reinterpret_cast<__nv_bfloat16*>(W16[p]) : nullptr};
     if (sgd && !W16[p]) return fail(EDL_ERR_SHAPE, "linear_bwd_weight_grouped_sgd[%d]: missing bf16 copy", p);
     ga.tile_start[p] = tiles;
-    tiles += ((N[p] + 127) / 128) * ((K[p] + bn - 1) / bn);
+    tiles += use_pair ? ((N[p] + 255) / 256) * ((K[p] + 255) / 256) : ((N[p] + 127) / 128) * ((K[p] + bn - 1) / bn);
   }
   ga.tile_start[count] = tiles;
-  cudaError_t e = launch_gemm_grouped_bwd_weight(maps, ga, grid_cap(as_stream(stream)), as_stream(stream), sgd);
+  cudaError_t e = use_pair ? launch_gemm_grouped_pair_bwd_weight(maps, ga, cap, as_stream(stream), sgd)
+                           : launch_gemm_grouped_bwd_weight(maps, ga, cap, as_stream(stream), sgd);
   if (e != cudaSuccess) return cuda_fail(e, "linear_bwd_weight_grouped");
   if (db) {
     ColsumGroup g = {};

@@ -612,6 +612,113 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------------------------------ grouped CTA-pair GEMM
+// The grouped dW launch (below) on 256 x 256 pair tiles: the pair kernel's
+// roles and barriers with a static pair schedule (tile t -> (problem, m0, n0)
+// through ga.tile_start, counted in pair tiles). Both operands MN-major.
+template <int BN, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_grouped_pair_kernel(const __grid_constant__ GroupMaps maps, GroupArgs ga) {
+  using Cfg = PairCfg<BN>;
+  constexpr int S = Cfg::kStages;
+  constexpr uint32_t kTmemCols = tmem_cols_for(2 * BN);
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * Cfg::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kBBytes + Cfg::kEpiBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();
+  if (warp == 0 && lane == 0) {
+    for (int p = 0; p < ga.count; ++p) { prefetch_tmap(&maps.a[p]); prefetch_tmap(&maps.b[p]); }
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 8); }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_pair<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();
+
+  const int tiles = ga.tile_start[ga.count];
+  const int pair = static_cast<int>(blockIdx.x) / 2;
+  const int npairs = static_cast<int>(gridDim.x) / 2;
+  auto locate = [&](int t, int& p, int& m0, int& n0) {
+    p = 0;
+    while (p + 1 < ga.count && t >= ga.tile_start[p + 1]) ++p;
+    const int local = t - ga.tile_start[p];
+    const int num_m = (ga.M[p] + 2 * kBM - 1) / (2 * kBM);
+    m0 = (local % num_m) * 2 * kBM + static_cast<int>(rank) * kBM;
+    n0 = (local / num_m) * BN;
+  };
+  const uint32_t full0 = mapa(smem_u32(full), 0);
+  const uint32_t tempty0 = mapa(smem_u32(tempty), 0);
+
+  if (warp == 0 && lane == 0) {
+    uint32_t g = 0;
+    for (int t = pair; t < tiles; t += npairs) {
+      int p, m0, n0;
+      locate(t, p, m0, n0);
+      const int nk = (ga.K[p] + kBK - 1) / kBK;
+      for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int s = g % S;
+        mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
+        if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * Cfg::kStageBytes);
+        load_kblock_pair<BN, A_MN, B_MN>(&maps.a[p], &maps.b[p], sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes,
+                                         full0 + 8 * s, m0, n0 + static_cast<int>(rank) * Cfg::kHalfN, kb * kBK);
+      }
+    }
+  } else if (warp == 1 && lane == 0 && rank == 0) {
+    uint32_t g = 0, i = 0;
+    for (int t = pair; t < tiles; t += npairs, ++i) {
+      int p, m0, n0;
+      locate(t, p, m0, n0);
+      const int nk = (ga.K[p] + kBK - 1) / kBK;
+      const uint32_t as = i & 1;
+      mbar_wait_cluster(&tempty[as], ((i >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + as * BN;
+      for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int s = g % S;
+        mbar_wait(&full[s], (g / S) & 1);
+        tc_fence_after();
+        mma_kblock_pair<BN, A_MN, B_MN>(d, smem_u32(sA + s * Cfg::kABytes), smem_u32(sB + s * Cfg::kBBytes),
+                                        kb == 0);
+        umma_commit_pair(&empty[s]);
+      }
+      umma_commit_pair(&tfull[as]);
+    }
+  } else if (warp >= 4) {
+    const int e = warp - 4;
+    uint32_t i = 0;
+    for (int t = pair; t < tiles; t += npairs, ++i) {
+      int p, m0, n0;
+      locate(t, p, m0, n0);
+      const uint32_t as = i & 1;
+      mbar_wait(&tfull[as], (i >> 1) & 1);
+      tc_fence_after();
+      epilogue_tile<BN, EPI>(ga.ep[p], tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN,
+                             m0 + 32 * e + lane, ga.M[p], n0, ga.N[p], nullptr);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty0 + 8 * as);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair<kTmemCols>(tmem_base);
+}
+
 // ------------------------------------------------------------------ grouped GEMM
 // Several independent problems in ONE persistent launch (the student's dW_l
 // for every layer: each alone has 32-192 output tiles, too few for 148 SMs;
@@ -1143,6 +1250,25 @@ cudaError_t launch_gemm_grouped_bwd_weight(const GroupMaps& maps, const GroupArg
                                            cudaStream_t stream, bool fused_sgd) {
   return fused_sgd ? launch_grouped_t<EPI_SGD_F32>(maps, ga, num_sms, stream)
                    : launch_grouped_t<EPI_F32>(maps, ga, num_sms, stream);
+}
+
+template <int EPI>
+static cudaError_t launch_grouped_pair_t(const GroupMaps& maps, const GroupArgs& ga, int num_sms,
+                                         cudaStream_t stream) {
+  constexpr int BN = 256;
+  auto kern = gemm_grouped_pair_kernel<BN, true, true, EPI>;
+  cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), PairCfg<BN>::kSmem);
+  if (e != cudaSuccess) return e;
+  const int tiles = ga.tile_start[ga.count];
+  const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
+  if (pairs < 1) return cudaErrorInvalidValue;
+  return launch_pdl(kern, dim3(2 * pairs), dim3(kThreads), PairCfg<BN>::kSmem, stream, 2, maps, ga);
+}
+
+cudaError_t launch_gemm_grouped_pair_bwd_weight(const GroupMaps& maps, const GroupArgs& ga, int num_sms,
+                                                cudaStream_t stream, bool fused_sgd) {
+  return fused_sgd ? launch_grouped_pair_t<EPI_SGD_F32>(maps, ga, num_sms, stream)
+                   : launch_grouped_pair_t<EPI_F32>(maps, ga, num_sms, stream);
 }
 
 int grouped_tile_bn() { return 256; }

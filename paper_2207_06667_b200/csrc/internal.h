@@ -85,6 +85,9 @@ struct GroupArgs {
 cudaError_t launch_gemm_grouped_bwd_weight(const GroupMaps& maps, const GroupArgs& ga, int num_sms,
                                            cudaStream_t stream, bool fused_sgd = false);
 int grouped_tile_bn();
+// The same on 256 x 256 CTA-pair tiles; ga.tile_start counts pair tiles.
+cudaError_t launch_gemm_grouped_pair_bwd_weight(const GroupMaps& maps, const GroupArgs& ga, int num_sms,
+                                                cudaStream_t stream, bool fused_sgd = false);
 
 cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
                         int M, int N, int K, const EpiArgs& ep, int num_sms,

@@ -205,10 +205,13 @@ def test_topk_hits_tie_rule(lib):
     assert hits.item() == 1   # constant logits: only class 0 ranks first
 
 
-def test_linear_bwd_weight_grouped_matches_reference(lib):
+@pytest.mark.parametrize("B,shapes", [
+    (300, [(208, 112), (64, 208), (16, 64)]),                    # single-CTA tiles
+    (4096, [(2048, 3072), (1024, 2048), (1008, 1024)]),          # cfg3 student: CTA-pair tiles
+    (4000, [(2000, 3008), (1008, 1984), (528, 1008)]),           # pair tiles, every dim ragged
+])
+def test_linear_bwd_weight_grouped_matches_reference(lib, B, shapes):
     # three student-like layers of different shapes in one launch
-    B = 300
-    shapes = [(208, 112), (64, 208), (16, 64)]    # (N_out, K_in), padded
     dys = [_padded(_rand(B, n, seed=20 + i), B, n) for i, (n, k) in enumerate(shapes)]
     xs = [_padded(_rand(B, k, seed=30 + i), B, k) for i, (n, k) in enumerate(shapes)]
     dws = [torch.full((n, k), float("nan"), device="cuda") for n, k in shapes]
