@@ -115,13 +115,17 @@ class ClockSampler:
             self._stop.wait(0.2)
 
     def __enter__(self):
+        self._edge_sample()      # the region's first instant (the thread can lag behind the enqueue loop's GIL)
         self._t.start()
         return self
 
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=6)
-        if not self.rows and self._nv is not None:   # region shorter than one period: sample at its end
+        self._edge_sample()      # and its last: the work was just enqueued / drained, clocks still loaded
+
+    def _edge_sample(self):
+        if self._nv is not None:
             try:
                 self._sample_nvml()
             except Exception:
@@ -401,7 +405,10 @@ def main():
     # ---------------- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = _e2e(cfg, samples, labels, teacher, student_h, tcfg, B, W, K, world, rank, dev, barrier)
+        e2e = _e2e_edl(cfg, samples, labels, teacher, student_h, tcfg, B, W, K, world, rank, dev, barrier, reserve,
+                       student_stream)
+        e2e["online_pipeline"] = _e2e(cfg, samples, labels, teacher, student_h, tcfg, B, W, K, world, rank, dev,
+                                      barrier)
 
     # ---------------- CPU baseline (oracle port, rank 0 only, bounded sample)
     cpu = None
@@ -568,6 +575,131 @@ def _teacher_rate(teacher, sampler, cfg, B, dev):
     e.record()
     torch.cuda.synchronize()
     return round(B * n / (s.elapsed_time(e) / 1e3), 1)
+
+
+class _StreamedRing:
+    """The EDL e2e input path: iteration it's batch is copied from pinned host
+    memory into ring slot it % R on a copy stream LOOKAHEAD iterations before
+    its first reader, and the teacher worker and the student gather it by row
+    index exactly as from a DeviceDataset (same interface: samples / labels /
+    dim / device; rows_for / batch_for / batch_size as a sampler)."""
+
+    LOOKAHEAD = 4
+
+    def __init__(self, host_x, host_y, dim, dev, ring_slots):
+        import torch
+        self.host_x, self.host_y = host_x, host_y
+        self.batch_size = B = host_x.shape[1]
+        self.R = ring_slots
+        self.dim, self.device, self.data = dim, dev, self
+        self.samples = torch.zeros(self.R * B, host_x.shape[2], dtype=torch.bfloat16, device=dev)
+        self.labels = torch.zeros(self.R * B, dtype=torch.int64, device=dev)
+        self.rows = [torch.arange(j * B, (j + 1) * B, device=dev) for j in range(self.R)]
+        self.copy = torch.cuda.Stream(dev)
+        self.landed: dict = {}          # iteration -> event (copy done)
+        self.free = [None] * self.R     # slot -> event after the slot's last reader
+        self.owner = [None] * self.R    # slot -> iteration it holds
+        self.h2d_bytes = 0
+
+    def _upload(self, it):
+        import torch
+        j, B = it % self.R, self.batch_size
+        if self.owner[j] is not None and self.free[j] is None:
+            raise RuntimeError(f"ring slot {j} still holds unconsumed iteration {self.owner[j]}")
+        with torch.cuda.stream(self.copy):
+            if self.free[j] is not None:
+                self.copy.wait_event(self.free[j])
+            src = it % self.host_x.shape[0]
+            self.samples[j * B:(j + 1) * B].copy_(self.host_x[src], non_blocking=True)
+            self.labels[j * B:(j + 1) * B].copy_(self.host_y[src], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self.copy)
+        self.landed[it] = ev
+        self.owner[j], self.free[j] = it, None
+        self.h2d_bytes += self.host_x[src].numel() * 2 + self.host_y[src].numel() * 8
+
+    def rows_for(self, it):
+        for a in range(it, it + self.LOOKAHEAD + 1):
+            if a not in self.landed:
+                self._upload(a)
+        self.landed[it].synchronize()   # issued LOOKAHEAD iterations ago: normally already done
+        return self.rows[it % self.R]
+
+    def batch_for(self, it, out=None, stream=None):
+        from paper_2207_06667_b200.data import gather_batch
+        return gather_batch(self, self.rows_for(it), out, stream)
+
+    def consumed(self, it, stream):
+        """`stream` has passed the student's gather of `it` and its wait on the
+        teacher's soft labels (the teacher's gather precedes them): slot free."""
+        import torch
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        self.free[it % self.R] = ev
+        self.landed.pop(it, None)
+
+
+def _e2e_edl(cfg, samples, labels, teacher, student_h, tcfg, B, W, K, world, rank, dev, barrier, reserve,
+             student_stream):
+    """The headline metric end to end through the repo's public EDL API
+    (TeacherPool + TeacherWorker + DistilReader + StudentStep): every step's
+    inputs cross host->device from pinned memory inside the timed region (the
+    teacher and the student read the uploaded batch; no HBM-resident dataset),
+    and every step's loss is read back into pinned host memory."""
+    import torch
+
+    from paper_2207_06667_b200 import nnkit
+    from paper_2207_06667_b200.nnkit import Model
+    from paper_2207_06667_b200.reader import DistilReader, EventLog, SchedulerConfig, TeacherPool
+    from paper_2207_06667_b200.student import StudentStep
+    from paper_2207_06667_b200.teacher import TeacherConfig, TeacherWorker
+    Dp = nnkit.pad(cfg["dim"])
+    nb = 4
+    host_x = torch.zeros(nb, B, Dp, dtype=torch.bfloat16).pin_memory()
+    host_y = torch.zeros(nb, B, dtype=torch.int64).pin_memory()
+    n = samples.shape[0]
+    for j in range(nb):
+        lo = (j * B * world + rank * B) % (n - B)
+        host_x[j, :, :cfg["dim"]] = torch.from_numpy(samples[lo:lo + B].astype(np.float32)).to(torch.bfloat16)
+        host_y[j] = torch.from_numpy(labels[lo:lo + B])
+    sched = SchedulerConfig(lt=2, ut=8, pipeline_depth=2, acquire_cooldown=1e9)
+    ring = _StreamedRing(host_x, host_y, cfg["dim"], dev, ring_slots=sched.ut + _StreamedRing.LOOKAHEAD + 4)
+    loss_host = torch.zeros(W + K, dtype=torch.float32).pin_memory()
+    engine = StudentStep(Model.from_host(student_h, dev), tcfg, B, world, max_steps=W + K + 8)
+    pool = TeacherPool()
+    pool.register(TeacherWorker(TeacherConfig("t-e2e", cfg["T"], cfg["topk"]), teacher, ring, sm_reserve=reserve))
+
+    def run(start, count):
+        reader = DistilReader(f"student-e2e-{rank}", pool, sched, ring, start, start + count, 1, EventLog(),
+                              cfg["T"], cfg["topk"])
+        reader.acquire(1)
+        barrier()
+        bytes0 = ring.h2d_bytes
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(student_stream):
+            s.record()
+            for it in range(start, start + count):
+                batch = ring.batch_for(it, out=engine.batch)
+                soft = reader.consume(it)
+                ring.consumed(it, student_stream)
+                engine.step(batch, soft)
+                i = (engine._n - 1) % engine.losses.shape[0]
+                loss_host[it:it + 1].copy_(engine.losses[i:i + 1], non_blocking=True)
+            e.record()
+        barrier()
+        ok = reader.ledger()["ok"]
+        reader.close()
+        return s.elapsed_time(e) / 1e3, ring.h2d_bytes - bytes0, ok
+
+    run(0, W)
+    t, h2d, ok = run(W, K)
+    t = _max_over_ranks(t, world, dev)
+    torch.cuda.synchronize()
+    assert ok and np.isfinite(loss_host[W:W + K].numpy()).all()
+    return {"value": round(world * B * K / t, 1), "unit": "samples/s",
+            "h2d_bytes_per_step": int(round(h2d / K)), "d2h_bytes_per_step": 4,
+            "mode": "edl (decoupled) through TeacherPool/TeacherWorker/DistilReader/StudentStep; each step's batch "
+                    "uploaded from pinned host memory into a device ring read by the teacher worker and the student"}
 
 
 def _e2e(cfg, samples, labels, teacher, student_h, tcfg, B, W, K, world, rank, dev, barrier):
