@@ -225,6 +225,9 @@ def main():
                     help="colocated: teacher worker + student on every GPU; split: teacher GPUs feed "
                          "student GPUs over NVLink (EDL-Dist teacher pool)")
     ap.add_argument("--teachers", type=int, default=0, help="teacher GPUs for --placement split")
+    ap.add_argument("--split-depth", type=int, default=8, help="split placement: soft-label ring slots per student")
+    ap.add_argument("--split-transport", default="peer", choices=["peer", "nccl"],
+                    help="split placement soft-label handoff: NVLink peer copy + stream flags, or NCCL send/recv")
     ap.add_argument("--student-priority", default="high", choices=["normal", "high"],
                     help="CUDA stream priority of the student in the co-located EDL loop")
     ap.add_argument("--teacher-sm-reserve", type=int, default=-1,
@@ -458,7 +461,8 @@ def _split_main(args, cfg, world, rank, local, dev, ddata, teacher, student_h, t
     from paper_2207_06667_b200 import _lib
     from paper_2207_06667_b200.data import DeviceShardSampler
     from paper_2207_06667_b200.nnkit import Model
-    from paper_2207_06667_b200.pool import Placement, RemoteSoftLabels, teacher_serve
+    from paper_2207_06667_b200.pool import (PeerSoftLabelRing, PeerSoftLabels, Placement, RemoteSoftLabels,
+                                            teacher_serve)
     from paper_2207_06667_b200.student import StudentStep
     B, W, K = cfg["batch"], args.warmup, args.steps
     nt = args.teachers or max(1, round(world * 0.75))
@@ -466,10 +470,22 @@ def _split_main(args, cfg, world, rank, local, dev, ddata, teacher, student_h, t
     students = list(range(pl.n_students))
     sgroup = dist.new_group(students)
     is_student = pl.is_student(rank)
+    # soft labels cross NVLink by peer copy + stream-ordered flags (default),
+    # or as NCCL send/recv (--split-transport nccl)
+    ring = (PeerSoftLabelRing(pl, rank, B, cfg["topk"], cfg["T"], dev, depth=args.split_depth)
+            if args.split_transport == "peer" else None)
     if is_student:
         sampler = DeviceShardSampler(ddata, pl.n_students, rank, B, seed=0)
         engine = StudentStep(Model.from_host(student_h, dev), tcfg, B, pl.n_students, process_group=sgroup,
                              max_steps=W + K + 8, exchange=args.exchange)
+
+    if not is_student:
+        # leave SMs free for NCCL's send kernels: back-to-back persistent
+        # teacher GEMMs would otherwise hold every SM and delay each batch's
+        # transfer until the next batch's GEMM ends
+        reserve = args.teacher_sm_reserve if args.teacher_sm_reserve >= 0 else 8
+        _lib.call("edl_set_stream_max_ctas", torch.cuda.current_stream(dev).cuda_stream,
+                  max(1, _lib.load().edl_device_sms() - reserve))
 
     def run(start, count):
         barrier()
@@ -477,14 +493,15 @@ def _split_main(args, cfg, world, rank, local, dev, ddata, teacher, student_h, t
         l0 = _lib.launch_count
         s.record()
         if is_student:
-            rx = RemoteSoftLabels(pl, rank, B, cfg["topk"], cfg["T"], dev, start, start + count)
+            rx = (PeerSoftLabels(ring) if ring is not None
+                  else RemoteSoftLabels(pl, rank, B, cfg["topk"], cfg["T"], dev, start, start + count))
             for it in range(start, start + count):
                 batch = sampler.batch_for(it, out=engine.batch)
                 soft = rx.consume(it)
                 engine.step(batch, soft)
                 rx.released(it)
         else:
-            teacher_serve(pl, rank, teacher, ddata, B, 0, cfg["T"], cfg["topk"], start, start + count)
+            teacher_serve(pl, rank, teacher, ddata, B, 0, cfg["T"], cfg["topk"], start, start + count, ring=ring)
         e.record()
         barrier()
         return s.elapsed_time(e) / 1e3, _lib.launch_count - l0
@@ -492,6 +509,7 @@ def _split_main(args, cfg, world, rank, local, dev, ddata, teacher, student_h, t
     run(0, W)
     with ClockSampler(local) as clk:
         t, launches = run(W, K)
+    print(f"[split] rank {rank} {'student' if is_student else 'teacher'} region {t * 1e3:.2f} ms", file=sys.stderr)
     tmax = _max_over_ranks(t, world, dev)
     losses = engine.loss_values() if is_student else []
     ok = bool(np.isfinite(losses).all()) if is_student else True
@@ -503,7 +521,8 @@ def _split_main(args, cfg, world, rank, local, dev, ddata, teacher, student_h, t
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (make_blobs seed 0, random-init teacher seed 1 / student seed 0)",
             "config": {"workload": cfg["workload"], "placement": f"split {pl.n_teachers}T+{pl.n_students}S "
-                       "(teacher pool -> students over NVLink P2P, NCCL student all-reduce)",
+                       f"(teacher pool -> students over NVLink, {args.split_transport} handoff; NCCL student "
+                       "all-reduce)",
                        "mode": "edl (decoupled)", "global_batch": B * pl.n_students, "per_gpu_batch": B,
                        "topk": cfg["topk"], "parallelism": f"dp{pl.n_students}"},
             "gpu_launches": launches, "clocks": clk.summary(), "losses_finite": ok}), flush=True)

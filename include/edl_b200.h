@@ -125,6 +125,18 @@ int edl_kd_loss_fwd_bwd(const float* logits, long long ldz, const long long* lab
  * scale = eta / world_size folds the all-reduce mean (edl/allreduce.py:119). */
 int edl_sgd_step(float* p, void* p_bf16, const float* g, long long n, float scale, void* stream);
 
+/* Stream-ordered 32-bit flags for the teacher-pool -> student soft-label
+ * handoff over NVLink (split placement; replaces the INFER_REPLY delivery of
+ * edl/teacher_node.py:47-58 into DistilReader._accept_reply / consume,
+ * edl/student_node.py:407-457). addr is device memory of this GPU or a peer's
+ * (symmetric-memory signal pad). wait: later work on `stream` waits until
+ * (int32)(*addr - value) >= 0. write: *addr = value once all earlier work on
+ * `stream` (e.g. the peer copy of a soft-label batch) is complete and visible.
+ * Neither holds an SM (cuStreamWaitValue32 / cuStreamWriteValue32; one-thread
+ * kernels if the driver lacks stream memory operations). */
+int edl_stream_wait_geq(unsigned* addr, unsigned value, void* stream);
+int edl_stream_write_u32(unsigned* addr, unsigned value, void* stream);
+
 /* Data-parallel gradient exchange fused with SGD, over NVSwitch multicast.
  * Replaces, at world > 1, the ring all-reduce to the mean
  * (edl/allreduce.py:77-120, called at edl/student_node.py:741) followed by

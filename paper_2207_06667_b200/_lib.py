@@ -49,6 +49,8 @@ _SIGNATURES = {
                             c_float, c_float, c_float, c_void_p, c_void_p, c_void_p, c_void_p,
                             c_ll, c_void_p, c_void_p],
     "edl_sgd_step": [c_void_p, c_void_p, c_void_p, c_ll, c_float, c_void_p],
+    "edl_stream_wait_geq": [c_void_p, c_uint, c_void_p],
+    "edl_stream_write_u32": [c_void_p, c_uint, c_void_p],
     "edl_nvls_allreduce_sgd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_ll, c_void_p, c_int, c_int,
                                c_ll, c_float, c_uint, c_void_p],
     "edl_gather_rows": [c_void_p, c_ll, c_void_p, c_void_p, c_ll, c_int, c_int, c_void_p, c_void_p,
@@ -110,7 +112,9 @@ def check(rc: int, what: str) -> None:
 
 # kernel launches per C entry point (bench.py reports launches in its timed region)
 _LAUNCHES = {"edl_linear_bwd_weight": 3,   # GEMM + two column-sum passes when db is requested
-             "edl_kd_loss_fwd_bwd": 2}     # row pass + deterministic batch-mean pass
+             "edl_kd_loss_fwd_bwd": 2,     # row pass + deterministic batch-mean pass
+             "edl_stream_wait_geq": 0,     # stream memory ops, not kernels
+             "edl_stream_write_u32": 0}
 launch_count = 0
 
 

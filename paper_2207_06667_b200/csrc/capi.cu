@@ -445,6 +445,53 @@ int edl_kd_loss_fwd_bwd(const float* logits, long long ldz, const long long* lab
   return e == cudaSuccess ? 0 : cuda_fail(e, "kd_loss");
 }
 
+// Stream-ordered 32-bit flags: the split placement's soft-label handoff
+// (pool.PeerSoftLabelRing). cuStreamWaitValue32 / cuStreamWriteValue32 keep
+// the wait and the signal in the streams without holding an SM; a one-thread
+// kernel pair stands in if the driver reports stream memory ops unsupported.
+namespace {
+using PFN_value32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_value32 driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+    return reinterpret_cast<PFN_value32>(p);
+  return nullptr;
+}
+PFN_value32 wait_value_fn() {
+  static PFN_value32 fn = driver_fn("cuStreamWaitValue32");
+  return fn;
+}
+PFN_value32 write_value_fn() {
+  static PFN_value32 fn = driver_fn("cuStreamWriteValue32");
+  return fn;
+}
+}  // namespace
+
+int edl_stream_wait_geq(unsigned* addr, unsigned value, void* stream) {
+  if (!addr) return fail(EDL_ERR_SHAPE, "stream_wait_geq: null address");
+  PFN_value32 fn = wait_value_fn();
+  if (fn) {
+    const CUresult r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(addr), value, 0);
+    if (r == CUDA_SUCCESS) return 0;
+    if (r != CUDA_ERROR_NOT_SUPPORTED) return fail(EDL_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", static_cast<int>(r));
+  }
+  cudaError_t e = launch_flag_wait(addr, value, as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "stream_wait_geq");
+}
+
+int edl_stream_write_u32(unsigned* addr, unsigned value, void* stream) {
+  if (!addr) return fail(EDL_ERR_SHAPE, "stream_write_u32: null address");
+  PFN_value32 fn = write_value_fn();
+  if (fn) {
+    const CUresult r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(addr), value, 0);
+    if (r == CUDA_SUCCESS) return 0;
+    if (r != CUDA_ERROR_NOT_SUPPORTED) return fail(EDL_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", static_cast<int>(r));
+  }
+  cudaError_t e = launch_flag_write(addr, value, as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "stream_write_u32");
+}
+
 int edl_nvls_allreduce_sgd(float* mc_grad, float* mc_param, void* mc_param_bf16, const float* param,
                            unsigned* const* pads, long long pad_bytes, unsigned* counter, int rank, int world,
                            long long n, float scale, unsigned epoch, void* stream) {

@@ -148,6 +148,27 @@ __global__ void __launch_bounds__(kXThreads) nvls_allreduce_sgd_kernel(XArgs a) 
 
 }  // namespace
 
+namespace {
+// Fallbacks for edl_stream_wait_geq / edl_stream_write_u32 when the driver
+// has no stream memory operations: one thread spins / stores at system scope.
+__global__ void flag_wait_kernel(const uint32_t* addr, uint32_t value) {
+  griddep_wait();
+  wait_ge(addr, value);
+}
+__global__ void flag_write_kernel(uint32_t* addr, uint32_t value) {
+  griddep_wait();
+  fence_sys();
+  st_release_sys(addr, value);
+}
+}  // namespace
+
+cudaError_t launch_flag_wait(const uint32_t* addr, uint32_t value, cudaStream_t stream) {
+  return launch_pdl(flag_wait_kernel, dim3(1), dim3(1), 0, stream, 1, addr, value);
+}
+cudaError_t launch_flag_write(uint32_t* addr, uint32_t value, cudaStream_t stream) {
+  return launch_pdl(flag_write_kernel, dim3(1), dim3(1), 0, stream, 1, addr, value);
+}
+
 int nvls_max_blocks(int world, long long pad_bytes) {
   const long long slots = pad_bytes / 4;
   const long long rows = slots / world;   // row 0 + one per block

@@ -92,6 +92,9 @@ cudaError_t launch_gemm_grouped_pair_bwd_weight(const GroupMaps& maps, const Gro
 cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
                         int M, int N, int K, const EpiArgs& ep, int num_sms,
                         cudaStream_t stream);
+// Stream-ordered flag fallbacks (exchange.cu).
+cudaError_t launch_flag_wait(const uint32_t* addr, uint32_t value, cudaStream_t stream);
+cudaError_t launch_flag_write(uint32_t* addr, uint32_t value, cudaStream_t stream);
 // Fused gradient exchange + SGD over NVSwitch multicast (exchange.cu).
 int nvls_max_blocks(int world, long long pad_bytes);
 cudaError_t launch_nvls_allreduce_sgd(float* mc_grad, float* mc_param, void* mc_bf16, const float* param,

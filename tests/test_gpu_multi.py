@@ -216,3 +216,69 @@ def test_teacher_gpu_drop_and_readd_over_nvlink():
     a = ref.flatten(list(clean.model.weights), list(clean.model.biases))
     b = ref.flatten(list(faulty.model.weights), list(faulty.model.biases))
     assert np.array_equal(a, b)
+
+
+def _peer_ring_rank(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2207_06667_b200 import formats, nnkit
+    from paper_2207_06667_b200.data import DeviceDataset, DeviceShardSampler
+    from paper_2207_06667_b200.pool import PeerSoftLabelRing, PeerSoftLabels, Placement, teacher_serve
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    try:
+        pl = Placement(world, world - 1)                 # rank 0 student, the rest teachers
+        B, k, T, n_it = 64, 8, 2.0, 23
+        data = DeviceDataset(formats.make_blobs(0, 1024, 40, 30, 1.0), dev)
+        teacher = nnkit.Model.from_host(formats.init_model((40, 96, 30), 5), dev)
+        try:
+            ring = PeerSoftLabelRing(pl, rank, B, k, T, dev, depth=3)
+        except Exception as e:   # noqa: BLE001
+            q.put((rank, "unavailable", str(e)[:200]))
+            return
+        if rank == 0:
+            rx = PeerSoftLabels(ring)
+            sampler = DeviceShardSampler(data, 1, 0, B, seed=0)
+            bad = 0
+            for it in range(n_it):
+                soft = rx.consume(it)
+                # the student's own reference: the same teacher on the same rows, locally
+                want = nnkit.teacher_soft_labels(teacher, sampler.batch_for(it).inputs, T, k)
+                bad += int(not (torch.equal(soft.classes, want.classes) and torch.equal(soft.probs, want.probs)))
+                torch.cuda._sleep(2_000_000)             # a slow student: teachers must wait for credits
+                rx.released(it)
+            torch.cuda.synchronize()
+            q.put((rank, "ok", bad))
+        else:
+            served = teacher_serve(pl, rank, teacher, data, B, 0, T, k, 0, n_it, ring=ring)
+            torch.cuda.synchronize()
+            q.put((rank, "ok", served))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_peer_softlabel_ring_delivers_teacher_outputs():
+    """Split placement over NVLink peer memory (pool.PeerSoftLabelRing): each
+    iteration's (prob, class) batch lands in the student's ring bitwise equal
+    to the teacher head's output for that iteration's rows, in order, with the
+    ring (depth 3) wrapping many times behind a deliberately slow student."""
+    import torch.multiprocessing as mp
+    world = min(torch.cuda.device_count(), 3)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_peer_ring_rank, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict((r, (st, v)) for r, st, v in (q.get(timeout=300) for _ in ps))
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    if any(st == "unavailable" for st, _ in res.values()):
+        pytest.skip(f"no symmetric memory: {res}")
+    assert res[0][1] == 0
+    assert sum(v for r, (st, v) in res.items() if r > 0) == 23

@@ -74,39 +74,40 @@ def _spawn(fn, world=2):
 
 
 def _softlabel_stream(rank, world):
-    """Rank 1 = teacher, rank 0 = student; the same message order as
-    pool.teacher_serve / RemoteSoftLabels (probs then classes per iteration,
-    receives posted `depth` iterations ahead into a ring)."""
+    """Rank 1 = teacher, rank 0 = student; the same messages as
+    pool.teacher_serve / RemoteSoftLabels: one packed (prob, class) buffer
+    per iteration (pool.wire_slot) on the pair's own process group
+    (pool.pair_groups), receives posted `depth` iterations ahead into a ring."""
+    from paper_2207_06667_b200.pool import pair_groups, wire_slot
     pl = Placement(world, 1)
+    groups = pair_groups(pl)
+    g = groups[(0, 1)]
     B, k, depth, start, end = 8, 4, 3, 0, 11
     if rank == 1:
         for it in pl.iterations_of(1, 0, start, end):
-            probs = torch.full((B, k), float(it))
-            classes = torch.arange(B * k, dtype=torch.int32).view(B, k) + it
-            dist.isend(probs, 0).wait()
-            dist.isend(classes, 0).wait()
+            buf, out = wire_slot(B, k, 2.0, "cpu")
+            out.probs.fill_(float(it) + 0.5)
+            out.classes.copy_(torch.arange(B * k, dtype=torch.int32).view(B, k) + it)
+            dist.isend(buf, 0, group=g).wait()
         return None
-    slots = [(torch.empty(B, k), torch.empty(B, k, dtype=torch.int32)) for _ in range(depth)]
+    slots = [wire_slot(B, k, 2.0, "cpu") for _ in range(depth)]
     works, got, nxt = {}, [], start
     while nxt < min(start + depth, end):
-        src = pl.server(0, nxt)
-        works[nxt] = [dist.irecv(slots[nxt % depth][0], src), dist.irecv(slots[nxt % depth][1], src)]
+        works[nxt] = dist.irecv(slots[nxt % depth][0], pl.server(0, nxt), group=groups[(0, pl.server(0, nxt))])
         nxt += 1
     for it in range(start, end):
-        for w in works.pop(it):
-            w.wait()
-        p, c = slots[it % depth]
-        got.append((float(p[0, 0]), int(c[0, 0])))
+        works.pop(it).wait()
+        _, out = slots[it % depth]
+        got.append((float(out.probs[0, 0]), int(out.classes[0, 0])))
         if nxt < end:
-            src = pl.server(0, nxt)
-            works[nxt] = [dist.irecv(slots[nxt % depth][0], src), dist.irecv(slots[nxt % depth][1], src)]
+            works[nxt] = dist.irecv(slots[nxt % depth][0], pl.server(0, nxt), group=groups[(0, pl.server(0, nxt))])
             nxt += 1
     return got
 
 
 def test_gloo_softlabel_stream_order():
     out = _spawn(_softlabel_stream)
-    assert out[0] == [(float(i), i) for i in range(11)]
+    assert out[0] == [(float(i) + 0.5, i) for i in range(11)]
 
 
 def _grad_mean(rank, world):
