@@ -218,6 +218,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-online", action="store_true")
+    ap.add_argument("--overlap-exchange", action="store_true",
+                    help="N>1: all-reduce + SGD in two buckets on a comm stream, overlapping the next forward")
     ap.add_argument("--exchange", default="nccl", choices=["nvls", "nccl"],
                     help="N>1 student gradient exchange: NCCL all-reduce + SGD, or the fused NVSwitch-multicast "
                          "all-reduce+SGD kernel (slower on this pool, profiles/r01_exchange_ab.json)")
@@ -288,7 +290,8 @@ def main():
 
     # ---------------- EDL-Dist (decoupled, co-located teacher worker per GPU)
     student = Model.from_host(student_h, dev)
-    engine = StudentStep(student, tcfg, B, world, max_steps=W + K + 8, exchange=args.exchange)
+    engine = StudentStep(student, tcfg, B, world, max_steps=W + K + 8, exchange=args.exchange,
+                         overlap_exchange=args.overlap_exchange)
     pool = TeacherPool()
     # Same-box sweeps with the CTA-pair GEMMs (profiles/r01_reserve_sweep.txt):
     # N=1, reserve 0/8/16/24 -> 4.47-4.70 / 4.40-4.60 / 4.77-5.02 / 4.60-4.81
@@ -327,6 +330,7 @@ def main():
                 soft = reader.consume(it)
                 engine.step(batch, soft)
             host_s[0] = (time.perf_counter() - h0) / count   # host enqueue time per step (incl. waits)
+            engine.settle()   # N>1: the last step's exchange + SGD run on a comm stream
             e.record()
         if timed:
             torch.cuda.nvtx.range_pop()
@@ -352,7 +356,8 @@ def main():
     online_run = None
     if not args.no_online:
         student2 = Model.from_host(student_h, dev)
-        eng2 = StudentStep(student2, tcfg, B, world, max_steps=W + 2 * K + 8, exchange=args.exchange)
+        eng2 = StudentStep(student2, tcfg, B, world, max_steps=W + 2 * K + 8, exchange=args.exchange,
+                           overlap_exchange=args.overlap_exchange)
         tws = nnkit.Workspace(teacher, B)
         out = SoftLabels(torch.empty(B, cfg["topk"], device=dev),
                          torch.empty(B, cfg["topk"], dtype=torch.int32, device=dev), cfg["T"])
@@ -365,6 +370,7 @@ def main():
                 batch = sampler.batch_for(it, out=eng2.batch)
                 soft = nnkit.teacher_soft_labels(teacher, batch.inputs, cfg["T"], cfg["topk"], out=out, ws=tws)
                 eng2.step(batch, soft)
+            eng2.settle()
             e.record()
             barrier()
             return s.elapsed_time(e) / 1e3
@@ -500,6 +506,7 @@ def _split_main(args, cfg, world, rank, local, dev, ddata, teacher, student_h, t
                 soft = rx.consume(it)
                 engine.step(batch, soft)
                 rx.released(it)
+            engine.settle()
         else:
             teacher_serve(pl, rank, teacher, ddata, B, 0, cfg["T"], cfg["topk"], start, start + count, ring=ring)
         e.record()
@@ -704,6 +711,7 @@ def _e2e_edl(cfg, samples, labels, teacher, student_h, tcfg, B, W, K, world, ran
                 engine.step(batch, soft)
                 i = (engine._n - 1) % engine.losses.shape[0]
                 loss_host[it:it + 1].copy_(engine.losses[i:i + 1], non_blocking=True)
+            engine.settle()
             e.record()
         barrier()
         ok = reader.ledger()["ok"]
@@ -778,6 +786,7 @@ def _e2e(cfg, samples, labels, teacher, student_h, tcfg, B, W, K, world, rank, d
             ev = torch.cuda.Event()
             ev.record(main)
             used[j] = ev
+        eng.settle()
         e.record()
         barrier()
         return s.elapsed_time(e) / 1e3

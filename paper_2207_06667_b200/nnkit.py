@@ -291,13 +291,17 @@ def workspace_for(model: Model, batch_size: int) -> Workspace:
 # Core math (edl/nnkit.py:193-335)
 
 
-def _forward_into(model: Model, x: torch.Tensor, ws: Workspace, stream=None) -> torch.Tensor:
-    """acts[1..L-1] = tanh layers, ws.logits = last layer (fp32)."""
+def _forward_into(model: Model, x: torch.Tensor, ws: Workspace, stream=None, layer_ready=None) -> torch.Tensor:
+    """acts[1..L-1] = tanh layers, ws.logits = last layer (fp32). layer_ready[l]
+    (optional CUDA event) gates layer l's GEMM: its parameters are still being
+    updated on another stream (StudentStep's overlapped gradient exchange)."""
     L = model.layout
     B = x.shape[0]
     s = _stream(stream)
     h = x
     for l in range(L.layers):
+        if layer_ready is not None and layer_ready[l] is not None:
+            (stream or torch.cuda.current_stream()).wait_event(layer_ready[l])
         last = l == L.layers - 1
         out = ws.logits if last else ws.acts[l + 1]
         _lib.call("edl_linear_fwd", h.data_ptr(), h.stride(0), model.w_bf16(l).data_ptr(), L.dims_p[l],
@@ -380,7 +384,7 @@ def teacher_soft_labels(model: Model, inputs, temperature: float, k: int, out: S
 def kd_loss(model: Model, batch: Batch, soft: SoftLabels | None, cfg: TrainConfig,
             stream=None, ws: Workspace | None = None,
             loss_slot: torch.Tensor | None = None,
-            fused_sgd_eta: float | None = None) -> tuple[DeviceLoss, Gradients | None]:
+            fused_sgd_eta: float | None = None, layer_ready=None) -> tuple[DeviceLoss, Gradients | None]:
     """Combined distillation loss and analytic gradients (edl/nnkit.py:254-309):
     forward GEMMs -> fused loss/dlogits kernel -> backward GEMMs."""
     if cfg.beta > 0:
@@ -398,7 +402,7 @@ def kd_loss(model: Model, batch: Batch, soft: SoftLabels | None, cfg: TrainConfi
     L = model.layout
     ws = ws or workspace_for(model, B)
     s = _stream(stream)
-    _forward_into(model, x, ws, stream)
+    _forward_into(model, x, ws, stream, layer_ready)
     dz = ws.deltas[L.layers]
     q_vals = soft.probs if (soft is not None and cfg.beta > 0) else None
     q_idx = soft.classes if (soft is not None and cfg.beta > 0) else None

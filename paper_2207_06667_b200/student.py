@@ -26,7 +26,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import formats, nnkit
+from . import _lib, formats, nnkit
 from .data import DeviceDataset, DeviceShardSampler
 from .formats import Dataset, HostModel
 from .nnkit import Batch, Model, SoftLabels, TrainConfig, Workspace
@@ -76,6 +76,7 @@ class StudentConfig:
     consume_timeout: float | None = None
     k: int | None = None          # top-k soft labels; None -> min(classes, 32)
     exchange: str = "nccl"        # world > 1 gradient exchange: "nccl" or "nvls" (fused kernel, exchange.py)
+    overlap_exchange: bool = False  # nccl: bucketed exchange on a comm stream overlapping the next forward
 
     def __post_init__(self):
         if self.mode not in (MODE_EDL, MODE_NTRAIN, MODE_ONLINE):
@@ -152,7 +153,7 @@ class StudentStep:
 
     def __init__(self, model: Model, cfg: TrainConfig, batch_size: int, world_size: int = 1,
                  process_group=None, max_steps: int = 1 << 16, fuse_sgd: bool = True,
-                 exchange: str = "nccl"):
+                 exchange: str = "nccl", overlap_exchange: bool = False):
         self.model = model
         self.cfg = cfg
         self.world_size = world_size
@@ -176,6 +177,21 @@ class StudentStep:
                 self.exchange = NvlsGradientExchange(model, self.ws.grads, process_group)
             except ExchangeUnavailable:
                 self.exchange = None
+        # overlap_exchange (NCCL path): two buckets on a comm stream, layer 0
+        # first, so the next step's gather + layer-0 forward overlap the rest's
+        # all-reduce + SGD (each forward layer waits only for its own parameters)
+        L = model.layout
+        first = L.b_off[0] + L.dims_p[1]
+        self._buckets = [(0, first), (first, L.size)] if L.layers > 1 else [(0, L.size)]
+        self._bucket_of_layer = [0] + [len(self._buckets) - 1] * (L.layers - 1)
+        self._comm = torch.cuda.Stream(model.device) if world_size > 1 else None
+        self._ready = None
+        # Measured (profiles/r01_overlap_ab.txt, same box, N=4): the overlap
+        # lifts the synchronous online baseline 15.8 -> 16.4 M samples/s but
+        # leaves the EDL value flat (17.6 -> 17.6 M), and costs the
+        # host-coupled e2e path 15.6 -> 13.4 M: two NCCL calls a step add host
+        # latency where every step waits on its H2D upload. Opt-in.
+        self._overlap = overlap_exchange
 
     def step(self, batch: Batch, soft: SoftLabels | None) -> None:
         i = self._n % self.losses.shape[0]
@@ -183,15 +199,46 @@ class StudentStep:
             # single student: the update is fused into the dW / db kernels
             nnkit.kd_loss(self.model, batch, soft, self.cfg, ws=self.ws, loss_slot=self.losses[i:i + 1],
                           fused_sgd_eta=self.cfg.eta)
+        elif self.exchange is not None:
+            nnkit.kd_loss(self.model, batch, soft, self.cfg, ws=self.ws, loss_slot=self.losses[i:i + 1])
+            self.exchange.step(self.cfg.eta)
+        elif self.world_size > 1 and self._overlap:
+            nnkit.kd_loss(self.model, batch, soft, self.cfg, ws=self.ws, loss_slot=self.losses[i:i + 1],
+                          layer_ready=self._ready)
+            self._exchange_overlapped()
+        elif self.world_size > 1:
+            nnkit.kd_loss(self.model, batch, soft, self.cfg, ws=self.ws, loss_slot=self.losses[i:i + 1])
+            torch.distributed.all_reduce(self.ws.grads.flat, group=self.group)
+            nnkit.sgd_step(self.model, self.ws.grads, self.cfg.eta, self.world_size)
         else:
             nnkit.kd_loss(self.model, batch, soft, self.cfg, ws=self.ws, loss_slot=self.losses[i:i + 1])
-            if self.exchange is not None:
-                self.exchange.step(self.cfg.eta)
-            else:
-                if self.world_size > 1:
-                    torch.distributed.all_reduce(self.ws.grads.flat, group=self.group)
-                nnkit.sgd_step(self.model, self.ws.grads, self.cfg.eta, self.world_size)
+            nnkit.sgd_step(self.model, self.ws.grads, self.cfg.eta, 1)
         self._n += 1
+
+    def _exchange_overlapped(self) -> None:
+        """all-reduce + SGD per bucket on the comm stream (edl/student_node.py:
+        740-745); the next step's kd_loss waits per layer (layer_ready)."""
+        cur = torch.cuda.current_stream(self.model.device)
+        self._comm.wait_stream(cur)
+        g, p, p16 = self.ws.grads.flat, self.model.flat, self.model.flat_bf16
+        events = []
+        with torch.cuda.stream(self._comm):
+            for lo, hi in self._buckets:
+                torch.distributed.all_reduce(g[lo:hi], group=self.group)
+                _lib.call("edl_sgd_step", p[lo:hi].data_ptr(), p16[lo:hi].data_ptr(), g[lo:hi].data_ptr(), hi - lo,
+                          float(self.cfg.eta) / self.world_size, self._comm.cuda_stream)
+                ev = torch.cuda.Event()
+                ev.record(self._comm)
+                events.append(ev)
+        self._ready = [events[b] for b in self._bucket_of_layer]
+
+    def settle(self, stream=None) -> None:
+        """Order `stream` (default: current) after the last step's parameter
+        update: call before reading the model or closing a timed region."""
+        if self._ready is not None:
+            s = stream or torch.cuda.current_stream(self.model.device)
+            for ev in self._ready:
+                s.wait_event(ev)
 
     def loss_values(self) -> list[float]:
         return self.losses[:min(self._n, self.losses.shape[0])].tolist()
@@ -283,7 +330,8 @@ class StudentNode:
         host, start = self.initial_model()
         model = Model.from_host(host, self.dataset.device)
         engine = StudentStep(model, train_cfg, cfg.train.batch_size, cfg.world_size, self.group,
-                             max_steps=max(self.total_steps, 1), exchange=cfg.exchange)
+                             max_steps=max(self.total_steps, 1), exchange=cfg.exchange,
+                             overlap_exchange=cfg.overlap_exchange)
         engine._n = start
         reader = None
         online_out = None
@@ -313,10 +361,13 @@ class StudentNode:
             trained += 1
             done = it + 1
             if cfg.checkpoint_dir and cfg.rank == 0 and done % cfg.checkpoint_interval == 0:
+                engine.settle()
                 save_checkpoint(cfg.checkpoint_dir, model.to_host(), done, self.host_data.id, cfg.world_size)
                 self.events.append("checkpoint", iteration=done)
             if cfg.metrics_dir and done % self.sampler.batches_per_epoch == 0:
+                engine.settle()
                 self._record_epoch(done, model)
+        engine.settle()
         t1.record()
         torch.cuda.synchronize()
         span = t0.elapsed_time(t1) / 1e3

@@ -68,7 +68,7 @@ def _free_port():
     return p
 
 
-def _nccl_student(rank, world, port, q, exchange="nvls"):
+def _nccl_student(rank, world, port, q, exchange="nccl", overlap=False):
     import torch.distributed as dist
 
     from paper_2207_06667_b200 import formats
@@ -82,7 +82,7 @@ def _nccl_student(rank, world, port, q, exchange="nvls"):
         cfg = StudentConfig(rank=rank, world_size=world, mode="online",
                             data=DataSpec(seed=0, n=2048, dim=16, classes=10, spread=1.0),
                             train=TrainConfig(eta=0.05, alpha=0.5, beta=0.5, temperature=2.0, batch_size=32),
-                            max_steps=int(d["vc_steps"]), k=10, exchange=exchange)
+                            max_steps=int(d["vc_steps"]), k=10, exchange=exchange, overlap_exchange=overlap)
         node = StudentNode(cfg, teacher_model=_host(d["teacher"], (16, 256, 256, 10)))
         res = node.run()
         q.put((rank, ref.flatten(list(res.model.weights), list(res.model.biases))))
@@ -91,13 +91,13 @@ def _nccl_student(rank, world, port, q, exchange="nvls"):
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-@pytest.mark.parametrize("exchange", ["nvls", "nccl"])
-def test_two_students_nccl_vs_virtual_cluster(exchange):
+@pytest.mark.parametrize("exchange,overlap", [("nccl", False), ("nccl", True), ("nvls", False)])
+def test_two_students_nccl_vs_virtual_cluster(exchange, overlap):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_nccl_student, args=(r, 2, port, q, exchange)) for r in range(2)]
+    ps = [ctx.Process(target=_nccl_student, args=(r, 2, port, q, exchange, overlap)) for r in range(2)]
     for p in ps:
         p.start()
     out = dict(q.get(timeout=300) for _ in ps)
