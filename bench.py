@@ -326,8 +326,9 @@ def main():
             s.record()
             h0 = time.perf_counter()
             for it in range(start, start + count):
-                batch = sampler.batch_for(it, out=engine.batch)
                 soft = reader.consume(it)
+                # the teacher worker gathered this iteration's rows into the slot
+                batch = soft.batch if soft.batch is not None else sampler.batch_for(it, out=engine.batch)
                 engine.step(batch, soft)
             host_s[0] = (time.perf_counter() - h0) / count   # host enqueue time per step (incl. waits)
             engine.settle()   # N>1: the last step's exchange + SGD run on a comm stream
@@ -705,8 +706,8 @@ def _e2e_edl(cfg, samples, labels, teacher, student_h, tcfg, B, W, K, world, ran
         with torch.cuda.stream(student_stream):
             s.record()
             for it in range(start, start + count):
-                batch = ring.batch_for(it, out=engine.batch)
                 soft = reader.consume(it)
+                batch = soft.batch if soft.batch is not None else ring.batch_for(it, out=engine.batch)
                 ring.consumed(it, student_stream)
                 engine.step(batch, soft)
                 i = (engine._n - 1) % engine.losses.shape[0]

@@ -206,6 +206,10 @@ class SoftLabels:
     probs: torch.Tensor
     classes: torch.Tensor
     temperature: float
+    # the iteration's input batch when the teacher worker gathered it into the
+    # reader's slot on the student's device (DistilReader share_batch): the
+    # student trains on it instead of gathering the same rows again
+    batch: "Batch | None" = None
 
     @property
     def size(self) -> int:

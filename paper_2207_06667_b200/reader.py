@@ -209,15 +209,17 @@ class TeacherPool:
 
 
 class _Slot:
-    __slots__ = ("probs", "classes", "done", "release", "iteration", "teacher")
+    __slots__ = ("probs", "classes", "done", "release", "iteration", "teacher", "batch", "batch_filled")
 
-    def __init__(self, B: int, k: int, device):
+    def __init__(self, B: int, k: int, device, batch=None):
         self.probs = torch.empty(B, k, dtype=torch.float32, device=device)
         self.classes = torch.empty(B, k, dtype=torch.int32, device=device)
         self.done: torch.cuda.Event | None = None
         self.release: torch.cuda.Event | None = None
         self.iteration = -1
         self.teacher = None
+        self.batch = batch              # input buffers a same-device teacher gathers into
+        self.batch_filled = False
 
 
 class _TeacherHandle:
@@ -233,7 +235,7 @@ class DistilReader:
 
     def __init__(self, student_id: str, pool: TeacherPool, cfg: SchedulerConfig, sampler,
                  start_iteration: int, end_iteration: int, session: int, events: EventLog,
-                 expected_temperature: float, k: int, clock=None):
+                 expected_temperature: float, k: int, clock=None, share_batch: bool = True):
         self.student_id = student_id
         self.pool = pool
         self.cfg = cfg
@@ -244,6 +246,9 @@ class DistilReader:
         self.k = k
         self.clock = clock or time.monotonic
         self.device = sampler.data.device
+        # slots carry input buffers a same-device teacher gathers into, so the
+        # student trains on them instead of gathering the rows a second time
+        self.share_batch = share_batch and hasattr(getattr(sampler, "data", None), "samples")
         self._teachers: dict[str, _TeacherHandle] = {}
         self._ready: dict[int, _Slot] = {}
         self._free: list[_Slot] = []
@@ -300,8 +305,18 @@ class DistilReader:
 
     def _slot(self) -> _Slot:
         if self._free:
-            return self._free.pop()
-        return _Slot(self.sampler.batch_size, self.k, self.device)
+            slot = self._free.pop()
+        else:
+            batch = None
+            if self.share_batch:
+                from .nnkit import Batch
+                data = self.sampler.data
+                B = self.sampler.batch_size
+                batch = Batch(torch.empty(B, data.samples.shape[1], dtype=torch.bfloat16, device=self.device),
+                              torch.empty(B, dtype=torch.int64, device=self.device), data.dim)
+            slot = _Slot(self.sampler.batch_size, self.k, self.device, batch)
+        slot.batch_filled = False
+        return slot
 
     def _dispatch(self) -> None:
         while not self._stopped and self.sending_enabled and self._have_work():
@@ -409,7 +424,8 @@ class DistilReader:
         stream.wait_event(slot.done)
         self._last_consumed = slot
         self.pump()
-        return SoftLabels(slot.probs, slot.classes, self.expected_temperature)
+        return SoftLabels(slot.probs, slot.classes, self.expected_temperature,
+                          slot.batch if slot.batch_filled else None)
 
     def _inflight_slot(self, iteration: int):
         for h in self._teachers.values():

@@ -350,11 +350,14 @@ class StudentNode:
         for it in range(start, self.total_steps):
             if on_iteration is not None:
                 on_iteration(it, reader)
-            batch = self.sampler.batch_for(it, out=engine.batch)
             soft = None
             if cfg.mode == MODE_EDL:
                 soft = reader.consume(it, timeout=cfg.consume_timeout)
-            elif cfg.mode == MODE_ONLINE and train_cfg.beta > 0:
+            if soft is not None and soft.batch is not None:
+                batch = soft.batch            # gathered by the teacher worker into the reader slot
+            else:
+                batch = self.sampler.batch_for(it, out=engine.batch)
+            if cfg.mode == MODE_ONLINE and train_cfg.beta > 0:
                 soft = nnkit.teacher_soft_labels(self.teacher, batch.inputs, cfg.train.temperature, self.k,
                                                  out=online_out)
             engine.step(batch, soft)

@@ -118,8 +118,15 @@ class TeacherWorker:
                                     torch.empty(B, dtype=torch.int64, device=self.device), self.data.dim)
             if self._ws is None or self._ws.batch_size != B:
                 self._ws = nnkit.Workspace(self.model, B)
-            batch = gather_batch(self.data, rows, self._batch, self.stream)
             local = slot.probs.device == self.device
+            # gather straight into the student's slot when it offers input
+            # buffers on this device (reader share_batch): one gather per batch
+            target = self._batch
+            if local and getattr(slot, "batch", None) is not None and slot.batch.size == B:
+                target = slot.batch
+            batch = gather_batch(self.data, rows, target, self.stream)
+            if target is not self._batch:
+                slot.batch_filled = True
             if local:
                 out = SoftLabels(slot.probs, slot.classes, self.cfg.temperature)
             else:
