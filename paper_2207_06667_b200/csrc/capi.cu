@@ -111,6 +111,11 @@ int num_sms() {
 // Pick the N tile for `cap` CTAs: fewest waves x tile time (one tile's time
 // ~ bn + 48 fixed cost), widest tile on ties (best operand reuse).
 int pick_bn_cap(int M, int N, int cap) {
+  static const int forced = [] {
+    const char* v = getenv("EDL_FORCE_BN");   // tuning runs only: 64 / 128 / 256
+    return v ? atoi(v) : 0;
+  }();
+  if (forced == 64 || forced == 128 || forced == 256) return forced;
   int best = 256;
   long long best_cost = -1;
   for (int bn : {256, 128, 64}) {
