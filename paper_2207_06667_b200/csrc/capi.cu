@@ -52,17 +52,17 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 struct MapKey {
   const void* ptr;
   long long rows, cols, ld;
-  int box0, box1;
+  int box0, box1, kind;
   bool operator==(const MapKey& o) const {
     return ptr == o.ptr && rows == o.rows && cols == o.cols && ld == o.ld && box0 == o.box0 &&
-           box1 == o.box1;
+           box1 == o.box1 && kind == o.kind;
   }
 };
 struct MapKeyHash {
   size_t operator()(const MapKey& k) const {
     size_t h = std::hash<const void*>()(k.ptr);
     h ^= std::hash<long long>()(k.rows * 1000003LL + k.cols) + 0x9e3779b9 + (h << 6) + (h >> 2);
-    h ^= std::hash<long long>()(k.ld * 131 + k.box0 * 7 + k.box1) + 0x9e3779b9 + (h << 6) + (h >> 2);
+    h ^= std::hash<long long>()(k.ld * 131 + k.box0 * 7 + k.box1 * 3 + k.kind) + 0x9e3779b9 + (h << 6) + (h >> 2);
     return h;
   }
 };
@@ -70,11 +70,14 @@ struct MapKeyHash {
 std::mutex g_map_mu;
 std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
 
-// 2-D bf16 row-major matrix [rows][cols] with leading dimension ld (elements),
-// box {box0 along cols, box1 along rows}, 128-byte swizzle, zero OOB fill.
-int tensor_map(const void* ptr, long long rows, long long cols, long long ld, int box0, int box1,
-               CUtensorMap* out) {
-  MapKey key{ptr, rows, cols, ld, box0, box1};
+// 2-D row-major matrix [rows][cols] with leading dimension ld (elements),
+// box {box0 along cols, box1 along rows}, zero OOB fill. kind 0: bf16 GEMM
+// operand, 128-byte swizzle; 1: fp32 TMA-store output, 128-byte swizzle;
+// 2: bf16 TMA-store output, 64-byte swizzle (the epilogue's staging layouts).
+enum MapKind { kOperandBf16 = 0, kOutF32 = 1, kOutBf16 = 2 };
+int tensor_map_ex(const void* ptr, long long rows, long long cols, long long ld, int box0, int box1, int kind,
+                  CUtensorMap* out) {
+  MapKey key{ptr, rows, cols, ld, box0, box1, kind};
   {
     std::lock_guard<std::mutex> g(g_map_mu);
     auto it = g_maps.find(key);
@@ -82,15 +85,17 @@ int tensor_map(const void* ptr, long long rows, long long cols, long long ld, in
   }
   auto fn = encode_fn();
   if (!fn) return fail(EDL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * 2) % 16)
+  const long long esize = kind == kOutF32 ? 4 : 2;
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * esize) % 16)
     return fail(EDL_ERR_SHAPE, "TMA operand needs 16-byte aligned base and row pitch (ld=%lld)", ld);
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * esize)};
   cuuint32_t box[2] = {static_cast<cuuint32_t>(box0), static_cast<cuuint32_t>(box1)};
   cuuint32_t estr[2] = {1, 1};
   CUtensorMap m;
-  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
-                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  CUresult r = fn(&m, kind == kOutF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  kind == kOutBf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(EDL_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
   {
@@ -100,6 +105,15 @@ int tensor_map(const void* ptr, long long rows, long long cols, long long ld, in
   }
   *out = m;
   return 0;
+}
+
+int tensor_map(const void* ptr, long long rows, long long cols, long long ld, int box0, int box1,
+               CUtensorMap* out) {
+  return tensor_map_ex(ptr, rows, cols, ld, box0, box1, kOperandBf16, out);
+}
+// The TMA-store map of a GEMM output (32 x 32 boxes, one per epilogue warp chunk).
+int tensor_map_out(const void* ptr, long long rows, long long cols, long long ld, bool f32, CUtensorMap* out) {
+  return tensor_map_ex(ptr, rows, cols, ld, 32, 32, f32 ? kOutF32 : kOutBf16, out);
 }
 
 int num_sms() {
@@ -248,15 +262,17 @@ int edl_linear_fwd(const void* X, long long ldx, const void* W, long long ldw, c
   int rc;
   if ((rc = tensor_map(X, M, K, ldx, 64, 128, &ta))) return rc;
   EpiArgs ep{Y, ldy, bias, nullptr, 0, 1.0f, stream_sched(as_stream(stream))};
+  CUtensorMap ty;
+  if ((rc = tensor_map_out(Y, M, N, ldy, act == EDL_ACT_NONE, &ty))) return rc;
   const int pbn = pick_pair_bn(M, N, cap);
   cudaError_t e;
   if (pbn > 0) {
     if ((rc = tensor_map(W, N, K, ldw, 64, pbn / 2, &tb))) return rc;
-    e = launch_gemm_pair(kind, pbn, ta, tb, M, N, K, ep, cap, as_stream(stream));
+    e = launch_gemm_pair(kind, pbn, ta, tb, ty, M, N, K, ep, cap, as_stream(stream));
   } else {
     const int bn = pick_bn_cap(M, N, cap);
     if ((rc = tensor_map(W, N, K, ldw, 64, bn, &tb))) return rc;
-    e = launch_gemm(kind, bn, ta, tb, M, N, K, ep, cap, as_stream(stream));
+    e = launch_gemm(kind, bn, ta, tb, ty, M, N, K, ep, cap, as_stream(stream));
   }
   return e == cudaSuccess ? 0 : cuda_fail(e, "linear_fwd");
 }
@@ -274,9 +290,11 @@ int edl_linear_bwd_data(const void* dY, long long lddy, const void* W, long long
   if ((rc = tensor_map(W, N, K, ldw, 64, 64, &tb))) return rc;
   EpiArgs ep{dX, lddx, nullptr, reinterpret_cast<const __nv_bfloat16*>(H), ldh, 1.0f,
              stream_sched(as_stream(stream))};
+  CUtensorMap ty;
+  if ((rc = tensor_map_out(dX, M, K, lddx, false, &ty))) return rc;
   const int pbn = pick_pair_bn(M, K, cap);
-  cudaError_t e = pbn > 0 ? launch_gemm_pair(GemmKind::BwdData, pbn, ta, tb, M, K, N, ep, cap, as_stream(stream))
-                          : launch_gemm(GemmKind::BwdData, pick_bn_cap(M, K, cap), ta, tb, M, K, N, ep, cap,
+  cudaError_t e = pbn > 0 ? launch_gemm_pair(GemmKind::BwdData, pbn, ta, tb, ty, M, K, N, ep, cap, as_stream(stream))
+                          : launch_gemm(GemmKind::BwdData, pick_bn_cap(M, K, cap), ta, tb, ty, M, K, N, ep, cap,
                                         as_stream(stream));
   return e == cudaSuccess ? 0 : cuda_fail(e, "linear_bwd_data");
 }
@@ -293,7 +311,8 @@ int edl_linear_bwd_weight(const void* dY, long long lddy, const void* X, long lo
   if ((rc = tensor_map(dY, M, N, lddy, 64, 64, &ta))) return rc;
   if ((rc = tensor_map(X, M, K, ldx, 64, 64, &tb))) return rc;
   EpiArgs ep{dW, lddw, nullptr, nullptr, 0, scale, stream_sched(as_stream(stream))};
-  cudaError_t e = launch_gemm(GemmKind::BwdWeight, bn, ta, tb, N, K, M, ep, grid_cap(as_stream(stream)),
+  cudaError_t e = launch_gemm(GemmKind::BwdWeight, bn, ta, tb, ta /*unused: plain-store epilogue*/, N, K, M, ep,
+                              grid_cap(as_stream(stream)),
                               as_stream(stream));
   if (e != cudaSuccess) return cuda_fail(e, "linear_bwd_weight");
   if (db) {

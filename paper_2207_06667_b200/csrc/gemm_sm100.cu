@@ -38,7 +38,9 @@ struct GemmCfg {
   static constexpr uint32_t kBBytes = BN * kBK * 2;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr uint32_t kEpiBytes = 2 * BN * 4;   // double-buffered bias slice
-  static constexpr uint32_t kSmem = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t kStoreBytes = 4 * 4096;   // TMA-store staging, one 32x32 fp32 tile per epilogue warp
+  static constexpr uint32_t kSmem =
+      kStages * kStageBytes + kStoreBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 // Issue the TMA loads of one (A,B) k-block into stage buffers, with per-operand
@@ -279,11 +281,147 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& ep, uint32_t taddr,
   }
 }
 
+// ---- TMA-store epilogue (bias / tanh / (1-a^2) outputs)
+// A thread-per-row store pattern sends every warp store instruction to 32
+// different rows (16 B each): measured ~1.5-2 TB/s, the fixed cost that
+// dominated the one-wave GEMMs (scripts/gemm_scaling.py: ~11 us at K=64 for
+// a 4096 x 1008 fp32 output). Instead each epilogue warp writes its 32 x 32
+// chunk into a swizzled shared-memory tile and one TMA store moves it out in
+// full lines; ragged M / N edges are clipped by the tensor map.
+template <int EPI>
+__host__ __device__ constexpr bool epi_tma_store() {
+  return EPI == EPI_TANH_BF16 || EPI == EPI_BIAS_F32 || EPI == EPI_DTANH_BF16;
+}
+
+// The epilogue math of epilogue_store without its global stores (v in place).
+template <int EPI>
+__device__ __forceinline__ void epi_math(const EpiArgs& ep, int row, int M, int col0, int N, float (&v)[32],
+                                         const float* sb, const uint4* hpre) {
+  if constexpr (EPI == EPI_TANH_BF16 || EPI == EPI_BIAS_F32) {
+    if (sb != nullptr) {
+      const float4* b4 = reinterpret_cast<const float4*>(sb);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float4 b = b4[i];
+        v[4 * i] += b.x; v[4 * i + 1] += b.y; v[4 * i + 2] += b.z; v[4 * i + 3] += b.w;
+      }
+    } else if (ep.bias != nullptr) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < N) v[i] += __ldg(ep.bias + col0 + i);
+    }
+  }
+  if constexpr (EPI == EPI_TANH_BF16) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = tanh_fast(v[i]);
+  }
+  if constexpr (EPI == EPI_DTANH_BF16) {
+    if (row >= M) return;
+    if (hpre != nullptr) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&hpre[i]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float a = __bfloat162float(hb[j]);
+          v[8 * i + j] *= (1.0f - a * a);
+        }
+      }
+    } else {
+      const __nv_bfloat16* h = ep.aux + static_cast<size_t>(row) * ep.ld_aux + col0;
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < N) {
+          const float a = __bfloat162float(h[i]);
+          v[i] *= (1.0f - a * a);
+        }
+    }
+  }
+}
+
+// Thread `lane` writes its row's 32 values into the warp's staging tile in the
+// tensor map's swizzle: fp32 rows of 128 B (SWIZZLE_128B: 16-byte chunk i at
+// i ^ (row % 8)), bf16 rows of 64 B (SWIZZLE_64B: chunk i at i ^ ((row / 2) % 4)).
+// Both orders make the eight rows of each 128-bit store phase hit distinct banks.
+template <bool kF32>
+__device__ __forceinline__ void stage_chunk(uint8_t* stg, int lane, const float (&v)[32]) {
+  if constexpr (kF32) {
+    float4* base = reinterpret_cast<float4*>(stg + lane * 128);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) base[i ^ (lane & 7)] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+  } else {
+    uint4* base = reinterpret_cast<uint4*>(stg + lane * 64);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint4 q;
+      q.x = pack_bf16x2(v[8 * i + 0], v[8 * i + 1]);
+      q.y = pack_bf16x2(v[8 * i + 2], v[8 * i + 3]);
+      q.z = pack_bf16x2(v[8 * i + 4], v[8 * i + 5]);
+      q.w = pack_bf16x2(v[8 * i + 6], v[8 * i + 7]);
+      base[i ^ ((lane >> 1) & 3)] = q;
+    }
+  }
+}
+
+// epilogue_tile with the TMA-store path; row0 = first of this warp's 32 rows.
+template <int BN, int EPI>
+__device__ __forceinline__ void epilogue_tile_tma(const EpiArgs& ep, uint32_t taddr, int row0, int lane, int M,
+                                                  int n0, int N, const float* sb, const CUtensorMap* tmY,
+                                                  uint8_t* stg) {
+  constexpr bool kAux = EPI == EPI_DTANH_BF16;
+  const int row = row0 + lane;
+  const bool row_ok = row < M;
+  auto aux_ptr = [&](int c) {
+    return reinterpret_cast<const uint4*>(ep.aux + static_cast<size_t>(row) * ep.ld_aux + n0 + c);
+  };
+  uint4 h[4];
+  if constexpr (kAux) {
+    if (row_ok && n0 + 32 <= N) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) h[i] = __ldg(aux_ptr(0) + i);
+    }
+  }
+  uint32_t r[32];
+  tmem_ld32_issue(taddr, r);
+  tmem_ld_wait(r);
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 32) {
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+    uint4 hc[4];
+    if constexpr (kAux) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) hc[i] = h[i];
+      if (row_ok && c + 32 < BN && n0 + c + 64 <= N) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = __ldg(aux_ptr(c + 32) + i);
+      }
+    }
+    if (c + 32 < BN) tmem_ld32_issue(taddr + c + 32, r);
+    const bool live = n0 + c < N;   // warp-uniform
+    if (live) epi_math<EPI>(ep, row, M, n0 + c, N, v, sb != nullptr ? sb + c : nullptr,
+                            (kAux && n0 + c + 32 <= N) ? hc : nullptr);
+    if (live) {
+      if (lane == 0) bulk_wait_read0();        // the previous chunk has left the staging tile
+      __syncwarp();
+      stage_chunk<EPI == EPI_BIAS_F32>(stg, lane, v);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(tmY, stg, n0 + c, row0);
+        bulk_commit();
+      }
+    }
+    if (c + 32 < BN) tmem_ld_wait(r);
+  }
+}
+
 // ------------------------------------------------------------------ GEMM
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                int M, int N, int K, EpiArgs ep) {
+                const __grid_constant__ CUtensorMap tmY, int M, int N, int K, EpiArgs ep) {
   using Cfg = GemmCfg<BN>;
   unsigned* const sched = ep.sched;
   constexpr int S = Cfg::kStages;
@@ -293,8 +431,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
-  float* sbias = reinterpret_cast<float*>(sB + S * Cfg::kBBytes);   // [2][BN]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kBBytes + Cfg::kEpiBytes);
+  uint8_t* stg = sB + S * Cfg::kBBytes;                              // [4][4 KB] TMA-store staging
+  float* sbias = reinterpret_cast<float*>(stg + Cfg::kStoreBytes);   // [2][BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + Cfg::kStoreBytes + Cfg::kEpiBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -392,11 +531,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t as = i & 1;
       mbar_wait(&tfull[as], (i >> 1) & 1);
       tc_fence_after();
-      epilogue_tile<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e + lane,
-                             M, n0, N, epi_has_bias<EPI>() ? sb : nullptr);
+      if constexpr (epi_tma_store<EPI>())
+        epilogue_tile_tma<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e,
+                                   lane, M, n0, N, epi_has_bias<EPI>() ? sb : nullptr, &tmY, stg + e * 4096);
+      else
+        epilogue_tile<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e + lane,
+                               M, n0, N, epi_has_bias<EPI>() ? sb : nullptr);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[as]);
+    }
+    if constexpr (epi_tma_store<EPI>()) {   // this warp's TMA stores are complete before smem goes away
+      if (lane == 0) bulk_wait0();
+      __syncwarp();
     }
   }
   __syncthreads();
@@ -433,7 +580,8 @@ struct PairCfg {
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
   static constexpr uint32_t kEpiBytes = 2 * BN * 4;
-  static constexpr uint32_t kSmem = kStages * kStageBytes + kEpiBytes + 1024 + 256;
+  static constexpr uint32_t kStoreBytes = 4 * 4096;
+  static constexpr uint32_t kSmem = kStages * kStageBytes + kStoreBytes + kEpiBytes + 1024 + 256;
 };
 
 template <int BN, bool A_MN, bool B_MN>
@@ -472,7 +620,7 @@ __device__ __forceinline__ void mma_kblock_pair(uint32_t d_tmem, uint32_t a_base
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     int M, int N, int K, EpiArgs ep) {
+                     const __grid_constant__ CUtensorMap tmY, int M, int N, int K, EpiArgs ep) {
   using Cfg = PairCfg<BN>;
   unsigned* const sched = ep.sched;
   constexpr int S = Cfg::kStages;
@@ -482,8 +630,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
-  float* sbias = reinterpret_cast<float*>(sB + S * Cfg::kBBytes);   // [2][BN]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kBBytes + Cfg::kEpiBytes);
+  uint8_t* stg = sB + S * Cfg::kBBytes;                              // [4][4 KB] TMA-store staging
+  float* sbias = reinterpret_cast<float*>(stg + Cfg::kStoreBytes);   // [2][BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + Cfg::kStoreBytes + Cfg::kEpiBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -592,11 +741,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t as = i & 1;
       mbar_wait(&tfull[as], (i >> 1) & 1);
       tc_fence_after();
-      epilogue_tile<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e + lane,
-                             M, n0, N, epi_has_bias<EPI>() ? sb : nullptr);
+      if constexpr (epi_tma_store<EPI>())
+        epilogue_tile_tma<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e,
+                                   lane, M, n0, N, epi_has_bias<EPI>() ? sb : nullptr, &tmY, stg + e * 4096);
+      else
+        epilogue_tile<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e + lane,
+                               M, n0, N, epi_has_bias<EPI>() ? sb : nullptr);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty0 + 8 * as);
+    }
+    if constexpr (epi_tma_store<EPI>()) {
+      if (lane == 0) bulk_wait0();
+      __syncwarp();
     }
   }
   tc_fence_before();
@@ -735,8 +892,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
-  float* sbias = reinterpret_cast<float*>(sB + S * Cfg::kBBytes);   // [2][BN]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kBBytes + Cfg::kEpiBytes);
+  uint8_t* stg = sB + S * Cfg::kBBytes;                              // [4][4 KB] TMA-store staging
+  float* sbias = reinterpret_cast<float*>(stg + Cfg::kStoreBytes);   // [2][BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + Cfg::kStoreBytes + Cfg::kEpiBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -957,8 +1115,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
-  float* sbias = reinterpret_cast<float*>(sB + S * Cfg::kBBytes);   // [2][BN]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kBBytes + Cfg::kEpiBytes);
+  uint8_t* stg = sB + S * Cfg::kBBytes;                              // [4][4 KB] TMA-store staging
+  float* sbias = reinterpret_cast<float*>(stg + Cfg::kStoreBytes);   // [2][BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + Cfg::kStoreBytes + Cfg::kEpiBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
@@ -1159,76 +1318,75 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ------------------------------------------------------------------ launchers
 template <int BN, bool A_MN, bool B_MN, int EPI>
-static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N,
+static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, int M, int N,
                                  int K, const EpiArgs& ep, int num_sms, cudaStream_t stream) {
   auto kern = gemm_kernel<BN, A_MN, B_MN, EPI>;
   cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), GemmCfg<BN>::kSmem);
   if (e != cudaSuccess) return e;
   const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms ? tiles : num_sms;
-  return launch_pdl(kern, dim3(grid), dim3(kThreads), GemmCfg<BN>::kSmem, stream, 1, ta, tb, M, N, K, ep);
+  return launch_pdl(kern, dim3(grid), dim3(kThreads), GemmCfg<BN>::kSmem, stream, 1, ta, tb, ty, M, N, K, ep);
 }
 
 template <bool A_MN, bool B_MN, int EPI>
-static cudaError_t launch_gemm_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb, int M,
-                                  int N, int K, const EpiArgs& ep, int num_sms,
-                                  cudaStream_t stream) {
+static cudaError_t launch_gemm_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty,
+                                  int M, int N, int K, const EpiArgs& ep, int num_sms, cudaStream_t stream) {
   switch (bn) {
-    case 64: return launch_gemm_t<64, A_MN, B_MN, EPI>(ta, tb, M, N, K, ep, num_sms, stream);
-    case 128: return launch_gemm_t<128, A_MN, B_MN, EPI>(ta, tb, M, N, K, ep, num_sms, stream);
-    case 256: return launch_gemm_t<256, A_MN, B_MN, EPI>(ta, tb, M, N, K, ep, num_sms, stream);
+    case 64: return launch_gemm_t<64, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream);
+    case 128: return launch_gemm_t<128, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream);
+    case 256: return launch_gemm_t<256, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream);
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
-                        int M, int N, int K, const EpiArgs& ep, int num_sms,
+                        const CUtensorMap& ty, int M, int N, int K, const EpiArgs& ep, int num_sms,
                         cudaStream_t stream) {
   switch (kind) {
     case GemmKind::FwdTanh:
-      return launch_gemm_bn<false, false, EPI_TANH_BF16>(bn, ta, tb, M, N, K, ep, num_sms, stream);
+      return launch_gemm_bn<false, false, EPI_TANH_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
     case GemmKind::FwdLinear:
-      return launch_gemm_bn<false, false, EPI_BIAS_F32>(bn, ta, tb, M, N, K, ep, num_sms, stream);
+      return launch_gemm_bn<false, false, EPI_BIAS_F32>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
     case GemmKind::BwdData:
-      return launch_gemm_bn<false, true, EPI_DTANH_BF16>(bn, ta, tb, M, N, K, ep, num_sms, stream);
+      return launch_gemm_bn<false, true, EPI_DTANH_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
     case GemmKind::BwdWeight:
-      return launch_gemm_bn<true, true, EPI_F32>(bn, ta, tb, M, N, K, ep, num_sms, stream);
+      return launch_gemm_bn<true, true, EPI_F32>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
   }
   return cudaErrorInvalidValue;
 }
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
-static cudaError_t launch_pair_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
-                                 const EpiArgs& ep, int num_sms, cudaStream_t stream) {
+static cudaError_t launch_pair_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, int M, int N,
+                                 int K, const EpiArgs& ep, int num_sms, cudaStream_t stream) {
   auto kern = gemm_pair_kernel<BN, A_MN, B_MN, EPI>;
   cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), PairCfg<BN>::kSmem);
   if (e != cudaSuccess) return e;
   const int tiles = ((M + 2 * kBM - 1) / (2 * kBM)) * ((N + BN - 1) / BN);
   const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
   if (pairs < 1) return cudaErrorInvalidValue;
-  return launch_pdl(kern, dim3(2 * pairs), dim3(kThreads), PairCfg<BN>::kSmem, stream, 2, ta, tb, M, N, K, ep);
+  return launch_pdl(kern, dim3(2 * pairs), dim3(kThreads), PairCfg<BN>::kSmem, stream, 2, ta, tb, ty, M, N, K, ep);
 }
 
 template <bool A_MN, bool B_MN, int EPI>
-static cudaError_t launch_pair_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N,
-                                  int K, const EpiArgs& ep, int num_sms, cudaStream_t stream) {
+static cudaError_t launch_pair_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, int M,
+                                  int N, int K, const EpiArgs& ep, int num_sms, cudaStream_t stream) {
   switch (bn) {
-    case 128: return launch_pair_t<128, A_MN, B_MN, EPI>(ta, tb, M, N, K, ep, num_sms, stream);
-    case 256: return launch_pair_t<256, A_MN, B_MN, EPI>(ta, tb, M, N, K, ep, num_sms, stream);
+    case 128: return launch_pair_t<128, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream);
+    case 256: return launch_pair_t<256, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream);
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_gemm_pair(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
-                             int M, int N, int K, const EpiArgs& ep, int num_sms,
+                             const CUtensorMap& ty, int M, int N, int K, const EpiArgs& ep, int num_sms,
                              cudaStream_t stream) {
   switch (kind) {
     case GemmKind::FwdTanh:
-      return launch_pair_bn<false, false, EPI_TANH_BF16>(bn, ta, tb, M, N, K, ep, num_sms, stream);
+      return launch_pair_bn<false, false, EPI_TANH_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
     case GemmKind::FwdLinear:
-      return launch_pair_bn<false, false, EPI_BIAS_F32>(bn, ta, tb, M, N, K, ep, num_sms, stream);
+      return launch_pair_bn<false, false, EPI_BIAS_F32>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
     case GemmKind::BwdData:
-      return launch_pair_bn<false, true, EPI_DTANH_BF16>(bn, ta, tb, M, N, K, ep, num_sms, stream);
+      return launch_pair_bn<false, true, EPI_DTANH_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
     default:
       return cudaErrorInvalidValue;
   }

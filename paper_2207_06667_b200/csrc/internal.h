@@ -89,8 +89,10 @@ int grouped_tile_bn();
 cudaError_t launch_gemm_grouped_pair_bwd_weight(const GroupMaps& maps, const GroupArgs& ga, int num_sms,
                                                 cudaStream_t stream, bool fused_sgd = false);
 
+// ty: the output's TMA-store map (32 x 32 boxes; tensor_map_out) for the
+// bias / tanh / (1-a^2) epilogues; ignored (any valid map) for BwdWeight.
 cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
-                        int M, int N, int K, const EpiArgs& ep, int num_sms,
+                        const CUtensorMap& ty, int M, int N, int K, const EpiArgs& ep, int num_sms,
                         cudaStream_t stream);
 // Stream-ordered flag fallbacks (exchange.cu).
 cudaError_t launch_flag_wait(const uint32_t* addr, uint32_t value, cudaStream_t stream);
@@ -103,7 +105,7 @@ cudaError_t launch_nvls_allreduce_sgd(float* mc_grad, float* mc_param, void* mc_
 // 256 x bn tiles on CTA pairs (cta_group::2); bn in {128, 256}; B's tensor
 // map box covers bn/2 rows (K-major) or bn/2 columns (MN-major).
 cudaError_t launch_gemm_pair(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
-                             int M, int N, int K, const EpiArgs& ep, int num_sms,
+                             const CUtensorMap& ty, int M, int N, int K, const EpiArgs& ep, int num_sms,
                              cudaStream_t stream);
 cudaError_t launch_teacher_head(int bn, int kmax, const CUtensorMap& ta, const CUtensorMap& tb,
                                 int M, int N, int K, const HeadArgs& hp, cudaStream_t stream);
