@@ -37,10 +37,11 @@ struct GemmCfg {
   static constexpr uint32_t kABytes = kBM * kBK * 2;
   static constexpr uint32_t kBBytes = BN * kBK * 2;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-  static constexpr uint32_t kEpiBytes = 2 * BN * 4;   // double-buffered bias slice
-  static constexpr uint32_t kStoreBytes = 4 * 4096;   // TMA-store staging, one 32x32 fp32 tile per epilogue warp
+  static constexpr uint32_t kEpiBytes = BN * 4;          // the tile's bias slice
+  static constexpr uint32_t kStoreBytes = 4 * 2 * 4096;  // TMA-store staging: two 32x32 fp32 tiles per epilogue warp
   static constexpr uint32_t kSmem =
       kStages * kStageBytes + kStoreBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(kSmem <= 227 * 1024, "exceeds the sm_100 per-CTA shared memory limit");
 };
 
 // Issue the TMA loads of one (A,B) k-block into stage buffers, with per-operand
@@ -364,10 +365,13 @@ __device__ __forceinline__ void stage_chunk(uint8_t* stg, int lane, const float 
 }
 
 // epilogue_tile with the TMA-store path; row0 = first of this warp's 32 rows.
+// stg: this warp's two 4 KB staging tiles, used alternately by store count
+// (`stores`, per warp, carried across tiles) so a chunk is written while the
+// previous chunk's store is still reading the other tile.
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_tile_tma(const EpiArgs& ep, uint32_t taddr, int row0, int lane, int M,
                                                   int n0, int N, const float* sb, const CUtensorMap* tmY,
-                                                  uint8_t* stg) {
+                                                  uint8_t* stg, uint32_t& stores) {
   constexpr bool kAux = EPI == EPI_DTANH_BF16;
   const int row = row0 + lane;
   const bool row_ok = row < M;
@@ -403,15 +407,17 @@ __device__ __forceinline__ void epilogue_tile_tma(const EpiArgs& ep, uint32_t ta
     if (live) epi_math<EPI>(ep, row, M, n0 + c, N, v, sb != nullptr ? sb + c : nullptr,
                             (kAux && n0 + c + 32 <= N) ? hc : nullptr);
     if (live) {
-      if (lane == 0) bulk_wait_read0();        // the previous chunk has left the staging tile
+      uint8_t* buf = stg + (stores & 1) * 4096;
+      if (lane == 0) bulk_wait_read1();        // only the newest store (other tile) may still be reading
       __syncwarp();
-      stage_chunk<EPI == EPI_BIAS_F32>(stg, lane, v);
+      stage_chunk<EPI == EPI_BIAS_F32>(buf, lane, v);
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        tma_store_2d(tmY, stg, n0 + c, row0);
+        tma_store_2d(tmY, buf, n0 + c, row0);
         bulk_commit();
       }
+      ++stores;
     }
     if (c + 32 < BN) tmem_ld_wait(r);
   }
@@ -431,8 +437,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
-  uint8_t* stg = sB + S * Cfg::kBBytes;                              // [4][4 KB] TMA-store staging
-  float* sbias = reinterpret_cast<float*>(stg + Cfg::kStoreBytes);   // [2][BN]
+  uint8_t* stg = sB + S * Cfg::kBBytes;                              // [4 warps][2][4 KB] TMA-store staging
+  float* sbias = reinterpret_cast<float*>(stg + Cfg::kStoreBytes);   // [BN]
   uint64_t* full = reinterpret_cast<uint64_t*>(stg + Cfg::kStoreBytes + Cfg::kEpiBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
@@ -517,6 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     const int e = warp - 4;
+    uint32_t stores = 0;
     for (uint32_t i = 0;; ++i) {
       const int slot = i & 3;
       mbar_wait(&tile_full[slot], (i >> 2) & 1);
@@ -525,7 +532,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(&tile_empty[slot]);
       if (t >= tiles) break;
       const int m0 = (t % num_m) * kBM, n0 = (t / num_m) * BN;
-      float* sb = sbias + (i & 1) * BN;
+      float* sb = sbias;
       stage_bias<BN, EPI>(ep, sb, n0, N, static_cast<int>(threadIdx.x) - 128);
       if constexpr (epi_has_bias<EPI>()) epi_bar_sync();
       const uint32_t as = i & 1;
@@ -533,10 +540,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       if constexpr (epi_tma_store<EPI>())
         epilogue_tile_tma<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e,
-                                   lane, M, n0, N, epi_has_bias<EPI>() ? sb : nullptr, &tmY, stg + e * 4096);
+                                   lane, M, n0, N, epi_has_bias<EPI>() ? sb : nullptr, &tmY, stg + e * 8192, stores);
       else
         epilogue_tile<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e + lane,
                                M, n0, N, epi_has_bias<EPI>() ? sb : nullptr);
+      if constexpr (epi_has_bias<EPI>()) epi_bar_sync();   // every warp is done with the bias slice
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[as]);
@@ -579,9 +587,10 @@ struct PairCfg {
   static constexpr uint32_t kBBytes = kHalfN * kBK * 2;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
-  static constexpr uint32_t kEpiBytes = 2 * BN * 4;
-  static constexpr uint32_t kStoreBytes = 4 * 4096;
+  static constexpr uint32_t kEpiBytes = BN * 4;
+  static constexpr uint32_t kStoreBytes = 4 * 2 * 4096;
   static constexpr uint32_t kSmem = kStages * kStageBytes + kStoreBytes + kEpiBytes + 1024 + 256;
+  static_assert(kSmem <= 227 * 1024, "exceeds the sm_100 per-CTA shared memory limit");
 };
 
 template <int BN, bool A_MN, bool B_MN>
@@ -630,8 +639,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
-  uint8_t* stg = sB + S * Cfg::kBBytes;                              // [4][4 KB] TMA-store staging
-  float* sbias = reinterpret_cast<float*>(stg + Cfg::kStoreBytes);   // [2][BN]
+  uint8_t* stg = sB + S * Cfg::kBBytes;                              // [4 warps][2][4 KB] TMA-store staging
+  float* sbias = reinterpret_cast<float*>(stg + Cfg::kStoreBytes);   // [BN]
   uint64_t* full = reinterpret_cast<uint64_t*>(stg + Cfg::kStoreBytes + Cfg::kEpiBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
@@ -728,6 +737,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     const int e = warp - 4;
+    uint32_t stores = 0;
     for (uint32_t i = 0;; ++i) {
       const int t = take_tile(i);
       __syncwarp();
@@ -735,7 +745,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (t >= tiles) break;
       const int m0 = (t % num_m) * 2 * kBM + static_cast<int>(rank) * kBM;
       const int n0 = (t / num_m) * BN;
-      float* sb = sbias + (i & 1) * BN;
+      float* sb = sbias;
       stage_bias<BN, EPI>(ep, sb, n0, N, static_cast<int>(threadIdx.x) - 128);
       if constexpr (epi_has_bias<EPI>()) epi_bar_sync();
       const uint32_t as = i & 1;
@@ -743,10 +753,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       if constexpr (epi_tma_store<EPI>())
         epilogue_tile_tma<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e,
-                                   lane, M, n0, N, epi_has_bias<EPI>() ? sb : nullptr, &tmY, stg + e * 4096);
+                                   lane, M, n0, N, epi_has_bias<EPI>() ? sb : nullptr, &tmY, stg + e * 8192, stores);
       else
         epilogue_tile<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e + lane,
                                M, n0, N, epi_has_bias<EPI>() ? sb : nullptr);
+      if constexpr (epi_has_bias<EPI>()) epi_bar_sync();   // every warp is done with the bias slice
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty0 + 8 * as);
@@ -892,8 +903,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
-  uint8_t* stg = sB + S * Cfg::kBBytes;                              // [4][4 KB] TMA-store staging
-  float* sbias = reinterpret_cast<float*>(stg + Cfg::kStoreBytes);   // [2][BN]
+  uint8_t* stg = sB + S * Cfg::kBBytes;                              // [4 warps][2][4 KB] TMA-store staging
+  float* sbias = reinterpret_cast<float*>(stg + Cfg::kStoreBytes);   // [BN]
   uint64_t* full = reinterpret_cast<uint64_t*>(stg + Cfg::kStoreBytes + Cfg::kEpiBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
@@ -1115,8 +1126,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
-  uint8_t* stg = sB + S * Cfg::kBBytes;                              // [4][4 KB] TMA-store staging
-  float* sbias = reinterpret_cast<float*>(stg + Cfg::kStoreBytes);   // [2][BN]
+  uint8_t* stg = sB + S * Cfg::kBBytes;                              // [4 warps][2][4 KB] TMA-store staging
+  float* sbias = reinterpret_cast<float*>(stg + Cfg::kStoreBytes);   // [BN]
   uint64_t* full = reinterpret_cast<uint64_t*>(stg + Cfg::kStoreBytes + Cfg::kEpiBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
