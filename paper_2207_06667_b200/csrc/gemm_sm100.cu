@@ -423,6 +423,27 @@ __device__ __forceinline__ void epilogue_tile_tma(const EpiArgs& ep, uint32_t ta
   }
 }
 
+// Tile raster: groups of kRasterGroup m-tiles, m fastest inside a group,
+// then n, then the next group. A wave of ~148 tiles then covers a
+// kRasterGroup x ~(148 / kRasterGroup) block, and the group's A panels stay
+// L2-resident across the waves that sweep its n range. With plain m-fastest
+// order every wave re-read the whole A operand from DRAM (teacher layer 2:
+// 676 MB per launch against 256 MB algorithmic, profiles/).
+// Only when A is too big to stay resident anyway: with a 25 MB A (teacher
+// layer 1) m-fastest already reads it once, and grouping would re-read B.
+constexpr int kRasterGroup = 8;
+__device__ __forceinline__ int raster_group(int num_m, int M, int K) {
+  return static_cast<long long>(M) * K * 2 > (32ll << 20) ? kRasterGroup : num_m;
+}
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int group, int& mt, int& nt) {
+  const int per_group = group * num_n;
+  const int g = t / per_group;
+  const int r = t - g * per_group;
+  const int gm = num_m - g * group < group ? num_m - g * group : group;
+  mt = g * group + r % gm;
+  nt = r / gm;
+}
+
 // ------------------------------------------------------------------ GEMM
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -469,6 +490,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n;
   const int nk = (K + kBK - 1) / kBK;
+  const int rgroup = raster_group(num_m, M, K);
 
   // Dynamic tile scheduler: the producer claims tiles from a per-stream
   // global counter and publishes them to the MMA and epilogue roles through a
@@ -491,7 +513,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       tile_ring[slot] = t;
       mbar_arrive(&tile_full[slot]);
       if (t >= tiles) break;
-      const int m0 = (t % num_m) * kBM, n0 = (t / num_m) * BN;
+      int mt, nt;
+      tile_coords(t, num_m, num_n, rgroup, mt, nt);
+      const int m0 = mt * kBM, n0 = nt * BN;
       for (int kb = 0; kb < nk; ++kb, ++g) {
         const int s = g % S;
         mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
@@ -531,7 +555,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tile_empty[slot]);
       if (t >= tiles) break;
-      const int m0 = (t % num_m) * kBM, n0 = (t / num_m) * BN;
+      int mt, nt;
+      tile_coords(t, num_m, num_n, rgroup, mt, nt);
+      const int m0 = mt * kBM, n0 = nt * BN;
       float* sb = sbias;
       stage_bias<BN, EPI>(ep, sb, n0, N, static_cast<int>(threadIdx.x) - 128);
       if constexpr (epi_has_bias<EPI>()) epi_bar_sync();
@@ -673,6 +699,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n;
   const int nk = (K + kBK - 1) / kBK;
+  const int rgroup = raster_group(num_m, M, K);
   const int pair = static_cast<int>(blockIdx.x) / 2;
   const int npairs = static_cast<int>(gridDim.x) / 2;
   const uint32_t full0 = mapa(smem_u32(full), 0);           // rank 0's full[0]
@@ -705,8 +732,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         release_tile(i);
       }
       if (t >= tiles) break;
-      const int m0 = (t % num_m) * 2 * kBM + static_cast<int>(rank) * kBM;
-      const int n0 = (t / num_m) * BN + static_cast<int>(rank) * Cfg::kHalfN;
+      int mt, nt;
+      tile_coords(t, num_m, num_n, rgroup, mt, nt);
+      const int m0 = mt * 2 * kBM + static_cast<int>(rank) * kBM;
+      const int n0 = nt * BN + static_cast<int>(rank) * Cfg::kHalfN;
       for (int kb = 0; kb < nk; ++kb, ++g) {
         const int s = g % S;
         mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
@@ -743,8 +772,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) release_tile(i);
       if (t >= tiles) break;
-      const int m0 = (t % num_m) * 2 * kBM + static_cast<int>(rank) * kBM;
-      const int n0 = (t / num_m) * BN;
+      int mt, nt;
+      tile_coords(t, num_m, num_n, rgroup, mt, nt);
+      const int m0 = mt * 2 * kBM + static_cast<int>(rank) * kBM;
+      const int n0 = nt * BN;
       float* sb = sbias;
       stage_bias<BN, EPI>(ep, sb, n0, N, static_cast<int>(threadIdx.x) - 128);
       if constexpr (epi_has_bias<EPI>()) epi_bar_sync();
