@@ -50,12 +50,15 @@ int edl_set_stream_max_ctas(void* stream, int max_ctas);
 /* One dense layer of edl.nnkit.forward (edl/nnkit.py:223-234, `z = h @ w.T + b`
  * at :232, tanh at :233). X: bf16 [M][ldx] (K used), W: bf16 [N][ldw], bias:
  * fp32 [N]. act=EDL_ACT_TANH writes bf16 Y [M][ldy]; EDL_ACT_NONE writes fp32.
- * tcgen05 GEMM, TMA-fed, fused bias/activation epilogue. */
+ * tcgen05 GEMM, TMA-fed, fused bias/activation epilogue, TMA-stored output:
+ * every operand AND Y need a 16-byte aligned base and row pitch
+ * (ld * element size % 16 == 0), else EDL_ERR_SHAPE. */
 int edl_linear_fwd(const void* X, long long ldx, const void* W, long long ldw, const float* bias,
                    void* Y, long long ldy, int M, int N, int K, int act, void* stream);
 
 /* Backprop through one tanh layer, edl/nnkit.py:308:
- *   dX[M][K] = (dY[M][N] @ W[N][K]) * (1 - H[M][K]^2)      (all bf16) */
+ *   dX[M][K] = (dY[M][N] @ W[N][K]) * (1 - H[M][K]^2)      (all bf16)
+ * Same alignment rule as edl_linear_fwd (dX is TMA-stored). */
 int edl_linear_bwd_data(const void* dY, long long lddy, const void* W, long long ldw,
                         const void* H, long long ldh, void* dX, long long lddx, int M, int N,
                         int K, void* stream);
