@@ -1,12 +1,14 @@
 """Teacher pool on dedicated GPUs feeding student GPUs over NVLink.
 
 BASELINE.json configs[2] / SURVEY §8(e): a pool of teacher ranks produces
-soft labels for the student ranks' batches; each batch's (prob, class) pairs
-cross NVLink as one NCCL point-to-point transfer (teacher rank -> owning
-student rank) on NCCL's side stream, straight into a slot of the student's
-device ring. The student ranks run data-parallel SGD with the gradient
-all-reduced over an NCCL group that contains students only, so teacher
-churn never re-forms the student communicator.
+soft labels for the student ranks' batches; each batch's packed (prob, class)
+pairs cross NVLink straight into a slot of the student's device ring, either
+by peer copy with stream-ordered READY / CREDIT flags (PeerSoftLabelRing, the
+default: no NCCL, no host waits, no SM held while waiting) or as one NCCL
+send/recv per batch (teacher_serve / RemoteSoftLabels without a ring). The
+student ranks run data-parallel SGD with the gradient all-reduced over an
+NCCL group that contains students only, so teacher churn never re-forms the
+student communicator.
 
 Requests need no wire message: every teacher rank holds a replica of the
 HBM-resident dataset and of each student's ShardSampler (same seed, rank and
