@@ -36,6 +36,8 @@ extern "C" {
 
 #define EDL_ACT_NONE 0 /* z = x W^T + b, fp32 out (logit layer)           */
 #define EDL_ACT_TANH 1 /* h = tanh(x W^T + b), bf16 out (hidden layers)   */
+#define EDL_ACT_RELU 2 /* h = relu(x W^T + b), bf16 out (cfg4 conv layers) */
+#define EDL_ACT_IDENT 3 /* h = x W^T + b, bf16 out (cfg4 shortcut projections) */
 
 int edl_version(void);
 const char* edl_last_error(void);
@@ -55,6 +57,27 @@ int edl_set_stream_max_ctas(void* stream, int max_ctas);
  * (ld * element size % 16 == 0), else EDL_ERR_SHAPE. */
 int edl_linear_fwd(const void* X, long long ldx, const void* W, long long ldw, const float* bias,
                    void* Y, long long ldy, int M, int N, int K, int act, void* stream);
+
+/* ---- cfg4 (ResNet-style teacher, BASELINE.json configs[3]; the reference has
+ * no convolutions). A convolution is edl_im2col_nhwc into a
+ * caller workspace followed by edl_linear_fwd (act RELU) or
+ * edl_linear_fwd_residual with the folded-BN weights W[K_out][R*S*C] and bias.
+ * Activations: NHWC bf16, C a multiple of 8 (16 keeps TMA rows aligned). */
+
+/* Y = relu(X W^T + b + R): a ResNet block's last convolution with its
+ * shortcut R (bf16 [M][ldr], same shape as Y). Alignment as edl_linear_fwd. */
+int edl_linear_fwd_residual(const void* X, long long ldx, const void* W, long long ldw, const float* bias,
+                            const void* R, long long ldr, void* Y, long long ldy, int M, int N, int K,
+                            void* stream);
+/* out[(n,p,q)][(r,s,c)] = x[n][p*stride-pad+r][q*stride-pad+s][c] (0 outside),
+ * P = (H + 2pad - R)/stride + 1, Q likewise; out row pitch ldo >= R*S*C. */
+int edl_im2col_nhwc(const void* x, int N, int H, int W, int C, int R, int S, int stride, int pad, void* out,
+                    long long ldo, void* stream);
+/* k x k max pool (stride, zero-extended window never wins: -inf padding). */
+int edl_maxpool_nhwc(const void* x, int N, int H, int W, int C, int k, int stride, int pad, void* out,
+                     void* stream);
+/* Global average pool: out[n][c] = mean over H*W of x[n][.][.][c] (bf16). */
+int edl_avgpool_nhwc(const void* x, int N, int HW, int C, void* out, long long ldo, void* stream);
 
 /* Backprop through one tanh layer, edl/nnkit.py:308:
  *   dX[M][K] = (dY[M][N] @ W[N][K]) * (1 - H[M][K]^2)      (all bf16)

@@ -255,8 +255,12 @@ int edl_linear_fwd(const void* X, long long ldx, const void* W, long long ldw, c
                    void* Y, long long ldy, int M, int N, int K, int act, void* stream) {
   if (M < 1 || N < 1 || K < 1 || ldx < K || ldw < K || ldy < N)
     return fail(EDL_ERR_SHAPE, "linear_fwd: bad shape M=%d N=%d K=%d", M, N, K);
-  if (act != EDL_ACT_TANH && act != EDL_ACT_NONE) return fail(EDL_ERR_SHAPE, "linear_fwd: bad act %d", act);
-  const GemmKind kind = act == EDL_ACT_TANH ? GemmKind::FwdTanh : GemmKind::FwdLinear;
+  if (act != EDL_ACT_TANH && act != EDL_ACT_NONE && act != EDL_ACT_RELU && act != EDL_ACT_IDENT)
+    return fail(EDL_ERR_SHAPE, "linear_fwd: bad act %d", act);
+  const GemmKind kind = act == EDL_ACT_TANH    ? GemmKind::FwdTanh
+                        : act == EDL_ACT_RELU  ? GemmKind::FwdRelu
+                        : act == EDL_ACT_IDENT ? GemmKind::FwdIdentBf16
+                                               : GemmKind::FwdLinear;
   const int cap = grid_cap(as_stream(stream));
   CUtensorMap ta, tb;
   int rc;
@@ -275,6 +279,60 @@ int edl_linear_fwd(const void* X, long long ldx, const void* W, long long ldw, c
     e = launch_gemm(kind, bn, ta, tb, ty, M, N, K, ep, cap, as_stream(stream));
   }
   return e == cudaSuccess ? 0 : cuda_fail(e, "linear_fwd");
+}
+
+int edl_linear_fwd_residual(const void* X, long long ldx, const void* W, long long ldw, const float* bias,
+                            const void* R, long long ldr, void* Y, long long ldy, int M, int N, int K,
+                            void* stream) {
+  if (M < 1 || N < 1 || K < 1 || ldx < K || ldw < K || ldy < N || ldr < N || !R)
+    return fail(EDL_ERR_SHAPE, "linear_fwd_residual: bad shape M=%d N=%d K=%d", M, N, K);
+  const int cap = grid_cap(as_stream(stream));
+  CUtensorMap ta, tb, ty;
+  int rc;
+  if ((rc = tensor_map(X, M, K, ldx, 64, 128, &ta))) return rc;
+  if ((rc = tensor_map_out(Y, M, N, ldy, false, &ty))) return rc;
+  EpiArgs ep{Y, ldy, bias, reinterpret_cast<const __nv_bfloat16*>(R), ldr, 1.0f, stream_sched(as_stream(stream))};
+  const int pbn = pick_pair_bn(M, N, cap);
+  cudaError_t e;
+  if (pbn > 0) {
+    if ((rc = tensor_map(W, N, K, ldw, 64, pbn / 2, &tb))) return rc;
+    e = launch_gemm_pair(GemmKind::FwdRelu, pbn, ta, tb, ty, M, N, K, ep, cap, as_stream(stream));
+  } else {
+    const int bn = pick_bn_cap(M, N, cap);
+    if ((rc = tensor_map(W, N, K, ldw, 64, bn, &tb))) return rc;
+    e = launch_gemm(GemmKind::FwdRelu, bn, ta, tb, ty, M, N, K, ep, cap, as_stream(stream));
+  }
+  return e == cudaSuccess ? 0 : cuda_fail(e, "linear_fwd_residual");
+}
+
+int edl_im2col_nhwc(const void* x, int N, int H, int W, int C, int R, int S, int stride, int pad, void* out,
+                    long long ldo, void* stream) {
+  if (N < 1 || H < 1 || W < 1 || C < 8 || C % 8 || R < 1 || S < 1 || stride < 1 || pad < 0 ||
+      ldo < static_cast<long long>(R) * S * C || ldo % 8)
+    return fail(EDL_ERR_SHAPE, "im2col_nhwc: bad shape N=%d H=%d W=%d C=%d R=%d S=%d ldo=%lld", N, H, W, C, R, S, ldo);
+  const int P = (H + 2 * pad - R) / stride + 1, Q = (W + 2 * pad - S) / stride + 1;
+  if (P < 1 || Q < 1) return fail(EDL_ERR_SHAPE, "im2col_nhwc: empty output");
+  cudaError_t e = launch_im2col_nhwc(reinterpret_cast<const __nv_bfloat16*>(x), N, H, W, C, R, S, stride, pad, P, Q,
+                                     reinterpret_cast<__nv_bfloat16*>(out), ldo, as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "im2col_nhwc");
+}
+
+int edl_maxpool_nhwc(const void* x, int N, int H, int W, int C, int k, int stride, int pad, void* out,
+                     void* stream) {
+  if (N < 1 || H < 1 || W < 1 || C < 8 || C % 8 || k < 1 || stride < 1 || pad < 0 || pad >= k)
+    return fail(EDL_ERR_SHAPE, "maxpool_nhwc: bad shape");
+  const int P = (H + 2 * pad - k) / stride + 1, Q = (W + 2 * pad - k) / stride + 1;
+  if (P < 1 || Q < 1) return fail(EDL_ERR_SHAPE, "maxpool_nhwc: empty output");
+  cudaError_t e = launch_maxpool_nhwc(reinterpret_cast<const __nv_bfloat16*>(x), N, H, W, C, k, stride, pad, P, Q,
+                                      reinterpret_cast<__nv_bfloat16*>(out), as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "maxpool_nhwc");
+}
+
+int edl_avgpool_nhwc(const void* x, int N, int HW, int C, void* out, long long ldo, void* stream) {
+  if (N < 1 || HW < 1 || C < 8 || C % 8 || ldo < C || ldo % 8) return fail(EDL_ERR_SHAPE, "avgpool_nhwc: bad shape");
+  cudaError_t e = launch_avgpool_nhwc(reinterpret_cast<const __nv_bfloat16*>(x), N, HW, C,
+                                      reinterpret_cast<__nv_bfloat16*>(out), ldo, as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "avgpool_nhwc");
 }
 
 int edl_linear_bwd_data(const void* dY, long long lddy, const void* W, long long ldw,

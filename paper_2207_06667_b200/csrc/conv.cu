@@ -1,0 +1,134 @@
+// conv.cu — the data-movement kernels of the cfg4 (ResNet-style) teacher
+// path (BASELINE.json configs[3]). The reference has no
+// convolutions; parity is against torch.nn.functional on the
+// CPU. Activations are NHWC bf16 with C padded to a multiple of 16, so every
+// row of the implicit GEMM is 16-byte aligned for TMA.
+//
+//   im2col_nhwc      conv as GEMM: A[(n,p,q)][(r,s,c)] (zero outside the image),
+//                    multiplied by W[k][(r,s,c)] in the tcgen05 GEMM whose
+//                    epilogue adds the folded-BN bias, the residual, and ReLU
+//   maxpool_nhwc     k x k / stride window max (ResNet stem)
+//   avgpool_nhwc     global average pool -> [N][C] (the head GEMM's input)
+#include "internal.h"
+#include "sm100.cuh"
+
+namespace edl {
+
+namespace {
+
+// One thread per 16-byte (8-channel) vector of the im2col matrix.
+__global__ void __launch_bounds__(256) im2col_nhwc_kernel(const __nv_bfloat16* __restrict__ x, int N, int H, int W,
+                                                          int C, int R, int S, int stride, int pad, int P, int Q,
+                                                          __nv_bfloat16* __restrict__ out, long long ldo) {
+  griddep_wait();
+  const int cv = C / 8;                       // 8-channel vectors per pixel
+  const long long per_row = static_cast<long long>(R) * S * cv;
+  const long long total = static_cast<long long>(N) * P * Q * per_row;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long m = i / per_row;
+    const int j = static_cast<int>(i - m * per_row);
+    const int c8 = j % cv;
+    const int rs = j / cv;
+    const int s = rs % S, r = rs / S;
+    const int q = static_cast<int>(m % Q);
+    const int p = static_cast<int>((m / Q) % P);
+    const int n = static_cast<int>(m / (static_cast<long long>(P) * Q));
+    const int h = p * stride - pad + r, w = q * stride - pad + s;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (h >= 0 && h < H && w >= 0 && w < W)
+      v = __ldg(reinterpret_cast<const uint4*>(x + ((static_cast<long long>(n) * H + h) * W + w) * C) + c8);
+    *reinterpret_cast<uint4*>(out + m * ldo + static_cast<long long>(rs) * C + 8 * c8) = v;
+  }
+}
+
+__global__ void __launch_bounds__(256) maxpool_nhwc_kernel(const __nv_bfloat16* __restrict__ x, int N, int H, int W,
+                                                           int C, int k, int stride, int pad, int P, int Q,
+                                                           __nv_bfloat16* __restrict__ out) {
+  griddep_wait();
+  const int cv = C / 8;
+  const long long total = static_cast<long long>(N) * P * Q * cv;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int c8 = static_cast<int>(i % cv);
+    const long long m = i / cv;
+    const int q = static_cast<int>(m % Q);
+    const int p = static_cast<int>((m / Q) % P);
+    const int n = static_cast<int>(m / (static_cast<long long>(P) * Q));
+    float best[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) best[j] = -INFINITY;
+    for (int r = 0; r < k; ++r) {
+      const int h = p * stride - pad + r;
+      if (h < 0 || h >= H) continue;
+      for (int s = 0; s < k; ++s) {
+        const int w = q * stride - pad + s;
+        if (w < 0 || w >= W) continue;
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(x + ((static_cast<long long>(n) * H + h) * W + w) * C) + c8);
+        const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) best[j] = fmaxf(best[j], __bfloat162float(b[j]));
+      }
+    }
+    uint4 o;
+    o.x = pack_bf16x2(best[0], best[1]);
+    o.y = pack_bf16x2(best[2], best[3]);
+    o.z = pack_bf16x2(best[4], best[5]);
+    o.w = pack_bf16x2(best[6], best[7]);
+    *reinterpret_cast<uint4*>(out + m * C + 8 * c8) = o;
+  }
+}
+
+// Global average pool: block = one image; threads over 8-channel vectors,
+// each summing its channels over all H*W pixels (coalesced across threads).
+__global__ void __launch_bounds__(256) avgpool_nhwc_kernel(const __nv_bfloat16* __restrict__ x, int HW, int C,
+                                                           __nv_bfloat16* __restrict__ out, long long ldo) {
+  griddep_wait();
+  const int n = blockIdx.x;
+  const int cv = C / 8;
+  const float inv = 1.0f / static_cast<float>(HW);
+  for (int c8 = threadIdx.x; c8 < cv; c8 += blockDim.x) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const __nv_bfloat16* base = x + static_cast<long long>(n) * HW * C + 8 * c8;
+    for (int i = 0; i < HW; ++i) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(base + static_cast<long long>(i) * C));
+      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(b[j]);
+    }
+    uint4 o;
+    o.x = pack_bf16x2(acc[0] * inv, acc[1] * inv);
+    o.y = pack_bf16x2(acc[2] * inv, acc[3] * inv);
+    o.z = pack_bf16x2(acc[4] * inv, acc[5] * inv);
+    o.w = pack_bf16x2(acc[6] * inv, acc[7] * inv);
+    *reinterpret_cast<uint4*>(out + n * ldo + 8 * c8) = o;
+  }
+}
+
+int grid_for(long long work) {
+  long long b = (work + 255) / 256;
+  return static_cast<int>(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
+}
+
+}  // namespace
+
+cudaError_t launch_im2col_nhwc(const __nv_bfloat16* x, int N, int H, int W, int C, int R, int S, int stride,
+                               int pad, int P, int Q, __nv_bfloat16* out, long long ldo, cudaStream_t stream) {
+  const long long work = static_cast<long long>(N) * P * Q * R * S * (C / 8);
+  return launch_pdl(im2col_nhwc_kernel, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, R, S, stride,
+                    pad, P, Q, out, ldo);
+}
+
+cudaError_t launch_maxpool_nhwc(const __nv_bfloat16* x, int N, int H, int W, int C, int k, int stride, int pad,
+                                int P, int Q, __nv_bfloat16* out, cudaStream_t stream) {
+  const long long work = static_cast<long long>(N) * P * Q * (C / 8);
+  return launch_pdl(maxpool_nhwc_kernel, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, k, stride, pad,
+                    P, Q, out);
+}
+
+cudaError_t launch_avgpool_nhwc(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* out, long long ldo,
+                                cudaStream_t stream) {
+  return launch_pdl(avgpool_nhwc_kernel, dim3(N), dim3(256), 0, stream, 1, x, HW, C, out, ldo);
+}
+
+}  // namespace edl

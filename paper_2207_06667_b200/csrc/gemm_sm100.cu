@@ -95,7 +95,7 @@ __device__ __forceinline__ void mma_kblock(uint32_t d_tmem, uint32_t a_base, uin
 // ------------------------------------------------------------------ epilogues
 template <int EPI>
 __host__ __device__ constexpr bool epi_has_bias() {
-  return EPI == EPI_TANH_BF16 || EPI == EPI_BIAS_F32;
+  return EPI == EPI_TANH_BF16 || EPI == EPI_BIAS_F32 || EPI == EPI_RELU_BF16 || EPI == EPI_BIAS_BF16;
 }
 
 // sb: this chunk's 32 bias values staged in shared memory (stage_bias), or
@@ -291,14 +291,15 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& ep, uint32_t taddr,
 // full lines; ragged M / N edges are clipped by the tensor map.
 template <int EPI>
 __host__ __device__ constexpr bool epi_tma_store() {
-  return EPI == EPI_TANH_BF16 || EPI == EPI_BIAS_F32 || EPI == EPI_DTANH_BF16;
+  return EPI == EPI_TANH_BF16 || EPI == EPI_BIAS_F32 || EPI == EPI_DTANH_BF16 || EPI == EPI_RELU_BF16 ||
+         EPI == EPI_BIAS_BF16;
 }
 
 // The epilogue math of epilogue_store without its global stores (v in place).
 template <int EPI>
 __device__ __forceinline__ void epi_math(const EpiArgs& ep, int row, int M, int col0, int N, float (&v)[32],
                                          const float* sb, const uint4* hpre) {
-  if constexpr (EPI == EPI_TANH_BF16 || EPI == EPI_BIAS_F32) {
+  if constexpr (EPI == EPI_TANH_BF16 || EPI == EPI_BIAS_F32 || EPI == EPI_RELU_BF16 || EPI == EPI_BIAS_BF16) {
     if (sb != nullptr) {
       const float4* b4 = reinterpret_cast<const float4*>(sb);
 #pragma unroll
@@ -315,6 +316,26 @@ __device__ __forceinline__ void epi_math(const EpiArgs& ep, int row, int M, int 
   if constexpr (EPI == EPI_TANH_BF16) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = tanh_fast(v[i]);
+  }
+  if constexpr (EPI == EPI_RELU_BF16) {
+    // residual (ResNet shortcut, bf16, same shape as the output), then ReLU
+    if (ep.aux != nullptr && row < M) {
+      if (hpre != nullptr) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&hpre[i]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[8 * i + j] += __bfloat162float(hb[j]);
+        }
+      } else {
+        const __nv_bfloat16* h = ep.aux + static_cast<size_t>(row) * ep.ld_aux + col0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (col0 + i < N) v[i] += __bfloat162float(h[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
   }
   if constexpr (EPI == EPI_DTANH_BF16) {
     if (row >= M) return;
@@ -372,9 +393,10 @@ template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_tile_tma(const EpiArgs& ep, uint32_t taddr, int row0, int lane, int M,
                                                   int n0, int N, const float* sb, const CUtensorMap* tmY,
                                                   uint8_t* stg, uint32_t& stores) {
-  constexpr bool kAux = EPI == EPI_DTANH_BF16;
+  // the (1 - a^2) factor or the residual: a bf16 row segment per chunk
+  constexpr bool kAux = EPI == EPI_DTANH_BF16 || EPI == EPI_RELU_BF16;
   const int row = row0 + lane;
-  const bool row_ok = row < M;
+  const bool row_ok = row < M && (EPI != EPI_RELU_BF16 || ep.aux != nullptr);
   auto aux_ptr = [&](int c) {
     return reinterpret_cast<const uint4*>(ep.aux + static_cast<size_t>(row) * ep.ld_aux + n0 + c);
   };
@@ -410,7 +432,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const EpiArgs& ep, uint32_t ta
       uint8_t* buf = stg + (stores & 1) * 4096;
       if (lane == 0) bulk_wait_read1();        // only the newest store (other tile) may still be reading
       __syncwarp();
-      stage_chunk<EPI == EPI_BIAS_F32>(buf, lane, v);
+      stage_chunk<EPI == EPI_BIAS_F32>(buf, lane, v);   // bf16 tile unless the fp32 logits
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
@@ -1393,6 +1415,10 @@ cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUte
       return launch_gemm_bn<false, true, EPI_DTANH_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
     case GemmKind::BwdWeight:
       return launch_gemm_bn<true, true, EPI_F32>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
+    case GemmKind::FwdRelu:
+      return launch_gemm_bn<false, false, EPI_RELU_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
+    case GemmKind::FwdIdentBf16:
+      return launch_gemm_bn<false, false, EPI_BIAS_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
   }
   return cudaErrorInvalidValue;
 }
@@ -1429,6 +1455,10 @@ cudaError_t launch_gemm_pair(GemmKind kind, int bn, const CUtensorMap& ta, const
       return launch_pair_bn<false, false, EPI_BIAS_F32>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
     case GemmKind::BwdData:
       return launch_pair_bn<false, true, EPI_DTANH_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
+    case GemmKind::FwdRelu:
+      return launch_pair_bn<false, false, EPI_RELU_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
+    case GemmKind::FwdIdentBf16:
+      return launch_pair_bn<false, false, EPI_BIAS_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
     default:
       return cudaErrorInvalidValue;
   }

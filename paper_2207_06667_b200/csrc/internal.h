@@ -48,6 +48,8 @@ enum EpiMode : int {
   EPI_DTANH_BF16 = 2,  // out(bf16) = acc * (1 - aux^2)
   EPI_F32 = 3,         // out(f32)  = acc * scale
   EPI_SGD_F32 = 4,     // out(f32) -= scale * acc in place; out_bf16 = bf16(out)
+  EPI_RELU_BF16 = 5,   // out(bf16) = relu(acc + bias [+ aux residual]) (conv layers, cfg4)
+  EPI_BIAS_BF16 = 6,   // out(bf16) = acc + bias (cfg4 shortcut projections)
 };
 
 struct EpiArgs {
@@ -69,7 +71,7 @@ struct HeadArgs {
   int* idx;
 };
 
-enum class GemmKind { FwdTanh, FwdLinear, BwdData, BwdWeight };
+enum class GemmKind { FwdTanh, FwdLinear, BwdData, BwdWeight, FwdRelu, FwdIdentBf16 };
 
 constexpr int kMaxGroup = 4;
 struct GroupMaps {
@@ -109,6 +111,14 @@ cudaError_t launch_gemm_pair(GemmKind kind, int bn, const CUtensorMap& ta, const
                              cudaStream_t stream);
 cudaError_t launch_teacher_head(int bn, int kmax, const CUtensorMap& ta, const CUtensorMap& tb,
                                 int M, int N, int K, const HeadArgs& hp, cudaStream_t stream);
+
+// cfg4 data movement (conv.cu): NHWC bf16, C a multiple of 8
+cudaError_t launch_im2col_nhwc(const __nv_bfloat16* x, int N, int H, int W, int C, int R, int S, int stride,
+                               int pad, int P, int Q, __nv_bfloat16* out, long long ldo, cudaStream_t stream);
+cudaError_t launch_maxpool_nhwc(const __nv_bfloat16* x, int N, int H, int W, int C, int k, int stride, int pad,
+                                int P, int Q, __nv_bfloat16* out, cudaStream_t stream);
+cudaError_t launch_avgpool_nhwc(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* out, long long ldo,
+                                cudaStream_t stream);
 
 // SIMT kernels (kernels.cu)
 cudaError_t launch_kd_loss(const float* logits, long long ld_z, const int64_t* labels,

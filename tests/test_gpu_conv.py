@@ -1,0 +1,129 @@
+"""cfg4 (ResNet-style teacher) on the device vs the torch CPU stand-in oracle
+(oracle/resnet_ref.py: the reference has no convolutions).
+
+Tolerances: a single conv layer is compared with both sides storing bf16, so
+the difference is fp32 accumulation order plus at most one bf16 rounding
+flip: <= 1e-2 relative to the layer's max. Through a whole network the flips
+compound: pooled features <= 3e-2 relative, soft-label probabilities
+<= 5e-3 absolute, top-k class ids exact wherever the oracle's logit gap
+between the k-th and (k+1)-th class exceeds 5e-2.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import resnet_ref as ref
+
+pytestmark = pytest.mark.gpu
+
+
+def _s():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _rel(a, b):
+    return (a - b).abs().max().item() / max(1e-6, b.abs().max().item())
+
+
+@pytest.mark.parametrize("N,C,H,K,k,stride,relu,residual", [
+    (2, 16, 15, 32, 3, 1, True, False),
+    (2, 3, 32, 64, 7, 2, True, False),
+    (3, 64, 9, 128, 1, 2, False, False),
+    (2, 48, 8, 96, 1, 1, True, True),
+    (2, 32, 12, 32, 3, 1, True, True),
+])
+def test_conv_layer_vs_torch(N, C, H, K, k, stride, relu, residual):
+    from paper_2207_06667_b200 import _lib
+    from paper_2207_06667_b200.resnet import HostConv, _DevConv, to_nhwc
+    rng = np.random.default_rng(C * 31 + K)
+    hc = HostConv((rng.normal(0, np.sqrt(2.0 / (C * k * k)), size=(K, C, k, k))).astype(np.float32),
+                  rng.normal(0, 0.1, size=K).astype(np.float32), stride, k // 2, relu)
+    dc = _DevConv(hc, "cuda")
+    imgs = rng.normal(size=(N, C, H, H)).astype(np.float32)
+    x = to_nhwc(imgs, "cuda")
+    oh, ow = dc.out_hw(H, H)
+    M = N * oh * ow
+    out = torch.empty(N, oh, ow, dc.cout_p, dtype=torch.bfloat16, device="cuda")
+    if k == 1 and stride == 1:
+        a, lda = x, dc.cin_p
+    else:
+        a = torch.empty(M, dc.kdim, dtype=torch.bfloat16, device="cuda")
+        lda = dc.kdim
+        _lib.call("edl_im2col_nhwc", x.data_ptr(), N, H, H, dc.cin_p, k, k, stride, dc.pad, a.data_ptr(), lda, _s())
+    xin = ref._bf(torch.from_numpy(imgs))
+    res_t = None
+    if residual:
+        r = rng.normal(size=(N, K, oh, ow)).astype(np.float32)
+        res_t = ref._bf(torch.from_numpy(r))
+        rd = to_nhwc(r, "cuda")
+        _lib.call("edl_linear_fwd_residual", a.data_ptr(), lda, dc.w.data_ptr(), dc.kdim, dc.b.data_ptr(),
+                  rd.data_ptr(), dc.cout_p, out.data_ptr(), dc.cout_p, M, dc.cout_p, dc.kdim, _s())
+    else:
+        _lib.call("edl_linear_fwd", a.data_ptr(), lda, dc.w.data_ptr(), dc.kdim, dc.b.data_ptr(), out.data_ptr(),
+                  dc.cout_p, M, dc.cout_p, dc.kdim, _lib.EDL_ACT_RELU if relu else _lib.EDL_ACT_IDENT, _s())
+    torch.cuda.synchronize()
+    want = ref._conv(xin, hc, res_t)                         # NCHW
+    got = out[..., :K].float().cpu().permute(0, 3, 1, 2)
+    assert _rel(got, want) < 1e-2
+
+
+def test_pools_vs_torch():
+    import torch.nn.functional as F
+
+    from paper_2207_06667_b200 import _lib
+    from paper_2207_06667_b200.resnet import to_nhwc
+    rng = np.random.default_rng(7)
+    imgs = rng.normal(size=(3, 24, 13, 13)).astype(np.float32)
+    x = to_nhwc(imgs, "cuda")
+    C = x.shape[-1]
+    mp = torch.empty(3, 7, 7, C, dtype=torch.bfloat16, device="cuda")
+    _lib.call("edl_maxpool_nhwc", x.data_ptr(), 3, 13, 13, C, 3, 2, 1, mp.data_ptr(), _s())
+    ap = torch.empty(3, C, dtype=torch.bfloat16, device="cuda")
+    _lib.call("edl_avgpool_nhwc", x.data_ptr(), 3, 169, C, ap.data_ptr(), C, _s())
+    torch.cuda.synchronize()
+    xin = ref._bf(torch.from_numpy(imgs))
+    assert torch.equal(mp[..., :24].float().cpu().permute(0, 3, 1, 2), F.max_pool2d(xin, 3, 2, 1))
+    assert _rel(ap[:, :24].float().cpu(), xin.mean(dim=(2, 3))) < 1e-2
+
+
+@pytest.mark.parametrize("block", ["basic", "bottleneck"])
+def test_small_resnet_soft_labels_vs_torch(block):
+    from paper_2207_06667_b200.resnet import ResNetConfig, ResNetTeacher, init_resnet, to_nhwc
+    cfg = ResNetConfig(block=block, layers=(1, 1, 1, 1), width=16, classes=40, image=32)
+    net = init_resnet(cfg, 3)
+    B, k, T = 6, 5, 2.0
+    imgs = np.random.default_rng(5).normal(size=(B, 3, 32, 32)).astype(np.float32)
+    teacher = ResNetTeacher(net, "cuda", B)
+    x = to_nhwc(imgs, "cuda")
+    f = teacher.features(x)[:, :net.fc_w.shape[1]].float().cpu()
+    soft = teacher.soft_labels(x, T, k)
+    torch.cuda.synchronize()
+    fw = ref.features(net, imgs)
+    assert _rel(f, fw) < 3e-2
+    z = ref.logits(net, imgs)
+    p = torch.softmax(z / T, dim=1)
+    zs = torch.sort(z, dim=1, descending=True).values
+    safe = (zs[:, k - 1] - zs[:, k]) > 5e-2
+    order = torch.argsort(-z, dim=1, stable=True)[:, :k]
+    idx = soft.classes.cpu().long()
+    assert torch.equal(idx[safe], order[safe])
+    np.testing.assert_allclose(soft.probs.cpu().numpy(), torch.gather(p, 1, idx).numpy(), atol=5e-3)
+
+
+def test_resnet50_style_full_size_vs_torch():
+    """cfg4's teacher shape (bottleneck [3,4,6,3], width 64, 224^2, 1000
+    classes) at batch 2: the whole network against the CPU oracle."""
+    from paper_2207_06667_b200.resnet import ResNetConfig, ResNetTeacher, init_resnet, to_nhwc
+    cfg = ResNetConfig()
+    net = init_resnet(cfg, 11)
+    imgs = np.random.default_rng(2).normal(size=(2, 3, 224, 224)).astype(np.float32)
+    teacher = ResNetTeacher(net, "cuda", 2)
+    x = to_nhwc(imgs, "cuda")
+    f = teacher.features(x)[:, :2048].float().cpu()
+    soft = teacher.soft_labels(x, 2.0, 16)
+    torch.cuda.synchronize()
+    assert torch.isfinite(f).all()
+    assert _rel(f, ref.features(net, imgs)) < 3e-2
+    z = ref.logits(net, imgs)
+    assert torch.equal(soft.classes.cpu().long()[:, 0], torch.argmax(z, dim=1))
