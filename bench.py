@@ -218,6 +218,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-online", action="store_true")
+    ap.add_argument("--no-cfg4", action="store_true", help="skip the cfg4 (ResNet teacher) secondary measurement")
     ap.add_argument("--overlap-exchange", action="store_true",
                     help="N>1: all-reduce + SGD in two buckets on a comm stream, overlapping the next forward")
     ap.add_argument("--exchange", default="nccl", choices=["nvls", "nccl"],
@@ -453,6 +454,11 @@ def main():
                 line["cfg2_small_mlp"] = _small_config_graph(dev)
             except Exception as exc:   # secondary measurement; never sinks the headline line
                 line["cfg2_small_mlp"] = {"error": repr(exc)[:200]}
+            if not args.no_cfg4:
+                try:
+                    line["cfg4_teacher_infer"] = _cfg4_teacher_rate(dev, peak_sust)
+                except Exception as exc:   # secondary measurement
+                    line["cfg4_teacher_infer"] = {"error": repr(exc)[:200]}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -534,6 +540,36 @@ def _split_main(args, cfg, world, rank, local, dev, ddata, teacher, student_h, t
                        "mode": "edl (decoupled)", "global_batch": B * pl.n_students, "per_gpu_batch": B,
                        "topk": cfg["topk"], "parallelism": f"dp{pl.n_students}"},
             "gpu_launches": launches, "clocks": clk.summary(), "losses_finite": ok}), flush=True)
+
+
+def _cfg4_teacher_rate(dev, peak_sust, batch=64, iters=10, warmup=3):
+    """cfg4 (BASELINE configs[3]) first slice: the ResNet-style teacher's
+    inference (ResNet-50-style bottleneck [3,4,6,3], 224^2, 1000 classes,
+    folded BN) through the fused softmax + top-16 head, random init weights,
+    synthetic images; two input batches alternate (each 103 MB > L2)."""
+    import torch
+
+    from paper_2207_06667_b200.resnet import ResNetConfig, ResNetTeacher, init_resnet, to_nhwc
+    cfg = ResNetConfig()
+    teacher = ResNetTeacher(init_resnet(cfg, 1), dev, batch)
+    rng = np.random.default_rng(0)
+    xs = [to_nhwc(rng.normal(size=(batch, 3, cfg.image, cfg.image)).astype(np.float32), dev) for _ in range(2)]
+    for i in range(warmup):
+        teacher.soft_labels(xs[i % 2], 2.0, 16)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for i in range(iters):
+        teacher.soft_labels(xs[i % 2], 2.0, 16)
+    e.record()
+    torch.cuda.synchronize()
+    t = s.elapsed_time(e) / 1e3 / iters
+    flop = teacher.flops_per_sample()
+    return {"model": "resnet50-style teacher (bottleneck [3,4,6,3], width 64, folded BN), 224x224, 1000 classes, "
+                     "top-16 head", "batch": batch, "samples_per_s": round(batch / t, 1), "ms_per_batch": round(t * 1e3, 3),
+            "gflop_per_sample": round(flop / 1e9, 3), "tflops": round(batch * flop / t / 1e12, 1),
+            "frac_of_sustained": round(batch * flop / t / 1e12 / peak_sust, 4),
+            "note": "explicit NHWC im2col gather + tcgen05 GEMMs (round-1 slice; the student side is round 2)"}
 
 
 def _small_config_graph(dev, steps=200, warmup=20):

@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define EDL_B200_ABI_VERSION 1
+#define EDL_B200_ABI_VERSION 2
 
 /* status codes: mirror edl.nnkit's exception classes (edl/nnkit.py:31-40) */
 #define EDL_OK 0
@@ -70,9 +70,12 @@ int edl_linear_fwd_residual(const void* X, long long ldx, const void* W, long lo
                             const void* R, long long ldr, void* Y, long long ldy, int M, int N, int K,
                             void* stream);
 /* out[(n,p,q)][(r,s,c)] = x[n][p*stride-pad+r][q*stride-pad+s][c] (0 outside),
- * P = (H + 2pad - R)/stride + 1, Q likewise; out row pitch ldo >= R*S*C. */
-int edl_im2col_nhwc(const void* x, int N, int H, int W, int C, int R, int S, int stride, int pad, void* out,
-                    long long ldo, void* stream);
+ * P = (H + 2pad - R)/stride + 1, Q likewise. x has C channels (pitch);
+ * c_used == C: row pitch ldo >= R*S*C; c_used < C (e.g. the RGB stem): only
+ * channels < c_used are gathered, densely, K = R*S*c_used, the row zero-padded
+ * to ldo. */
+int edl_im2col_nhwc(const void* x, int N, int H, int W, int C, int c_used, int R, int S, int stride, int pad,
+                    void* out, long long ldo, void* stream);
 /* k x k max pool (stride, zero-extended window never wins: -inf padding). */
 int edl_maxpool_nhwc(const void* x, int N, int H, int W, int C, int k, int stride, int pad, void* out,
                      void* stream);

@@ -33,7 +33,8 @@ _SIGNATURES = {
                        c_int, c_int, c_void_p],
     "edl_linear_fwd_residual": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_void_p, c_ll, c_void_p, c_ll, c_int,
                                 c_int, c_int, c_void_p],
-    "edl_im2col_nhwc": [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_ll, c_void_p],
+    "edl_im2col_nhwc": [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_ll,
+                        c_void_p],
     "edl_maxpool_nhwc": [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p],
     "edl_avgpool_nhwc": [c_void_p, c_int, c_int, c_int, c_void_p, c_ll, c_void_p],
     "edl_linear_bwd_data": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_ll,
@@ -68,7 +69,7 @@ _RESTYPES = {"edl_last_error": c_char_p, "edl_colsum_workspace_floats": c_ll,
 
 EDL_ERR_SHAPE, EDL_ERR_NUMERIC, EDL_ERR_PARAM, EDL_ERR_CUDA = -1, -2, -3, -4
 EDL_ACT_NONE, EDL_ACT_TANH, EDL_ACT_RELU, EDL_ACT_IDENT = 0, 1, 2, 3
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 def exported_symbols() -> list[str]:

@@ -305,15 +305,15 @@ int edl_linear_fwd_residual(const void* X, long long ldx, const void* W, long lo
   return e == cudaSuccess ? 0 : cuda_fail(e, "linear_fwd_residual");
 }
 
-int edl_im2col_nhwc(const void* x, int N, int H, int W, int C, int R, int S, int stride, int pad, void* out,
-                    long long ldo, void* stream) {
-  if (N < 1 || H < 1 || W < 1 || C < 8 || C % 8 || R < 1 || S < 1 || stride < 1 || pad < 0 ||
-      ldo < static_cast<long long>(R) * S * C || ldo % 8)
+int edl_im2col_nhwc(const void* x, int N, int H, int W, int C, int c_used, int R, int S, int stride, int pad,
+                    void* out, long long ldo, void* stream) {
+  if (N < 1 || H < 1 || W < 1 || C < 8 || C % 8 || c_used < 1 || c_used > C || R < 1 || S < 1 || stride < 1 ||
+      pad < 0 || ldo < static_cast<long long>(R) * S * (c_used < C ? c_used : C) || ldo % 8)
     return fail(EDL_ERR_SHAPE, "im2col_nhwc: bad shape N=%d H=%d W=%d C=%d R=%d S=%d ldo=%lld", N, H, W, C, R, S, ldo);
   const int P = (H + 2 * pad - R) / stride + 1, Q = (W + 2 * pad - S) / stride + 1;
   if (P < 1 || Q < 1) return fail(EDL_ERR_SHAPE, "im2col_nhwc: empty output");
-  cudaError_t e = launch_im2col_nhwc(reinterpret_cast<const __nv_bfloat16*>(x), N, H, W, C, R, S, stride, pad, P, Q,
-                                     reinterpret_cast<__nv_bfloat16*>(out), ldo, as_stream(stream));
+  cudaError_t e = launch_im2col_nhwc(reinterpret_cast<const __nv_bfloat16*>(x), N, H, W, C, c_used, R, S, stride, pad,
+                                     P, Q, reinterpret_cast<__nv_bfloat16*>(out), ldo, as_stream(stream));
   return e == cudaSuccess ? 0 : cuda_fail(e, "im2col_nhwc");
 }
 

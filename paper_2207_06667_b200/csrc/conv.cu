@@ -42,6 +42,45 @@ __global__ void __launch_bounds__(256) im2col_nhwc_kernel(const __nv_bfloat16* _
   }
 }
 
+// Packed variant for inputs with few used channels (the RGB stem): the K
+// index runs over (r, s, c < c_used) densely, so a 7x7x3 stem has K = 147
+// (padded to ldo) instead of 7x7x16. One thread per 16-byte output chunk.
+__global__ void __launch_bounds__(256) im2col_nhwc_packed_kernel(const __nv_bfloat16* __restrict__ x, int N, int H,
+                                                                 int W, int C, int c_used, int R, int S, int stride,
+                                                                 int pad, int P, int Q,
+                                                                 __nv_bfloat16* __restrict__ out, long long ldo) {
+  griddep_wait();
+  const int kreal = R * S * c_used;
+  const int chunks = static_cast<int>(ldo / 8);
+  const long long total = static_cast<long long>(N) * P * Q * chunks;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long m = i / chunks;
+    const int ch = static_cast<int>(i - m * chunks);
+    const int q = static_cast<int>(m % Q);
+    const int p = static_cast<int>((m / Q) % P);
+    const int n = static_cast<int>(m / (static_cast<long long>(P) * Q));
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int kidx = 8 * ch + j;
+      v[j] = 0.f;
+      if (kidx < kreal) {
+        const int c = kidx % c_used, rs = kidx / c_used;
+        const int h = p * stride - pad + rs / S, w = q * stride - pad + rs % S;
+        if (h >= 0 && h < H && w >= 0 && w < W)
+          v[j] = __bfloat162float(x[((static_cast<long long>(n) * H + h) * W + w) * C + c]);
+      }
+    }
+    uint4 o;
+    o.x = pack_bf16x2(v[0], v[1]);
+    o.y = pack_bf16x2(v[2], v[3]);
+    o.z = pack_bf16x2(v[4], v[5]);
+    o.w = pack_bf16x2(v[6], v[7]);
+    *reinterpret_cast<uint4*>(out + m * ldo + 8 * ch) = o;
+  }
+}
+
 __global__ void __launch_bounds__(256) maxpool_nhwc_kernel(const __nv_bfloat16* __restrict__ x, int N, int H, int W,
                                                            int C, int k, int stride, int pad, int P, int Q,
                                                            __nv_bfloat16* __restrict__ out) {
@@ -112,8 +151,14 @@ int grid_for(long long work) {
 
 }  // namespace
 
-cudaError_t launch_im2col_nhwc(const __nv_bfloat16* x, int N, int H, int W, int C, int R, int S, int stride,
-                               int pad, int P, int Q, __nv_bfloat16* out, long long ldo, cudaStream_t stream) {
+cudaError_t launch_im2col_nhwc(const __nv_bfloat16* x, int N, int H, int W, int C, int c_used, int R, int S,
+                               int stride, int pad, int P, int Q, __nv_bfloat16* out, long long ldo,
+                               cudaStream_t stream) {
+  if (c_used < C) {
+    const long long work = static_cast<long long>(N) * P * Q * (ldo / 8);
+    return launch_pdl(im2col_nhwc_packed_kernel, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, c_used,
+                      R, S, stride, pad, P, Q, out, ldo);
+  }
   const long long work = static_cast<long long>(N) * P * Q * R * S * (C / 8);
   return launch_pdl(im2col_nhwc_kernel, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, R, S, stride,
                     pad, P, Q, out, ldo);

@@ -113,8 +113,9 @@ cudaError_t launch_teacher_head(int bn, int kmax, const CUtensorMap& ta, const C
                                 int M, int N, int K, const HeadArgs& hp, cudaStream_t stream);
 
 // cfg4 data movement (conv.cu): NHWC bf16, C a multiple of 8
-cudaError_t launch_im2col_nhwc(const __nv_bfloat16* x, int N, int H, int W, int C, int R, int S, int stride,
-                               int pad, int P, int Q, __nv_bfloat16* out, long long ldo, cudaStream_t stream);
+cudaError_t launch_im2col_nhwc(const __nv_bfloat16* x, int N, int H, int W, int C, int c_used, int R, int S,
+                               int stride, int pad, int P, int Q, __nv_bfloat16* out, long long ldo,
+                               cudaStream_t stream);
 cudaError_t launch_maxpool_nhwc(const __nv_bfloat16* x, int N, int H, int W, int C, int k, int stride, int pad,
                                 int P, int Q, __nv_bfloat16* out, cudaStream_t stream);
 cudaError_t launch_avgpool_nhwc(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* out, long long ldo,

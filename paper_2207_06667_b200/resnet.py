@@ -98,14 +98,24 @@ def init_resnet(cfg: ResNetConfig, seed: int) -> HostResNet:
 
 
 class _DevConv:
-    """Device form: W bf16 [cout_p][k*k*cin_p] in im2col (r, s, c) order, b fp32 [cout_p]."""
+    """Device form: W bf16 [cout_p][kdim] in im2col (r, s, c) order, b fp32 [cout_p].
+    Inputs with fewer than 8 channels (the RGB stem) use the packed im2col:
+    K = k*k*cin padded to 16, instead of k*k*pad(cin)."""
 
     def __init__(self, c: HostConv, dev):
         cout, cin, k, _ = c.w.shape
         self.k, self.stride, self.pad, self.relu = k, c.stride, c.pad, c.relu
-        self.cin_p, self.cout_p = pad(cin), pad(cout)
-        w = np.zeros((self.cout_p, k, k, self.cin_p), dtype=np.float32)
-        w[:cout, :, :, :cin] = c.w.transpose(0, 2, 3, 1)
+        self.cin, self.cin_p, self.cout_p = cin, pad(cin), pad(cout)
+        self.packed = cin < 8
+        wt = c.w.transpose(0, 2, 3, 1)                      # [cout][k][k][cin]
+        if self.packed:
+            self._kdim = pad(k * k * cin)
+            w = np.zeros((self.cout_p, self._kdim), dtype=np.float32)
+            w[:cout, :k * k * cin] = wt.reshape(cout, -1)
+        else:
+            self._kdim = k * k * self.cin_p
+            w = np.zeros((self.cout_p, k, k, self.cin_p), dtype=np.float32)
+            w[:cout, :, :, :cin] = wt
         self.w = torch.from_numpy(w.reshape(self.cout_p, -1)).to(dev).to(torch.bfloat16)
         b = np.zeros(self.cout_p, dtype=np.float32)
         b[:cout] = c.b
@@ -116,7 +126,7 @@ class _DevConv:
 
     @property
     def kdim(self):
-        return self.k * self.k * self.cin_p
+        return self._kdim
 
 
 class ResNetTeacher:
@@ -141,7 +151,6 @@ class ResNetTeacher:
         H = W = self.cfg.image
         self.in_c = pad(self.cfg.in_channels)
         h, w = self.stem.out_hw(H, W)
-        self.plan = []                                     # (kind, conv, in, out, H, W, residual)
         col = B * h * w * self.stem.kdim
         self.x0 = torch.empty(B, h, w, self.stem.cout_p, dtype=torch.bfloat16, device=dev)
         ph, pw = (h + 2 - 3) // 2 + 1, (w + 2 - 3) // 2 + 1
@@ -177,8 +186,8 @@ class ResNetTeacher:
             a, lda = x, c.cin_p                            # NHWC already is the GEMM's A
         else:
             a, lda = self.col, c.kdim
-            _lib.call("edl_im2col_nhwc", x.data_ptr(), self.B, h, w, c.cin_p, c.k, c.k, c.stride, c.pad,
-                      self.col.data_ptr(), lda, s)
+            _lib.call("edl_im2col_nhwc", x.data_ptr(), self.B, h, w, c.cin_p, c.cin if c.packed else c.cin_p,
+                      c.k, c.k, c.stride, c.pad, self.col.data_ptr(), lda, s)
         if residual is not None:
             _lib.call("edl_linear_fwd_residual", a.data_ptr(), lda, c.w.data_ptr(), c.kdim, c.b.data_ptr(),
                       residual.data_ptr(), c.cout_p, out.data_ptr(), c.cout_p, M, c.cout_p, c.kdim, s)

@@ -50,7 +50,8 @@ def test_conv_layer_vs_torch(N, C, H, K, k, stride, relu, residual):
     else:
         a = torch.empty(M, dc.kdim, dtype=torch.bfloat16, device="cuda")
         lda = dc.kdim
-        _lib.call("edl_im2col_nhwc", x.data_ptr(), N, H, H, dc.cin_p, k, k, stride, dc.pad, a.data_ptr(), lda, _s())
+        _lib.call("edl_im2col_nhwc", x.data_ptr(), N, H, H, dc.cin_p, dc.cin if dc.packed else dc.cin_p, k, k,
+                  stride, dc.pad, a.data_ptr(), lda, _s())
     xin = ref._bf(torch.from_numpy(imgs))
     res_t = None
     if residual:
