@@ -82,8 +82,26 @@ int edl_maxpool_nhwc(const void* x, int N, int H, int W, int C, int k, int strid
 /* Global average pool: out[n][c] = mean over H*W of x[n][.][.][c] (bf16). */
 int edl_avgpool_nhwc(const void* x, int N, int HW, int C, void* out, long long ldo, void* stream);
 
+/* cfg4 student backward (BN-free ResNet-18-style): the data gradient of a
+ * convolution is edl_linear_bwd_data with H = NULL (dcol = dZ W, no tanh
+ * factor) followed by this gather:
+ *   dx[n][h][w][c] = (sum of dcol over the windows covering (h, w) [+ add])
+ *                    * (mask > 0 if mask != NULL)
+ * i.e. straight to the previous ReLU layer's pre-activation gradient, with the
+ * block shortcut's gradient in `add`. Deterministic (gather, fixed order). */
+int edl_col2im_nhwc(const void* dcol, long long ldc, int N, int H, int W, int C, int R, int S, int stride, int pad,
+                    const void* add, const void* mask, void* dx, void* stream);
+/* dx[n][i][c] = df[n][c] / HW (* (mask > 0)): global average pool backward. */
+int edl_avgpool_bwd_nhwc(const void* df, long long ldf, int N, int HW, int C, const void* mask, void* dx,
+                         void* stream);
+/* Max pool backward: each input collects the gradients of the windows whose
+ * first maximum it is (torch's tie rule) (* (mask > 0)). */
+int edl_maxpool_bwd_nhwc(const void* x, int N, int H, int W, int C, int k, int stride, int pad, const void* dy,
+                         const void* mask, void* dx, void* stream);
+
 /* Backprop through one tanh layer, edl/nnkit.py:308:
  *   dX[M][K] = (dY[M][N] @ W[N][K]) * (1 - H[M][K]^2)      (all bf16)
+ * H = NULL: dX = dY @ W (the conv column gradient, cfg4).
  * Same alignment rule as edl_linear_fwd (dX is TMA-stored). */
 int edl_linear_bwd_data(const void* dY, long long lddy, const void* W, long long ldw,
                         const void* H, long long ldh, void* dX, long long lddx, int M, int N,

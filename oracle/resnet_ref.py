@@ -46,3 +46,58 @@ def features(net, images: np.ndarray) -> torch.Tensor:
 def logits(net, images: np.ndarray) -> torch.Tensor:
     f = features(net, images)
     return f @ _bf(torch.from_numpy(net.fc_w)).T + torch.from_numpy(net.fc_b)
+
+
+def student_loss_and_grads(net, images: np.ndarray, labels: np.ndarray, q_dense: np.ndarray, alpha: float,
+                           beta: float, T: float):
+    """BN-free ResNet-18-style student (resnet.init_student_resnet) trained
+    with the reference's KD loss (edl/nnkit.py:283-295: alpha * CE(z, y) +
+    beta * T^2 * CE(q, softmax(z / T)), batch mean) by torch autograd on the
+    CPU, from bf16-rounded weights (the device's operands). Forward values
+    are rounded to bf16 where the device stores them (conv / shortcut
+    outputs, pooled features) by straight-through rounding, which changes
+    values but not the gradient formulas; the device's bf16 deltas remain
+    the only storage difference. Returns (loss,
+    {"stem": (dW, db), "blocks": [((dW1, db1), (dW2, db2), sc or None)],
+    "fc": (dW, db)}) in torch layout (fp32)."""
+    def leaf(a):
+        return _bf(torch.from_numpy(np.asarray(a, dtype=np.float32))).requires_grad_(True)
+
+    def st(t):
+        return t + (_bf(t.detach()) - t.detach())
+
+    def conv(x, c, p, residual=None):
+        y = F.conv2d(x, p[0], p[1], stride=c.stride, padding=c.pad)
+        if residual is not None:
+            y = y + residual
+        return st(torch.relu(y) if (c.relu or residual is not None) else y)
+
+    P = {"stem": (leaf(net.stem.w), torch.from_numpy(net.stem.b).clone().requires_grad_(True))}
+    blocks = []
+    for blk in net.blocks:
+        p1 = (leaf(blk.convs[0].w), torch.from_numpy(blk.convs[0].b).clone().requires_grad_(True))
+        p2 = (leaf(blk.convs[1].w), torch.from_numpy(blk.convs[1].b).clone().requires_grad_(True))
+        ps = None
+        if blk.shortcut is not None:
+            ps = (leaf(blk.shortcut.w), torch.from_numpy(blk.shortcut.b).clone().requires_grad_(True))
+        blocks.append((p1, p2, ps))
+    fc = (leaf(net.fc_w), torch.from_numpy(net.fc_b).clone().requires_grad_(True))
+    x = _bf(torch.from_numpy(np.asarray(images, dtype=np.float32)))
+    x = conv(x, net.stem, P["stem"])
+    x = F.max_pool2d(x, 3, 2, 1)
+    for blk, (p1, p2, ps) in zip(net.blocks, blocks):
+        sc = conv(x, blk.shortcut, ps) if ps is not None else x
+        h = conv(x, blk.convs[0], p1)
+        x = conv(h, blk.convs[1], p2, sc)
+    f = st(x.mean(dim=(2, 3)))
+    z = f @ fc[0].T + fc[1]
+    y = torch.from_numpy(np.asarray(labels, dtype=np.int64))
+    hard = -torch.log_softmax(z, dim=1)[torch.arange(z.shape[0]), y]
+    q = torch.from_numpy(np.asarray(q_dense, dtype=np.float32))
+    soft = -(q * torch.log_softmax(z / T, dim=1)).sum(dim=1) * T * T
+    loss = (alpha * hard + beta * soft).mean()
+    loss.backward()
+    g = lambda p: (p[0].grad.detach(), p[1].grad.detach())  # noqa: E731
+    return float(loss.detach()), {"stem": g(P["stem"]),
+                         "blocks": [(g(p1), g(p2), g(ps) if ps is not None else None) for p1, p2, ps in blocks],
+                         "fc": g(fc)}

@@ -37,6 +37,11 @@ _SIGNATURES = {
                         c_void_p],
     "edl_maxpool_nhwc": [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p],
     "edl_avgpool_nhwc": [c_void_p, c_int, c_int, c_int, c_void_p, c_ll, c_void_p],
+    "edl_col2im_nhwc": [c_void_p, c_ll, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p,
+                        c_void_p, c_void_p],
+    "edl_avgpool_bwd_nhwc": [c_void_p, c_ll, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p],
+    "edl_maxpool_bwd_nhwc": [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p,
+                             c_void_p],
     "edl_linear_bwd_data": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_ll,
                             c_int, c_int, c_int, c_void_p],
     "edl_linear_bwd_weight": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_ll, c_void_p,

@@ -338,8 +338,9 @@ int edl_avgpool_nhwc(const void* x, int N, int HW, int C, void* out, long long l
 int edl_linear_bwd_data(const void* dY, long long lddy, const void* W, long long ldw,
                         const void* H, long long ldh, void* dX, long long lddx, int M, int N,
                         int K, void* stream) {
-  if (M < 1 || N < 1 || K < 1 || lddy < N || ldw < K || ldh < K || lddx < K)
+  if (M < 1 || N < 1 || K < 1 || lddy < N || ldw < K || (H && ldh < K) || lddx < K)
     return fail(EDL_ERR_SHAPE, "linear_bwd_data: bad shape M=%d N=%d K=%d", M, N, K);
+  const GemmKind kind = H ? GemmKind::BwdData : GemmKind::BwdDataPlain;   // H null: no (1 - a^2)
   const int cap = grid_cap(as_stream(stream));
   CUtensorMap ta, tb;
   int rc;
@@ -351,10 +352,45 @@ int edl_linear_bwd_data(const void* dY, long long lddy, const void* W, long long
   CUtensorMap ty;
   if ((rc = tensor_map_out(dX, M, K, lddx, false, &ty))) return rc;
   const int pbn = pick_pair_bn(M, K, cap);
-  cudaError_t e = pbn > 0 ? launch_gemm_pair(GemmKind::BwdData, pbn, ta, tb, ty, M, K, N, ep, cap, as_stream(stream))
-                          : launch_gemm(GemmKind::BwdData, pick_bn_cap(M, K, cap), ta, tb, ty, M, K, N, ep, cap,
+  cudaError_t e = pbn > 0 ? launch_gemm_pair(kind, pbn, ta, tb, ty, M, K, N, ep, cap, as_stream(stream))
+                          : launch_gemm(kind, pick_bn_cap(M, K, cap), ta, tb, ty, M, K, N, ep, cap,
                                         as_stream(stream));
   return e == cudaSuccess ? 0 : cuda_fail(e, "linear_bwd_data");
+}
+
+int edl_col2im_nhwc(const void* dcol, long long ldc, int N, int H, int W, int C, int R, int S, int stride, int pad,
+                    const void* add, const void* mask, void* dx, void* stream) {
+  if (N < 1 || H < 1 || W < 1 || C < 8 || C % 8 || R < 1 || S < 1 || stride < 1 || pad < 0 ||
+      ldc < static_cast<long long>(R) * S * C || ldc % 8)
+    return fail(EDL_ERR_SHAPE, "col2im_nhwc: bad shape");
+  const int P = (H + 2 * pad - R) / stride + 1, Q = (W + 2 * pad - S) / stride + 1;
+  if (P < 1 || Q < 1) return fail(EDL_ERR_SHAPE, "col2im_nhwc: empty output");
+  cudaError_t e = launch_col2im_nhwc(reinterpret_cast<const __nv_bfloat16*>(dcol), ldc, N, H, W, C, R, S, stride, pad,
+                                     P, Q, reinterpret_cast<const __nv_bfloat16*>(add),
+                                     reinterpret_cast<const __nv_bfloat16*>(mask),
+                                     reinterpret_cast<__nv_bfloat16*>(dx), as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "col2im_nhwc");
+}
+
+int edl_avgpool_bwd_nhwc(const void* df, long long ldf, int N, int HW, int C, const void* mask, void* dx,
+                         void* stream) {
+  if (N < 1 || HW < 1 || C < 8 || C % 8 || ldf < C || ldf % 8) return fail(EDL_ERR_SHAPE, "avgpool_bwd_nhwc: bad shape");
+  cudaError_t e = launch_avgpool_bwd_nhwc(reinterpret_cast<const __nv_bfloat16*>(df), ldf, N, HW, C,
+                                          reinterpret_cast<const __nv_bfloat16*>(mask),
+                                          reinterpret_cast<__nv_bfloat16*>(dx), as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "avgpool_bwd_nhwc");
+}
+
+int edl_maxpool_bwd_nhwc(const void* x, int N, int H, int W, int C, int k, int stride, int pad, const void* dy,
+                         const void* mask, void* dx, void* stream) {
+  if (N < 1 || H < 1 || W < 1 || C < 1 || k < 1 || stride < 1 || pad < 0 || pad >= k)
+    return fail(EDL_ERR_SHAPE, "maxpool_bwd_nhwc: bad shape");
+  const int P = (H + 2 * pad - k) / stride + 1, Q = (W + 2 * pad - k) / stride + 1;
+  cudaError_t e = launch_maxpool_bwd_nhwc(reinterpret_cast<const __nv_bfloat16*>(x), N, H, W, C, k, stride, pad, P, Q,
+                                          reinterpret_cast<const __nv_bfloat16*>(dy),
+                                          reinterpret_cast<const __nv_bfloat16*>(mask),
+                                          reinterpret_cast<__nv_bfloat16*>(dx), as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "maxpool_bwd_nhwc");
 }
 
 int edl_linear_bwd_weight(const void* dY, long long lddy, const void* X, long long ldx, float* dW,

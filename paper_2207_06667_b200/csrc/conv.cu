@@ -144,6 +144,152 @@ __global__ void __launch_bounds__(256) avgpool_nhwc_kernel(const __nv_bfloat16* 
   }
 }
 
+// ---- backward (cfg4 student)
+// dx[n][h][w][c] = sum over (r, s) with h = p*stride - pad + r, w = q*stride -
+// pad + s of dcol[(n,p,q)][(r,s,c)]  (+ add[n][h][w][c]), then times
+// (mask[n][h][w][c] > 0) if mask is given: the gradient w.r.t. a ReLU
+// layer's pre-activation straight from the next conv's column gradient. A
+// gather (each output summed by one thread in a fixed order): deterministic.
+__global__ void __launch_bounds__(256) col2im_nhwc_kernel(const __nv_bfloat16* __restrict__ dcol, long long ldc,
+                                                          int N, int H, int W, int C, int R, int S, int stride,
+                                                          int pad, int P, int Q, const __nv_bfloat16* __restrict__ add,
+                                                          const __nv_bfloat16* __restrict__ mask,
+                                                          __nv_bfloat16* __restrict__ dx) {
+  griddep_wait();
+  const int cv = C / 8;
+  const long long total = static_cast<long long>(N) * H * W * cv;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int c8 = static_cast<int>(i % cv);
+    const long long pix = i / cv;
+    const int w = static_cast<int>(pix % W);
+    const int h = static_cast<int>((pix / W) % H);
+    const int n = static_cast<int>(pix / (static_cast<long long>(H) * W));
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int r = 0; r < R; ++r) {
+      const int ph = h + pad - r;
+      if (ph < 0 || ph % stride) continue;
+      const int p = ph / stride;
+      if (p >= P) continue;
+      for (int s = 0; s < S; ++s) {
+        const int qw = w + pad - s;
+        if (qw < 0 || qw % stride) continue;
+        const int q = qw / stride;
+        if (q >= Q) continue;
+        const long long m = (static_cast<long long>(n) * P + p) * Q + q;
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(dcol + m * ldc + (static_cast<long long>(r) * S + s) * C) + c8);
+        const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(b[j]);
+      }
+    }
+    const long long off = pix * C + 8 * c8;
+    if (add != nullptr) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(add + off));
+      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(b[j]);
+    }
+    if (mask != nullptr) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(mask + off));
+      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = __bfloat162float(b[j]) > 0.f ? acc[j] : 0.f;
+    }
+    uint4 o;
+    o.x = pack_bf16x2(acc[0], acc[1]);
+    o.y = pack_bf16x2(acc[2], acc[3]);
+    o.z = pack_bf16x2(acc[4], acc[5]);
+    o.w = pack_bf16x2(acc[6], acc[7]);
+    *reinterpret_cast<uint4*>(dx + off) = o;
+  }
+}
+
+// Global average pool backward: dx[n][i][c] = df[n][c] / HW, times
+// (mask[n][i][c] > 0) if given (the last block's output ReLU).
+__global__ void __launch_bounds__(256) avgpool_bwd_nhwc_kernel(const __nv_bfloat16* __restrict__ df, long long ldf,
+                                                               int N, int HW, int C,
+                                                               const __nv_bfloat16* __restrict__ mask,
+                                                               __nv_bfloat16* __restrict__ dx) {
+  griddep_wait();
+  const int cv = C / 8;
+  const float inv = 1.0f / static_cast<float>(HW);
+  const long long total = static_cast<long long>(N) * HW * cv;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int c8 = static_cast<int>(i % cv);
+    const long long pix = i / cv;
+    const int n = static_cast<int>(pix / HW);
+    const uint4 g = __ldg(reinterpret_cast<const uint4*>(df + n * ldf) + c8);
+    const __nv_bfloat16* gb = reinterpret_cast<const __nv_bfloat16*>(&g);
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __bfloat162float(gb[j]) * inv;
+    if (mask != nullptr) {
+      const uint4 m = __ldg(reinterpret_cast<const uint4*>(mask + pix * C) + c8);
+      const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&m);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __bfloat162float(mb[j]) > 0.f ? v[j] : 0.f;
+    }
+    uint4 o;
+    o.x = pack_bf16x2(v[0], v[1]);
+    o.y = pack_bf16x2(v[2], v[3]);
+    o.z = pack_bf16x2(v[4], v[5]);
+    o.w = pack_bf16x2(v[6], v[7]);
+    *reinterpret_cast<uint4*>(dx + pix * C + 8 * c8) = o;
+  }
+}
+
+// Max pool backward as a gather: each input element collects the gradients of
+// the windows whose FIRST maximum (scan order r, s) it is, as torch does;
+// times (mask > 0) if given.
+__global__ void __launch_bounds__(256) maxpool_bwd_nhwc_kernel(const __nv_bfloat16* __restrict__ x, int N, int H,
+                                                               int W, int C, int k, int stride, int pad, int P,
+                                                               int Q, const __nv_bfloat16* __restrict__ dy,
+                                                               const __nv_bfloat16* __restrict__ mask,
+                                                               __nv_bfloat16* __restrict__ dx) {
+  griddep_wait();
+  const long long total = static_cast<long long>(N) * H * W * C;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % C);
+    const long long pix = i / C;
+    const int w = static_cast<int>(pix % W);
+    const int h = static_cast<int>((pix / W) % H);
+    const int n = static_cast<int>(pix / (static_cast<long long>(H) * W));
+    float acc = 0.f;
+    for (int r = 0; r < k; ++r) {
+      const int ph = h + pad - r;
+      if (ph < 0 || ph % stride) continue;
+      const int p = ph / stride;
+      if (p >= P) continue;
+      for (int s = 0; s < k; ++s) {
+        const int qw = w + pad - s;
+        if (qw < 0 || qw % stride) continue;
+        const int q = qw / stride;
+        if (q >= Q) continue;
+        // the window (p, q): is (h, w) its first maximum?
+        float best = -INFINITY;
+        int bh = -1, bw = -1;
+        for (int rr = 0; rr < k; ++rr) {
+          const int hh = p * stride - pad + rr;
+          if (hh < 0 || hh >= H) continue;
+          for (int ss = 0; ss < k; ++ss) {
+            const int ww = q * stride - pad + ss;
+            if (ww < 0 || ww >= W) continue;
+            const float v = __bfloat162float(x[((static_cast<long long>(n) * H + hh) * W + ww) * C + c]);
+            if (v > best) { best = v; bh = hh; bw = ww; }
+          }
+        }
+        if (bh == h && bw == w)
+          acc += __bfloat162float(dy[((static_cast<long long>(n) * P + p) * Q + q) * C + c]);
+      }
+    }
+    if (mask != nullptr && !(__bfloat162float(mask[i]) > 0.f)) acc = 0.f;
+    dx[i] = __float2bfloat16_rn(acc);
+  }
+}
+
 int grid_for(long long work) {
   long long b = (work + 255) / 256;
   return static_cast<int>(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
@@ -174,6 +320,29 @@ cudaError_t launch_maxpool_nhwc(const __nv_bfloat16* x, int N, int H, int W, int
 cudaError_t launch_avgpool_nhwc(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* out, long long ldo,
                                 cudaStream_t stream) {
   return launch_pdl(avgpool_nhwc_kernel, dim3(N), dim3(256), 0, stream, 1, x, HW, C, out, ldo);
+}
+
+cudaError_t launch_col2im_nhwc(const __nv_bfloat16* dcol, long long ldc, int N, int H, int W, int C, int R, int S,
+                               int stride, int pad, int P, int Q, const __nv_bfloat16* add,
+                               const __nv_bfloat16* mask, __nv_bfloat16* dx, cudaStream_t stream) {
+  const long long work = static_cast<long long>(N) * H * W * (C / 8);
+  return launch_pdl(col2im_nhwc_kernel, dim3(grid_for(work)), dim3(256), 0, stream, 1, dcol, ldc, N, H, W, C, R, S,
+                    stride, pad, P, Q, add, mask, dx);
+}
+
+cudaError_t launch_avgpool_bwd_nhwc(const __nv_bfloat16* df, long long ldf, int N, int HW, int C,
+                                    const __nv_bfloat16* mask, __nv_bfloat16* dx, cudaStream_t stream) {
+  const long long work = static_cast<long long>(N) * HW * (C / 8);
+  return launch_pdl(avgpool_bwd_nhwc_kernel, dim3(grid_for(work)), dim3(256), 0, stream, 1, df, ldf, N, HW, C, mask,
+                    dx);
+}
+
+cudaError_t launch_maxpool_bwd_nhwc(const __nv_bfloat16* x, int N, int H, int W, int C, int k, int stride, int pad,
+                                    int P, int Q, const __nv_bfloat16* dy, const __nv_bfloat16* mask,
+                                    __nv_bfloat16* dx, cudaStream_t stream) {
+  const long long work = static_cast<long long>(N) * H * W * C;
+  return launch_pdl(maxpool_bwd_nhwc_kernel, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, k, stride,
+                    pad, P, Q, dy, mask, dx);
 }
 
 }  // namespace edl

@@ -1419,6 +1419,8 @@ cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUte
       return launch_gemm_bn<false, false, EPI_RELU_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
     case GemmKind::FwdIdentBf16:
       return launch_gemm_bn<false, false, EPI_BIAS_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
+    case GemmKind::BwdDataPlain:
+      return launch_gemm_bn<false, true, EPI_BIAS_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
   }
   return cudaErrorInvalidValue;
 }
@@ -1459,6 +1461,8 @@ cudaError_t launch_gemm_pair(GemmKind kind, int bn, const CUtensorMap& ta, const
       return launch_pair_bn<false, false, EPI_RELU_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
     case GemmKind::FwdIdentBf16:
       return launch_pair_bn<false, false, EPI_BIAS_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
+    case GemmKind::BwdDataPlain:
+      return launch_pair_bn<false, true, EPI_BIAS_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
     default:
       return cudaErrorInvalidValue;
   }

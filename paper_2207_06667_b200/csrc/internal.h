@@ -71,7 +71,7 @@ struct HeadArgs {
   int* idx;
 };
 
-enum class GemmKind { FwdTanh, FwdLinear, BwdData, BwdWeight, FwdRelu, FwdIdentBf16 };
+enum class GemmKind { FwdTanh, FwdLinear, BwdData, BwdWeight, FwdRelu, FwdIdentBf16, BwdDataPlain };
 
 constexpr int kMaxGroup = 4;
 struct GroupMaps {
@@ -120,6 +120,14 @@ cudaError_t launch_maxpool_nhwc(const __nv_bfloat16* x, int N, int H, int W, int
                                 int P, int Q, __nv_bfloat16* out, cudaStream_t stream);
 cudaError_t launch_avgpool_nhwc(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* out, long long ldo,
                                 cudaStream_t stream);
+cudaError_t launch_col2im_nhwc(const __nv_bfloat16* dcol, long long ldc, int N, int H, int W, int C, int R, int S,
+                               int stride, int pad, int P, int Q, const __nv_bfloat16* add,
+                               const __nv_bfloat16* mask, __nv_bfloat16* dx, cudaStream_t stream);
+cudaError_t launch_avgpool_bwd_nhwc(const __nv_bfloat16* df, long long ldf, int N, int HW, int C,
+                                    const __nv_bfloat16* mask, __nv_bfloat16* dx, cudaStream_t stream);
+cudaError_t launch_maxpool_bwd_nhwc(const __nv_bfloat16* x, int N, int H, int W, int C, int k, int stride, int pad,
+                                    int P, int Q, const __nv_bfloat16* dy, const __nv_bfloat16* mask,
+                                    __nv_bfloat16* dx, cudaStream_t stream);
 
 // SIMT kernels (kernels.cu)
 cudaError_t launch_kd_loss(const float* logits, long long ld_z, const int64_t* labels,

@@ -264,3 +264,286 @@ def to_nhwc(images: np.ndarray, device) -> torch.Tensor:
     x = torch.zeros(n, h, w, pad(c), dtype=torch.bfloat16, device=device)
     x[..., :c] = torch.from_numpy(np.ascontiguousarray(images.transpose(0, 2, 3, 1), dtype=np.float32)).to(device).to(torch.bfloat16)
     return x
+
+
+# ---------------------------------------------------------------------------
+# cfg4 student: BN-free ResNet-18-style training step (basic blocks; each
+# residual branch's second conv starts small, Fixup-style, since training-mode
+# BatchNorm is not on this path yet). Parameters live in one flat fp32 master
+# + bf16 copy (Model's layout idea), gradients in one flat fp32 vector, so SGD
+# is one edl_sgd_step.
+
+@dataclass(frozen=True)
+class StudentResNetConfig:
+    layers: tuple = (2, 2, 2, 2)
+    width: int = 64
+    classes: int = 1000
+    image: int = 224
+    in_channels: int = 3
+
+
+def init_student_resnet(cfg: StudentResNetConfig, seed: int) -> HostResNet:
+    rng = np.random.default_rng(seed)
+    rcfg = ResNetConfig(block="basic", layers=cfg.layers, width=cfg.width, classes=cfg.classes, image=cfg.image,
+                        in_channels=cfg.in_channels)
+    net = HostResNet(rcfg, _conv(rng, cfg.in_channels, cfg.width, 7, 2))
+    net.stem.pad = 3
+    net.stem.b[:] = 0.0
+    cin = cfg.width
+    for stage, n in enumerate(cfg.layers):
+        cout = cfg.width * (2 ** stage)
+        for i in range(n):
+            stride = 2 if (i == 0 and stage > 0) else 1
+            c1 = _conv(rng, cin, cout, 3, stride)
+            c2 = _conv(rng, cout, cout, 3, 1, relu=True, gain=0.25)
+            shortcut = None
+            if stride != 1 or cin != cout:
+                shortcut = _conv(rng, cin, cout, 1, stride, relu=False)
+                shortcut.pad = 0
+            net.blocks.append(HostBlock([c1, c2], shortcut))
+            cin = cout
+    net.fc_w = (rng.normal(0.0, np.sqrt(1.0 / cin), size=(cfg.classes, cin))).astype(np.float32)
+    net.fc_b = np.zeros(cfg.classes, dtype=np.float32)
+    return net
+
+
+class _Param:
+    """A [rows][cols] weight + [rows] bias view pair inside the flat buffers."""
+
+    def __init__(self, off_w, rows, cols, off_b):
+        self.off_w, self.rows, self.cols, self.off_b = off_w, rows, cols, off_b
+
+
+class ResNetStudent:
+    """Device BN-free ResNet-18-style student: forward, KD loss (the same fused
+    kernel as the MLP students), full backward and SGD, for a fixed batch."""
+
+    def __init__(self, host: HostResNet, device=None, batch_size: int = 64):
+        self.device = dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.B = B = batch_size
+        self.cfg = host.cfg
+        self.convs = [_DevConv(host.stem, "cpu")]
+        self.block_idx = []                                 # (conv1, conv2, shortcut or None) indices
+        for blk in host.blocks:
+            i1 = len(self.convs); self.convs.append(_DevConv(blk.convs[0], "cpu"))
+            i2 = len(self.convs); self.convs.append(_DevConv(blk.convs[1], "cpu"))
+            isc = None
+            if blk.shortcut is not None:
+                isc = len(self.convs); self.convs.append(_DevConv(blk.shortcut, "cpu"))
+            self.block_idx.append((i1, i2, isc))
+        feat = host.fc_w.shape[1]
+        self.feat_p = pad(feat)
+        self.classes = host.fc_w.shape[0]
+        self.classes_p = pad(self.classes)
+        # flat layout: every conv [cout_p][kdim] + bias [cout_p], then fc [classes_p][feat_p] + [classes_p]
+        self.params, off = [], 0
+        for c in self.convs:
+            p = _Param(off, c.cout_p, c.kdim, off + c.cout_p * c.kdim)
+            off = p.off_b + c.cout_p
+            self.params.append(p)
+        self.fc = _Param(off, self.classes_p, self.feat_p, off + self.classes_p * self.feat_p)
+        self.size = self.fc.off_b + self.classes_p
+        flat = torch.zeros(self.size, dtype=torch.float32)
+        for c, p in zip(self.convs, self.params):
+            flat[p.off_w:p.off_w + p.rows * p.cols] = c.w.float().reshape(-1)
+            flat[p.off_b:p.off_b + p.rows] = c.b
+        fcw = torch.zeros(self.classes_p, self.feat_p)
+        fcw[:self.classes, :feat] = torch.from_numpy(host.fc_w)
+        flat[self.fc.off_w:self.fc.off_w + self.classes_p * self.feat_p] = fcw.reshape(-1)
+        flat[self.fc.off_b:self.fc.off_b + self.classes] = torch.from_numpy(host.fc_b)
+        self.flat = flat.to(dev)
+        self.flat_bf16 = self.flat.to(torch.bfloat16)
+        self.grads = torch.zeros(self.size, dtype=torch.float32, device=dev)
+        for c in self.convs:                                # device copies are views into the flat buffers
+            c.w = c.b = None
+        # activations (post-ReLU outputs are kept for the backward masks)
+        H = self.cfg.image
+        stem = self.convs[0]
+        h, w = stem.out_hw(H, H)
+        self.stem_hw = (h, w)
+        self.y0 = torch.empty(B, h, w, stem.cout_p, dtype=torch.bfloat16, device=dev)
+        ph, pw = (h + 2 - 3) // 2 + 1, (w + 2 - 3) // 2 + 1
+        self.pool_hw = (ph, pw)
+        self.x1 = torch.empty(B, ph, pw, stem.cout_p, dtype=torch.bfloat16, device=dev)
+        col = B * h * w * stem.kdim
+        self.acts, hw = [], (ph, pw)                        # per block: (in_hw, h1, sc, y)
+        for i1, i2, isc in self.block_idx:
+            c1, c2 = self.convs[i1], self.convs[i2]
+            oh, ow = c1.out_hw(*hw)
+            h1 = torch.empty(B, oh, ow, c1.cout_p, dtype=torch.bfloat16, device=dev)
+            y = torch.empty(B, oh, ow, c2.cout_p, dtype=torch.bfloat16, device=dev)
+            sc = torch.empty(B, oh, ow, c2.cout_p, dtype=torch.bfloat16, device=dev) if isc is not None else None
+            col = max(col, B * oh * ow * max(c1.kdim, c2.kdim))
+            self.acts.append((hw, h1, sc, y))
+            hw = (oh, ow)
+        self.final_hw = hw
+        self.col = torch.empty(col, dtype=torch.bfloat16, device=dev)
+        # backward buffers: gradient ping-pong at the largest activation size + a shortcut buffer
+        big = max(B * h * w * stem.cout_p, max(a[1].numel() for a in self.acts))
+        self.g = [torch.empty(big, dtype=torch.bfloat16, device=dev) for _ in range(3)]
+        self.features = torch.empty(B, self.feat_p, dtype=torch.bfloat16, device=dev)
+        self.logits = torch.empty(B, self.classes_p, dtype=torch.float32, device=dev)
+        self.dlogits = torch.empty(B, self.classes_p, dtype=torch.bfloat16, device=dev)
+        self.dfeat = torch.empty(B, self.feat_p, dtype=torch.bfloat16, device=dev)
+        self.row_loss = torch.empty(B, dtype=torch.float32, device=dev)
+        self.loss = torch.zeros(1, dtype=torch.float32, device=dev)
+        self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        ws = _lib.load().edl_colsum_workspace_floats(B * h * w, max(c.cout_p for c in self.convs))
+        self.colsum_ws = torch.empty(max(int(ws), _lib.load().edl_colsum_workspace_floats(B, self.classes_p), 1),
+                                     dtype=torch.float32, device=dev)
+
+    # views
+    def _w16(self, p):
+        return self.flat_bf16[p.off_w:p.off_w + p.rows * p.cols]
+
+    def _b(self, p):
+        return self.flat[p.off_b:p.off_b + p.rows]
+
+    def _gw(self, p):
+        return self.grads[p.off_w:p.off_w + p.rows * p.cols]
+
+    def _gb(self, p):
+        return self.grads[p.off_b:p.off_b + p.rows]
+
+    def _im2col(self, c, x, hw, s):
+        if c.k == 1 and c.stride == 1:
+            return x, c.cin_p
+        _lib.call("edl_im2col_nhwc", x.data_ptr(), self.B, hw[0], hw[1], c.cin_p, c.cin if c.packed else c.cin_p,
+                  c.k, c.k, c.stride, c.pad, self.col.data_ptr(), c.kdim, s)
+        return self.col, c.kdim
+
+    def _fwd(self, i, x, hw, out, residual, s):
+        c, p = self.convs[i], self.params[i]
+        oh, ow = c.out_hw(*hw)
+        a, lda = self._im2col(c, x, hw, s)
+        M = self.B * oh * ow
+        if residual is not None:
+            _lib.call("edl_linear_fwd_residual", a.data_ptr(), lda, self._w16(p).data_ptr(), c.kdim,
+                      self._b(p).data_ptr(), residual.data_ptr(), c.cout_p, out.data_ptr(), c.cout_p, M, c.cout_p,
+                      c.kdim, s)
+        else:
+            _lib.call("edl_linear_fwd", a.data_ptr(), lda, self._w16(p).data_ptr(), c.kdim, self._b(p).data_ptr(),
+                      out.data_ptr(), c.cout_p, M, c.cout_p, c.kdim,
+                      _lib.EDL_ACT_RELU if c.relu else _lib.EDL_ACT_IDENT, s)
+
+    def forward(self, x, s):
+        self._fwd(0, x, (self.cfg.image, self.cfg.image), self.y0, None, s)
+        h, w = self.stem_hw
+        _lib.call("edl_maxpool_nhwc", self.y0.data_ptr(), self.B, h, w, self.y0.shape[-1], 3, 2, 1,
+                  self.x1.data_ptr(), s)
+        cur = self.x1
+        for (i1, i2, isc), (hw, h1, sc, y) in zip(self.block_idx, self.acts):
+            shortcut = cur
+            if isc is not None:
+                self._fwd(isc, cur, hw, sc, None, s)
+                shortcut = sc
+            self._fwd(i1, cur, hw, h1, None, s)
+            self._fwd(i2, h1, self.convs[i1].out_hw(*hw), y, shortcut, s)
+            cur = y
+        fh, fw = self.final_hw
+        _lib.call("edl_avgpool_nhwc", cur.data_ptr(), self.B, fh * fw, cur.shape[-1], self.features.data_ptr(),
+                  self.feat_p, s)
+        _lib.call("edl_linear_fwd", self.features.data_ptr(), self.feat_p, self._w16(self.fc).data_ptr(), self.feat_p,
+                  self._b(self.fc).data_ptr(), self.logits.data_ptr(), self.classes_p, self.B, self.classes_p,
+                  self.feat_p, _lib.EDL_ACT_NONE, s)
+
+    def _wgrad(self, i, dz, x, hw, s):
+        """dW_i = dz^T im2col(x), db_i = colsum(dz) (fp32, into the flat gradient)."""
+        c, p = self.convs[i], self.params[i]
+        oh, ow = c.out_hw(*hw)
+        a, lda = self._im2col(c, x, hw, s)
+        M = self.B * oh * ow
+        _lib.call("edl_linear_bwd_weight", dz.data_ptr(), c.cout_p, a.data_ptr(), lda, self._gw(p).data_ptr(), c.kdim,
+                  self._gb(p).data_ptr(), self.colsum_ws.data_ptr(), M, c.cout_p, c.kdim, 1.0, s)
+
+    def _dgrad(self, i, dz, hw, out, add, mask, s):
+        """out = col2im(dz W_i) (+ add) (* mask > 0): the gradient w.r.t. conv i's input."""
+        c, p = self.convs[i], self.params[i]
+        oh, ow = c.out_hw(*hw)
+        M = self.B * oh * ow
+        dcol = self.col[:M * c.kdim]
+        _lib.call("edl_linear_bwd_data", dz.data_ptr(), c.cout_p, self._w16(p).data_ptr(), c.kdim, None, 0,
+                  dcol.data_ptr(), c.kdim, M, c.cout_p, c.kdim, s)
+        _lib.call("edl_col2im_nhwc", dcol.data_ptr(), c.kdim, self.B, hw[0], hw[1], c.cin_p, c.k, c.k, c.stride,
+                  c.pad, None if add is None else add.data_ptr(), None if mask is None else mask.data_ptr(),
+                  out.data_ptr(), s)
+
+    def train_step(self, x, hard_labels, soft: SoftLabels | None, alpha: float, beta: float, temperature: float,
+                   eta: float, stream=None):
+        """Forward, fused KD loss (edl/nnkit.py:283-309 semantics), backward, SGD."""
+        s = (stream or torch.cuda.current_stream()).cuda_stream
+        B = self.B
+        self.forward(x, s)
+        q_vals = soft.probs if (soft is not None and beta > 0) else None
+        q_idx = soft.classes if (soft is not None and beta > 0) else None
+        k = soft.probs.shape[1] if q_vals is not None else 0
+        _lib.call("edl_kd_loss_fwd_bwd", self.logits.data_ptr(), self.classes_p, hard_labels.data_ptr(),
+                  None if q_vals is None else q_vals.data_ptr(), None if q_idx is None else q_idx.data_ptr(), B,
+                  self.classes, k, float(alpha), float(beta), float(temperature), self.row_loss.data_ptr(),
+                  self.loss.data_ptr(), self.ticket.data_ptr(), self.dlogits.data_ptr(), self.classes_p,
+                  self.status.data_ptr(), s)
+        # head: dW_fc / db_fc, dfeat = dz W_fc
+        _lib.call("edl_linear_bwd_weight", self.dlogits.data_ptr(), self.classes_p, self.features.data_ptr(),
+                  self.feat_p, self._gw(self.fc).data_ptr(), self.feat_p, self._gb(self.fc).data_ptr(),
+                  self.colsum_ws.data_ptr(), B, self.classes_p, self.feat_p, 1.0, s)
+        _lib.call("edl_linear_bwd_data", self.dlogits.data_ptr(), self.classes_p, self._w16(self.fc).data_ptr(),
+                  self.feat_p, None, 0, self.dfeat.data_ptr(), self.feat_p, B, self.classes_p, self.feat_p, s)
+        # the last block output's ReLU: dZ = avgpool_bwd(dfeat) * (y > 0)
+        fh, fw = self.final_hw
+        y_last = self.acts[-1][3]
+        dz = self.g[0][:y_last.numel()].view_as(y_last)
+        _lib.call("edl_avgpool_bwd_nhwc", self.dfeat.data_ptr(), self.feat_p, B, fh * fw, y_last.shape[-1],
+                  y_last.data_ptr(), dz.data_ptr(), s)
+        cur = 0                                             # dz lives in self.g[cur]
+        for bi in range(len(self.block_idx) - 1, -1, -1):
+            i1, i2, isc = self.block_idx[bi]
+            hw, h1, sc, y = self.acts[bi]
+            xin = self.x1 if bi == 0 else self.acts[bi - 1][3]
+            h1_hw = self.convs[i1].out_hw(*hw)
+            b1, b2 = [j for j in range(3) if j != cur]
+            # conv2: dW2, db2; dZ1 = col2im(dZ2 W2) * (h1 > 0)
+            self._wgrad(i2, dz, h1, h1_hw, s)
+            dz1 = self.g[b1][:h1.numel()].view_as(h1)
+            self._dgrad(i2, dz, h1_hw, dz1, None, h1, s)
+            # the shortcut's gradient (projection: its own dW / dgrad; identity: dZ2)
+            if isc is not None:
+                self._wgrad(isc, dz, xin, hw, s)
+                add = self.g[b2][:xin.numel()].view_as(xin)
+                self._dgrad(isc, dz, hw, add, None, None, s)
+                out_buf = cur                               # dZ2's last reader ran above (stream order)
+            else:
+                add = dz
+                out_buf = b2
+            # conv1: dW1, db1; dX = col2im(dZ1 W1) + shortcut gradient, masked by the input's ReLU
+            self._wgrad(i1, dz1, xin, hw, s)
+            dx = self.g[out_buf][:xin.numel()].view_as(xin)
+            self._dgrad(i1, dz1, hw, dx, add, xin if bi > 0 else None, s)
+            dz, cur = dx, out_buf
+        # maxpool + stem ReLU, then the stem's weight gradient (the images need no gradient)
+        h, w = self.stem_hw
+        dy0 = self.g[(cur + 1) % 3][:self.y0.numel()].view_as(self.y0)
+        _lib.call("edl_maxpool_bwd_nhwc", self.y0.data_ptr(), B, h, w, self.y0.shape[-1], 3, 2, 1, dz.data_ptr(),
+                  self.y0.data_ptr(), dy0.data_ptr(), s)
+        self._wgrad(0, dy0, x, (self.cfg.image, self.cfg.image), s)
+        _lib.call("edl_sgd_step", self.flat.data_ptr(), self.flat_bf16.data_ptr(), self.grads.data_ptr(), self.size,
+                  float(eta), s)
+        return self.loss
+
+    def flops_per_sample(self) -> float:
+        """Algorithmic GEMM FLOPs per image for one training step: forward,
+        dgrad (all but the stem) and wgrad."""
+        total = 0.0
+        H = self.cfg.image
+        for idx, c in enumerate(self.convs):
+            if idx == 0:
+                oh, ow = c.out_hw(H, H)
+                total += 2 * 2.0 * oh * ow * c.cout_p * c.kdim
+                continue
+        for (i1, i2, isc), (hw, _, _, _) in zip(self.block_idx, self.acts):
+            for i, inhw in ((i1, hw), (i2, self.convs[i1].out_hw(*hw))) + (((isc, hw),) if isc is not None else ()):
+                c = self.convs[i]
+                oh, ow = c.out_hw(*inhw)
+                total += 3 * 2.0 * oh * ow * c.cout_p * c.kdim
+        total += 3 * 2.0 * self.classes_p * self.feat_p
+        return total
