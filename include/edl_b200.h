@@ -98,6 +98,15 @@ int edl_avgpool_bwd_nhwc(const void* df, long long ldf, int N, int HW, int C, co
  * first maximum it is (torch's tie rule) (* (mask > 0)). */
 int edl_maxpool_bwd_nhwc(const void* x, int N, int H, int W, int C, int k, int stride, int pad, const void* dy,
                          const void* mask, void* dx, void* stream);
+/* Training pair: the forward max pool also records, per output window and
+ * 8-channel vector, one 32-bit word of 4-bit first-maximum positions r*k+s
+ * (argmax: unsigned [N][P][Q][C/8], k*k <= 15); the backward then gathers
+ * from those words instead of re-scanning every window. Same results as
+ * edl_maxpool_nhwc / edl_maxpool_bwd_nhwc. */
+int edl_maxpool_argmax_nhwc(const void* x, int N, int H, int W, int C, int k, int stride, int pad, void* out,
+                            unsigned* argmax, void* stream);
+int edl_maxpool_bwd_argmax_nhwc(const unsigned* argmax, int N, int H, int W, int C, int k, int stride, int pad,
+                                const void* dy, const void* mask, void* dx, void* stream);
 
 /* Backprop through one tanh layer, edl/nnkit.py:308:
  *   dX[M][K] = (dY[M][N] @ W[N][K]) * (1 - H[M][K]^2)      (all bf16)
@@ -115,6 +124,17 @@ int edl_linear_bwd_weight(const void* dY, long long lddy, const void* X, long lo
                           long long lddw, float* db, float* workspace, int M, int N, int K,
                           float scale, void* stream);
 long long edl_colsum_workspace_floats(int M, int N);
+
+/* The same gradients for tall reductions (conv layers: M = B*H*W pixels, few
+ * output tiles): split-K tcgen05 partials + a fixed-order reduce
+ * (deterministic), operands swapped when N < 128 so the 128-row MMA is full,
+ * and a tall column sum for db. workspace: workspace_floats >=
+ * edl_bwd_weight_workspace_floats(M, N, K) for the planned split; a smaller
+ * workspace only narrows the split. */
+int edl_linear_bwd_weight_ws(const void* dY, long long lddy, const void* X, long long ldx, float* dW,
+                             long long lddw, float* db, float* workspace, long long workspace_floats, int M, int N,
+                             int K, float scale, void* stream);
+long long edl_bwd_weight_workspace_floats(int M, int N, int K);
 
 /* The same for up to 4 independent layers in ONE persistent tcgen05 launch
  * (host arrays of per-layer pointers / sizes). The backward pass issues every

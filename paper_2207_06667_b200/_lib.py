@@ -42,6 +42,10 @@ _SIGNATURES = {
     "edl_avgpool_bwd_nhwc": [c_void_p, c_ll, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p],
     "edl_maxpool_bwd_nhwc": [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p,
                              c_void_p],
+    "edl_maxpool_argmax_nhwc": [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p,
+                                c_void_p],
+    "edl_maxpool_bwd_argmax_nhwc": [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p,
+                                    c_void_p, c_void_p],
     "edl_linear_bwd_data": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_ll,
                             c_int, c_int, c_int, c_void_p],
     "edl_linear_bwd_weight": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_ll, c_void_p,
@@ -51,6 +55,9 @@ _SIGNATURES = {
     "edl_linear_bwd_weight_grouped_sgd": [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                           c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                           c_float, c_void_p],
+    "edl_linear_bwd_weight_ws": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_void_p, c_ll, c_int,
+                                 c_int, c_int, c_float, c_void_p],
+    "edl_bwd_weight_workspace_floats": [c_int, c_int, c_int],
     "edl_colsum_workspace_floats": [c_int, c_int],
     "edl_colsum_group_workspace_floats": [c_int, c_void_p, c_void_p],
     "edl_teacher_head_softmax_topk": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_int, c_int,
@@ -70,6 +77,7 @@ _SIGNATURES = {
     "edl_cast_bf16": [c_void_p, c_ll, c_void_p, c_ll, c_int, c_int, c_void_p],
 }
 _RESTYPES = {"edl_last_error": c_char_p, "edl_colsum_workspace_floats": c_ll,
+             "edl_bwd_weight_workspace_floats": c_ll,
              "edl_colsum_group_workspace_floats": c_ll}
 
 EDL_ERR_SHAPE, EDL_ERR_NUMERIC, EDL_ERR_PARAM, EDL_ERR_CUDA = -1, -2, -3, -4
@@ -123,6 +131,7 @@ def check(rc: int, what: str) -> None:
 
 # kernel launches per C entry point (bench.py reports launches in its timed region)
 _LAUNCHES = {"edl_linear_bwd_weight": 3,   # GEMM + two column-sum passes when db is requested
+             "edl_linear_bwd_weight_ws": 4,   # split-K GEMM + reduce + two column-sum passes (at most)
              "edl_kd_loss_fwd_bwd": 2,     # row pass + deterministic batch-mean pass
              "edl_stream_wait_geq": 0,     # stream memory ops, not kernels
              "edl_stream_write_u32": 0}

@@ -170,6 +170,63 @@ int pick_pair_bn(int M, int N, int cap) {
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Weight-gradient plan for tall reductions (conv layers: dW[N][K] reduced over
+// M = B*H*W pixels, as few as 5 output tiles). Split-K gives the SMs work:
+// split s reduces k-blocks [s*kps, (s+1)*kps) into its own fp32 partial, and a
+// fixed-order reduce kernel sums them (deterministic). With N < 128 output
+// rows the operands swap (GEMM M = K, N = N) so the 128-row MMA is not half
+// empty; the reduce then transposes back to [N][K]. Cost model (us): waves x
+// max(k-blocks per item x 0.069 x bn/64 [one 128 x 64 x 64 k-block at the
+// per-SM tensor peak], the item's fp32 epilogue at ~50 GB/s per SM) + 0.5 per
+// wave, plus the partials' HBM round trip at 5 TB/s and ~2 us for the reduce.
+struct WgradPlan {
+  bool swap = false;
+  int bn = 64;
+  int ksplit = 1;
+  int gm = 0, gn = 0;
+  bool reduce() const { return swap || ksplit > 1; }
+  long long partial_floats() const { return reduce() ? static_cast<long long>(ksplit) * gm * gn : 0; }
+};
+
+WgradPlan plan_wgrad(int M, int N, int K, int cap, long long max_partial_floats) {
+  WgradPlan p;
+  p.swap = N < 128 && K > N;
+  p.gm = p.swap ? K : N;
+  p.gn = p.swap ? N : K;
+  if (p.swap && static_cast<long long>(p.gm) * p.gn > max_partial_floats) {
+    p.swap = false;
+    p.gm = N;
+    p.gn = K;
+  }
+  p.bn = p.gn <= 64 ? 64 : (p.gn <= 128 ? 128 : 256);
+  const long long tiles = static_cast<long long>((p.gm + 127) / 128) * ((p.gn + p.bn - 1) / p.bn);
+  const int nk = (M + 63) / 64;
+  const double t_kb = 0.069 * p.bn / 64.0;
+  const double t_epi = 128.0 * p.bn * 4 / 5e4;
+  const double gmn = static_cast<double>(p.gm) * p.gn;
+  double best = -1.0;
+  const int kmax = nk < 1024 ? nk : 1024;
+  for (int ks = 1; ks <= kmax; ++ks) {
+    const int kps = (nk + ks - 1) / ks;
+    if ((nk + kps - 1) / kps != ks) continue;          // only splits with no empty tail
+    if (ks > 1 && static_cast<double>(ks) * gmn > static_cast<double>(max_partial_floats)) break;
+    const long long waves = (tiles * ks + cap - 1) / cap;
+    const double item = kps * t_kb > t_epi ? kps * t_kb : t_epi;
+    double cost = waves * (item + 0.5);
+    if (ks > 1 || p.swap) cost += 2.0 * ks * gmn * 4 / 5e6 + 2.0;
+    if (best < 0 || cost < best) { best = cost; p.ksplit = ks; }
+  }
+  return p;
+}
+
+long long wgrad_workspace_floats(int M, int N, int K, int cap) {
+  const WgradPlan p = plan_wgrad(M, N, K, cap, 1LL << 40);
+  long long w = p.partial_floats();
+  const long long cs = colsum_tall_ok(N) ? static_cast<long long>(colsum_tall_blocks(M, cap)) * N
+                                         : colsum_workspace_floats(1, &M, &N);
+  return w > cs ? w : cs;
+}
+
 std::mutex g_attr_mu;
 std::unordered_map<const void*, unsigned long long> g_attr_done;  // kernel -> device bitmask
 
@@ -324,8 +381,33 @@ int edl_maxpool_nhwc(const void* x, int N, int H, int W, int C, int k, int strid
   const int P = (H + 2 * pad - k) / stride + 1, Q = (W + 2 * pad - k) / stride + 1;
   if (P < 1 || Q < 1) return fail(EDL_ERR_SHAPE, "maxpool_nhwc: empty output");
   cudaError_t e = launch_maxpool_nhwc(reinterpret_cast<const __nv_bfloat16*>(x), N, H, W, C, k, stride, pad, P, Q,
-                                      reinterpret_cast<__nv_bfloat16*>(out), as_stream(stream));
+                                      reinterpret_cast<__nv_bfloat16*>(out), nullptr, as_stream(stream));
   return e == cudaSuccess ? 0 : cuda_fail(e, "maxpool_nhwc");
+}
+
+int edl_maxpool_argmax_nhwc(const void* x, int N, int H, int W, int C, int k, int stride, int pad, void* out,
+                            unsigned* argmax, void* stream) {
+  if (N < 1 || H < 1 || W < 1 || C < 8 || C % 8 || k < 1 || k * k > 15 || stride < 1 || pad < 0 || pad >= k ||
+      !argmax)
+    return fail(EDL_ERR_SHAPE, "maxpool_argmax_nhwc: bad shape");
+  const int P = (H + 2 * pad - k) / stride + 1, Q = (W + 2 * pad - k) / stride + 1;
+  if (P < 1 || Q < 1) return fail(EDL_ERR_SHAPE, "maxpool_argmax_nhwc: empty output");
+  cudaError_t e = launch_maxpool_nhwc(reinterpret_cast<const __nv_bfloat16*>(x), N, H, W, C, k, stride, pad, P, Q,
+                                      reinterpret_cast<__nv_bfloat16*>(out), argmax, as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "maxpool_argmax_nhwc");
+}
+
+int edl_maxpool_bwd_argmax_nhwc(const unsigned* argmax, int N, int H, int W, int C, int k, int stride, int pad,
+                                const void* dy, const void* mask, void* dx, void* stream) {
+  if (N < 1 || H < 1 || W < 1 || C < 8 || C % 8 || k < 1 || k * k > 15 || stride < 1 || pad < 0 || pad >= k ||
+      !argmax)
+    return fail(EDL_ERR_SHAPE, "maxpool_bwd_argmax_nhwc: bad shape");
+  const int P = (H + 2 * pad - k) / stride + 1, Q = (W + 2 * pad - k) / stride + 1;
+  cudaError_t e = launch_maxpool_bwd_argmax_nhwc(argmax, N, H, W, C, k, stride, pad, P, Q,
+                                                 reinterpret_cast<const __nv_bfloat16*>(dy),
+                                                 reinterpret_cast<const __nv_bfloat16*>(mask),
+                                                 reinterpret_cast<__nv_bfloat16*>(dx), as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "maxpool_bwd_argmax_nhwc");
 }
 
 int edl_avgpool_nhwc(const void* x, int N, int HW, int C, void* out, long long ldo, void* stream) {
@@ -383,7 +465,7 @@ int edl_avgpool_bwd_nhwc(const void* df, long long ldf, int N, int HW, int C, co
 
 int edl_maxpool_bwd_nhwc(const void* x, int N, int H, int W, int C, int k, int stride, int pad, const void* dy,
                          const void* mask, void* dx, void* stream) {
-  if (N < 1 || H < 1 || W < 1 || C < 1 || k < 1 || stride < 1 || pad < 0 || pad >= k)
+  if (N < 1 || H < 1 || W < 1 || C < 8 || C % 8 || k < 1 || k * k > 15 || stride < 1 || pad < 0 || pad >= k)
     return fail(EDL_ERR_SHAPE, "maxpool_bwd_nhwc: bad shape");
   const int P = (H + 2 * pad - k) / stride + 1, Q = (W + 2 * pad - k) / stride + 1;
   cudaError_t e = launch_maxpool_bwd_nhwc(reinterpret_cast<const __nv_bfloat16*>(x), N, H, W, C, k, stride, pad, P, Q,
@@ -514,6 +596,50 @@ int edl_linear_bwd_weight_grouped_sgd(int count, const void* const* dY, const lo
 }
 
 long long edl_colsum_workspace_floats(int M, int N) { return colsum_workspace_floats(1, &M, &N); }
+
+long long edl_bwd_weight_workspace_floats(int M, int N, int K) {
+  if (M < 1 || N < 1 || K < 1) return -1;
+  return wgrad_workspace_floats(M, N, K, num_sms());
+}
+
+int edl_linear_bwd_weight_ws(const void* dY, long long lddy, const void* X, long long ldx, float* dW,
+                             long long lddw, float* db, float* workspace, long long workspace_floats, int M, int N,
+                             int K, float scale, void* stream) {
+  if (M < 1 || N < 1 || K < 1 || lddy < N || ldx < K || lddw < K)
+    return fail(EDL_ERR_SHAPE, "linear_bwd_weight_ws: bad shape M=%d N=%d K=%d", M, N, K);
+  if (!workspace || workspace_floats < 0)
+    return fail(EDL_ERR_SHAPE, "linear_bwd_weight_ws: workspace required");
+  cudaStream_t st = as_stream(stream);
+  const int cap = grid_cap(st);
+  const WgradPlan p = plan_wgrad(M, N, K, cap, workspace_floats);
+  CUtensorMap ta, tb;
+  int rc;
+  // dY [M][N] and X [M][K] both read as [red=M][MN]; swapped: A = X^T, B = dY^T
+  if ((rc = tensor_map(p.swap ? X : dY, M, p.swap ? K : N, p.swap ? ldx : lddy, 64, 64, &ta))) return rc;
+  if ((rc = tensor_map(p.swap ? dY : X, M, p.swap ? N : K, p.swap ? lddy : ldx, 64, 64, &tb))) return rc;
+  EpiArgs ep{p.reduce() ? static_cast<void*>(workspace) : static_cast<void*>(dW), p.reduce() ? p.gn : lddw,
+             nullptr, nullptr, 0, scale, stream_sched(st)};
+  ep.ksplit = p.ksplit;
+  ep.split_stride = static_cast<long long>(p.gm) * p.gn;
+  cudaError_t e = launch_gemm(GemmKind::BwdWeight, p.bn, ta, tb, ta, p.gm, p.gn, M, ep, cap, st);
+  if (e != cudaSuccess) return cuda_fail(e, "linear_bwd_weight_ws");
+  if (p.reduce()) {
+    e = launch_splitk_reduce(workspace, p.ksplit, ep.split_stride, p.gm, p.gn, p.swap, dW, lddw, cap, st);
+    if (e != cudaSuccess) return cuda_fail(e, "splitk_reduce");
+  }
+  if (db) {   // the workspace is free again (stream order)
+    const long long need = colsum_tall_ok(N) ? static_cast<long long>(colsum_tall_blocks(M, cap)) * N
+                                             : colsum_workspace_floats(1, &M, &N);
+    if (need > workspace_floats)
+      return fail(EDL_ERR_SHAPE, "linear_bwd_weight_ws: workspace %lld < %lld floats", workspace_floats, need);
+    e = colsum_tall_ok(N) ? launch_colsum_tall(reinterpret_cast<const __nv_bfloat16*>(dY), lddy, M, N, workspace,
+                                               db, scale, cap, st)
+                          : launch_colsum(reinterpret_cast<const __nv_bfloat16*>(dY), lddy, M, N, workspace, db,
+                                          scale, st);
+    if (e != cudaSuccess) return cuda_fail(e, "colsum");
+  }
+  return 0;
+}
 
 long long edl_colsum_group_workspace_floats(int count, const int* M, const int* N) {
   if (count < 1 || count > kMaxGroup) return -1;

@@ -16,85 +16,116 @@ namespace edl {
 
 namespace {
 
-// One thread per 16-byte (8-channel) vector of the im2col matrix.
+// One thread per 16-byte (8-channel) vector of the im2col matrix. I is the
+// element-index type: int whenever the element count fits (64-bit division
+// and modulo in the index decomposition cost more than the copy itself).
+template <typename I>
 __global__ void __launch_bounds__(256) im2col_nhwc_kernel(const __nv_bfloat16* __restrict__ x, int N, int H, int W,
                                                           int C, int R, int S, int stride, int pad, int P, int Q,
                                                           __nv_bfloat16* __restrict__ out, long long ldo) {
   griddep_wait();
   const int cv = C / 8;                       // 8-channel vectors per pixel
-  const long long per_row = static_cast<long long>(R) * S * cv;
-  const long long total = static_cast<long long>(N) * P * Q * per_row;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long m = i / per_row;
+  const int per_row = R * S * cv;
+  const I total = static_cast<I>(N) * P * Q * per_row;
+  for (I i = blockIdx.x * static_cast<I>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<I>(gridDim.x) * blockDim.x) {
+    const I m = i / per_row;
     const int j = static_cast<int>(i - m * per_row);
     const int c8 = j % cv;
     const int rs = j / cv;
     const int s = rs % S, r = rs / S;
     const int q = static_cast<int>(m % Q);
-    const int p = static_cast<int>((m / Q) % P);
-    const int n = static_cast<int>(m / (static_cast<long long>(P) * Q));
+    const I nq = m / Q;
+    const int p = static_cast<int>(nq % P);
+    const int n = static_cast<int>(nq / P);
     const int h = p * stride - pad + r, w = q * stride - pad + s;
     uint4 v = make_uint4(0u, 0u, 0u, 0u);
     if (h >= 0 && h < H && w >= 0 && w < W)
       v = __ldg(reinterpret_cast<const uint4*>(x + ((static_cast<long long>(n) * H + h) * W + w) * C) + c8);
-    *reinterpret_cast<uint4*>(out + m * ldo + static_cast<long long>(rs) * C + 8 * c8) = v;
+    *reinterpret_cast<uint4*>(out + static_cast<long long>(m) * ldo + static_cast<long long>(rs) * C + 8 * c8) = v;
   }
 }
 
 // Packed variant for inputs with few used channels (the RGB stem): the K
 // index runs over (r, s, c < c_used) densely, so a 7x7x3 stem has K = 147
-// (padded to ldo) instead of 7x7x16. One thread per 16-byte output chunk.
+// (padded to ldo) instead of 7x7x16. A block builds kPackQ consecutive output
+// pixels of one output row: the R x Wt input patch they read is staged in
+// shared memory with coalesced 16-byte loads (zeros outside the image), a
+// per-block table maps each K index to its patch offset (no divisions in the
+// gather), and the block's kPackQ * ldo outputs are one contiguous span
+// written as coalesced 16-byte stores.
+constexpr int kPackQ = 32;
+constexpr int kPackMaxK = 1024;
+
 __global__ void __launch_bounds__(256) im2col_nhwc_packed_kernel(const __nv_bfloat16* __restrict__ x, int N, int H,
                                                                  int W, int C, int c_used, int R, int S, int stride,
                                                                  int pad, int P, int Q,
                                                                  __nv_bfloat16* __restrict__ out, long long ldo) {
   griddep_wait();
+  extern __shared__ __align__(16) uint8_t psm[];
+  int* tab = reinterpret_cast<int*>(psm);                                  // [ldo]
+  __nv_bfloat16* patch = reinterpret_cast<__nv_bfloat16*>(psm + kPackMaxK * 4);
+  const int qblocks = (Q + kPackQ - 1) / kPackQ;
+  const int qb = blockIdx.x % qblocks;
+  const long long np = blockIdx.x / qblocks;
+  const int p = static_cast<int>(np % P), n = static_cast<int>(np / P);
+  const int q0 = qb * kPackQ;
+  const int Wt = (kPackQ - 1) * stride + S;
   const int kreal = R * S * c_used;
+  for (int k = threadIdx.x; k < ldo; k += blockDim.x) {
+    const int c = k % c_used, rs = k / c_used;
+    tab[k] = k < kreal ? ((rs / S) * Wt + rs % S) * C + c : -1;
+  }
+  const int cv = C / 8;
+  const int h0 = p * stride - pad, w0 = q0 * stride - pad;
+  for (int i = threadIdx.x; i < R * Wt * cv; i += blockDim.x) {
+    const int c8 = i % cv, pix = i / cv;
+    const int wl = pix % Wt, r = pix / Wt;
+    const int h = h0 + r, w = w0 + wl;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (h >= 0 && h < H && w >= 0 && w < W)
+      v = __ldg(reinterpret_cast<const uint4*>(x + ((static_cast<long long>(n) * H + h) * W + w) * C) + c8);
+    reinterpret_cast<uint4*>(patch)[i] = v;
+  }
+  __syncthreads();
   const int chunks = static_cast<int>(ldo / 8);
-  const long long total = static_cast<long long>(N) * P * Q * chunks;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long m = i / chunks;
-    const int ch = static_cast<int>(i - m * chunks);
-    const int q = static_cast<int>(m % Q);
-    const int p = static_cast<int>((m / Q) % P);
-    const int n = static_cast<int>(m / (static_cast<long long>(P) * Q));
-    float v[8];
+  const int nq = Q - q0 < kPackQ ? Q - q0 : kPackQ;
+  __nv_bfloat16* dst = out + ((static_cast<long long>(n) * P + p) * Q + q0) * ldo;
+  for (int i = threadIdx.x; i < nq * chunks; i += blockDim.x) {
+    const int ql = i / chunks, ch = i - ql * chunks;
+    const unsigned short* pb = reinterpret_cast<const unsigned short*>(patch) + ql * stride * C;
+    uint32_t v[4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int kidx = 8 * ch + j;
-      v[j] = 0.f;
-      if (kidx < kreal) {
-        const int c = kidx % c_used, rs = kidx / c_used;
-        const int h = p * stride - pad + rs / S, w = q * stride - pad + rs % S;
-        if (h >= 0 && h < H && w >= 0 && w < W)
-          v[j] = __bfloat162float(x[((static_cast<long long>(n) * H + h) * W + w) * C + c]);
-      }
+    for (int j = 0; j < 4; ++j) {
+      const int t0 = tab[8 * ch + 2 * j], t1 = tab[8 * ch + 2 * j + 1];
+      const uint32_t lo = t0 >= 0 ? pb[t0] : 0u, hi = t1 >= 0 ? pb[t1] : 0u;
+      v[j] = lo | (hi << 16);
     }
-    uint4 o;
-    o.x = pack_bf16x2(v[0], v[1]);
-    o.y = pack_bf16x2(v[2], v[3]);
-    o.z = pack_bf16x2(v[4], v[5]);
-    o.w = pack_bf16x2(v[6], v[7]);
-    *reinterpret_cast<uint4*>(out + m * ldo + 8 * ch) = o;
+    reinterpret_cast<uint4*>(dst)[i] = make_uint4(v[0], v[1], v[2], v[3]);
   }
 }
 
+// argmax (training): per (window, 8-channel vector) one 32-bit word of 4-bit
+// window positions r * k + s of the FIRST maximum in scan order (torch's
+// rule), for maxpool_bwd_argmax_nhwc_kernel.
+template <typename I>
 __global__ void __launch_bounds__(256) maxpool_nhwc_kernel(const __nv_bfloat16* __restrict__ x, int N, int H, int W,
                                                            int C, int k, int stride, int pad, int P, int Q,
-                                                           __nv_bfloat16* __restrict__ out) {
+                                                           __nv_bfloat16* __restrict__ out,
+                                                           uint32_t* __restrict__ argmax) {
   griddep_wait();
   const int cv = C / 8;
-  const long long total = static_cast<long long>(N) * P * Q * cv;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+  const I total = static_cast<I>(N) * P * Q * cv;
+  for (I i = blockIdx.x * static_cast<I>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<I>(gridDim.x) * blockDim.x) {
     const int c8 = static_cast<int>(i % cv);
-    const long long m = i / cv;
+    const I m = i / cv;
     const int q = static_cast<int>(m % Q);
-    const int p = static_cast<int>((m / Q) % P);
-    const int n = static_cast<int>(m / (static_cast<long long>(P) * Q));
+    const I nq = m / Q;
+    const int p = static_cast<int>(nq % P);
+    const int n = static_cast<int>(nq / P);
     float best[8];
+    uint32_t arg = 0xFFFFFFFFu;
 #pragma unroll
     for (int j = 0; j < 8; ++j) best[j] = -INFINITY;
     for (int r = 0; r < k; ++r) {
@@ -106,7 +137,13 @@ __global__ void __launch_bounds__(256) maxpool_nhwc_kernel(const __nv_bfloat16* 
         const uint4 v = __ldg(reinterpret_cast<const uint4*>(x + ((static_cast<long long>(n) * H + h) * W + w) * C) + c8);
         const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) best[j] = fmaxf(best[j], __bfloat162float(b[j]));
+        for (int j = 0; j < 8; ++j) {
+          const float f = __bfloat162float(b[j]);
+          if (f > best[j]) {
+            best[j] = f;
+            arg = (arg & ~(0xFu << (4 * j))) | (static_cast<uint32_t>(r * k + s) << (4 * j));
+          }
+        }
       }
     }
     uint4 o;
@@ -114,7 +151,8 @@ __global__ void __launch_bounds__(256) maxpool_nhwc_kernel(const __nv_bfloat16* 
     o.y = pack_bf16x2(best[2], best[3]);
     o.z = pack_bf16x2(best[4], best[5]);
     o.w = pack_bf16x2(best[6], best[7]);
-    *reinterpret_cast<uint4*>(out + m * C + 8 * c8) = o;
+    *reinterpret_cast<uint4*>(out + static_cast<long long>(m) * C + 8 * c8) = o;
+    if (argmax != nullptr) argmax[i] = arg;
   }
 }
 
@@ -150,6 +188,7 @@ __global__ void __launch_bounds__(256) avgpool_nhwc_kernel(const __nv_bfloat16* 
 // (mask[n][h][w][c] > 0) if mask is given: the gradient w.r.t. a ReLU
 // layer's pre-activation straight from the next conv's column gradient. A
 // gather (each output summed by one thread in a fixed order): deterministic.
+template <typename I>
 __global__ void __launch_bounds__(256) col2im_nhwc_kernel(const __nv_bfloat16* __restrict__ dcol, long long ldc,
                                                           int N, int H, int W, int C, int R, int S, int stride,
                                                           int pad, int P, int Q, const __nv_bfloat16* __restrict__ add,
@@ -157,14 +196,15 @@ __global__ void __launch_bounds__(256) col2im_nhwc_kernel(const __nv_bfloat16* _
                                                           __nv_bfloat16* __restrict__ dx) {
   griddep_wait();
   const int cv = C / 8;
-  const long long total = static_cast<long long>(N) * H * W * cv;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+  const I total = static_cast<I>(N) * H * W * cv;
+  for (I i = blockIdx.x * static_cast<I>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<I>(gridDim.x) * blockDim.x) {
     const int c8 = static_cast<int>(i % cv);
-    const long long pix = i / cv;
+    const I pix = i / cv;
     const int w = static_cast<int>(pix % W);
-    const int h = static_cast<int>((pix / W) % H);
-    const int n = static_cast<int>(pix / (static_cast<long long>(H) * W));
+    const I nh = pix / W;
+    const int h = static_cast<int>(nh % H);
+    const int n = static_cast<int>(nh / H);
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int r = 0; r < R; ++r) {
       const int ph = h + pad - r;
@@ -183,7 +223,7 @@ __global__ void __launch_bounds__(256) col2im_nhwc_kernel(const __nv_bfloat16* _
         for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(b[j]);
       }
     }
-    const long long off = pix * C + 8 * c8;
+    const long long off = static_cast<long long>(pix) * C + 8 * c8;
     if (add != nullptr) {
       const uint4 v = __ldg(reinterpret_cast<const uint4*>(add + off));
       const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v);
@@ -242,22 +282,25 @@ __global__ void __launch_bounds__(256) avgpool_bwd_nhwc_kernel(const __nv_bfloat
 
 // Max pool backward as a gather: each input element collects the gradients of
 // the windows whose FIRST maximum (scan order r, s) it is, as torch does;
-// times (mask > 0) if given.
+// times (mask > 0) if given. One thread per (pixel, 8-channel vector): each
+// window's per-channel argmax comes from k*k 16-byte loads (L1-resident: the
+// neighbouring threads read the same windows).
 __global__ void __launch_bounds__(256) maxpool_bwd_nhwc_kernel(const __nv_bfloat16* __restrict__ x, int N, int H,
                                                                int W, int C, int k, int stride, int pad, int P,
                                                                int Q, const __nv_bfloat16* __restrict__ dy,
                                                                const __nv_bfloat16* __restrict__ mask,
                                                                __nv_bfloat16* __restrict__ dx) {
   griddep_wait();
-  const long long total = static_cast<long long>(N) * H * W * C;
+  const int cv = C / 8;
+  const long long total = static_cast<long long>(N) * H * W * cv;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int c = static_cast<int>(i % C);
-    const long long pix = i / C;
+    const int c8 = static_cast<int>(i % cv);
+    const long long pix = i / cv;
     const int w = static_cast<int>(pix % W);
     const int h = static_cast<int>((pix / W) % H);
     const int n = static_cast<int>(pix / (static_cast<long long>(H) * W));
-    float acc = 0.f;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int r = 0; r < k; ++r) {
       const int ph = h + pad - r;
       if (ph < 0 || ph % stride) continue;
@@ -268,27 +311,113 @@ __global__ void __launch_bounds__(256) maxpool_bwd_nhwc_kernel(const __nv_bfloat
         if (qw < 0 || qw % stride) continue;
         const int q = qw / stride;
         if (q >= Q) continue;
-        // the window (p, q): is (h, w) its first maximum?
-        float best = -INFINITY;
-        int bh = -1, bw = -1;
+        // the window (p, q): which channels have (h, w) as their first maximum?
+        float best[8];
+        uint32_t arg = 0xFFFFFFFFu;           // 4-bit window positions (k * k <= 15)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) best[j] = -INFINITY;
         for (int rr = 0; rr < k; ++rr) {
           const int hh = p * stride - pad + rr;
           if (hh < 0 || hh >= H) continue;
           for (int ss = 0; ss < k; ++ss) {
             const int ww = q * stride - pad + ss;
             if (ww < 0 || ww >= W) continue;
-            const float v = __bfloat162float(x[((static_cast<long long>(n) * H + hh) * W + ww) * C + c]);
-            if (v > best) { best = v; bh = hh; bw = ww; }
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(x + ((static_cast<long long>(n) * H + hh) * W + ww) * C) + c8);
+            const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float f = __bfloat162float(b[j]);
+              if (f > best[j]) {
+                best[j] = f;
+                arg = (arg & ~(0xFu << (4 * j))) | (static_cast<uint32_t>(rr * k + ss) << (4 * j));
+              }
+            }
           }
         }
-        if (bh == h && bw == w)
-          acc += __bfloat162float(dy[((static_cast<long long>(n) * P + p) * Q + q) * C + c]);
+        const int mine = r * k + s;
+        const uint4 g = __ldg(reinterpret_cast<const uint4*>(dy + ((static_cast<long long>(n) * P + p) * Q + q) * C) + c8);
+        const __nv_bfloat16* gb = reinterpret_cast<const __nv_bfloat16*>(&g);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (((arg >> (4 * j)) & 0xFu) == static_cast<uint32_t>(mine)) acc[j] += __bfloat162float(gb[j]);
       }
     }
-    if (mask != nullptr && !(__bfloat162float(mask[i]) > 0.f)) acc = 0.f;
-    dx[i] = __float2bfloat16_rn(acc);
+    const long long off = pix * C + 8 * c8;
+    if (mask != nullptr) {
+      const uint4 m = __ldg(reinterpret_cast<const uint4*>(mask + off));
+      const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&m);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = __bfloat162float(mb[j]) > 0.f ? acc[j] : 0.f;
+    }
+    uint4 o;
+    o.x = pack_bf16x2(acc[0], acc[1]);
+    o.y = pack_bf16x2(acc[2], acc[3]);
+    o.z = pack_bf16x2(acc[4], acc[5]);
+    o.w = pack_bf16x2(acc[6], acc[7]);
+    *reinterpret_cast<uint4*>(dx + off) = o;
   }
 }
+
+// Max pool backward from the forward's argmax words: each input element
+// collects dy of the windows whose recorded first maximum it is (<= 4 windows
+// for 3x3 / 2), times (mask > 0) if given. One 4-byte word + one 16-byte dy
+// load per window and 8-channel vector.
+template <typename I>
+__global__ void __launch_bounds__(256) maxpool_bwd_argmax_nhwc_kernel(const uint32_t* __restrict__ argmax, int N,
+                                                                      int H, int W, int C, int k, int stride, int pad,
+                                                                      int P, int Q,
+                                                                      const __nv_bfloat16* __restrict__ dy,
+                                                                      const __nv_bfloat16* __restrict__ mask,
+                                                                      __nv_bfloat16* __restrict__ dx) {
+  griddep_wait();
+  const int cv = C / 8;
+  const I total = static_cast<I>(N) * H * W * cv;
+  for (I i = blockIdx.x * static_cast<I>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<I>(gridDim.x) * blockDim.x) {
+    const int c8 = static_cast<int>(i % cv);
+    const I pix = i / cv;
+    const int w = static_cast<int>(pix % W);
+    const I nh = pix / W;
+    const int h = static_cast<int>(nh % H);
+    const int n = static_cast<int>(nh / H);
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int r = 0; r < k; ++r) {
+      const int ph = h + pad - r;
+      if (ph < 0 || ph % stride) continue;
+      const int p = ph / stride;
+      if (p >= P) continue;
+      for (int s = 0; s < k; ++s) {
+        const int qw = w + pad - s;
+        if (qw < 0 || qw % stride) continue;
+        const int q = qw / stride;
+        if (q >= Q) continue;
+        const long long win = (static_cast<long long>(n) * P + p) * Q + q;
+        const uint32_t arg = __ldg(argmax + win * cv + c8);
+        const uint32_t mine = static_cast<uint32_t>(r * k + s);
+        const uint4 g = __ldg(reinterpret_cast<const uint4*>(dy + win * C) + c8);
+        const __nv_bfloat16* gb = reinterpret_cast<const __nv_bfloat16*>(&g);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (((arg >> (4 * j)) & 0xFu) == mine) acc[j] += __bfloat162float(gb[j]);
+      }
+    }
+    const long long off = static_cast<long long>(pix) * C + 8 * c8;
+    if (mask != nullptr) {
+      const uint4 m = __ldg(reinterpret_cast<const uint4*>(mask + off));
+      const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&m);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = __bfloat162float(mb[j]) > 0.f ? acc[j] : 0.f;
+    }
+    uint4 o;
+    o.x = pack_bf16x2(acc[0], acc[1]);
+    o.y = pack_bf16x2(acc[2], acc[3]);
+    o.z = pack_bf16x2(acc[4], acc[5]);
+    o.w = pack_bf16x2(acc[6], acc[7]);
+    *reinterpret_cast<uint4*>(dx + off) = o;
+  }
+}
+
+bool fits32(long long n) { return n < (1LL << 31) - (1LL << 24); }
 
 int grid_for(long long work) {
   long long b = (work + 255) / 256;
@@ -301,20 +430,35 @@ cudaError_t launch_im2col_nhwc(const __nv_bfloat16* x, int N, int H, int W, int 
                                int stride, int pad, int P, int Q, __nv_bfloat16* out, long long ldo,
                                cudaStream_t stream) {
   if (c_used < C) {
-    const long long work = static_cast<long long>(N) * P * Q * (ldo / 8);
-    return launch_pdl(im2col_nhwc_packed_kernel, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, c_used,
-                      R, S, stride, pad, P, Q, out, ldo);
+    if (ldo > kPackMaxK || ldo % 8) return cudaErrorInvalidValue;
+    const int Wt = (kPackQ - 1) * stride + S;
+    const int smem = kPackMaxK * 4 + R * Wt * C * 2;
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    if (smem > 48 * 1024) {
+      cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(im2col_nhwc_packed_kernel), smem);
+      if (e != cudaSuccess) return e;
+    }
+    const long long blocks = static_cast<long long>(N) * P * ((Q + kPackQ - 1) / kPackQ);
+    return launch_pdl(im2col_nhwc_packed_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), smem, stream, 1, x,
+                      N, H, W, C, c_used, R, S, stride, pad, P, Q, out, ldo);
   }
   const long long work = static_cast<long long>(N) * P * Q * R * S * (C / 8);
-  return launch_pdl(im2col_nhwc_kernel, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, R, S, stride,
-                    pad, P, Q, out, ldo);
+  if (fits32(work))
+    return launch_pdl(im2col_nhwc_kernel<int>, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, R, S,
+                      stride, pad, P, Q, out, ldo);
+  return launch_pdl(im2col_nhwc_kernel<long long>, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, R,
+                    S, stride, pad, P, Q, out, ldo);
 }
 
 cudaError_t launch_maxpool_nhwc(const __nv_bfloat16* x, int N, int H, int W, int C, int k, int stride, int pad,
-                                int P, int Q, __nv_bfloat16* out, cudaStream_t stream) {
+                                int P, int Q, __nv_bfloat16* out, uint32_t* argmax, cudaStream_t stream) {
+  if (argmax != nullptr && k * k > 15) return cudaErrorInvalidValue;
   const long long work = static_cast<long long>(N) * P * Q * (C / 8);
-  return launch_pdl(maxpool_nhwc_kernel, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, k, stride, pad,
-                    P, Q, out);
+  if (fits32(work))
+    return launch_pdl(maxpool_nhwc_kernel<int>, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, k,
+                      stride, pad, P, Q, out, argmax);
+  return launch_pdl(maxpool_nhwc_kernel<long long>, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, k,
+                    stride, pad, P, Q, out, argmax);
 }
 
 cudaError_t launch_avgpool_nhwc(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* out, long long ldo,
@@ -326,8 +470,11 @@ cudaError_t launch_col2im_nhwc(const __nv_bfloat16* dcol, long long ldc, int N, 
                                int stride, int pad, int P, int Q, const __nv_bfloat16* add,
                                const __nv_bfloat16* mask, __nv_bfloat16* dx, cudaStream_t stream) {
   const long long work = static_cast<long long>(N) * H * W * (C / 8);
-  return launch_pdl(col2im_nhwc_kernel, dim3(grid_for(work)), dim3(256), 0, stream, 1, dcol, ldc, N, H, W, C, R, S,
-                    stride, pad, P, Q, add, mask, dx);
+  if (fits32(work))
+    return launch_pdl(col2im_nhwc_kernel<int>, dim3(grid_for(work)), dim3(256), 0, stream, 1, dcol, ldc, N, H, W, C,
+                      R, S, stride, pad, P, Q, add, mask, dx);
+  return launch_pdl(col2im_nhwc_kernel<long long>, dim3(grid_for(work)), dim3(256), 0, stream, 1, dcol, ldc, N, H, W,
+                    C, R, S, stride, pad, P, Q, add, mask, dx);
 }
 
 cudaError_t launch_avgpool_bwd_nhwc(const __nv_bfloat16* df, long long ldf, int N, int HW, int C,
@@ -340,9 +487,22 @@ cudaError_t launch_avgpool_bwd_nhwc(const __nv_bfloat16* df, long long ldf, int 
 cudaError_t launch_maxpool_bwd_nhwc(const __nv_bfloat16* x, int N, int H, int W, int C, int k, int stride, int pad,
                                     int P, int Q, const __nv_bfloat16* dy, const __nv_bfloat16* mask,
                                     __nv_bfloat16* dx, cudaStream_t stream) {
-  const long long work = static_cast<long long>(N) * H * W * C;
+  if (k * k > 15) return cudaErrorInvalidValue;
+  const long long work = static_cast<long long>(N) * H * W * (C / 8);
   return launch_pdl(maxpool_bwd_nhwc_kernel, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, k, stride,
                     pad, P, Q, dy, mask, dx);
+}
+
+cudaError_t launch_maxpool_bwd_argmax_nhwc(const uint32_t* argmax, int N, int H, int W, int C, int k, int stride,
+                                           int pad, int P, int Q, const __nv_bfloat16* dy, const __nv_bfloat16* mask,
+                                           __nv_bfloat16* dx, cudaStream_t stream) {
+  if (k * k > 15) return cudaErrorInvalidValue;
+  const long long work = static_cast<long long>(N) * H * W * (C / 8);
+  if (fits32(work))
+    return launch_pdl(maxpool_bwd_argmax_nhwc_kernel<int>, dim3(grid_for(work)), dim3(256), 0, stream, 1, argmax, N,
+                      H, W, C, k, stride, pad, P, Q, dy, mask, dx);
+  return launch_pdl(maxpool_bwd_argmax_nhwc_kernel<long long>, dim3(grid_for(work)), dim3(256), 0, stream, 1, argmax,
+                    N, H, W, C, k, stride, pad, P, Q, dy, mask, dx);
 }
 
 }  // namespace edl

@@ -510,9 +510,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int num_m = (M + kBM - 1) / kBM;
   const int num_n = (N + BN - 1) / BN;
-  const int tiles = num_m * num_n;
-  const int nk = (K + kBK - 1) / kBK;
+  const int mn_tiles = num_m * num_n;
+  const int tiles = mn_tiles * ep.ksplit;
+  const int nk_all = (K + kBK - 1) / kBK;
+  const int kps = (nk_all + ep.ksplit - 1) / ep.ksplit;   // k-blocks per split
   const int rgroup = raster_group(num_m, M, K);
+  // work item t -> (split, output tile, k-block range)
+  auto decode = [&](int t, int& mt, int& nt, int& kb0, int& kb1) -> int {
+    const int split = t / mn_tiles;
+    tile_coords(t - split * mn_tiles, num_m, num_n, rgroup, mt, nt);
+    kb0 = split * kps;
+    kb1 = kb0 + kps < nk_all ? kb0 + kps : nk_all;
+    return split;
+  };
 
   // Dynamic tile scheduler: the producer claims tiles from a per-stream
   // global counter and publishes them to the MMA and epilogue roles through a
@@ -535,10 +545,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       tile_ring[slot] = t;
       mbar_arrive(&tile_full[slot]);
       if (t >= tiles) break;
-      int mt, nt;
-      tile_coords(t, num_m, num_n, rgroup, mt, nt);
+      int mt, nt, kb0, kb1;
+      decode(t, mt, nt, kb0, kb1);
       const int m0 = mt * kBM, n0 = nt * BN;
-      for (int kb = 0; kb < nk; ++kb, ++g) {
+      for (int kb = kb0; kb < kb1; ++kb, ++g) {
         const int s = g % S;
         mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
         load_kblock<BN, A_MN, B_MN>(&tmA, &tmB, sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes,
@@ -553,16 +563,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int t = tile_ring[slot];
       mbar_arrive(&tile_empty[slot]);
       if (t >= tiles) break;
+      int mt, nt, kb0, kb1;
+      decode(t, mt, nt, kb0, kb1);
       const uint32_t as = i & 1;
       mbar_wait(&tempty[as], ((i >> 1) & 1) ^ 1);
       tc_fence_after();
       const uint32_t d = tmem_base + as * BN;
-      for (int kb = 0; kb < nk; ++kb, ++g) {
+      for (int kb = kb0; kb < kb1; ++kb, ++g) {
         const int s = g % S;
         mbar_wait(&full[s], (g / S) & 1);
         tc_fence_after();
         mma_kblock<BN, A_MN, B_MN>(d, smem_u32(sA + s * Cfg::kABytes),
-                                   smem_u32(sB + s * Cfg::kBBytes), kb == 0);
+                                   smem_u32(sB + s * Cfg::kBBytes), kb == kb0);
         umma_commit(&empty[s]);
       }
       umma_commit(&tfull[as]);
@@ -577,20 +589,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tile_empty[slot]);
       if (t >= tiles) break;
-      int mt, nt;
-      tile_coords(t, num_m, num_n, rgroup, mt, nt);
+      int mt, nt, kb0, kb1;
+      const int split = decode(t, mt, nt, kb0, kb1);
       const int m0 = mt * kBM, n0 = nt * BN;
+      EpiArgs eps = ep;
+      if (split) eps.out = static_cast<float*>(ep.out) + split * ep.split_stride;
       float* sb = sbias;
-      stage_bias<BN, EPI>(ep, sb, n0, N, static_cast<int>(threadIdx.x) - 128);
+      stage_bias<BN, EPI>(eps, sb, n0, N, static_cast<int>(threadIdx.x) - 128);
       if constexpr (epi_has_bias<EPI>()) epi_bar_sync();
       const uint32_t as = i & 1;
       mbar_wait(&tfull[as], (i >> 1) & 1);
       tc_fence_after();
       if constexpr (epi_tma_store<EPI>())
-        epilogue_tile_tma<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e,
+        epilogue_tile_tma<BN, EPI>(eps, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e,
                                    lane, M, n0, N, epi_has_bias<EPI>() ? sb : nullptr, &tmY, stg + e * 8192, stores);
       else
-        epilogue_tile<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e + lane,
+        epilogue_tile<BN, EPI>(eps, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e + lane,
                                M, n0, N, epi_has_bias<EPI>() ? sb : nullptr);
       if constexpr (epi_has_bias<EPI>()) epi_bar_sync();   // every warp is done with the bias slice
       tc_fence_before();
@@ -1387,7 +1401,7 @@ static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, c
   auto kern = gemm_kernel<BN, A_MN, B_MN, EPI>;
   cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), GemmCfg<BN>::kSmem);
   if (e != cudaSuccess) return e;
-  const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
+  const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN) * ep.ksplit;
   const int grid = tiles < num_sms ? tiles : num_sms;
   return launch_pdl(kern, dim3(grid), dim3(kThreads), GemmCfg<BN>::kSmem, stream, 1, ta, tb, ty, M, N, K, ep);
 }

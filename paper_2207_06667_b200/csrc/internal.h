@@ -61,6 +61,10 @@ struct EpiArgs {
   float scale;
   unsigned* sched = nullptr;  // per-stream {next tile, CTAs done}; null -> static schedule
   __nv_bfloat16* out_bf16 = nullptr;  // EPI_SGD_F32: bf16 copy of `out` (same ld)
+  // split-K (gemm_kernel only): work item t = (split, tile); split s reduces
+  // k-blocks [s * kps, (s + 1) * kps) into out + s * split_stride
+  int ksplit = 1;
+  long long split_stride = 0;
 };
 
 struct HeadArgs {
@@ -117,7 +121,10 @@ cudaError_t launch_im2col_nhwc(const __nv_bfloat16* x, int N, int H, int W, int 
                                int stride, int pad, int P, int Q, __nv_bfloat16* out, long long ldo,
                                cudaStream_t stream);
 cudaError_t launch_maxpool_nhwc(const __nv_bfloat16* x, int N, int H, int W, int C, int k, int stride, int pad,
-                                int P, int Q, __nv_bfloat16* out, cudaStream_t stream);
+                                int P, int Q, __nv_bfloat16* out, uint32_t* argmax, cudaStream_t stream);
+cudaError_t launch_maxpool_bwd_argmax_nhwc(const uint32_t* argmax, int N, int H, int W, int C, int k, int stride,
+                                           int pad, int P, int Q, const __nv_bfloat16* dy, const __nv_bfloat16* mask,
+                                           __nv_bfloat16* dx, cudaStream_t stream);
 cudaError_t launch_avgpool_nhwc(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* out, long long ldo,
                                 cudaStream_t stream);
 cudaError_t launch_col2im_nhwc(const __nv_bfloat16* dcol, long long ldc, int N, int H, int W, int C, int R, int S,
@@ -158,6 +165,15 @@ struct ColsumGroup {
   int blk_start[kMaxGroup + 1];
 };
 cudaError_t launch_colsum_group(ColsumGroup g, cudaStream_t stream);
+// tall-skinny column sums (conv bias gradients): G = colsum_tall_blocks(M, sms)
+// blocks, workspace G * N floats; N % 8 == 0, N <= 2048 (colsum_tall_ok)
+int colsum_tall_blocks(int M, int sms);
+bool colsum_tall_ok(int N);
+cudaError_t launch_colsum_tall(const __nv_bfloat16* x, long long ld, int M, int N, float* partial, float* out,
+                               float scale, int sms, cudaStream_t stream);
+// split-K partial sums P[ksplit][GM][GN] -> out (transposed: out[GN][GM])
+cudaError_t launch_splitk_reduce(const float* P, int ksplit, long long sstride, int GM, int GN, bool transposed,
+                                 float* out, long long ldo, int sms, cudaStream_t stream);
 long long colsum_workspace_floats(int count, const int* M, const int* N);
 cudaError_t launch_topk_hits(const float* logits, long long ld, const int64_t* labels, int B,
                              int K, int k, unsigned* hits, cudaStream_t stream);

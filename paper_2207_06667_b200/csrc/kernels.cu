@@ -444,6 +444,151 @@ cudaError_t launch_colsum(const __nv_bfloat16* x, long long ld, int M, int N, fl
   return launch_colsum_group(g, stream);
 }
 
+// ------------------------------------------------------------------ tall column sums
+// Conv bias gradients: colsum over M = B*H*W rows (up to ~1.6M) of N <= 2048
+// columns. Block b owns rows [b * rpb, (b + 1) * rpb) of every column: thread
+// = (row lane, 8-column vector), four independent 16-byte loads in flight per
+// thread; row lanes combine through shared memory in a fixed order, and the
+// final pass sums the per-block partials in block order (deterministic).
+__global__ void __launch_bounds__(256) colsum_tall_partial_kernel(const __nv_bfloat16* __restrict__ x, long long ld,
+                                                                  int M, int N, int rpb, float* __restrict__ partial) {
+  griddep_wait();
+  __shared__ float red[256 * 8];
+  const int cv = N / 8;
+  const int rpp = blockDim.x / cv;        // rows in flight per pass
+  const int rl = threadIdx.x / cv, c8 = threadIdx.x % cv;
+  const int r0 = blockIdx.x * rpb;
+  const int r1 = r0 + rpb < M ? r0 + rpb : M;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  auto add = [&](const uint4& q) {
+    const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&q);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(h[j]);
+  };
+  if (rl < rpp) {
+    const __nv_bfloat16* base = x + 8 * c8;
+    int r = r0 + rl;
+    for (; r + 3 * rpp < r1; r += 4 * rpp) {
+      uint4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        q[u] = __ldg(reinterpret_cast<const uint4*>(base + static_cast<long long>(r + u * rpp) * ld));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) add(q[u]);
+    }
+    for (; r < r1; r += rpp) add(__ldg(reinterpret_cast<const uint4*>(base + static_cast<long long>(r) * ld)));
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) red[threadIdx.x * 8 + j] = acc[j];
+  __syncthreads();
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    float s = 0.f;
+    for (int q = 0; q < rpp; ++q) s += red[(q * cv + n / 8) * 8 + n % 8];
+    partial[static_cast<long long>(blockIdx.x) * N + n] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) colsum_tall_final_kernel(const float* __restrict__ partial, int G, int N,
+                                                                float* __restrict__ out, float scale) {
+  griddep_wait();
+  __shared__ float red[8][32];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int n = blockIdx.x * 32 + lane;
+  float s = 0.f;
+  if (n < N)
+    for (int b = warp; b < G; b += 8) s += __ldcg(partial + static_cast<long long>(b) * N + n);
+  red[warp][lane] = s;
+  __syncthreads();
+  if (warp != 0 || n >= N) return;
+#pragma unroll
+  for (int w = 1; w < 8; ++w) s += red[w][lane];
+  out[n] = s * scale;
+}
+
+int colsum_tall_blocks(int M, int sms) {
+  const int g = 2 * sms;
+  const int by_rows = (M + 255) / 256;    // at least 256 rows per block
+  return by_rows < g ? (by_rows < 1 ? 1 : by_rows) : g;
+}
+
+bool colsum_tall_ok(int N) { return N % 8 == 0 && N >= 8 && N <= 2048; }
+
+cudaError_t launch_colsum_tall(const __nv_bfloat16* x, long long ld, int M, int N, float* partial, float* out,
+                               float scale, int sms, cudaStream_t stream) {
+  const int G = colsum_tall_blocks(M, sms);
+  const int rpb = (M + G - 1) / G;
+  cudaError_t e = launch_pdl(colsum_tall_partial_kernel, dim3(G), dim3(256), 0, stream, 1, x, ld, M, N, rpb, partial);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(colsum_tall_final_kernel, dim3((N + 31) / 32), dim3(256), 0, stream, 1,
+                    static_cast<const float*>(partial), G, N, out, scale);
+}
+
+// ------------------------------------------------------------------ split-K reduce
+// out = sum over s of P[s] (fixed order). P[s] is [GM][GN] fp32; transposed:
+// out[r][c] = sum_s P[s][c][r] (the swapped-operand weight gradient, GEMM M =
+// kdim, N = cout, back to the [cout][kdim] layout) through a 32 x 33 smem tile.
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ P, int ksplit,
+                                                            long long sstride, int GM, int GN,
+                                                            float* __restrict__ out, long long ldo) {
+  griddep_wait();
+  const long long total = static_cast<long long>(GM) * GN;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float a[4] = {0.f, 0.f, 0.f, 0.f};
+    int s = 0;
+    for (; s + 3 < ksplit; s += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] += __ldcg(P + (s + u) * sstride + i);
+    }
+    for (; s < ksplit; ++s) a[0] += __ldcg(P + s * sstride + i);
+    const int r = static_cast<int>(i / GN), c = static_cast<int>(i % GN);
+    out[r * ldo + c] = (a[0] + a[1]) + (a[2] + a[3]);
+  }
+}
+
+__global__ void __launch_bounds__(256) splitk_reduce_t_kernel(const float* __restrict__ P, int ksplit,
+                                                              long long sstride, int GM, int GN,
+                                                              float* __restrict__ out, long long ldo) {
+  griddep_wait();
+  __shared__ float tile[32][33];
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  const int r0 = blockIdx.x * 32;       // output rows = GEMM columns (GN)
+  const int c0 = blockIdx.y * 32;       // output cols = GEMM rows (GM)
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = c0 + ty + 8 * j, r = r0 + tx;
+    float a[4] = {0.f, 0.f, 0.f, 0.f};
+    if (c < GM && r < GN) {
+      const float* src = P + static_cast<long long>(c) * GN + r;
+      int s = 0;
+      for (; s + 3 < ksplit; s += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a[u] += __ldcg(src + (s + u) * sstride);
+      }
+      for (; s < ksplit; ++s) a[0] += __ldcg(src + s * sstride);
+    }
+    tile[ty + 8 * j][tx] = (a[0] + a[1]) + (a[2] + a[3]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int r = r0 + ty + 8 * j, c = c0 + tx;
+    if (r < GN && c < GM) out[r * ldo + c] = tile[tx][ty + 8 * j];
+  }
+}
+
+cudaError_t launch_splitk_reduce(const float* P, int ksplit, long long sstride, int GM, int GN, bool transposed,
+                                 float* out, long long ldo, int sms, cudaStream_t stream) {
+  if (transposed)
+    return launch_pdl(splitk_reduce_t_kernel, dim3((GN + 31) / 32, (GM + 31) / 32), dim3(256), 0, stream, 1, P,
+                      ksplit, sstride, GM, GN, out, ldo);
+  const long long total = static_cast<long long>(GM) * GN;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 16LL * sms) blocks = 16LL * sms;
+  return launch_pdl(splitk_reduce_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, stream, 1, P, ksplit,
+                    sstride, GM, GN, out, ldo);
+}
+
 // ------------------------------------------------------------------ top-k accuracy
 __global__ void topk_hits_kernel(const float* __restrict__ z, long long ld,
                                  const int64_t* __restrict__ labels, int B, int K, int k,

@@ -365,6 +365,7 @@ class ResNetStudent:
         ph, pw = (h + 2 - 3) // 2 + 1, (w + 2 - 3) // 2 + 1
         self.pool_hw = (ph, pw)
         self.x1 = torch.empty(B, ph, pw, stem.cout_p, dtype=torch.bfloat16, device=dev)
+        self.pool_arg = torch.empty(B * ph * pw * stem.cout_p // 8, dtype=torch.int32, device=dev)
         col = B * h * w * stem.kdim
         self.acts, hw = [], (ph, pw)                        # per block: (in_hw, h1, sc, y)
         for i1, i2, isc in self.block_idx:
@@ -377,6 +378,23 @@ class ResNetStudent:
             self.acts.append((hw, h1, sc, y))
             hw = (oh, ow)
         self.final_hw = hw
+        # every im2col conv keeps its forward column matrix for its weight
+        # gradient (a few GB at batch 128 against 180 GB of HBM: the backward
+        # never re-gathers); self.col is the data-gradient scratch
+        self.in_hw = [(H, H)] + [None] * (len(self.convs) - 1)
+        for (i1, i2, isc), (hw_in, _, _, _) in zip(self.block_idx, self.acts):
+            self.in_hw[i1] = hw_in
+            self.in_hw[i2] = self.convs[i1].out_hw(*hw_in)
+            if isc is not None:
+                self.in_hw[isc] = hw_in
+        self.cols, ws = [], 0
+        for i, c in enumerate(self.convs):
+            oh, ow = c.out_hw(*self.in_hw[i])
+            M = B * oh * ow
+            self.cols.append(None if (c.k == 1 and c.stride == 1) else
+                             torch.empty(M, c.kdim, dtype=torch.bfloat16, device=dev))
+            ws = max(ws, int(_lib.load().edl_bwd_weight_workspace_floats(M, c.cout_p, c.kdim)))
+        self.wgrad_ws = torch.empty(max(ws, 1), dtype=torch.float32, device=dev)
         self.col = torch.empty(col, dtype=torch.bfloat16, device=dev)
         # backward buffers: gradient ping-pong at the largest activation size + a shortcut buffer
         big = max(B * h * w * stem.cout_p, max(a[1].numel() for a in self.acts))
@@ -389,9 +407,8 @@ class ResNetStudent:
         self.loss = torch.zeros(1, dtype=torch.float32, device=dev)
         self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
-        ws = _lib.load().edl_colsum_workspace_floats(B * h * w, max(c.cout_p for c in self.convs))
-        self.colsum_ws = torch.empty(max(int(ws), _lib.load().edl_colsum_workspace_floats(B, self.classes_p), 1),
-                                     dtype=torch.float32, device=dev)
+        self.colsum_ws = torch.empty(max(int(_lib.load().edl_colsum_workspace_floats(B, self.classes_p)), 1),
+                                     dtype=torch.float32, device=dev)   # the head's db
 
     # views
     def _w16(self, p):
@@ -406,17 +423,18 @@ class ResNetStudent:
     def _gb(self, p):
         return self.grads[p.off_b:p.off_b + p.rows]
 
-    def _im2col(self, c, x, hw, s):
+    def _im2col(self, i, x, hw, s):
+        c = self.convs[i]
         if c.k == 1 and c.stride == 1:
             return x, c.cin_p
         _lib.call("edl_im2col_nhwc", x.data_ptr(), self.B, hw[0], hw[1], c.cin_p, c.cin if c.packed else c.cin_p,
-                  c.k, c.k, c.stride, c.pad, self.col.data_ptr(), c.kdim, s)
-        return self.col, c.kdim
+                  c.k, c.k, c.stride, c.pad, self.cols[i].data_ptr(), c.kdim, s)
+        return self.cols[i], c.kdim
 
     def _fwd(self, i, x, hw, out, residual, s):
         c, p = self.convs[i], self.params[i]
         oh, ow = c.out_hw(*hw)
-        a, lda = self._im2col(c, x, hw, s)
+        a, lda = self._im2col(i, x, hw, s)
         M = self.B * oh * ow
         if residual is not None:
             _lib.call("edl_linear_fwd_residual", a.data_ptr(), lda, self._w16(p).data_ptr(), c.kdim,
@@ -430,8 +448,8 @@ class ResNetStudent:
     def forward(self, x, s):
         self._fwd(0, x, (self.cfg.image, self.cfg.image), self.y0, None, s)
         h, w = self.stem_hw
-        _lib.call("edl_maxpool_nhwc", self.y0.data_ptr(), self.B, h, w, self.y0.shape[-1], 3, 2, 1,
-                  self.x1.data_ptr(), s)
+        _lib.call("edl_maxpool_argmax_nhwc", self.y0.data_ptr(), self.B, h, w, self.y0.shape[-1], 3, 2, 1,
+                  self.x1.data_ptr(), self.pool_arg.data_ptr(), s)
         cur = self.x1
         for (i1, i2, isc), (hw, h1, sc, y) in zip(self.block_idx, self.acts):
             shortcut = cur
@@ -449,13 +467,16 @@ class ResNetStudent:
                   self.feat_p, _lib.EDL_ACT_NONE, s)
 
     def _wgrad(self, i, dz, x, hw, s):
-        """dW_i = dz^T im2col(x), db_i = colsum(dz) (fp32, into the flat gradient)."""
+        """dW_i = dz^T im2col(x), db_i = colsum(dz) (fp32, into the flat gradient);
+        im2col(x) is the forward's kept column matrix. Split-K tcgen05 GEMM
+        (edl_linear_bwd_weight_ws): the reduction runs over all B*H*W pixels."""
         c, p = self.convs[i], self.params[i]
         oh, ow = c.out_hw(*hw)
-        a, lda = self._im2col(c, x, hw, s)
+        a, lda = (x, c.cin_p) if self.cols[i] is None else (self.cols[i], c.kdim)
         M = self.B * oh * ow
-        _lib.call("edl_linear_bwd_weight", dz.data_ptr(), c.cout_p, a.data_ptr(), lda, self._gw(p).data_ptr(), c.kdim,
-                  self._gb(p).data_ptr(), self.colsum_ws.data_ptr(), M, c.cout_p, c.kdim, 1.0, s)
+        _lib.call("edl_linear_bwd_weight_ws", dz.data_ptr(), c.cout_p, a.data_ptr(), lda, self._gw(p).data_ptr(),
+                  c.kdim, self._gb(p).data_ptr(), self.wgrad_ws.data_ptr(), self.wgrad_ws.numel(), M, c.cout_p,
+                  c.kdim, 1.0, s)
 
     def _dgrad(self, i, dz, hw, out, add, mask, s):
         """out = col2im(dz W_i) (+ add) (* mask > 0): the gradient w.r.t. conv i's input."""
@@ -523,8 +544,8 @@ class ResNetStudent:
         # maxpool + stem ReLU, then the stem's weight gradient (the images need no gradient)
         h, w = self.stem_hw
         dy0 = self.g[(cur + 1) % 3][:self.y0.numel()].view_as(self.y0)
-        _lib.call("edl_maxpool_bwd_nhwc", self.y0.data_ptr(), B, h, w, self.y0.shape[-1], 3, 2, 1, dz.data_ptr(),
-                  self.y0.data_ptr(), dy0.data_ptr(), s)
+        _lib.call("edl_maxpool_bwd_argmax_nhwc", self.pool_arg.data_ptr(), B, h, w, self.y0.shape[-1], 3, 2, 1,
+                  dz.data_ptr(), self.y0.data_ptr(), dy0.data_ptr(), s)
         self._wgrad(0, dy0, x, (self.cfg.image, self.cfg.image), s)
         _lib.call("edl_sgd_step", self.flat.data_ptr(), self.flat_bf16.data_ptr(), self.grads.data_ptr(), self.size,
                   float(eta), s)

@@ -202,3 +202,74 @@ def test_resnet_student_sgd_updates_flat_master():
     torch.testing.assert_close(student.flat, p0 - 0.1 * student.grads, rtol=1e-6, atol=1e-6)
     assert torch.equal(student.flat_bf16, student.flat.to(torch.bfloat16))
     assert student.grads.abs().sum().item() > 0
+
+
+@pytest.mark.parametrize("M,N,K,ld_pad,ws_scale", [
+    (401408, 64, 576, 0, 1.0),      # stage-1 3x3 conv at batch 128: swapped operands, deep split
+    (200704, 64, 160, 0, 1.0),      # the packed stem (K = 147 padded to 160)
+    (6272, 512, 4608, 0, 1.0),      # stage-4 3x3 conv: many tiles, shallow split
+    (25088, 256, 128, 16, 1.0),     # 1x1 projection, padded leading dimensions
+    (50000, 64, 576, 0, 0.05),      # a starved workspace narrows the split (still exact)
+    (777, 48, 40, 0, 1.0),          # ragged: M, N, K not tile multiples
+])
+def test_bwd_weight_splitk_vs_torch(M, N, K, ld_pad, ws_scale):
+    """edl_linear_bwd_weight_ws (split-K tcgen05 partials + fixed-order reduce,
+    tall column sums): dW = dY^T X and db = colsum(dY) against torch in fp32
+    from the same bf16 operands; fp32 accumulation order only: <= 2e-3
+    relative to the max, and bitwise identical across two runs."""
+    from paper_2207_06667_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    dy = torch.randn(M, N + ld_pad, device="cuda", generator=g).to(torch.bfloat16)
+    x = torch.randn(M, K + ld_pad, device="cuda", generator=g).to(torch.bfloat16)
+    lib = _lib.load()
+    need = int(lib.edl_bwd_weight_workspace_floats(M, N, K))
+    assert need > 0
+    # a starved workspace still holds the tall column sum's partials (2 x SMs x N floats)
+    floats = need if ws_scale >= 1 else max(int(need * ws_scale), 2 * 148 * N)
+    ws = torch.empty(need, device="cuda")
+    outs = []
+    for _ in range(2):
+        dw = torch.full((N, K + ld_pad), float("nan"), device="cuda")
+        db = torch.empty(N, device="cuda")
+        _lib.call("edl_linear_bwd_weight_ws", dy.data_ptr(), dy.stride(0), x.data_ptr(), x.stride(0), dw.data_ptr(),
+                  dw.stride(0), db.data_ptr(), ws.data_ptr(), floats, M, N, K, 0.5,
+                  _s())
+        outs.append((dw[:, :K].clone(), db.clone()))
+    torch.cuda.synchronize()
+    want_w = 0.5 * dy[:, :N].float().T @ x[:, :K].float()
+    want_b = 0.5 * dy[:, :N].float().sum(0)
+    assert _rel(outs[0][0], want_w) < 2e-3
+    assert _rel(outs[0][1], want_b) < 2e-3
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+def test_maxpool_bwd_vs_torch_with_ties():
+    """edl_maxpool_bwd_nhwc (3x3 / 2 / pad 1, the stem pool) against torch
+    autograd, on integer-valued inputs so windows have tied maxima: the
+    gradient goes to the first maximum in scan order, as torch's does."""
+    import torch.nn.functional as F
+
+    from paper_2207_06667_b200 import _lib
+    from paper_2207_06667_b200.resnet import to_nhwc
+    rng = np.random.default_rng(3)
+    x = rng.integers(-3, 4, size=(3, 16, 17, 17)).astype(np.float32)
+    gy = rng.normal(size=(3, 16, 9, 9)).astype(np.float32)
+    xt = torch.from_numpy(x).requires_grad_(True)
+    F.max_pool2d(xt, 3, 2, 1).backward(ref._bf(torch.from_numpy(gy)))
+    xd, dyd = to_nhwc(x, "cuda"), to_nhwc(gy, "cuda")
+    dx = torch.empty_like(xd)
+    _lib.call("edl_maxpool_bwd_nhwc", xd.data_ptr(), 3, 17, 17, 16, 3, 2, 1, dyd.data_ptr(), None, dx.data_ptr(), _s())
+    # the training pair: forward records the argmax words, backward gathers from them
+    y_plain = torch.empty(3, 9, 9, 16, dtype=torch.bfloat16, device="cuda")
+    y_arg = torch.empty_like(y_plain)
+    arg = torch.empty(3 * 9 * 9 * 2, dtype=torch.int32, device="cuda")
+    _lib.call("edl_maxpool_nhwc", xd.data_ptr(), 3, 17, 17, 16, 3, 2, 1, y_plain.data_ptr(), _s())
+    _lib.call("edl_maxpool_argmax_nhwc", xd.data_ptr(), 3, 17, 17, 16, 3, 2, 1, y_arg.data_ptr(), arg.data_ptr(), _s())
+    dx2 = torch.empty_like(xd)
+    _lib.call("edl_maxpool_bwd_argmax_nhwc", arg.data_ptr(), 3, 17, 17, 16, 3, 2, 1, dyd.data_ptr(), None,
+              dx2.data_ptr(), _s())
+    torch.cuda.synchronize()
+    got = dx.float().cpu().permute(0, 3, 1, 2)
+    torch.testing.assert_close(got, ref._bf(xt.grad), rtol=1e-2, atol=1e-2)
+    assert torch.equal(y_arg, y_plain)
+    assert torch.equal(dx2, dx)
