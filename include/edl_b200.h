@@ -82,6 +82,17 @@ int edl_maxpool_nhwc(const void* x, int N, int H, int W, int C, int k, int strid
 /* Global average pool: out[n][c] = mean over H*W of x[n][.][.][c] (bf16). */
 int edl_avgpool_nhwc(const void* x, int N, int HW, int C, void* out, long long ldo, void* stream);
 
+/* Implicit-GEMM convolution (cfg4), NHWC bf16 with
+ * C % 64 == 0: y[n][p][q][k] = act(sum over (r, s, c) of
+ * x[n][p*stride-pad+r][q*stride-pad+s][c] * w[k][(r*S+s)*C+c] + bias[k]
+ * (+ residual[(n,p,q)][k])). The tcgen05 GEMM's producer loads its A tiles
+ * straight from x with TMA im2col loads (one filter tap x 64 channels per
+ * k-block): no column matrix in HBM. act: EDL_ACT_RELU or EDL_ACT_IDENT;
+ * residual (optional) needs EDL_ACT_RELU. y: [N*P*Q][ldy], TMA-stored. */
+int edl_conv_fwd_nhwc(const void* x, int N, int H, int W, int C, const void* w, long long ldw, const float* bias,
+                      int K, int R, int S, int stride, int pad, const void* residual, long long ldr, void* y,
+                      long long ldy, int act, void* stream);
+
 /* cfg4 student backward (BN-free ResNet-18-style): the data gradient of a
  * convolution is edl_linear_bwd_data with H = NULL (dcol = dZ W, no tanh
  * factor) followed by this gather:

@@ -33,6 +33,8 @@ _SIGNATURES = {
                        c_int, c_int, c_void_p],
     "edl_linear_fwd_residual": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_void_p, c_ll, c_void_p, c_ll, c_int,
                                 c_int, c_int, c_void_p],
+    "edl_conv_fwd_nhwc": [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_ll, c_void_p, c_int, c_int, c_int, c_int,
+                          c_int, c_void_p, c_ll, c_void_p, c_ll, c_int, c_void_p],
     "edl_im2col_nhwc": [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_ll,
                         c_void_p],
     "edl_maxpool_nhwc": [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p],

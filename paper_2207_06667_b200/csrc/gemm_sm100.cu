@@ -65,6 +65,37 @@ __device__ __forceinline__ void load_kblock(const CUtensorMap* tmA, const CUtens
   }
 }
 
+// Implicit-GEMM convolution: the output tile's first pixel m0 -> its window
+// corner (wb, hb) in image nb; k-block kb -> filter tap (r, s) and 64-channel
+// block cb (K = (r, s, c), c fastest, C a multiple of 64).
+struct ConvTile {
+  int wb, hb, nb;
+};
+__device__ __forceinline__ ConvTile conv_tile(const ConvGeom& cv, int m0) {
+  const int pq = cv.P * cv.Q;
+  const int nb = m0 / pq, rem = m0 - nb * pq;
+  const int p = rem / cv.Q, q = rem - p * cv.Q;
+  return ConvTile{q * cv.stride - cv.pad, p * cv.stride - cv.pad, nb};
+}
+__device__ __forceinline__ void conv_tap(const ConvGeom& cv, int kb, int& cb, int& r, int& s) {
+  const int rs = kb / cv.cblocks;
+  cb = kb - rs * cv.cblocks;
+  r = rs / cv.S;
+  s = rs - r * cv.S;
+}
+
+template <int BN>
+__device__ __forceinline__ void load_kblock_conv(const CUtensorMap* tmA, const CUtensorMap* tmB, uint8_t* sa,
+                                                 uint8_t* sb, uint64_t* bar, const ConvGeom& cv, const ConvTile& ct,
+                                                 int n0, int kb, uint64_t pb) {
+  mbar_arrive_expect_tx(bar, GemmCfg<BN>::kStageBytes);
+  int cb, r, s;
+  conv_tap(cv, kb, cb, r, s);
+  tma_load_im2col_4d(sa, tmA, bar, cb * 64, ct.wb, ct.hb, ct.nb, static_cast<uint16_t>(s),
+                     static_cast<uint16_t>(r));
+  tma_load_2d_hint(sb, tmB, bar, kb * kBK, n0, pb);
+}
+
 // L2 policy per operand. Measured on B200 (profiles/): evict_last on the
 // re-read activations + evict_first on the streamed weights RAISED teacher
 // layer-2 DRAM reads (619 -> 683 MB/launch) and lowered tensor-pipe activity,
@@ -548,6 +579,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       int mt, nt, kb0, kb1;
       decode(t, mt, nt, kb0, kb1);
       const int m0 = mt * kBM, n0 = nt * BN;
+      if constexpr (!A_MN && !B_MN) {
+        if (ep.conv.Q > 0) {   // implicit-GEMM convolution: A tiles from the im2col map
+          const ConvTile ct = conv_tile(ep.conv, m0);
+          for (int kb = kb0; kb < kb1; ++kb, ++g) {
+            const int s = g % S;
+            mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
+            load_kblock_conv<BN>(&tmA, &tmB, sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes, &full[s], ep.conv, ct,
+                                 n0, kb, pb);
+          }
+          continue;
+        }
+      }
       for (int kb = kb0; kb < kb1; ++kb, ++g) {
         const int s = g % S;
         mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
@@ -772,6 +815,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       tile_coords(t, num_m, num_n, rgroup, mt, nt);
       const int m0 = mt * 2 * kBM + static_cast<int>(rank) * kBM;
       const int n0 = nt * BN + static_cast<int>(rank) * Cfg::kHalfN;
+      if constexpr (!A_MN && !B_MN) {
+        if (ep.conv.Q > 0) {   // implicit-GEMM convolution: this CTA's 128 A rows from the im2col map
+          const ConvTile ct = conv_tile(ep.conv, m0);
+          for (int kb = 0; kb < nk; ++kb, ++g) {
+            const int s = g % S;
+            mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
+            if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * Cfg::kStageBytes);
+            int cb, r, fs;
+            conv_tap(ep.conv, kb, cb, r, fs);
+            tma_load_im2col_4d_pair(sA + s * Cfg::kABytes, &tmA, full0 + 8 * s, cb * 64, ct.wb, ct.hb, ct.nb,
+                                    static_cast<uint16_t>(fs), static_cast<uint16_t>(r));
+            tma_load_2d_pair(sB + s * Cfg::kBBytes, &tmB, full0 + 8 * s, kb * kBK, n0);
+          }
+          continue;
+        }
+      }
       for (int kb = 0; kb < nk; ++kb, ++g) {
         const int s = g % S;
         mbar_wait(&empty[s], ((g / S) & 1) ^ 1);

@@ -52,6 +52,15 @@ enum EpiMode : int {
   EPI_BIAS_BF16 = 6,   // out(bf16) = acc + bias (cfg4 shortcut projections)
 };
 
+// Implicit-GEMM convolution geometry (A = im2col of an NHWC tensor through a
+// TMA im2col map; K index = (r, s, c) with 64-channel blocks). Q == 0: plain GEMM.
+struct ConvGeom {
+  int P = 0, Q = 0;       // output rows / cols per image
+  int stride = 1, pad = 0;
+  int S = 1;              // filter width (taps per filter row)
+  int cblocks = 1;        // C / 64
+};
+
 struct EpiArgs {
   void* out;
   long long ld_out;
@@ -65,6 +74,7 @@ struct EpiArgs {
   // k-blocks [s * kps, (s + 1) * kps) into out + s * split_stride
   int ksplit = 1;
   long long split_stride = 0;
+  ConvGeom conv;          // A operand from an im2col map (gemm_kernel / gemm_pair_kernel, K-major A)
 };
 
 struct HeadArgs {

@@ -125,6 +125,19 @@ class _DevConv:
         return (h + 2 * self.pad - self.k) // self.stride + 1, (w + 2 * self.pad - self.k) // self.stride + 1
 
     @property
+    def implicit(self) -> bool:
+        """Implicit GEMM (edl_conv_fwd_nhwc: TMA im2col loads, no column
+        matrix) for every windowed conv on >= 64-channel inputs; the packed
+        RGB stem keeps its explicit im2col, 1x1 / stride-1 convs are plain GEMMs."""
+        return not self.packed and self.cin_p % 64 == 0 and not (self.k == 1 and self.stride == 1)
+
+    def fwd_implicit(self, x, n, h, w, out, residual, s):
+        act = _lib.EDL_ACT_RELU if (self.relu or residual is not None) else _lib.EDL_ACT_IDENT
+        _lib.call("edl_conv_fwd_nhwc", x.data_ptr(), n, h, w, self.cin_p, self.w.data_ptr(), self.kdim,
+                  self.b.data_ptr(), self.cout_p, self.k, self.k, self.stride, self.pad,
+                  None if residual is None else residual.data_ptr(), self.cout_p, out.data_ptr(), self.cout_p, act, s)
+
+    @property
     def kdim(self):
         return self._kdim
 
@@ -164,13 +177,13 @@ class ResNetTeacher:
             outs = []
             for c in convs:
                 oh, ow = c.out_hw(bh, bw)
-                col = max(col, B * oh * ow * c.kdim if (c.k > 1 or c.stride > 1) else 0)
+                col = max(col, B * oh * ow * c.kdim if ((c.k > 1 or c.stride > 1) and not c.implicit) else 0)
                 outs.append(torch.empty(B, oh, ow, c.cout_p, dtype=torch.bfloat16, device=dev))
                 bh, bw = oh, ow
             sc_out = None
             if sc is not None:
                 oh, ow = sc.out_hw(h, w)
-                col = max(col, B * oh * ow * sc.kdim if sc.stride > 1 else 0)
+                col = max(col, B * oh * ow * sc.kdim if (sc.stride > 1 and not sc.implicit) else 0)
                 sc_out = torch.empty(B, oh, ow, sc.cout_p, dtype=torch.bfloat16, device=dev)
             self.buffers.append((outs, sc_out, h, w))
             h, w = bh, bw
@@ -182,6 +195,9 @@ class ResNetTeacher:
     def _conv(self, c: _DevConv, x, h, w, out, residual, s):
         oh, ow = c.out_hw(h, w)
         M = self.B * oh * ow
+        if c.implicit:
+            c.fwd_implicit(x, self.B, h, w, out, residual, s)
+            return oh, ow
         if c.k == 1 and c.stride == 1:
             a, lda = x, c.cin_p                            # NHWC already is the GEMM's A
         else:

@@ -273,3 +273,55 @@ def test_maxpool_bwd_vs_torch_with_ties():
     torch.testing.assert_close(got, ref._bf(xt.grad), rtol=1e-2, atol=1e-2)
     assert torch.equal(y_arg, y_plain)
     assert torch.equal(dx2, dx)
+
+
+@pytest.mark.parametrize("N,C,H,K,k,stride,relu,residual", [
+    (2, 64, 14, 64, 3, 1, True, False),
+    (1, 64, 8, 64, 3, 1, True, False),          # < 128 KB input: the im2col descriptor workaround
+    (2, 64, 15, 128, 3, 2, True, False),        # stride 2, odd size
+    (3, 128, 9, 256, 1, 2, False, False),       # 1x1 stride-2 projection
+    (2, 128, 12, 128, 3, 1, True, True),        # residual + ReLU
+    (4, 256, 7, 512, 3, 1, True, False),
+    (64, 64, 56, 64, 3, 1, True, True),         # a ResNet stage-1 layer at batch 64 (pair tiles)
+])
+def test_conv_fwd_implicit_vs_torch_and_explicit(N, C, H, K, k, stride, relu, residual):
+    """edl_conv_fwd_nhwc (TMA im2col loads, no column matrix) against
+    torch conv2d (bf16 operands, fp32 math; <= 1e-2 of the max) and against
+    the explicit im2col + GEMM path: same K order, same tiles, so the two are
+    bitwise identical."""
+    from paper_2207_06667_b200 import _lib
+    from paper_2207_06667_b200.resnet import HostConv, _DevConv, to_nhwc
+    rng = np.random.default_rng(C * 7 + K + H)
+    hc = HostConv((rng.normal(0, np.sqrt(2.0 / (C * k * k)), size=(K, C, k, k))).astype(np.float32),
+                  rng.normal(0, 0.1, size=K).astype(np.float32), stride, k // 2, relu)
+    dc = _DevConv(hc, "cuda")
+    imgs = rng.normal(size=(N, C, H, H)).astype(np.float32)
+    x = to_nhwc(imgs, "cuda")
+    oh, ow = dc.out_hw(H, H)
+    M = N * oh * ow
+    act = _lib.EDL_ACT_RELU if (relu or residual) else _lib.EDL_ACT_IDENT
+    res_t, rd = None, None
+    if residual:
+        r = rng.normal(size=(N, K, oh, ow)).astype(np.float32)
+        res_t = ref._bf(torch.from_numpy(r))
+        rd = to_nhwc(r, "cuda")
+    y = torch.empty(N, oh, ow, dc.cout_p, dtype=torch.bfloat16, device="cuda")
+    _lib.call("edl_conv_fwd_nhwc", x.data_ptr(), N, H, H, dc.cin_p, dc.w.data_ptr(), dc.kdim, dc.b.data_ptr(),
+              dc.cout_p, k, k, stride, dc.pad, None if rd is None else rd.data_ptr(), dc.cout_p, y.data_ptr(),
+              dc.cout_p, act, _s())
+    # explicit path
+    col = torch.empty(M, dc.kdim, dtype=torch.bfloat16, device="cuda")
+    _lib.call("edl_im2col_nhwc", x.data_ptr(), N, H, H, dc.cin_p, dc.cin_p, k, k, stride, dc.pad, col.data_ptr(),
+              dc.kdim, _s())
+    y2 = torch.empty_like(y)
+    if residual:
+        _lib.call("edl_linear_fwd_residual", col.data_ptr(), dc.kdim, dc.w.data_ptr(), dc.kdim, dc.b.data_ptr(),
+                  rd.data_ptr(), dc.cout_p, y2.data_ptr(), dc.cout_p, M, dc.cout_p, dc.kdim, _s())
+    else:
+        _lib.call("edl_linear_fwd", col.data_ptr(), dc.kdim, dc.w.data_ptr(), dc.kdim, dc.b.data_ptr(), y2.data_ptr(),
+                  dc.cout_p, M, dc.cout_p, dc.kdim, act, _s())
+    torch.cuda.synchronize()
+    want = ref._conv(ref._bf(torch.from_numpy(imgs)), hc, res_t)
+    got = y[..., :K].float().cpu().permute(0, 3, 1, 2)
+    assert _rel(got, want) < 1e-2
+    assert torch.equal(y, y2)
