@@ -93,6 +93,26 @@ int edl_conv_fwd_nhwc(const void* x, int N, int H, int W, int C, const void* w, 
                       int K, int R, int S, int stride, int pad, const void* residual, long long ldr, void* y,
                       long long ldy, int act, void* stream);
 
+/* Its weight gradient: dW[k][(r,s,c)] = scale * sum over output pixels of
+ * dY[(n,p,q)][k] * x[n][p*stride-pad+r][q*stride-pad+s][c] (+ db = scale *
+ * colsum dY), the split-K plan of edl_linear_bwd_weight_ws with the im2col
+ * operand read through a TMA im2col map (64 pixels x 64 channels per box).
+ * workspace: edl_bwd_weight_workspace_floats(N*P*Q, K, R*S*C) floats. */
+int edl_conv_bwd_weight_nhwc(const void* x, int N, int H, int W, int C, int R, int S, int stride, int pad,
+                             const void* dY, long long lddy, int K, float* dW, long long lddw, float* db,
+                             float* workspace, long long workspace_floats, float scale, void* stream);
+
+/* Data gradient of a stride-1 convolution as an implicit-GEMM convolution of
+ * dZ [N][P][Q][K] (K % 64 == 0) with the flipped filter (edl_conv_flip_weights:
+ * wf [C][(r, s, k)] from w [K][(r, s, c)]) at padding R-1-pad:
+ *   dx[n][h][w][c] = (sum ... [+ add]) * (mask > 0 if mask)     (bf16, [N][H][W][C])
+ * add: the residual branch's gradient; mask: the layer input's stored ReLU
+ * output. Replaces edl_linear_bwd_data + edl_col2im_nhwc for stride 1. */
+int edl_conv_flip_weights(const void* w, long long ldw, int K, int C, int R, int S, void* wf, long long ldf,
+                          void* stream);
+int edl_conv_dgrad_nhwc(const void* dz, int N, int P, int Q, int K, const void* wf, long long ldf, int C, int R,
+                        int S, int pad, const void* add, const void* mask, void* dx, void* stream);
+
 /* cfg4 student backward (BN-free ResNet-18-style): the data gradient of a
  * convolution is edl_linear_bwd_data with H = NULL (dcol = dZ W, no tanh
  * factor) followed by this gather:

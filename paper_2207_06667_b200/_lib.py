@@ -35,6 +35,11 @@ _SIGNATURES = {
                                 c_int, c_int, c_void_p],
     "edl_conv_fwd_nhwc": [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_ll, c_void_p, c_int, c_int, c_int, c_int,
                           c_int, c_void_p, c_ll, c_void_p, c_ll, c_int, c_void_p],
+    "edl_conv_bwd_weight_nhwc": [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_ll,
+                                 c_int, c_void_p, c_ll, c_void_p, c_void_p, c_ll, c_float, c_void_p],
+    "edl_conv_flip_weights": [c_void_p, c_ll, c_int, c_int, c_int, c_int, c_void_p, c_ll, c_void_p],
+    "edl_conv_dgrad_nhwc": [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_ll, c_int, c_int, c_int, c_int,
+                            c_void_p, c_void_p, c_void_p, c_void_p],
     "edl_im2col_nhwc": [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_ll,
                         c_void_p],
     "edl_maxpool_nhwc": [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p],
@@ -134,6 +139,7 @@ def check(rc: int, what: str) -> None:
 # kernel launches per C entry point (bench.py reports launches in its timed region)
 _LAUNCHES = {"edl_linear_bwd_weight": 3,   # GEMM + two column-sum passes when db is requested
              "edl_linear_bwd_weight_ws": 4,   # split-K GEMM + reduce + two column-sum passes (at most)
+             "edl_conv_bwd_weight_nhwc": 4,   # the same plan with an im2col operand
              "edl_kd_loss_fwd_bwd": 2,     # row pass + deterministic batch-mean pass
              "edl_stream_wait_geq": 0,     # stream memory ops, not kernels
              "edl_stream_write_u32": 0}

@@ -419,6 +419,50 @@ int edl_conv_fwd_nhwc(const void* x, int N, int H, int W, int C, const void* w, 
   return e == cudaSuccess ? 0 : cuda_fail(e, "conv_fwd_nhwc");
 }
 
+int edl_conv_flip_weights(const void* w, long long ldw, int K, int C, int R, int S, void* wf, long long ldf,
+                          void* stream) {
+  if (K < 1 || C < 1 || R < 1 || S < 1 || ldw < static_cast<long long>(R) * S * C ||
+      ldf < static_cast<long long>(R) * S * K || !w || !wf)
+    return fail(EDL_ERR_SHAPE, "conv_flip_weights: bad shape");
+  cudaError_t e = launch_conv_flip_weights(reinterpret_cast<const __nv_bfloat16*>(w), ldw, K, C, R, S,
+                                           reinterpret_cast<__nv_bfloat16*>(wf), ldf, as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "conv_flip_weights");
+}
+
+int edl_conv_dgrad_nhwc(const void* dz, int N, int P, int Q, int K, const void* wf, long long ldf, int C, int R,
+                        int S, int pad, const void* add, const void* mask, void* dx, void* stream) {
+  const int pd = R - 1 - pad;
+  if (N < 1 || P < 1 || Q < 1 || K < 64 || K % 64 || C < 1 || R < 1 || S < 1 || R > 16 || S > 16 || pad < 0 ||
+      pd < 0 || R - 1 - pad != S - 1 - pad || ldf < static_cast<long long>(R) * S * K)
+    return fail(EDL_ERR_SHAPE, "conv_dgrad_nhwc: bad shape");
+  const int H = P + 2 * pd - R + 1, W = Q + 2 * pd - S + 1;
+  if (H < 1 || W < 1) return fail(EDL_ERR_SHAPE, "conv_dgrad_nhwc: empty output");
+  const long long Ml = static_cast<long long>(N) * H * W;
+  if (Ml > (1LL << 31) - 256) return fail(EDL_ERR_SHAPE, "conv_dgrad_nhwc: too many pixels");
+  const int M = static_cast<int>(Ml), Kd = R * S * K;
+  cudaStream_t st = as_stream(stream);
+  const int cap = grid_cap(st);
+  CUtensorMap ta, tb, ty;
+  int rc;
+  if ((rc = conv_map(dz, N, P, Q, K, R, S, 1, pd, 128, &ta))) return rc;
+  if ((rc = tensor_map_out(dx, M, C, C, false, &ty))) return rc;
+  EpiArgs ep{dx, C, nullptr, reinterpret_cast<const __nv_bfloat16*>(add), add ? C : 0, 1.0f, stream_sched(st)};
+  ep.aux2 = reinterpret_cast<const __nv_bfloat16*>(mask);
+  ep.ld_aux2 = mask ? C : 0;
+  ep.conv = ConvGeom{H, W, 1, pd, S, K / 64};
+  const int pbn = pick_pair_bn(M, C, cap);
+  cudaError_t e;
+  if (pbn > 0) {
+    if ((rc = tensor_map(wf, C, Kd, ldf, 64, pbn / 2, &tb))) return rc;
+    e = launch_gemm_pair(GemmKind::ConvDgrad, pbn, ta, tb, ty, M, C, Kd, ep, cap, st);
+  } else {
+    const int bn = pick_bn_cap(M, C, cap);
+    if ((rc = tensor_map(wf, C, Kd, ldf, 64, bn, &tb))) return rc;
+    e = launch_gemm(GemmKind::ConvDgrad, bn, ta, tb, ty, M, C, Kd, ep, cap, st);
+  }
+  return e == cudaSuccess ? 0 : cuda_fail(e, "conv_dgrad_nhwc");
+}
+
 int edl_linear_fwd_residual(const void* X, long long ldx, const void* W, long long ldw, const float* bias,
                             const void* R, long long ldr, void* Y, long long ldy, int M, int N, int K,
                             void* stream) {
@@ -683,11 +727,14 @@ long long edl_bwd_weight_workspace_floats(int M, int N, int K) {
   return wgrad_workspace_floats(M, N, K, num_sms());
 }
 
-int edl_linear_bwd_weight_ws(const void* dY, long long lddy, const void* X, long long ldx, float* dW,
-                             long long lddw, float* db, float* workspace, long long workspace_floats, int M, int N,
-                             int K, float scale, void* stream) {
-  if (M < 1 || N < 1 || K < 1 || lddy < N || ldx < K || lddw < K)
-    return fail(EDL_ERR_SHAPE, "linear_bwd_weight_ws: bad shape M=%d N=%d K=%d", M, N, K);
+}  // extern "C"
+
+namespace {
+// dW = scale dY^T X over M rows (+ db), split-K planned; conv != nullptr: X is
+// the im2col matrix of an NHWC tensor, read through a TMA im2col map (`xmap`).
+int bwd_weight_ws_impl(const void* dY, long long lddy, const void* X, long long ldx, const CUtensorMap* xmap,
+                       const ConvGeom* conv, float* dW, long long lddw, float* db, float* workspace,
+                       long long workspace_floats, int M, int N, int K, float scale, void* stream) {
   if (!workspace || workspace_floats < 0)
     return fail(EDL_ERR_SHAPE, "linear_bwd_weight_ws: workspace required");
   cudaStream_t st = as_stream(stream);
@@ -696,10 +743,21 @@ int edl_linear_bwd_weight_ws(const void* dY, long long lddy, const void* X, long
   CUtensorMap ta, tb;
   int rc;
   // dY [M][N] and X [M][K] both read as [red=M][MN]; swapped: A = X^T, B = dY^T
-  if ((rc = tensor_map(p.swap ? X : dY, M, p.swap ? K : N, p.swap ? ldx : lddy, 64, 64, &ta))) return rc;
-  if ((rc = tensor_map(p.swap ? dY : X, M, p.swap ? N : K, p.swap ? lddy : ldx, 64, 64, &tb))) return rc;
+  if (p.swap) {
+    if (xmap) ta = *xmap;
+    else if ((rc = tensor_map(X, M, K, ldx, 64, 64, &ta))) return rc;
+    if ((rc = tensor_map(dY, M, N, lddy, 64, 64, &tb))) return rc;
+  } else {
+    if ((rc = tensor_map(dY, M, N, lddy, 64, 64, &ta))) return rc;
+    if (xmap) tb = *xmap;
+    else if ((rc = tensor_map(X, M, K, ldx, 64, 64, &tb))) return rc;
+  }
   EpiArgs ep{p.reduce() ? static_cast<void*>(workspace) : static_cast<void*>(dW), p.reduce() ? p.gn : lddw,
              nullptr, nullptr, 0, scale, stream_sched(st)};
+  if (conv) {
+    ep.conv = *conv;
+    ep.conv.operand = p.swap ? 0 : 1;
+  }
   ep.ksplit = p.ksplit;
   ep.split_stride = static_cast<long long>(p.gm) * p.gn;
   cudaError_t e = launch_gemm(GemmKind::BwdWeight, p.bn, ta, tb, ta, p.gm, p.gn, M, ep, cap, st);
@@ -720,6 +778,38 @@ int edl_linear_bwd_weight_ws(const void* dY, long long lddy, const void* X, long
     if (e != cudaSuccess) return cuda_fail(e, "colsum");
   }
   return 0;
+}
+}  // namespace
+
+extern "C" {
+
+int edl_linear_bwd_weight_ws(const void* dY, long long lddy, const void* X, long long ldx, float* dW,
+                             long long lddw, float* db, float* workspace, long long workspace_floats, int M, int N,
+                             int K, float scale, void* stream) {
+  if (M < 1 || N < 1 || K < 1 || lddy < N || ldx < K || lddw < K)
+    return fail(EDL_ERR_SHAPE, "linear_bwd_weight_ws: bad shape M=%d N=%d K=%d", M, N, K);
+  return bwd_weight_ws_impl(dY, lddy, X, ldx, nullptr, nullptr, dW, lddw, db, workspace, workspace_floats, M, N, K,
+                            scale, stream);
+}
+
+int edl_conv_bwd_weight_nhwc(const void* x, int N, int H, int W, int C, int R, int S, int stride, int pad,
+                             const void* dY, long long lddy, int K, float* dW, long long lddw, float* db,
+                             float* workspace, long long workspace_floats, float scale, void* stream) {
+  if (N < 1 || H < 1 || W < 1 || C < 64 || C % 64 || K < 1 || R < 1 || S < 1 || stride < 1 || stride > 8 ||
+      pad < 0 || R > 16 || S > 16)
+    return fail(EDL_ERR_SHAPE, "conv_bwd_weight_nhwc: bad shape");
+  const int P = (H + 2 * pad - R) / stride + 1, Q = (W + 2 * pad - S) / stride + 1;
+  if (P < 1 || Q < 1) return fail(EDL_ERR_SHAPE, "conv_bwd_weight_nhwc: empty output");
+  const long long Ml = static_cast<long long>(N) * P * Q;
+  const int Kd = R * S * C;
+  if (Ml > (1LL << 31) - 256 || lddy < K || lddw < Kd)
+    return fail(EDL_ERR_SHAPE, "conv_bwd_weight_nhwc: bad leading dimension");
+  CUtensorMap xm;
+  int rc;
+  if ((rc = conv_map(x, N, H, W, C, R, S, stride, pad, 64, &xm))) return rc;
+  const ConvGeom g{P, Q, stride, pad, S, C / 64};
+  return bwd_weight_ws_impl(dY, lddy, nullptr, 0, &xm, &g, dW, lddw, db, workspace, workspace_floats,
+                            static_cast<int>(Ml), K, Kd, scale, stream);
 }
 
 long long edl_colsum_group_workspace_floats(int count, const int* M, const int* N) {

@@ -505,4 +505,29 @@ cudaError_t launch_maxpool_bwd_argmax_nhwc(const uint32_t* argmax, int N, int H,
                     N, H, W, C, k, stride, pad, P, Q, dy, mask, dx);
 }
 
+// Data-gradient weights of a stride-1 convolution: the transposed, spatially
+// flipped filter wf[c][(r', s', k)] = w[k][((R-1-r') * S + (S-1-s')) * C + c],
+// so dX = conv(dZ, wf, pad' = R - 1 - pad) runs through the forward
+// implicit-GEMM kernel. One thread per output element (weights are small).
+__global__ void __launch_bounds__(256) conv_flip_weights_kernel(const __nv_bfloat16* __restrict__ w, long long ldw,
+                                                                int K, int C, int RS,
+                                                                __nv_bfloat16* __restrict__ wf, long long ldf) {
+  griddep_wait();
+  const long long total = static_cast<long long>(C) * RS * K;
+  for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < total;
+       o += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(o % K);
+    const long long t = o / K;
+    const int rs = static_cast<int>(t % RS), c = static_cast<int>(t / RS);
+    wf[c * ldf + static_cast<long long>(rs) * K + k] = w[k * ldw + static_cast<long long>(RS - 1 - rs) * C + c];
+  }
+}
+
+cudaError_t launch_conv_flip_weights(const __nv_bfloat16* w, long long ldw, int K, int C, int R, int S,
+                                     __nv_bfloat16* wf, long long ldf, cudaStream_t stream) {
+  const long long work = static_cast<long long>(C) * R * S * K;
+  return launch_pdl(conv_flip_weights_kernel, dim3(grid_for(work)), dim3(256), 0, stream, 1, w, ldw, K, C, R * S, wf,
+                    ldf);
+}
+
 }  // namespace edl

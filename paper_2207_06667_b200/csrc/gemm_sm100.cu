@@ -96,6 +96,41 @@ __device__ __forceinline__ void load_kblock_conv(const CUtensorMap* tmA, const C
   tma_load_2d_hint(sb, tmB, bar, kb * kBK, n0, pb);
 }
 
+// Weight gradient of a convolution: the reduction runs over output pixels
+// (k-block kb = pixels [64 kb, 64 kb + 64)), the im2col operand is MN-major
+// with MN index (r, s, c): each 64-wide MN chunk is one im2col box of 64
+// pixels x 64 channels at one filter tap. Chunks past the real K (r >= R)
+// load in-range garbage that only feeds discarded output rows.
+template <int BN>
+__device__ __forceinline__ void load_kblock_conv_wgrad(const CUtensorMap* tmA, const CUtensorMap* tmB, uint8_t* sa,
+                                                       uint8_t* sb, uint64_t* bar, const ConvGeom& cv, int m0,
+                                                       int n0, int kb, uint64_t pa, uint64_t pb) {
+  mbar_arrive_expect_tx(bar, GemmCfg<BN>::kStageBytes);
+  const ConvTile ct = conv_tile(cv, kb * kBK);
+  const int k0 = kb * kBK;
+  if (cv.operand == 0) {
+#pragma unroll
+    for (int j = 0; j < kBM / 64; ++j) {
+      int cb, r, s;
+      conv_tap(cv, m0 / 64 + j, cb, r, s);
+      tma_load_im2col_4d(sa + j * 8192, tmA, bar, cb * 64, ct.wb, ct.hb, ct.nb, static_cast<uint16_t>(s),
+                         static_cast<uint16_t>(r));
+    }
+#pragma unroll
+    for (int j = 0; j < BN / 64; ++j) tma_load_2d_hint(sb + j * 8192, tmB, bar, n0 + 64 * j, k0, pb);
+  } else {
+#pragma unroll
+    for (int j = 0; j < kBM / 64; ++j) tma_load_2d_hint(sa + j * 8192, tmA, bar, m0 + 64 * j, k0, pa);
+#pragma unroll
+    for (int j = 0; j < BN / 64; ++j) {
+      int cb, r, s;
+      conv_tap(cv, n0 / 64 + j, cb, r, s);
+      tma_load_im2col_4d(sb + j * 8192, tmB, bar, cb * 64, ct.wb, ct.hb, ct.nb, static_cast<uint16_t>(s),
+                         static_cast<uint16_t>(r));
+    }
+  }
+}
+
 // L2 policy per operand. Measured on B200 (profiles/): evict_last on the
 // re-read activations + evict_first on the streamed weights RAISED teacher
 // layer-2 DRAM reads (619 -> 683 MB/launch) and lowered tensor-pipe activity,
@@ -323,7 +358,25 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& ep, uint32_t taddr,
 template <int EPI>
 __host__ __device__ constexpr bool epi_tma_store() {
   return EPI == EPI_TANH_BF16 || EPI == EPI_BIAS_F32 || EPI == EPI_DTANH_BF16 || EPI == EPI_RELU_BF16 ||
-         EPI == EPI_BIAS_BF16;
+         EPI == EPI_BIAS_BF16 || EPI == EPI_DRELU_BF16;
+}
+
+// 32 bf16 of row `row` at col0 (+ ld), 16-byte loads when the chunk is full.
+__device__ __forceinline__ void load_row32(const __nv_bfloat16* base, long long ld, int row, int col0, int N,
+                                           float (&o)[32]) {
+  const __nv_bfloat16* h = base + static_cast<size_t>(row) * ld + col0;
+  if (col0 + 32 <= N) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(h) + i);
+      const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&q);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[8 * i + j] = __bfloat162float(hb[j]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) o[i] = col0 + i < N ? __bfloat162float(h[i]) : 0.f;
+  }
 }
 
 // The epilogue math of epilogue_store without its global stores (v in place).
@@ -367,6 +420,22 @@ __device__ __forceinline__ void epi_math(const EpiArgs& ep, int row, int M, int 
     }
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+  }
+  if constexpr (EPI == EPI_DRELU_BF16) {
+    // conv data gradient: + the shortcut branch's gradient, then the ReLU
+    // derivative of the layer input (its stored post-ReLU activation > 0)
+    if (row >= M) return;
+    float t[32];
+    if (ep.aux != nullptr) {
+      load_row32(ep.aux, ep.ld_aux, row, col0, N, t);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += t[i];
+    }
+    if (ep.aux2 != nullptr) {
+      load_row32(ep.aux2, ep.ld_aux2, row, col0, N, t);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = t[i] > 0.f ? v[i] : 0.f;
+    }
   }
   if constexpr (EPI == EPI_DTANH_BF16) {
     if (row >= M) return;
@@ -587,6 +656,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
             load_kblock_conv<BN>(&tmA, &tmB, sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes, &full[s], ep.conv, ct,
                                  n0, kb, pb);
+          }
+          continue;
+        }
+      }
+      if constexpr (A_MN && B_MN) {
+        if (ep.conv.Q > 0) {   // convolution weight gradient: the im2col operand from its map
+          for (int kb = kb0; kb < kb1; ++kb, ++g) {
+            const int s = g % S;
+            mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
+            load_kblock_conv_wgrad<BN>(&tmA, &tmB, sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes, &full[s],
+                                       ep.conv, m0, n0, kb, pa, pb);
           }
           continue;
         }
@@ -1494,6 +1574,8 @@ cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUte
       return launch_gemm_bn<false, false, EPI_BIAS_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
     case GemmKind::BwdDataPlain:
       return launch_gemm_bn<false, true, EPI_BIAS_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
+    case GemmKind::ConvDgrad:
+      return launch_gemm_bn<false, false, EPI_DRELU_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
   }
   return cudaErrorInvalidValue;
 }
@@ -1536,6 +1618,8 @@ cudaError_t launch_gemm_pair(GemmKind kind, int bn, const CUtensorMap& ta, const
       return launch_pair_bn<false, false, EPI_BIAS_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
     case GemmKind::BwdDataPlain:
       return launch_pair_bn<false, true, EPI_BIAS_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
+    case GemmKind::ConvDgrad:
+      return launch_pair_bn<false, false, EPI_DRELU_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
     default:
       return cudaErrorInvalidValue;
   }

@@ -50,6 +50,7 @@ enum EpiMode : int {
   EPI_SGD_F32 = 4,     // out(f32) -= scale * acc in place; out_bf16 = bf16(out)
   EPI_RELU_BF16 = 5,   // out(bf16) = relu(acc + bias [+ aux residual]) (conv layers, cfg4)
   EPI_BIAS_BF16 = 6,   // out(bf16) = acc + bias (cfg4 shortcut projections)
+  EPI_DRELU_BF16 = 7,  // out(bf16) = (acc [+ aux]) * (aux2 > 0): a conv data gradient through a ReLU
 };
 
 // Implicit-GEMM convolution geometry (A = im2col of an NHWC tensor through a
@@ -59,6 +60,9 @@ struct ConvGeom {
   int stride = 1, pad = 0;
   int S = 1;              // filter width (taps per filter row)
   int cblocks = 1;        // C / 64
+  // weight gradient (MN-major operands, K = pixels): which operand is the
+  // im2col matrix, read as [pixels][(r, s, c)] 64 x 64 boxes -- 0: A, 1: B
+  int operand = 0;
 };
 
 struct EpiArgs {
@@ -75,6 +79,8 @@ struct EpiArgs {
   int ksplit = 1;
   long long split_stride = 0;
   ConvGeom conv;          // A operand from an im2col map (gemm_kernel / gemm_pair_kernel, K-major A)
+  const __nv_bfloat16* aux2 = nullptr;   // EPI_DRELU_BF16: the ReLU mask (the layer's output), ld_aux2
+  long long ld_aux2 = 0;
 };
 
 struct HeadArgs {
@@ -85,7 +91,7 @@ struct HeadArgs {
   int* idx;
 };
 
-enum class GemmKind { FwdTanh, FwdLinear, BwdData, BwdWeight, FwdRelu, FwdIdentBf16, BwdDataPlain };
+enum class GemmKind { FwdTanh, FwdLinear, BwdData, BwdWeight, FwdRelu, FwdIdentBf16, BwdDataPlain, ConvDgrad };
 
 constexpr int kMaxGroup = 4;
 struct GroupMaps {
@@ -132,6 +138,8 @@ cudaError_t launch_im2col_nhwc(const __nv_bfloat16* x, int N, int H, int W, int 
                                cudaStream_t stream);
 cudaError_t launch_maxpool_nhwc(const __nv_bfloat16* x, int N, int H, int W, int C, int k, int stride, int pad,
                                 int P, int Q, __nv_bfloat16* out, uint32_t* argmax, cudaStream_t stream);
+cudaError_t launch_conv_flip_weights(const __nv_bfloat16* w, long long ldw, int K, int C, int R, int S,
+                                     __nv_bfloat16* wf, long long ldf, cudaStream_t stream);
 cudaError_t launch_maxpool_bwd_argmax_nhwc(const uint32_t* argmax, int N, int H, int W, int C, int k, int stride,
                                            int pad, int P, int Q, const __nv_bfloat16* dy, const __nv_bfloat16* mask,
                                            __nv_bfloat16* dx, cudaStream_t stream);

@@ -506,8 +506,8 @@ __global__ void __launch_bounds__(256) colsum_tall_final_kernel(const float* __r
 }
 
 int colsum_tall_blocks(int M, int sms) {
-  const int g = 2 * sms;
-  const int by_rows = (M + 255) / 256;    // at least 256 rows per block
+  const int g = 8 * sms;                  // 8 x 256 threads per SM: enough loads in flight for HBM
+  const int by_rows = (M + 127) / 128;    // at least 128 rows per block
   return by_rows < g ? (by_rows < 1 ? 1 : by_rows) : g;
 }
 

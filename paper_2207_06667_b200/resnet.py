@@ -394,9 +394,10 @@ class ResNetStudent:
             self.acts.append((hw, h1, sc, y))
             hw = (oh, ow)
         self.final_hw = hw
-        # every im2col conv keeps its forward column matrix for its weight
-        # gradient (a few GB at batch 128 against 180 GB of HBM: the backward
-        # never re-gathers); self.col is the data-gradient scratch
+        # implicit-GEMM convs (>= 64 input channels) read their input through
+        # TMA im2col maps in the forward and the weight gradient: no column
+        # matrix. The packed RGB stem keeps its forward column matrix for its
+        # weight gradient; self.col is the data-gradient scratch
         self.in_hw = [(H, H)] + [None] * (len(self.convs) - 1)
         for (i1, i2, isc), (hw_in, _, _, _) in zip(self.block_idx, self.acts):
             self.in_hw[i1] = hw_in
@@ -407,10 +408,14 @@ class ResNetStudent:
         for i, c in enumerate(self.convs):
             oh, ow = c.out_hw(*self.in_hw[i])
             M = B * oh * ow
-            self.cols.append(None if (c.k == 1 and c.stride == 1) else
+            self.cols.append(None if (c.k == 1 and c.stride == 1) or c.implicit else
                              torch.empty(M, c.kdim, dtype=torch.bfloat16, device=dev))
             ws = max(ws, int(_lib.load().edl_bwd_weight_workspace_floats(M, c.cout_p, c.kdim)))
         self.wgrad_ws = torch.empty(max(ws, 1), dtype=torch.float32, device=dev)
+        # stride-1 data gradients run as implicit-GEMM convolutions of dZ with
+        # the flipped filter (refreshed from the forward's bf16 weights each step)
+        self.wflip = [torch.empty(c.cin_p, c.k * c.k * c.cout_p, dtype=torch.bfloat16, device=dev)
+                      if i > 0 and self._dgrad_implicit(c) else None for i, c in enumerate(self.convs)]
         self.col = torch.empty(col, dtype=torch.bfloat16, device=dev)
         # backward buffers: gradient ping-pong at the largest activation size + a shortcut buffer
         big = max(B * h * w * stem.cout_p, max(a[1].numel() for a in self.acts))
@@ -450,6 +455,12 @@ class ResNetStudent:
     def _fwd(self, i, x, hw, out, residual, s):
         c, p = self.convs[i], self.params[i]
         oh, ow = c.out_hw(*hw)
+        if c.implicit:
+            act = _lib.EDL_ACT_RELU if (c.relu or residual is not None) else _lib.EDL_ACT_IDENT
+            _lib.call("edl_conv_fwd_nhwc", x.data_ptr(), self.B, hw[0], hw[1], c.cin_p, self._w16(p).data_ptr(),
+                      c.kdim, self._b(p).data_ptr(), c.cout_p, c.k, c.k, c.stride, c.pad,
+                      None if residual is None else residual.data_ptr(), c.cout_p, out.data_ptr(), c.cout_p, act, s)
+            return
         a, lda = self._im2col(i, x, hw, s)
         M = self.B * oh * ow
         if residual is not None:
@@ -488,16 +499,33 @@ class ResNetStudent:
         (edl_linear_bwd_weight_ws): the reduction runs over all B*H*W pixels."""
         c, p = self.convs[i], self.params[i]
         oh, ow = c.out_hw(*hw)
-        a, lda = (x, c.cin_p) if self.cols[i] is None else (self.cols[i], c.kdim)
         M = self.B * oh * ow
+        if c.implicit:
+            _lib.call("edl_conv_bwd_weight_nhwc", x.data_ptr(), self.B, hw[0], hw[1], c.cin_p, c.k, c.k, c.stride,
+                      c.pad, dz.data_ptr(), c.cout_p, c.cout_p, self._gw(p).data_ptr(), c.kdim,
+                      self._gb(p).data_ptr(), self.wgrad_ws.data_ptr(), self.wgrad_ws.numel(), 1.0, s)
+            return
+        a, lda = (x, c.cin_p) if self.cols[i] is None else (self.cols[i], c.kdim)
         _lib.call("edl_linear_bwd_weight_ws", dz.data_ptr(), c.cout_p, a.data_ptr(), lda, self._gw(p).data_ptr(),
                   c.kdim, self._gb(p).data_ptr(), self.wgrad_ws.data_ptr(), self.wgrad_ws.numel(), M, c.cout_p,
                   c.kdim, 1.0, s)
 
+    @staticmethod
+    def _dgrad_implicit(c) -> bool:
+        return c.stride == 1 and not c.packed and c.cout_p % 64 == 0 and c.pad == c.k // 2
+
     def _dgrad(self, i, dz, hw, out, add, mask, s):
-        """out = col2im(dz W_i) (+ add) (* mask > 0): the gradient w.r.t. conv i's input."""
+        """out = col2im(dz W_i) (+ add) (* mask > 0): the gradient w.r.t. conv i's input.
+        Stride 1: one implicit-GEMM convolution of dz with the flipped filter
+        (edl_conv_dgrad_nhwc, add and mask in its epilogue); stride 2: the
+        column gradient dz W_i, then the col2im gather."""
         c, p = self.convs[i], self.params[i]
         oh, ow = c.out_hw(*hw)
+        if self.wflip[i] is not None:
+            _lib.call("edl_conv_dgrad_nhwc", dz.data_ptr(), self.B, oh, ow, c.cout_p, self.wflip[i].data_ptr(),
+                      self.wflip[i].stride(0), c.cin_p, c.k, c.k, c.pad, None if add is None else add.data_ptr(),
+                      None if mask is None else mask.data_ptr(), out.data_ptr(), s)
+            return
         M = self.B * oh * ow
         dcol = self.col[:M * c.kdim]
         _lib.call("edl_linear_bwd_data", dz.data_ptr(), c.cout_p, self._w16(p).data_ptr(), c.kdim, None, 0,
@@ -512,6 +540,10 @@ class ResNetStudent:
         s = (stream or torch.cuda.current_stream()).cuda_stream
         B = self.B
         self.forward(x, s)
+        for c, p, wf in zip(self.convs, self.params, self.wflip):
+            if wf is not None:
+                _lib.call("edl_conv_flip_weights", self._w16(p).data_ptr(), c.kdim, c.cout_p, c.cin_p, c.k, c.k,
+                          wf.data_ptr(), wf.stride(0), s)
         q_vals = soft.probs if (soft is not None and beta > 0) else None
         q_idx = soft.classes if (soft is not None and beta > 0) else None
         k = soft.probs.shape[1] if q_vals is not None else 0

@@ -325,3 +325,80 @@ def test_conv_fwd_implicit_vs_torch_and_explicit(N, C, H, K, k, stride, relu, re
     got = y[..., :K].float().cpu().permute(0, 3, 1, 2)
     assert _rel(got, want) < 1e-2
     assert torch.equal(y, y2)
+
+
+@pytest.mark.parametrize("N,C,H,K,k,stride", [
+    (2, 64, 14, 64, 3, 1),          # cout < 128: swapped operands (im2col = A)
+    (2, 64, 15, 128, 3, 2),         # stride 2, im2col = B
+    (3, 128, 9, 256, 1, 2),         # 1x1 stride-2 projection
+    (2, 256, 7, 512, 3, 1),
+    (32, 64, 56, 64, 3, 1),         # a ResNet stage-1 layer at batch 32: deep split
+])
+def test_conv_bwd_weight_implicit_vs_explicit(N, C, H, K, k, stride):
+    """edl_conv_bwd_weight_nhwc (im2col operand through a TMA im2col map)
+    against the explicit column matrix through edl_linear_bwd_weight_ws
+    (same split plan and order: bitwise equal) and torch in fp32."""
+    from paper_2207_06667_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(N * H + K)
+    x = torch.randn(N, H, H, C, device="cuda", generator=g).to(torch.bfloat16)
+    pad_ = k // 2
+    P = (H + 2 * pad_ - k) // stride + 1
+    M = N * P * P
+    Kd = k * k * C
+    dy = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    lib = _lib.load()
+    ws = torch.empty(int(lib.edl_bwd_weight_workspace_floats(M, K, Kd)), device="cuda")
+    dw1, db1 = torch.empty(K, Kd, device="cuda"), torch.empty(K, device="cuda")
+    _lib.call("edl_conv_bwd_weight_nhwc", x.data_ptr(), N, H, H, C, k, k, stride, pad_, dy.data_ptr(), K, K,
+              dw1.data_ptr(), Kd, db1.data_ptr(), ws.data_ptr(), ws.numel(), 1.0, _s())
+    col = torch.empty(M, Kd, dtype=torch.bfloat16, device="cuda")
+    _lib.call("edl_im2col_nhwc", x.data_ptr(), N, H, H, C, C, k, k, stride, pad_, col.data_ptr(), Kd, _s())
+    dw2, db2 = torch.empty_like(dw1), torch.empty_like(db1)
+    _lib.call("edl_linear_bwd_weight_ws", dy.data_ptr(), K, col.data_ptr(), Kd, dw2.data_ptr(), Kd, db2.data_ptr(),
+              ws.data_ptr(), ws.numel(), M, K, Kd, 1.0, _s())
+    torch.cuda.synchronize()
+    assert torch.equal(dw1, dw2) and torch.equal(db1, db2)
+    want = dy.float().T @ col.float()
+    assert _rel(dw1, want) < 2e-3
+
+
+@pytest.mark.parametrize("N,C,H,K,k,use_add,use_mask", [
+    (2, 64, 14, 64, 3, False, True),     # conv2 of a block: mask only
+    (2, 64, 14, 64, 3, True, True),      # conv1: + shortcut gradient, masked by the block input
+    (2, 128, 9, 64, 3, True, False),     # add only (block 0's input has no ReLU mask here)
+    (3, 16, 8, 128, 3, False, False),    # narrow output channels (C = 16)
+    (2, 256, 7, 512, 3, False, True),
+    (32, 64, 56, 64, 3, True, True),     # a stage-1 layer at batch 32
+])
+def test_conv_dgrad_implicit_vs_torch(N, C, H, K, k, use_add, use_mask):
+    """edl_conv_dgrad_nhwc (stride 1: dZ convolved with the flipped filter,
+    implicit GEMM, fused + add and ReLU mask) against torch autograd through
+    conv2d in fp32 from the same bf16 values: <= 1e-2 of the max."""
+    import torch.nn.functional as F
+
+    from paper_2207_06667_b200 import _lib
+    g = torch.Generator().manual_seed(N * C + K + H)
+    pad_ = k // 2
+    w = ref._bf(torch.randn(K, C, k, k, generator=g) * (2.0 / (C * k * k)) ** 0.5)
+    dz = ref._bf(torch.randn(N, K, H, H, generator=g))
+    add = ref._bf(torch.randn(N, C, H, H, generator=g)) if use_add else None
+    mask = ref._bf(torch.randn(N, C, H, H, generator=g)) if use_mask else None
+    x = torch.zeros(N, C, H, H, requires_grad=True)
+    F.conv2d(x, w, padding=pad_).backward(dz)
+    want = x.grad + (add if add is not None else 0)
+    if mask is not None:
+        want = want * (mask > 0)
+    nhwc = lambda t: t.permute(0, 2, 3, 1).contiguous().to(torch.bfloat16).cuda()  # noqa: E731
+    wd = w.permute(0, 2, 3, 1).reshape(K, -1).contiguous().to(torch.bfloat16).cuda()   # [K][(r,s,c)]
+    wf = torch.empty(C, k * k * K, dtype=torch.bfloat16, device="cuda")
+    _lib.call("edl_conv_flip_weights", wd.data_ptr(), wd.stride(0), K, C, k, k, wf.data_ptr(), wf.stride(0), _s())
+    dzd = nhwc(dz)
+    add_d = None if add is None else nhwc(add)       # keep the device copies alive across the launch
+    mask_d = None if mask is None else nhwc(mask)
+    dx = torch.empty(N, H, H, C, dtype=torch.bfloat16, device="cuda")
+    _lib.call("edl_conv_dgrad_nhwc", dzd.data_ptr(), N, H, H, K, wf.data_ptr(), wf.stride(0), C, k, k, pad_,
+              None if add_d is None else add_d.data_ptr(), None if mask_d is None else mask_d.data_ptr(),
+              dx.data_ptr(), _s())
+    torch.cuda.synchronize()
+    got = dx.float().cpu().permute(0, 3, 1, 2)
+    assert _rel(got, want) < 1e-2
