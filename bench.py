@@ -459,6 +459,10 @@ def main():
                     line["cfg4_teacher_infer"] = _cfg4_teacher_rate(dev, peak_sust)
                 except Exception as exc:   # secondary measurement
                     line["cfg4_teacher_infer"] = {"error": repr(exc)[:200]}
+                try:
+                    line["cfg4_student_train"] = _cfg4_student_rate(dev, peak_sust)
+                except Exception as exc:   # secondary measurement
+                    line["cfg4_student_train"] = {"error": repr(exc)[:200]}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -570,7 +574,49 @@ def _cfg4_teacher_rate(dev, peak_sust, batch=256, iters=6, warmup=2):
                      "top-16 head", "batch": batch, "samples_per_s": round(batch / t, 1), "ms_per_batch": round(t * 1e3, 3),
             "gflop_per_sample": round(flop / 1e9, 3), "tflops": round(batch * flop / t / 1e12, 1),
             "frac_of_sustained": round(batch * flop / t / 1e12 / peak_sust, 4),
-            "note": "explicit NHWC im2col gather + tcgen05 GEMMs (round-1 slice; the student side is round 2)"}
+            "note": "implicit-GEMM convolutions (TMA im2col loads into the tcgen05 GEMM), packed explicit im2col "
+                    "for the RGB stem only"}
+
+
+def _cfg4_student_rate(dev, peak_sust, batch=256, iters=6, warmup=2):
+    """cfg4 (BASELINE configs[3]) student: the BN-free ResNet-18-style KD
+    training step (forward, fused KD loss, implicit-GEMM weight / data
+    gradients, SGD) alone, and co-located with the ResNet-50-style teacher
+    (online: the teacher's top-16 soft labels for the same batch, then the
+    student step, one stream), 224^2 synthetic images, 1000 classes, random
+    init; two input batches alternate (each 25.7 MB of NHWC bf16, activations
+    ~10 GB per step: far beyond L2)."""
+    import torch
+
+    from paper_2207_06667_b200.resnet import (ResNetConfig, ResNetStudent, ResNetTeacher, StudentResNetConfig,
+                                              init_resnet, init_student_resnet, to_nhwc)
+    st = ResNetStudent(init_student_resnet(StudentResNetConfig(), 0), dev, batch)
+    te = ResNetTeacher(init_resnet(ResNetConfig(), 1), dev, batch)
+    rng = np.random.default_rng(0)
+    xs = [to_nhwc(rng.normal(size=(batch, 3, 224, 224)).astype(np.float32), dev) for _ in range(2)]
+    ys = [torch.from_numpy(rng.integers(0, 1000, size=batch)).to(dev) for _ in range(2)]
+    out = {"model": "resnet18-style student (basic [2,2,2,2], width 64, BN-free) <- resnet50-style teacher, 224x224, "
+                    "1000 classes, top-16 soft labels, alpha = beta = 0.5, T = 2", "batch": batch}
+    for name, with_teacher in (("student_only", False), ("online_colocated", True)):
+        def step(i):
+            soft = te.soft_labels(xs[i % 2], 2.0, 16) if with_teacher else None
+            return st.train_step(xs[i % 2], ys[i % 2], soft, 0.5, 0.5 if with_teacher else 0.0, 2.0, 1e-3)
+        for i in range(warmup):
+            step(i)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for i in range(iters):
+            loss = step(i)
+        e.record()
+        torch.cuda.synchronize()
+        t = s.elapsed_time(e) / 1e3 / iters
+        flop = st.flops_per_sample() + (te.flops_per_sample() if with_teacher else 0.0)
+        out[name] = {"samples_per_s": round(batch / t, 1), "ms_per_step": round(t * 1e3, 3),
+                     "gflop_per_sample": round(flop / 1e9, 3), "tflops": round(batch * flop / t / 1e12, 1),
+                     "frac_of_sustained": round(batch * flop / t / 1e12 / peak_sust, 4),
+                     "loss_finite": bool(np.isfinite(loss.item()))}
+    return out
 
 
 def _small_config_graph(dev, steps=200, warmup=20):

@@ -221,7 +221,8 @@ cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 // empty; the reduce then transposes back to [N][K]. Cost model (us): waves x
 // max(k-blocks per item x 0.069 x bn/64 [one 128 x 64 x 64 k-block at the
 // per-SM tensor peak], the item's fp32 epilogue at ~50 GB/s per SM) + 0.5 per
-// wave, plus the partials' HBM round trip at 5 TB/s and ~2 us for the reduce.
+// wave, plus the reduce: the partials' HBM round trip at 5 TB/s, its chain of
+// ks loads per thread (8 in flight, ~0.35 us per round) and ~2 us of launch.
 struct WgradPlan {
   bool swap = false;
   int bn = 64;
@@ -256,7 +257,9 @@ WgradPlan plan_wgrad(int M, int N, int K, int cap, long long max_partial_floats)
     const long long waves = (tiles * ks + cap - 1) / cap;
     const double item = kps * t_kb > t_epi ? kps * t_kb : t_epi;
     double cost = waves * (item + 0.5);
-    if (ks > 1 || p.swap) cost += 2.0 * ks * gmn * 4 / 5e6 + 2.0;
+    // the reduce: partials' HBM round trip + its per-thread chain of ks loads
+    // (8 in flight, ~0.35 us L2 latency each round) + launch
+    if (ks > 1 || p.swap) cost += 2.0 * ks * gmn * 4 / 5e6 + 0.35 * ((ks + 7) / 8) + 2.0;
     if (best < 0 || cost < best) { best = cost; p.ksplit = ks; }
   }
   return p;

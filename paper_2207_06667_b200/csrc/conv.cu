@@ -360,33 +360,34 @@ __global__ void __launch_bounds__(256) maxpool_bwd_nhwc_kernel(const __nv_bfloat
 
 // Max pool backward from the forward's argmax words: each input element
 // collects dy of the windows whose recorded first maximum it is (<= 4 windows
-// for 3x3 / 2), times (mask > 0) if given. One 4-byte word + one 16-byte dy
-// load per window and 8-channel vector.
-template <typename I>
+// for 3x3 / 2), times (mask > 0) if given. One block per input row (n, h),
+// threads over (w, 8-channel vector): one 4-byte word + one 16-byte dy load
+// per window. KK / ST: compile-time window / stride (0: runtime k, stride).
+template <int KK, int ST>
 __global__ void __launch_bounds__(256) maxpool_bwd_argmax_nhwc_kernel(const uint32_t* __restrict__ argmax, int N,
-                                                                      int H, int W, int C, int k, int stride, int pad,
-                                                                      int P, int Q,
+                                                                      int H, int W, int C, int k_rt, int stride_rt,
+                                                                      int pad, int P, int Q,
                                                                       const __nv_bfloat16* __restrict__ dy,
                                                                       const __nv_bfloat16* __restrict__ mask,
                                                                       __nv_bfloat16* __restrict__ dx) {
   griddep_wait();
+  const int k = KK > 0 ? KK : k_rt;
+  const int stride = ST > 0 ? ST : stride_rt;
+  const int n = blockIdx.x / H, h = blockIdx.x - (blockIdx.x / H) * H;
   const int cv = C / 8;
-  const I total = static_cast<I>(N) * H * W * cv;
-  for (I i = blockIdx.x * static_cast<I>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<I>(gridDim.x) * blockDim.x) {
-    const int c8 = static_cast<int>(i % cv);
-    const I pix = i / cv;
-    const int w = static_cast<int>(pix % W);
-    const I nh = pix / W;
-    const int h = static_cast<int>(nh % H);
-    const int n = static_cast<int>(nh / H);
+  for (int i = threadIdx.x; i < W * cv; i += blockDim.x) {
+    const int w = i / cv, c8 = i - w * cv;
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int r = 0; r < k; ++r) {
+#pragma unroll
+    for (int r = 0; r < (KK > 0 ? KK : 16); ++r) {
+      if (KK == 0 && r >= k) break;
       const int ph = h + pad - r;
       if (ph < 0 || ph % stride) continue;
       const int p = ph / stride;
       if (p >= P) continue;
-      for (int s = 0; s < k; ++s) {
+#pragma unroll
+      for (int s = 0; s < (KK > 0 ? KK : 16); ++s) {
+        if (KK == 0 && s >= k) break;
         const int qw = w + pad - s;
         if (qw < 0 || qw % stride) continue;
         const int q = qw / stride;
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(256) maxpool_bwd_argmax_nhwc_kernel(const uint
           if (((arg >> (4 * j)) & 0xFu) == mine) acc[j] += __bfloat162float(gb[j]);
       }
     }
-    const long long off = static_cast<long long>(pix) * C + 8 * c8;
+    const long long off = ((static_cast<long long>(n) * H + h) * W + w) * C + 8 * c8;
     if (mask != nullptr) {
       const uint4 m = __ldg(reinterpret_cast<const uint4*>(mask + off));
       const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&m);
@@ -496,13 +497,15 @@ cudaError_t launch_maxpool_bwd_nhwc(const __nv_bfloat16* x, int N, int H, int W,
 cudaError_t launch_maxpool_bwd_argmax_nhwc(const uint32_t* argmax, int N, int H, int W, int C, int k, int stride,
                                            int pad, int P, int Q, const __nv_bfloat16* dy, const __nv_bfloat16* mask,
                                            __nv_bfloat16* dx, cudaStream_t stream) {
-  if (k * k > 15) return cudaErrorInvalidValue;
-  const long long work = static_cast<long long>(N) * H * W * (C / 8);
-  if (fits32(work))
-    return launch_pdl(maxpool_bwd_argmax_nhwc_kernel<int>, dim3(grid_for(work)), dim3(256), 0, stream, 1, argmax, N,
-                      H, W, C, k, stride, pad, P, Q, dy, mask, dx);
-  return launch_pdl(maxpool_bwd_argmax_nhwc_kernel<long long>, dim3(grid_for(work)), dim3(256), 0, stream, 1, argmax,
-                    N, H, W, C, k, stride, pad, P, Q, dy, mask, dx);
+  if (k * k > 15 || k > 16) return cudaErrorInvalidValue;
+  const long long rows = static_cast<long long>(N) * H;
+  if (rows > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const int threads = W * (C / 8) >= 256 ? 256 : ((W * (C / 8) + 31) / 32) * 32;
+  if (k == 3 && stride == 2)
+    return launch_pdl(maxpool_bwd_argmax_nhwc_kernel<3, 2>, dim3(static_cast<unsigned>(rows)), dim3(threads), 0,
+                      stream, 1, argmax, N, H, W, C, k, stride, pad, P, Q, dy, mask, dx);
+  return launch_pdl(maxpool_bwd_argmax_nhwc_kernel<0, 0>, dim3(static_cast<unsigned>(rows)), dim3(threads), 0, stream,
+                    1, argmax, N, H, W, C, k, stride, pad, P, Q, dy, mask, dx);
 }
 
 // Data-gradient weights of a stride-1 convolution: the transposed, spatially

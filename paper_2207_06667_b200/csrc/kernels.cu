@@ -488,20 +488,30 @@ __global__ void __launch_bounds__(256) colsum_tall_partial_kernel(const __nv_bfl
   }
 }
 
-__global__ void __launch_bounds__(256) colsum_tall_final_kernel(const float* __restrict__ partial, int G, int N,
-                                                                float* __restrict__ out, float scale) {
+// 32 columns per block, 32 warps striding the partial rows with 8 loads in
+// flight each (a 2-block grid for N = 64, so the parallelism has to come from
+// inside the block), combined in a fixed order.
+__global__ void __launch_bounds__(1024) colsum_tall_final_kernel(const float* __restrict__ partial, int G, int N,
+                                                                 float* __restrict__ out, float scale) {
   griddep_wait();
-  __shared__ float red[8][32];
+  __shared__ float red[32][33];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int n = blockIdx.x * 32 + lane;
-  float s = 0.f;
-  if (n < N)
-    for (int b = warp; b < G; b += 8) s += __ldcg(partial + static_cast<long long>(b) * N + n);
-  red[warp][lane] = s;
+  float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (n < N) {
+    int b = warp;
+    for (; b + 7 * 32 < G; b += 8 * 32) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] += __ldcg(partial + static_cast<long long>(b + 32 * u) * N + n);
+    }
+    for (; b < G; b += 32) a[0] += __ldcg(partial + static_cast<long long>(b) * N + n);
+  }
+  red[warp][lane] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
   __syncthreads();
   if (warp != 0 || n >= N) return;
+  float s = 0.f;
 #pragma unroll
-  for (int w = 1; w < 8; ++w) s += red[w][lane];
+  for (int w = 0; w < 32; ++w) s += red[w][lane];
   out[n] = s * scale;
 }
 
@@ -519,7 +529,7 @@ cudaError_t launch_colsum_tall(const __nv_bfloat16* x, long long ld, int M, int 
   const int rpb = (M + G - 1) / G;
   cudaError_t e = launch_pdl(colsum_tall_partial_kernel, dim3(G), dim3(256), 0, stream, 1, x, ld, M, N, rpb, partial);
   if (e != cudaSuccess) return e;
-  return launch_pdl(colsum_tall_final_kernel, dim3((N + 31) / 32), dim3(256), 0, stream, 1,
+  return launch_pdl(colsum_tall_final_kernel, dim3((N + 31) / 32), dim3(1024), 0, stream, 1,
                     static_cast<const float*>(partial), G, N, out, scale);
 }
 
@@ -534,15 +544,15 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
   const long long total = static_cast<long long>(GM) * GN;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    float a[4] = {0.f, 0.f, 0.f, 0.f};
+    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     int s = 0;
-    for (; s + 3 < ksplit; s += 4) {
+    for (; s + 7 < ksplit; s += 8) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) a[u] += __ldcg(P + (s + u) * sstride + i);
+      for (int u = 0; u < 8; ++u) a[u] += __ldcg(P + (s + u) * sstride + i);
     }
     for (; s < ksplit; ++s) a[0] += __ldcg(P + s * sstride + i);
     const int r = static_cast<int>(i / GN), c = static_cast<int>(i % GN);
-    out[r * ldo + c] = (a[0] + a[1]) + (a[2] + a[3]);
+    out[r * ldo + c] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
   }
 }
 
@@ -557,17 +567,17 @@ __global__ void __launch_bounds__(256) splitk_reduce_t_kernel(const float* __res
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int c = c0 + ty + 8 * j, r = r0 + tx;
-    float a[4] = {0.f, 0.f, 0.f, 0.f};
+    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (c < GM && r < GN) {
       const float* src = P + static_cast<long long>(c) * GN + r;
       int s = 0;
-      for (; s + 3 < ksplit; s += 4) {
+      for (; s + 7 < ksplit; s += 8) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) a[u] += __ldcg(src + (s + u) * sstride);
+        for (int u = 0; u < 8; ++u) a[u] += __ldcg(src + (s + u) * sstride);
       }
       for (; s < ksplit; ++s) a[0] += __ldcg(src + s * sstride);
     }
-    tile[ty + 8 * j][tx] = (a[0] + a[1]) + (a[2] + a[3]);
+    tile[ty + 8 * j][tx] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
   }
   __syncthreads();
 #pragma unroll

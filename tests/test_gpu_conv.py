@@ -243,7 +243,8 @@ def test_bwd_weight_splitk_vs_torch(M, N, K, ld_pad, ws_scale):
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
 
 
-def test_maxpool_bwd_vs_torch_with_ties():
+@pytest.mark.parametrize("k,st,pd", [(3, 2, 1), (2, 2, 0)])
+def test_maxpool_bwd_vs_torch_with_ties(k, st, pd):
     """edl_maxpool_bwd_nhwc (3x3 / 2 / pad 1, the stem pool) against torch
     autograd, on integer-valued inputs so windows have tied maxima: the
     gradient goes to the first maximum in scan order, as torch's does."""
@@ -253,20 +254,21 @@ def test_maxpool_bwd_vs_torch_with_ties():
     from paper_2207_06667_b200.resnet import to_nhwc
     rng = np.random.default_rng(3)
     x = rng.integers(-3, 4, size=(3, 16, 17, 17)).astype(np.float32)
-    gy = rng.normal(size=(3, 16, 9, 9)).astype(np.float32)
+    P = (17 + 2 * pd - k) // st + 1
+    gy = rng.normal(size=(3, 16, P, P)).astype(np.float32)
     xt = torch.from_numpy(x).requires_grad_(True)
-    F.max_pool2d(xt, 3, 2, 1).backward(ref._bf(torch.from_numpy(gy)))
+    F.max_pool2d(xt, k, st, pd).backward(ref._bf(torch.from_numpy(gy)))
     xd, dyd = to_nhwc(x, "cuda"), to_nhwc(gy, "cuda")
     dx = torch.empty_like(xd)
-    _lib.call("edl_maxpool_bwd_nhwc", xd.data_ptr(), 3, 17, 17, 16, 3, 2, 1, dyd.data_ptr(), None, dx.data_ptr(), _s())
+    _lib.call("edl_maxpool_bwd_nhwc", xd.data_ptr(), 3, 17, 17, 16, k, st, pd, dyd.data_ptr(), None, dx.data_ptr(), _s())
     # the training pair: forward records the argmax words, backward gathers from them
-    y_plain = torch.empty(3, 9, 9, 16, dtype=torch.bfloat16, device="cuda")
+    y_plain = torch.empty(3, P, P, 16, dtype=torch.bfloat16, device="cuda")
     y_arg = torch.empty_like(y_plain)
-    arg = torch.empty(3 * 9 * 9 * 2, dtype=torch.int32, device="cuda")
-    _lib.call("edl_maxpool_nhwc", xd.data_ptr(), 3, 17, 17, 16, 3, 2, 1, y_plain.data_ptr(), _s())
-    _lib.call("edl_maxpool_argmax_nhwc", xd.data_ptr(), 3, 17, 17, 16, 3, 2, 1, y_arg.data_ptr(), arg.data_ptr(), _s())
+    arg = torch.empty(3 * P * P * 2, dtype=torch.int32, device="cuda")
+    _lib.call("edl_maxpool_nhwc", xd.data_ptr(), 3, 17, 17, 16, k, st, pd, y_plain.data_ptr(), _s())
+    _lib.call("edl_maxpool_argmax_nhwc", xd.data_ptr(), 3, 17, 17, 16, k, st, pd, y_arg.data_ptr(), arg.data_ptr(), _s())
     dx2 = torch.empty_like(xd)
-    _lib.call("edl_maxpool_bwd_argmax_nhwc", arg.data_ptr(), 3, 17, 17, 16, 3, 2, 1, dyd.data_ptr(), None,
+    _lib.call("edl_maxpool_bwd_argmax_nhwc", arg.data_ptr(), 3, 17, 17, 16, k, st, pd, dyd.data_ptr(), None,
               dx2.data_ptr(), _s())
     torch.cuda.synchronize()
     got = dx.float().cpu().permute(0, 3, 1, 2)
