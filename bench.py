@@ -616,7 +616,68 @@ def _cfg4_student_rate(dev, peak_sust, batch=256, iters=6, warmup=2):
                      "gflop_per_sample": round(flop / 1e9, 3), "tflops": round(batch * flop / t / 1e12, 1),
                      "frac_of_sustained": round(batch * flop / t / 1e12 / peak_sust, 4),
                      "loss_finite": bool(np.isfinite(loss.item()))}
+    out["edl_two_streams"] = _cfg4_edl_streams(st, te, xs, ys, batch, iters, warmup, peak_sust)
     return out
+
+
+def _cfg4_edl_streams(st, te, xs, ys, batch, iters, warmup, peak_sust, reserve=40):
+    """EDL-Dist's decoupling on one GPU for cfg4: the teacher infers batch
+    i + 1 on its own stream (its GEMMs capped at SMs - reserve CTAs through
+    edl_set_stream_max_ctas) while the student trains on batch i; soft
+    labels pass through a 2-slot ring ordered by CUDA events (ready: teacher
+    -> student; consumed: student -> teacher before a slot is rewritten)."""
+    import torch
+
+    from paper_2207_06667_b200 import _lib
+    from paper_2207_06667_b200.nnkit import SoftLabels
+    dev = st.device
+    ts, ss = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    _lib.call("edl_set_stream_max_ctas", ts.cuda_stream, max(1, _lib.load().edl_device_sms() - reserve))
+    slots = [SoftLabels(torch.empty(batch, 16, device=dev), torch.empty(batch, 16, dtype=torch.int32, device=dev), 2.0)
+             for _ in range(2)]
+    ready = [torch.cuda.Event() for _ in range(2)]
+    used = [torch.cuda.Event() for _ in range(2)]
+    torch.cuda.synchronize()
+
+    def teach(i):
+        with torch.cuda.stream(ts):
+            if i >= 2:
+                ts.wait_event(used[i % 2])
+            te.soft_labels(xs[i % 2], 2.0, 16, out=slots[i % 2], stream=ts)
+            ready[i % 2].record(ts)
+
+    def learn(i):
+        with torch.cuda.stream(ss):
+            ss.wait_event(ready[i % 2])
+            loss = st.train_step(xs[i % 2], ys[i % 2], slots[i % 2], 0.5, 0.5, 2.0, 1e-3, stream=ss)
+            used[i % 2].record(ss)
+        return loss
+
+    def run(start, count):
+        teach(start)
+        for i in range(start, start + count):
+            if i + 1 < start + count:
+                teach(i + 1)
+            loss = learn(i)
+        return loss
+
+    run(0, warmup)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(ss)
+    ts.wait_event(s)
+    loss = run(warmup, iters)
+    ts_done = torch.cuda.Event()
+    ts_done.record(ts)
+    ss.wait_event(ts_done)
+    e.record(ss)
+    torch.cuda.synchronize()
+    _lib.call("edl_set_stream_max_ctas", ts.cuda_stream, 0)
+    t = s.elapsed_time(e) / 1e3 / iters
+    flop = st.flops_per_sample() + te.flops_per_sample()
+    return {"samples_per_s": round(batch / t, 1), "ms_per_step": round(t * 1e3, 3),
+            "tflops": round(batch * flop / t / 1e12, 1), "frac_of_sustained": round(batch * flop / t / 1e12 / peak_sust, 4),
+            "teacher_sm_reserve": reserve, "loss_finite": bool(np.isfinite(loss.item()))}
 
 
 def _small_config_graph(dev, steps=200, warmup=20):
