@@ -84,15 +84,52 @@ __device__ __forceinline__ void conv_tap(const ConvGeom& cv, int kb, int& cb, in
   s = rs - r * cv.S;
 }
 
+// The producer walks k-blocks in order, so it advances (cb, s, r) and the
+// pixel cursor incrementally: a single thread issues every TMA of the CTA,
+// and two integer divisions per k-block (~60 dependent instructions) made
+// it the bottleneck of the 64- and 128-wide conv GEMMs (ncu source view:
+// ~130 producer instructions per k-block against 128-256 MMA cycles).
+struct TapCursor {
+  int cb, r, s;
+  TapCursor() = default;
+  __device__ __forceinline__ TapCursor(const ConvGeom& cv, int kb) { conv_tap(cv, kb, cb, r, s); }
+  __device__ __forceinline__ void next(const ConvGeom& cv) {
+    if (++cb == cv.cblocks) {
+      cb = 0;
+      if (++s == cv.S) { s = 0; ++r; }
+    }
+  }
+};
+// Window corner of output pixel m, advanced by 64 pixels per step (weight
+// gradient k-blocks).
+struct PixelCursor {
+  int q, p, nb;
+  __device__ __forceinline__ PixelCursor(const ConvGeom& cv, int m) {
+    const int pq = cv.P * cv.Q;
+    nb = m / pq;
+    const int rem = m - nb * pq;
+    p = rem / cv.Q;
+    q = rem - p * cv.Q;
+  }
+  __device__ __forceinline__ ConvTile tile(const ConvGeom& cv) const {
+    return ConvTile{q * cv.stride - cv.pad, p * cv.stride - cv.pad, nb};
+  }
+  __device__ __forceinline__ void advance64(const ConvGeom& cv) {
+    q += 64;
+    while (q >= cv.Q) {
+      q -= cv.Q;
+      if (++p == cv.P) { p = 0; ++nb; }
+    }
+  }
+};
+
 template <int BN>
 __device__ __forceinline__ void load_kblock_conv(const CUtensorMap* tmA, const CUtensorMap* tmB, uint8_t* sa,
-                                                 uint8_t* sb, uint64_t* bar, const ConvGeom& cv, const ConvTile& ct,
-                                                 int n0, int kb, uint64_t pb) {
+                                                 uint8_t* sb, uint64_t* bar, const ConvTile& ct,
+                                                 int n0, int kb, const TapCursor& tap, uint64_t pb) {
   mbar_arrive_expect_tx(bar, GemmCfg<BN>::kStageBytes);
-  int cb, r, s;
-  conv_tap(cv, kb, cb, r, s);
-  tma_load_im2col_4d(sa, tmA, bar, cb * 64, ct.wb, ct.hb, ct.nb, static_cast<uint16_t>(s),
-                     static_cast<uint16_t>(r));
+  tma_load_im2col_4d(sa, tmA, bar, tap.cb * 64, ct.wb, ct.hb, ct.nb, static_cast<uint16_t>(tap.s),
+                     static_cast<uint16_t>(tap.r));
   tma_load_2d_hint(sb, tmB, bar, kb * kBK, n0, pb);
 }
 
@@ -104,30 +141,24 @@ __device__ __forceinline__ void load_kblock_conv(const CUtensorMap* tmA, const C
 template <int BN>
 __device__ __forceinline__ void load_kblock_conv_wgrad(const CUtensorMap* tmA, const CUtensorMap* tmB, uint8_t* sa,
                                                        uint8_t* sb, uint64_t* bar, const ConvGeom& cv, int m0,
-                                                       int n0, int kb, uint64_t pa, uint64_t pb) {
+                                                       int n0, int kb, const ConvTile& ct, const TapCursor* taps,
+                                                       uint64_t pa, uint64_t pb) {
   mbar_arrive_expect_tx(bar, GemmCfg<BN>::kStageBytes);
-  const ConvTile ct = conv_tile(cv, kb * kBK);
   const int k0 = kb * kBK;
   if (cv.operand == 0) {
 #pragma unroll
-    for (int j = 0; j < kBM / 64; ++j) {
-      int cb, r, s;
-      conv_tap(cv, m0 / 64 + j, cb, r, s);
-      tma_load_im2col_4d(sa + j * 8192, tmA, bar, cb * 64, ct.wb, ct.hb, ct.nb, static_cast<uint16_t>(s),
-                         static_cast<uint16_t>(r));
-    }
+    for (int j = 0; j < kBM / 64; ++j)
+      tma_load_im2col_4d(sa + j * 8192, tmA, bar, taps[j].cb * 64, ct.wb, ct.hb, ct.nb,
+                         static_cast<uint16_t>(taps[j].s), static_cast<uint16_t>(taps[j].r));
 #pragma unroll
     for (int j = 0; j < BN / 64; ++j) tma_load_2d_hint(sb + j * 8192, tmB, bar, n0 + 64 * j, k0, pb);
   } else {
 #pragma unroll
     for (int j = 0; j < kBM / 64; ++j) tma_load_2d_hint(sa + j * 8192, tmA, bar, m0 + 64 * j, k0, pa);
 #pragma unroll
-    for (int j = 0; j < BN / 64; ++j) {
-      int cb, r, s;
-      conv_tap(cv, n0 / 64 + j, cb, r, s);
-      tma_load_im2col_4d(sb + j * 8192, tmB, bar, cb * 64, ct.wb, ct.hb, ct.nb, static_cast<uint16_t>(s),
-                         static_cast<uint16_t>(r));
-    }
+    for (int j = 0; j < BN / 64; ++j)
+      tma_load_im2col_4d(sb + j * 8192, tmB, bar, taps[j].cb * 64, ct.wb, ct.hb, ct.nb,
+                         static_cast<uint16_t>(taps[j].s), static_cast<uint16_t>(taps[j].r));
   }
 }
 
@@ -146,14 +177,16 @@ template <int BN, bool A_MN, bool B_MN>
 __device__ __forceinline__ void mma_kblock(uint32_t d_tmem, uint32_t a_base, uint32_t b_base,
                                            bool first) {
   constexpr uint32_t idesc = idesc_bf16_f32(kBM, BN, A_MN, B_MN);
+  // K-major: a 16-element K slice is 32 bytes further along each swizzled row.
+  // MN-major: a 16-row K slice is 16 * 128 bytes further; LBO = one 64-wide box.
+  // The descriptors are built once per k-block and stepped in their address
+  // field (addr >> 4 stays below 2^14 inside shared memory, so no carry).
+  const uint64_t ad0 = A_MN ? smem_desc_sw128(a_base, 8192, 1024) : smem_desc_sw128(a_base, 16, 1024);
+  const uint64_t bd0 = B_MN ? smem_desc_sw128(b_base, 8192, 1024) : smem_desc_sw128(b_base, 16, 1024);
 #pragma unroll
   for (int k = 0; k < kBK / 16; ++k) {
-    // K-major: a 16-element K slice is 32 bytes further along each swizzled row.
-    // MN-major: a 16-row K slice is 16 * 128 bytes further; LBO = one 64-wide box.
-    uint64_t ad = A_MN ? smem_desc_sw128(a_base + k * 2048, 8192, 1024)
-                       : smem_desc_sw128(a_base + k * 32, 16, 1024);
-    uint64_t bd = B_MN ? smem_desc_sw128(b_base + k * 2048, 8192, 1024)
-                       : smem_desc_sw128(b_base + k * 32, 16, 1024);
+    const uint64_t ad = ad0 + static_cast<uint64_t>(A_MN ? k * (2048 >> 4) : k * (32 >> 4));
+    const uint64_t bd = bd0 + static_cast<uint64_t>(B_MN ? k * (2048 >> 4) : k * (32 >> 4));
     umma_bf16(d_tmem, ad, bd, idesc, (first && k == 0) ? 0u : 1u);
   }
 }
@@ -651,22 +684,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (!A_MN && !B_MN) {
         if (ep.conv.Q > 0) {   // implicit-GEMM convolution: A tiles from the im2col map
           const ConvTile ct = conv_tile(ep.conv, m0);
-          for (int kb = kb0; kb < kb1; ++kb, ++g) {
+          TapCursor tap(ep.conv, kb0);
+          for (int kb = kb0; kb < kb1; ++kb, ++g, tap.next(ep.conv)) {
             const int s = g % S;
             mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
-            load_kblock_conv<BN>(&tmA, &tmB, sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes, &full[s], ep.conv, ct,
-                                 n0, kb, pb);
+            load_kblock_conv<BN>(&tmA, &tmB, sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes, &full[s], ct, n0, kb,
+                                 tap, pb);
           }
           continue;
         }
       }
       if constexpr (A_MN && B_MN) {
         if (ep.conv.Q > 0) {   // convolution weight gradient: the im2col operand from its map
-          for (int kb = kb0; kb < kb1; ++kb, ++g) {
+          constexpr int kTaps = (kBM > BN ? kBM : BN) / 64;
+          TapCursor taps[kTaps] = {};
+          const int mn0 = (ep.conv.operand == 0 ? m0 : n0) / 64;
+#pragma unroll
+          for (int j = 0; j < kTaps; ++j) taps[j] = TapCursor(ep.conv, mn0 + j);
+          PixelCursor px(ep.conv, kb0 * kBK);
+          for (int kb = kb0; kb < kb1; ++kb, ++g, px.advance64(ep.conv)) {
             const int s = g % S;
             mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
             load_kblock_conv_wgrad<BN>(&tmA, &tmB, sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes, &full[s],
-                                       ep.conv, m0, n0, kb, pa, pb);
+                                       ep.conv, m0, n0, kb, px.tile(ep.conv), taps, pa, pb);
           }
           continue;
         }
@@ -801,12 +841,12 @@ template <int BN, bool A_MN, bool B_MN>
 __device__ __forceinline__ void mma_kblock_pair(uint32_t d_tmem, uint32_t a_base, uint32_t b_base,
                                                 bool first) {
   constexpr uint32_t idesc = idesc_bf16_f32(2 * kBM, BN, A_MN, B_MN);
+  const uint64_t ad0 = A_MN ? smem_desc_sw128(a_base, 8192, 1024) : smem_desc_sw128(a_base, 16, 1024);
+  const uint64_t bd0 = B_MN ? smem_desc_sw128(b_base, 8192, 1024) : smem_desc_sw128(b_base, 16, 1024);
 #pragma unroll
   for (int k = 0; k < kBK / 16; ++k) {
-    uint64_t ad = A_MN ? smem_desc_sw128(a_base + k * 2048, 8192, 1024)
-                       : smem_desc_sw128(a_base + k * 32, 16, 1024);
-    uint64_t bd = B_MN ? smem_desc_sw128(b_base + k * 2048, 8192, 1024)
-                       : smem_desc_sw128(b_base + k * 32, 16, 1024);
+    const uint64_t ad = ad0 + static_cast<uint64_t>(A_MN ? k * (2048 >> 4) : k * (32 >> 4));
+    const uint64_t bd = bd0 + static_cast<uint64_t>(B_MN ? k * (2048 >> 4) : k * (32 >> 4));
     umma_bf16_pair(d_tmem, ad, bd, idesc, (first && k == 0) ? 0u : 1u);
   }
 }
@@ -898,14 +938,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (!A_MN && !B_MN) {
         if (ep.conv.Q > 0) {   // implicit-GEMM convolution: this CTA's 128 A rows from the im2col map
           const ConvTile ct = conv_tile(ep.conv, m0);
-          for (int kb = 0; kb < nk; ++kb, ++g) {
+          TapCursor tap(ep.conv, 0);
+          for (int kb = 0; kb < nk; ++kb, ++g, tap.next(ep.conv)) {
             const int s = g % S;
             mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
             if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * Cfg::kStageBytes);
-            int cb, r, fs;
-            conv_tap(ep.conv, kb, cb, r, fs);
-            tma_load_im2col_4d_pair(sA + s * Cfg::kABytes, &tmA, full0 + 8 * s, cb * 64, ct.wb, ct.hb, ct.nb,
-                                    static_cast<uint16_t>(fs), static_cast<uint16_t>(r));
+            tma_load_im2col_4d_pair(sA + s * Cfg::kABytes, &tmA, full0 + 8 * s, tap.cb * 64, ct.wb, ct.hb, ct.nb,
+                                    static_cast<uint16_t>(tap.s), static_cast<uint16_t>(tap.r));
             tma_load_2d_pair(sB + s * Cfg::kBBytes, &tmB, full0 + 8 * s, kb * kBK, n0);
           }
           continue;
