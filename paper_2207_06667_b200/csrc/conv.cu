@@ -50,58 +50,76 @@ __global__ void __launch_bounds__(256) im2col_nhwc_kernel(const __nv_bfloat16* _
 // index runs over (r, s, c < c_used) densely, so a 7x7x3 stem has K = 147
 // (padded to ldo) instead of 7x7x16. A block builds kPackQ consecutive output
 // pixels of one output row: the R x Wt input patch they read is staged in
-// shared memory with coalesced 16-byte loads (zeros outside the image), a
-// per-block table maps each K index to its patch offset (no divisions in the
-// gather), and the block's kPackQ * ldo outputs are one contiguous span
-// written as coalesced 16-byte stores.
-constexpr int kPackQ = 32;
-constexpr int kPackMaxK = 1024;
+// shared memory with coalesced 16-byte loads (zeros outside the image), and
+// the block's kPackQ * ldo outputs are one contiguous span written as
+// coalesced 16-byte stores.
+constexpr int kPackQ = 56;
 
+// The patch is staged COMPACT (c_used channels per pixel, rows of Wt pixels),
+// so the K run of one filter row (s, c) is contiguous in shared memory. With
+// the C-padded pixel pitch (32 B) the 7 taps of a filter row fell on 4 bank
+// groups and the 16-bit gathers ran ~8-way bank-conflicted (716 us at batch
+// 256, ~1.6 TB/s). Each thread owns one 16-byte output column chunk `ch`
+// (8 consecutive K indices) and walks the block's pixels with it, so its 8
+// patch offsets are computed once; threads ch = 0..chunks-1 of one pixel
+// write one contiguous output row.
 __global__ void __launch_bounds__(256) im2col_nhwc_packed_kernel(const __nv_bfloat16* __restrict__ x, int N, int H,
                                                                  int W, int C, int c_used, int R, int S, int stride,
                                                                  int pad, int P, int Q,
                                                                  __nv_bfloat16* __restrict__ out, long long ldo) {
   griddep_wait();
   extern __shared__ __align__(16) uint8_t psm[];
-  int* tab = reinterpret_cast<int*>(psm);                                  // [ldo]
-  __nv_bfloat16* patch = reinterpret_cast<__nv_bfloat16*>(psm + kPackMaxK * 4);
+  unsigned short* patch = reinterpret_cast<unsigned short*>(psm);   // [R][Wt][c_used]
   const int qblocks = (Q + kPackQ - 1) / kPackQ;
   const int qb = blockIdx.x % qblocks;
   const long long np = blockIdx.x / qblocks;
   const int p = static_cast<int>(np % P), n = static_cast<int>(np / P);
   const int q0 = qb * kPackQ;
-  const int Wt = (kPackQ - 1) * stride + S;
-  const int kreal = R * S * c_used;
-  for (int k = threadIdx.x; k < ldo; k += blockDim.x) {
-    const int c = k % c_used, rs = k / c_used;
-    tab[k] = k < kreal ? ((rs / S) * Wt + rs % S) * C + c : -1;
-  }
-  const int cv = C / 8;
+  const int nq = Q - q0 < kPackQ ? Q - q0 : kPackQ;
+  const int Wt = (nq - 1) * stride + S;
   const int h0 = p * stride - pad, w0 = q0 * stride - pad;
-  for (int i = threadIdx.x; i < R * Wt * cv; i += blockDim.x) {
-    const int c8 = i % cv, pix = i / cv;
-    const int wl = pix % Wt, r = pix / Wt;
+  // stage the used channels of the R x Wt input patch (zeros outside the image)
+  for (int i = threadIdx.x; i < R * Wt; i += blockDim.x) {
+    const int r = i / Wt, wl = i - r * Wt;
     const int h = h0 + r, w = w0 + wl;
-    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-    if (h >= 0 && h < H && w >= 0 && w < W)
-      v = __ldg(reinterpret_cast<const uint4*>(x + ((static_cast<long long>(n) * H + h) * W + w) * C) + c8);
-    reinterpret_cast<uint4*>(patch)[i] = v;
+    const bool in = h >= 0 && h < H && w >= 0 && w < W;
+    const __nv_bfloat16* px = x + ((static_cast<long long>(n) * H + (in ? h : 0)) * W + (in ? w : 0)) * C;
+    if (c_used <= 8) {   // one 16-byte load covers the used channels
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      if (in) v = __ldg(reinterpret_cast<const uint4*>(px));
+      const unsigned short* e = reinterpret_cast<const unsigned short*>(&v);
+      for (int c = 0; c < c_used; ++c) patch[i * c_used + c] = e[c];
+    } else {
+      const unsigned short* e = reinterpret_cast<const unsigned short*>(px);
+      for (int c = 0; c < c_used; ++c) patch[i * c_used + c] = in ? e[c] : static_cast<unsigned short>(0);
+    }
+  }
+  const int chunks = static_cast<int>(ldo / 8);
+  const int groups = blockDim.x / chunks;
+  const int ch = threadIdx.x % chunks, qg = threadIdx.x / chunks;
+  const int krow = S * c_used;            // K run of one filter row
+  const int kreal = R * krow;
+  const int rowpitch = Wt * c_used;
+  int off[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int k = 8 * ch + j;
+    const int r = k / krow;
+    off[j] = k < kreal ? r * rowpitch + (k - r * krow) : -1;
   }
   __syncthreads();
-  const int chunks = static_cast<int>(ldo / 8);
-  const int nq = Q - q0 < kPackQ ? Q - q0 : kPackQ;
-  __nv_bfloat16* dst = out + ((static_cast<long long>(n) * P + p) * Q + q0) * ldo;
-  for (int i = threadIdx.x; i < nq * chunks; i += blockDim.x) {
-    const int ql = i / chunks, ch = i - ql * chunks;
-    const unsigned short* pb = reinterpret_cast<const unsigned short*>(patch) + ql * stride * C;
+  if (qg >= groups) return;
+  uint4* dst = reinterpret_cast<uint4*>(out + ((static_cast<long long>(n) * P + p) * Q + q0) * ldo) + ch;
+  for (int ql = qg; ql < nq; ql += groups) {
+    const unsigned short* pb = patch + ql * stride * c_used;
     uint32_t v[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int t0 = tab[8 * ch + 2 * j], t1 = tab[8 * ch + 2 * j + 1];
-      const uint32_t lo = t0 >= 0 ? pb[t0] : 0u, hi = t1 >= 0 ? pb[t1] : 0u;
+      const uint32_t lo = off[2 * j] >= 0 ? pb[off[2 * j]] : 0u;
+      const uint32_t hi = off[2 * j + 1] >= 0 ? pb[off[2 * j + 1]] : 0u;
       v[j] = lo | (hi << 16);
     }
-    reinterpret_cast<uint4*>(dst)[i] = make_uint4(v[0], v[1], v[2], v[3]);
+    dst[static_cast<long long>(ql) * chunks] = make_uint4(v[0], v[1], v[2], v[3]);
   }
 }
 
@@ -431,9 +449,9 @@ cudaError_t launch_im2col_nhwc(const __nv_bfloat16* x, int N, int H, int W, int 
                                int stride, int pad, int P, int Q, __nv_bfloat16* out, long long ldo,
                                cudaStream_t stream) {
   if (c_used < C) {
-    if (ldo > kPackMaxK || ldo % 8) return cudaErrorInvalidValue;
+    if (ldo > 8 * 256 || ldo % 8) return cudaErrorInvalidValue;
     const int Wt = (kPackQ - 1) * stride + S;
-    const int smem = kPackMaxK * 4 + R * Wt * C * 2;
+    const int smem = R * Wt * c_used * 2;
     if (smem > 200 * 1024) return cudaErrorInvalidValue;
     if (smem > 48 * 1024) {
       cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(im2col_nhwc_packed_kernel), smem);
