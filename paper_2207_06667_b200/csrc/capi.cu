@@ -409,15 +409,17 @@ int edl_conv_fwd_nhwc(const void* x, int N, int H, int W, int C, const void* w, 
              stream_sched(st)};
   ep.conv = ConvGeom{P, Q, stride, pad, S, C / 64};
   const GemmKind kind = act == EDL_ACT_RELU ? GemmKind::FwdRelu : GemmKind::FwdIdentBf16;
+  CUtensorMap tr;   // the residual, streamed by TMA in the epilogue
+  if (residual && (rc = tensor_map_out(residual, M, K, ldr, false, &tr))) return rc;
   const int pbn = pick_pair_bn(M, K, cap);
   cudaError_t e;
   if (pbn > 0) {
     if ((rc = tensor_map(w, K, Kd, ldw, 64, pbn / 2, &tb))) return rc;
-    e = launch_gemm_pair(kind, pbn, ta, tb, ty, M, K, Kd, ep, cap, st);
+    e = launch_gemm_pair(kind, pbn, ta, tb, ty, M, K, Kd, ep, cap, st, residual ? &tr : nullptr);
   } else {
     const int bn = pick_bn_cap(M, K, cap);
     if ((rc = tensor_map(w, K, Kd, ldw, 64, bn, &tb))) return rc;
-    e = launch_gemm(kind, bn, ta, tb, ty, M, K, Kd, ep, cap, st);
+    e = launch_gemm(kind, bn, ta, tb, ty, M, K, Kd, ep, cap, st, residual ? &tr : nullptr);
   }
   return e == cudaSuccess ? 0 : cuda_fail(e, "conv_fwd_nhwc");
 }
@@ -477,15 +479,17 @@ int edl_linear_fwd_residual(const void* X, long long ldx, const void* W, long lo
   if ((rc = tensor_map(X, M, K, ldx, 64, 128, &ta))) return rc;
   if ((rc = tensor_map_out(Y, M, N, ldy, false, &ty))) return rc;
   EpiArgs ep{Y, ldy, bias, reinterpret_cast<const __nv_bfloat16*>(R), ldr, 1.0f, stream_sched(as_stream(stream))};
+  CUtensorMap tr;
+  if ((rc = tensor_map_out(R, M, N, ldr, false, &tr))) return rc;
   const int pbn = pick_pair_bn(M, N, cap);
   cudaError_t e;
   if (pbn > 0) {
     if ((rc = tensor_map(W, N, K, ldw, 64, pbn / 2, &tb))) return rc;
-    e = launch_gemm_pair(GemmKind::FwdRelu, pbn, ta, tb, ty, M, N, K, ep, cap, as_stream(stream));
+    e = launch_gemm_pair(GemmKind::FwdRelu, pbn, ta, tb, ty, M, N, K, ep, cap, as_stream(stream), &tr);
   } else {
     const int bn = pick_bn_cap(M, N, cap);
     if ((rc = tensor_map(W, N, K, ldw, 64, bn, &tb))) return rc;
-    e = launch_gemm(GemmKind::FwdRelu, bn, ta, tb, ty, M, N, K, ep, cap, as_stream(stream));
+    e = launch_gemm(GemmKind::FwdRelu, bn, ta, tb, ty, M, N, K, ep, cap, as_stream(stream), &tr);
   }
   return e == cudaSuccess ? 0 : cuda_fail(e, "linear_fwd_residual");
 }

@@ -40,7 +40,7 @@ struct GemmCfg {
   static constexpr uint32_t kEpiBytes = BN * 4;          // the tile's bias slice
   static constexpr uint32_t kStoreBytes = 4 * 2 * 4096;  // TMA-store staging: two 32x32 fp32 tiles per epilogue warp
   static constexpr uint32_t kSmem =
-      kStages * kStageBytes + kStoreBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
+      kStages * kStageBytes + kStoreBytes + kEpiBytes + 1024 /*align*/ + 320 /*barriers*/;
   static_assert(kSmem <= 227 * 1024, "exceeds the sm_100 per-CTA shared memory limit");
 };
 
@@ -522,14 +522,47 @@ __device__ __forceinline__ void stage_chunk(uint8_t* stg, int lane, const float 
 // stg: this warp's two 4 KB staging tiles, used alternately by store count
 // (`stores`, per warp, carried across tiles) so a chunk is written while the
 // previous chunk's store is still reading the other tile.
+// Residual stream for EPI_RELU_BF16 (conv layers with a shortcut): the
+// residual's 32 x 32 bf16 chunks arrive by TMA in the upper 2 KB of the
+// warp's two 4 KB store-staging tiles (a bf16 output chunk uses the lower
+// 2 KB), two chunks ahead, on two per-warp mbarriers. Per-thread 16-byte
+// __ldg's of 32 different rows, one chunk ahead, left the epilogue waiting on
+// DRAM: ~1/3 of its stall samples in the 1x1 expansion convs (finding 30).
+// ri / rc count issued / consumed chunks per warp (warp-uniform), buffer
+// (count & 1), phase (count >> 1) & 1.
+struct ResStream {
+  const CUtensorMap* map;
+  uint8_t* stg;
+  uint64_t* bar;      // this warp's two barriers
+  uint32_t ri, rc;
+  __device__ __forceinline__ void issue(int lane, int col, int row0) {
+    const uint32_t b = ri & 1;
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bar[b], 2048);
+      tma_load_2d(stg + b * 4096 + 2048, map, &bar[b], col, row0);
+    }
+    ++ri;
+  }
+  // this lane's row of the next chunk (bf16 SWIZZLE_64B: 16-byte unit i at i ^ ((row / 2) % 4))
+  __device__ __forceinline__ void take(int lane, uint4 (&h)[4]) {
+    const uint32_t b = rc & 1;
+    mbar_wait(&bar[b], (rc >> 1) & 1);
+    const uint4* src = reinterpret_cast<const uint4*>(stg + b * 4096 + 2048 + lane * 64);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = src[i ^ ((lane >> 1) & 3)];
+    ++rc;
+    __syncwarp();   // every lane has read the buffer before it is refilled
+  }
+};
+
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_tile_tma(const EpiArgs& ep, uint32_t taddr, int row0, int lane, int M,
                                                   int n0, int N, const float* sb, const CUtensorMap* tmY,
-                                                  uint8_t* stg, uint32_t& stores) {
+                                                  uint8_t* stg, uint32_t& stores, ResStream* rs = nullptr) {
   // the (1 - a^2) factor or the residual: a bf16 row segment per chunk
   constexpr bool kAux = EPI == EPI_DTANH_BF16 || EPI == EPI_RELU_BF16;
   const int row = row0 + lane;
-  const bool row_ok = row < M && (EPI != EPI_RELU_BF16 || ep.aux != nullptr);
+  const bool row_ok = row < M && (EPI != EPI_RELU_BF16 || (ep.aux != nullptr && rs == nullptr));
   auto aux_ptr = [&](int c) {
     return reinterpret_cast<const uint4*>(ep.aux + static_cast<size_t>(row) * ep.ld_aux + n0 + c);
   };
@@ -559,8 +592,14 @@ __device__ __forceinline__ void epilogue_tile_tma(const EpiArgs& ep, uint32_t ta
     }
     if (c + 32 < BN) tmem_ld32_issue(taddr + c + 32, r);
     const bool live = n0 + c < N;   // warp-uniform
-    if (live) epi_math<EPI>(ep, row, M, n0 + c, N, v, sb != nullptr ? sb + c : nullptr,
-                            (kAux && n0 + c + 32 <= N) ? hc : nullptr);
+    if (EPI == EPI_RELU_BF16 && rs != nullptr && live) {
+      rs->take(lane, hc);
+      if (c + 64 < BN && n0 + c + 64 < N) rs->issue(lane, n0 + c + 64, row0);
+      epi_math<EPI>(ep, row, M, n0 + c, N, v, sb != nullptr ? sb + c : nullptr, hc);
+    } else if (live) {
+      epi_math<EPI>(ep, row, M, n0 + c, N, v, sb != nullptr ? sb + c : nullptr,
+                    (kAux && n0 + c + 32 <= N) ? hc : nullptr);
+    }
     if (live) {
       uint8_t* buf = stg + (stores & 1) * 4096;
       if (lane == 0) bulk_wait_read1();        // only the newest store (other tile) may still be reading
@@ -603,7 +642,8 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int gro
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const __grid_constant__ CUtensorMap tmY, int M, int N, int K, EpiArgs ep) {
+                const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmR, int M, int N,
+                int K, EpiArgs ep) {
   using Cfg = GemmCfg<BN>;
   unsigned* const sched = ep.sched;
   constexpr int S = Cfg::kStages;
@@ -623,6 +663,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tile_empty = tile_full + 4;   // [4]
   int* tile_ring = reinterpret_cast<int*>(tile_empty + 4);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + 4);
+  uint64_t* rbar = reinterpret_cast<uint64_t*>(tmem_slot + 2);   // [4 warps][2] residual stream
+  // the residual of EPI_RELU_BF16 arrives by TMA (ResStream)
+  const bool tma_res = EPI == EPI_RELU_BF16 && ep.aux != nullptr;
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -632,6 +675,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
     for (int s = 0; s < 4; ++s) { mbar_init(&tile_full[s], 1); mbar_init(&tile_empty[s], 1 + 4); }
+    if (tma_res) {
+      prefetch_tmap(&tmR);
+      for (int s = 0; s < 8; ++s) mbar_init(&rbar[s], 1);
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
@@ -745,6 +792,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     const int e = warp - 4;
     uint32_t stores = 0;
+    ResStream rs{&tmR, stg + e * 8192, rbar + 2 * e, 0u, 0u};
+    int staged_n0 = -1;
     for (uint32_t i = 0;; ++i) {
       const int slot = i & 3;
       mbar_wait(&tile_full[slot], (i >> 2) & 1);
@@ -758,18 +807,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       EpiArgs eps = ep;
       if (split) eps.out = static_cast<float*>(ep.out) + split * ep.split_stride;
       float* sb = sbias;
-      stage_bias<BN, EPI>(eps, sb, n0, N, static_cast<int>(threadIdx.x) - 128);
-      if constexpr (epi_has_bias<EPI>()) epi_bar_sync();
+      if (tma_res) {   // the first two residual chunks load behind this tile's MMAs
+        rs.issue(lane, n0, m0 + 32 * e);
+        if (n0 + 32 < N) rs.issue(lane, n0 + 32, m0 + 32 * e);
+      }
+      // the bias slice only changes with n0 (one n-tile: staged once per CTA);
+      // the first barrier keeps a re-stage behind every warp's previous tile
+      if (epi_has_bias<EPI>() && n0 != staged_n0) {
+        if (staged_n0 >= 0) epi_bar_sync();
+        stage_bias<BN, EPI>(eps, sb, n0, N, static_cast<int>(threadIdx.x) - 128);
+        epi_bar_sync();
+        staged_n0 = n0;
+      }
       const uint32_t as = i & 1;
       mbar_wait(&tfull[as], (i >> 1) & 1);
       tc_fence_after();
       if constexpr (epi_tma_store<EPI>())
         epilogue_tile_tma<BN, EPI>(eps, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e,
-                                   lane, M, n0, N, epi_has_bias<EPI>() ? sb : nullptr, &tmY, stg + e * 8192, stores);
+                                   lane, M, n0, N, epi_has_bias<EPI>() ? sb : nullptr, &tmY, stg + e * 8192, stores,
+                                   tma_res ? &rs : nullptr);
       else
         epilogue_tile<BN, EPI>(eps, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e + lane,
                                M, n0, N, epi_has_bias<EPI>() ? sb : nullptr);
-      if constexpr (epi_has_bias<EPI>()) epi_bar_sync();   // every warp is done with the bias slice
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[as]);
@@ -814,7 +873,7 @@ struct PairCfg {
   static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
   static constexpr uint32_t kEpiBytes = BN * 4;
   static constexpr uint32_t kStoreBytes = 4 * 2 * 4096;
-  static constexpr uint32_t kSmem = kStages * kStageBytes + kStoreBytes + kEpiBytes + 1024 + 256;
+  static constexpr uint32_t kSmem = kStages * kStageBytes + kStoreBytes + kEpiBytes + 1024 + 320;
   static_assert(kSmem <= 227 * 1024, "exceeds the sm_100 per-CTA shared memory limit");
 };
 
@@ -854,7 +913,8 @@ __device__ __forceinline__ void mma_kblock_pair(uint32_t d_tmem, uint32_t a_base
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmY, int M, int N, int K, EpiArgs ep) {
+                     const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmR, int M, int N,
+                     int K, EpiArgs ep) {
   using Cfg = PairCfg<BN>;
   unsigned* const sched = ep.sched;
   constexpr int S = Cfg::kStages;
@@ -874,6 +934,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tile_empty = tile_full + 4;   // [4] (rank 0's is the one used)
   int* tile_ring = reinterpret_cast<int*>(tile_empty + 4);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + 4);
+  uint64_t* rbar = reinterpret_cast<uint64_t*>(tmem_slot + 2);   // [4 warps][2] residual stream
+  // the residual of EPI_RELU_BF16 arrives by TMA (ResStream)
+  const bool tma_res = EPI == EPI_RELU_BF16 && ep.aux != nullptr;
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -885,6 +948,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 8); }
     // tile ring: rank 0's MMA + 4 epilogue warps, rank 1's producer + 4 epilogue warps
     for (int s = 0; s < 4; ++s) { mbar_init(&tile_full[s], 1); mbar_init(&tile_empty[s], 10); }
+    if (tma_res) {
+      prefetch_tmap(&tmR);
+      for (int s = 0; s < 8; ++s) mbar_init(&rbar[s], 1);
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc_pair<kTmemCols>(tmem_slot);
@@ -912,7 +979,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_wait_cluster(&tile_full[slot], (i >> 2) & 1);
     return tile_ring[slot];
   };
-  auto release_tile = [&](uint32_t i) { mbar_arrive_cluster(tile_empty0 + 8 * (i & 3)); };
+  auto release_tile = [&](uint32_t i) { mbar_arrive_cluster_relaxed(tile_empty0 + 8 * (i & 3)); };
 
   if (warp == 0 && lane == 0) {
     uint32_t g = 0;
@@ -981,6 +1048,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     const int e = warp - 4;
     uint32_t stores = 0;
+    ResStream rs{&tmR, stg + e * 8192, rbar + 2 * e, 0u, 0u};
+    int staged_n0 = -1;
     for (uint32_t i = 0;; ++i) {
       const int t = take_tile(i);
       __syncwarp();
@@ -991,21 +1060,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m0 = mt * 2 * kBM + static_cast<int>(rank) * kBM;
       const int n0 = nt * BN;
       float* sb = sbias;
-      stage_bias<BN, EPI>(ep, sb, n0, N, static_cast<int>(threadIdx.x) - 128);
-      if constexpr (epi_has_bias<EPI>()) epi_bar_sync();
+      if (tma_res) {   // the first two residual chunks load behind this tile's MMAs
+        rs.issue(lane, n0, m0 + 32 * e);
+        if (n0 + 32 < N) rs.issue(lane, n0 + 32, m0 + 32 * e);
+      }
+      // the bias slice only changes with n0 (one n-tile: staged once per CTA);
+      // the first barrier keeps a re-stage behind every warp's previous tile
+      if (epi_has_bias<EPI>() && n0 != staged_n0) {
+        if (staged_n0 >= 0) epi_bar_sync();
+        stage_bias<BN, EPI>(ep, sb, n0, N, static_cast<int>(threadIdx.x) - 128);
+        epi_bar_sync();
+        staged_n0 = n0;
+      }
       const uint32_t as = i & 1;
       mbar_wait(&tfull[as], (i >> 1) & 1);
       tc_fence_after();
       if constexpr (epi_tma_store<EPI>())
         epilogue_tile_tma<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e,
-                                   lane, M, n0, N, epi_has_bias<EPI>() ? sb : nullptr, &tmY, stg + e * 8192, stores);
+                                   lane, M, n0, N, epi_has_bias<EPI>() ? sb : nullptr, &tmY, stg + e * 8192, stores,
+                                   tma_res ? &rs : nullptr);
       else
         epilogue_tile<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e + lane,
                                M, n0, N, epi_has_bias<EPI>() ? sb : nullptr);
-      if constexpr (epi_has_bias<EPI>()) epi_bar_sync();   // every warp is done with the bias slice
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty0 + 8 * as);
+      if (lane == 0) mbar_arrive_cluster_relaxed(tempty0 + 8 * as);
     }
     if constexpr (epi_tma_store<EPI>()) {
       if (lane == 0) bulk_wait0();
@@ -1123,7 +1202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                              m0 + 32 * e + lane, ga.M[p], n0, ga.N[p], nullptr);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty0 + 8 * as);
+      if (lane == 0) mbar_arrive_cluster_relaxed(tempty0 + 8 * as);
     }
   }
   tc_fence_before();
@@ -1575,29 +1654,33 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ------------------------------------------------------------------ launchers
 template <int BN, bool A_MN, bool B_MN, int EPI>
 static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, int M, int N,
-                                 int K, const EpiArgs& ep, int num_sms, cudaStream_t stream) {
+                                 int K, const EpiArgs& ep, int num_sms, cudaStream_t stream,
+                                 const CUtensorMap* tr) {
+  if (EPI == EPI_RELU_BF16 && ep.aux != nullptr && tr == nullptr) return cudaErrorInvalidValue;
   auto kern = gemm_kernel<BN, A_MN, B_MN, EPI>;
   cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), GemmCfg<BN>::kSmem);
   if (e != cudaSuccess) return e;
   const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN) * ep.ksplit;
   const int grid = tiles < num_sms ? tiles : num_sms;
-  return launch_pdl(kern, dim3(grid), dim3(kThreads), GemmCfg<BN>::kSmem, stream, 1, ta, tb, ty, M, N, K, ep);
+  return launch_pdl(kern, dim3(grid), dim3(kThreads), GemmCfg<BN>::kSmem, stream, 1, ta, tb, ty, tr ? *tr : ty, M, N,
+                    K, ep);
 }
 
 template <bool A_MN, bool B_MN, int EPI>
 static cudaError_t launch_gemm_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty,
-                                  int M, int N, int K, const EpiArgs& ep, int num_sms, cudaStream_t stream) {
+                                  int M, int N, int K, const EpiArgs& ep, int num_sms, cudaStream_t stream,
+                                  const CUtensorMap* tr = nullptr) {
   switch (bn) {
-    case 64: return launch_gemm_t<64, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream);
-    case 128: return launch_gemm_t<128, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream);
-    case 256: return launch_gemm_t<256, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream);
+    case 64: return launch_gemm_t<64, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream, tr);
+    case 128: return launch_gemm_t<128, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream, tr);
+    case 256: return launch_gemm_t<256, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream, tr);
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
                         const CUtensorMap& ty, int M, int N, int K, const EpiArgs& ep, int num_sms,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, const CUtensorMap* tr) {
   switch (kind) {
     case GemmKind::FwdTanh:
       return launch_gemm_bn<false, false, EPI_TANH_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
@@ -1608,7 +1691,7 @@ cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUte
     case GemmKind::BwdWeight:
       return launch_gemm_bn<true, true, EPI_F32>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
     case GemmKind::FwdRelu:
-      return launch_gemm_bn<false, false, EPI_RELU_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
+      return launch_gemm_bn<false, false, EPI_RELU_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream, tr);
     case GemmKind::FwdIdentBf16:
       return launch_gemm_bn<false, false, EPI_BIAS_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
     case GemmKind::BwdDataPlain:
@@ -1621,29 +1704,33 @@ cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUte
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
 static cudaError_t launch_pair_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, int M, int N,
-                                 int K, const EpiArgs& ep, int num_sms, cudaStream_t stream) {
+                                 int K, const EpiArgs& ep, int num_sms, cudaStream_t stream,
+                                 const CUtensorMap* tr) {
+  if (EPI == EPI_RELU_BF16 && ep.aux != nullptr && tr == nullptr) return cudaErrorInvalidValue;
   auto kern = gemm_pair_kernel<BN, A_MN, B_MN, EPI>;
   cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), PairCfg<BN>::kSmem);
   if (e != cudaSuccess) return e;
   const int tiles = ((M + 2 * kBM - 1) / (2 * kBM)) * ((N + BN - 1) / BN);
   const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
   if (pairs < 1) return cudaErrorInvalidValue;
-  return launch_pdl(kern, dim3(2 * pairs), dim3(kThreads), PairCfg<BN>::kSmem, stream, 2, ta, tb, ty, M, N, K, ep);
+  return launch_pdl(kern, dim3(2 * pairs), dim3(kThreads), PairCfg<BN>::kSmem, stream, 2, ta, tb, ty, tr ? *tr : ty,
+                    M, N, K, ep);
 }
 
 template <bool A_MN, bool B_MN, int EPI>
 static cudaError_t launch_pair_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, int M,
-                                  int N, int K, const EpiArgs& ep, int num_sms, cudaStream_t stream) {
+                                  int N, int K, const EpiArgs& ep, int num_sms, cudaStream_t stream,
+                                  const CUtensorMap* tr = nullptr) {
   switch (bn) {
-    case 128: return launch_pair_t<128, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream);
-    case 256: return launch_pair_t<256, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream);
+    case 128: return launch_pair_t<128, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream, tr);
+    case 256: return launch_pair_t<256, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream, tr);
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_gemm_pair(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
                              const CUtensorMap& ty, int M, int N, int K, const EpiArgs& ep, int num_sms,
-                             cudaStream_t stream) {
+                             cudaStream_t stream, const CUtensorMap* tr) {
   switch (kind) {
     case GemmKind::FwdTanh:
       return launch_pair_bn<false, false, EPI_TANH_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
@@ -1652,7 +1739,7 @@ cudaError_t launch_gemm_pair(GemmKind kind, int bn, const CUtensorMap& ta, const
     case GemmKind::BwdData:
       return launch_pair_bn<false, true, EPI_DTANH_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
     case GemmKind::FwdRelu:
-      return launch_pair_bn<false, false, EPI_RELU_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
+      return launch_pair_bn<false, false, EPI_RELU_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream, tr);
     case GemmKind::FwdIdentBf16:
       return launch_pair_bn<false, false, EPI_BIAS_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
     case GemmKind::BwdDataPlain:

@@ -113,9 +113,11 @@ cudaError_t launch_gemm_grouped_pair_bwd_weight(const GroupMaps& maps, const Gro
 
 // ty: the output's TMA-store map (32 x 32 boxes; tensor_map_out) for the
 // bias / tanh / (1-a^2) epilogues; ignored (any valid map) for BwdWeight.
+// tr: FwdRelu with a residual (ep.aux) only -- the residual's 32 x 32 box map
+// (tensor_map_out on ep.aux), streamed into shared memory by TMA.
 cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
                         const CUtensorMap& ty, int M, int N, int K, const EpiArgs& ep, int num_sms,
-                        cudaStream_t stream);
+                        cudaStream_t stream, const CUtensorMap* tr = nullptr);
 // Stream-ordered flag fallbacks (exchange.cu).
 cudaError_t launch_flag_wait(const uint32_t* addr, uint32_t value, cudaStream_t stream);
 cudaError_t launch_flag_write(uint32_t* addr, uint32_t value, cudaStream_t stream);
@@ -128,7 +130,7 @@ cudaError_t launch_nvls_allreduce_sgd(float* mc_grad, float* mc_param, void* mc_
 // map box covers bn/2 rows (K-major) or bn/2 columns (MN-major).
 cudaError_t launch_gemm_pair(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
                              const CUtensorMap& ty, int M, int N, int K, const EpiArgs& ep, int num_sms,
-                             cudaStream_t stream);
+                             cudaStream_t stream, const CUtensorMap* tr = nullptr);
 cudaError_t launch_teacher_head(int bn, int kmax, const CUtensorMap& ta, const CUtensorMap& tb,
                                 int M, int N, int K, const HeadArgs& hp, cudaStream_t stream);
 

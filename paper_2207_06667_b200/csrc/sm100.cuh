@@ -267,6 +267,13 @@ __device__ __forceinline__ void st_dsmem_s32(uint32_t addr, int v) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
 }
+// The same with relaxed semantics: for arrivals that publish no memory writes
+// (a TMEM accumulator or a tile-ring slot is free). The .release.cluster form
+// is a cluster-scope fence per arrive (ncu: MEMBAR stalls at the epilogue's
+// tmem-empty arrive in the K = 64 conv GEMMs, where it runs once per tile).
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
+}
 // Wait on a local mbarrier whose arrivals may come from another CTA of the
 // cluster, with cluster-scope acquire (their shared::cluster stores visible).
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
