@@ -674,7 +674,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tmB);
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
-    for (int s = 0; s < 4; ++s) { mbar_init(&tile_full[s], 1); mbar_init(&tile_empty[s], 1 + 4); }
+    // tile ring consumers: the MMA thread, the second producer, 4 epilogue warps
+    for (int s = 0; s < 4; ++s) { mbar_init(&tile_full[s], 1); mbar_init(&tile_empty[s], 2 + 4); }
     if (tma_res) {
       prefetch_tmap(&tmR);
       for (int s = 0; s < 8; ++s) mbar_init(&rbar[s], 1);
@@ -714,16 +715,31 @@ __global__ void __launch_bounds__(kThreads, 1)
     return sched ? static_cast<int>(atomicAdd(sched, 1u)) : static_cast<int>(blockIdx.x + i * gridDim.x);
   };
 
-  if (warp == 0 && lane == 0) {
+  if ((warp == 0 || warp == 3) && lane == 0) {
+    // Two producer threads split the k-blocks by parity (warp 0: even, warp 3:
+    // odd; S is even, so each owns every other stage). One thread's issue
+    // chain (barrier wait, expect_tx, two TMA issues, cursor update: ~50
+    // instructions at several cycles each) is longer than a 64- or 128-wide
+    // k-block's 128-256 MMA cycles (ncu, finding 32). Warp 0 claims tiles
+    // and publishes them; warp 3 reads them from the ring like the MMA role.
+    static_assert(S % 2 == 0, "the producer split needs an even stage count");
+    const uint32_t par = warp == 0 ? 0u : 1u;
     uint64_t pa, pb;
     gemm_policies<EPI>(pa, pb);
     uint32_t g = 0;
     for (int i = 0;; ++i) {
       const int slot = i & 3;
-      mbar_wait(&tile_empty[slot], ((i >> 2) & 1) ^ 1);
-      const int t = next_tile(i);
-      tile_ring[slot] = t;
-      mbar_arrive(&tile_full[slot]);
+      int t;
+      if (par == 0) {
+        mbar_wait(&tile_empty[slot], ((i >> 2) & 1) ^ 1);
+        t = next_tile(i);
+        tile_ring[slot] = t;
+        mbar_arrive(&tile_full[slot]);
+      } else {
+        mbar_wait(&tile_full[slot], (i >> 2) & 1);
+        t = tile_ring[slot];
+        mbar_arrive(&tile_empty[slot]);
+      }
       if (t >= tiles) break;
       int mt, nt, kb0, kb1;
       decode(t, mt, nt, kb0, kb1);
@@ -733,6 +749,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const ConvTile ct = conv_tile(ep.conv, m0);
           TapCursor tap(ep.conv, kb0);
           for (int kb = kb0; kb < kb1; ++kb, ++g, tap.next(ep.conv)) {
+            if ((g & 1u) != par) continue;
             const int s = g % S;
             mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
             load_kblock_conv<BN>(&tmA, &tmB, sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes, &full[s], ct, n0, kb,
@@ -750,6 +767,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < kTaps; ++j) taps[j] = TapCursor(ep.conv, mn0 + j);
           PixelCursor px(ep.conv, kb0 * kBK);
           for (int kb = kb0; kb < kb1; ++kb, ++g, px.advance64(ep.conv)) {
+            if ((g & 1u) != par) continue;
             const int s = g % S;
             mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
             load_kblock_conv_wgrad<BN>(&tmA, &tmB, sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes, &full[s],
@@ -759,6 +777,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       for (int kb = kb0; kb < kb1; ++kb, ++g) {
+        if ((g & 1u) != par) continue;
         const int s = g % S;
         mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
         load_kblock<BN, A_MN, B_MN>(&tmA, &tmB, sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes,
