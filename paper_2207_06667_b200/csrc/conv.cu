@@ -174,6 +174,130 @@ __global__ void __launch_bounds__(256) maxpool_nhwc_kernel(const __nv_bfloat16* 
   }
 }
 
+// 3x3 / stride 2 case of maxpool_nhwc_kernel (the stem pool): the nine
+// window loads are issued unconditionally from clamped addresses (invalid
+// taps masked to -inf afterwards), so each thread has all nine 16-byte loads
+// in flight; the generic kernel's bounds branches serialised them (240 us at
+// batch 256, ~2.2 TB/s). Same first-maximum scan order and argmax words.
+__global__ void __launch_bounds__(256) maxpool3s2_nhwc_kernel(const __nv_bfloat16* __restrict__ x, int N, int H,
+                                                              int W, int C, int pad, int P, int Q,
+                                                              __nv_bfloat16* __restrict__ out,
+                                                              uint32_t* __restrict__ argmax) {
+  griddep_wait();
+  const int cv = C / 8;
+  const int total = N * P * Q * cv;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c8 = i % cv;
+    const int m = i / cv;
+    const int q = m % Q;
+    const int nq = m / Q;
+    const int p = nq % P;
+    const int n = nq / P;
+    const int h0 = 2 * p - pad, w0 = 2 * q - pad;
+    uint4 v[9];
+    bool ok[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        const int h = h0 + r, w = w0 + s;
+        ok[3 * r + s] = h >= 0 && h < H && w >= 0 && w < W;
+        const int hc = h < 0 ? 0 : (h >= H ? H - 1 : h), wc = w < 0 ? 0 : (w >= W ? W - 1 : w);
+        v[3 * r + s] = __ldg(reinterpret_cast<const uint4*>(x + ((static_cast<long long>(n) * H + hc) * W + wc) * C) + c8);
+      }
+    }
+    float best[8];
+    uint32_t arg = 0xFFFFFFFFu;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) best[j] = -INFINITY;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v[t]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float f = ok[t] ? __bfloat162float(b[j]) : -INFINITY;
+        const bool gt = f > best[j];
+        best[j] = gt ? f : best[j];
+        arg = gt ? ((arg & ~(0xFu << (4 * j))) | (static_cast<uint32_t>(t) << (4 * j))) : arg;
+      }
+    }
+    uint4 o;
+    o.x = pack_bf16x2(best[0], best[1]);
+    o.y = pack_bf16x2(best[2], best[3]);
+    o.z = pack_bf16x2(best[4], best[5]);
+    o.w = pack_bf16x2(best[6], best[7]);
+    *reinterpret_cast<uint4*>(out + static_cast<long long>(m) * C + 8 * c8) = o;
+    if (argmax != nullptr) argmax[i] = arg;
+  }
+}
+
+// Stride-2 col2im with R, S <= 4: an output row h receives taps r = r0 and
+// r0 + 2 only (r0 = (h + pad) % 2), likewise s, so the <= 4 contributions
+// are enumerated directly and their loads issued together from clamped
+// addresses (masked afterwards), in the generic kernel's (r, s) order: the
+// same fp32 sums. The generic kernel's parity / bounds branches serialised
+// its loads (the student's stride-2 data gradients: 520 us per step).
+__global__ void __launch_bounds__(256) col2im_s2_nhwc_kernel(const __nv_bfloat16* __restrict__ dcol, long long ldc,
+                                                             int N, int H, int W, int C, int R, int S, int pad,
+                                                             int P, int Q, const __nv_bfloat16* __restrict__ add,
+                                                             const __nv_bfloat16* __restrict__ mask,
+                                                             __nv_bfloat16* __restrict__ dx) {
+  griddep_wait();
+  const int cv = C / 8;
+  const int total = N * H * W * cv;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c8 = i % cv;
+    const int pix = i / cv;
+    const int w = pix % W;
+    const int nh = pix / W;
+    const int h = nh % H;
+    const int n = nh / H;
+    const int r0 = (h + pad) & 1, s0 = (w + pad) & 1;
+    uint4 v[4];
+    bool ok[4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int r = r0 + 2 * a, s = s0 + 2 * b;
+        const int p = (h + pad - r) >> 1, q = (w + pad - s) >> 1;   // exact: h + pad - r is even
+        const bool valid = r < R && s < S && h + pad - r >= 0 && w + pad - s >= 0 && p < P && q < Q;
+        ok[2 * a + b] = valid;
+        const long long m = valid ? (static_cast<long long>(n) * P + p) * Q + q : 0;
+        const int rs = valid ? r * S + s : 0;
+        v[2 * a + b] = __ldg(reinterpret_cast<const uint4*>(dcol + m * ldc + static_cast<long long>(rs) * C) + c8);
+      }
+    }
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (!ok[t]) continue;
+      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v[t]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(b[j]);
+    }
+    const long long off = static_cast<long long>(pix) * C + 8 * c8;
+    if (add != nullptr) {
+      const uint4 a4 = __ldg(reinterpret_cast<const uint4*>(add + off));
+      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&a4);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(b[j]);
+    }
+    if (mask != nullptr) {
+      const uint4 m4 = __ldg(reinterpret_cast<const uint4*>(mask + off));
+      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&m4);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = __bfloat162float(b[j]) > 0.f ? acc[j] : 0.f;
+    }
+    uint4 o;
+    o.x = pack_bf16x2(acc[0], acc[1]);
+    o.y = pack_bf16x2(acc[2], acc[3]);
+    o.z = pack_bf16x2(acc[4], acc[5]);
+    o.w = pack_bf16x2(acc[6], acc[7]);
+    *reinterpret_cast<uint4*>(dx + off) = o;
+  }
+}
+
 // Global average pool: block = one image; threads over 8-channel vectors,
 // each summing its channels over all H*W pixels (coalesced across threads).
 __global__ void __launch_bounds__(256) avgpool_nhwc_kernel(const __nv_bfloat16* __restrict__ x, int HW, int C,
@@ -473,6 +597,9 @@ cudaError_t launch_maxpool_nhwc(const __nv_bfloat16* x, int N, int H, int W, int
                                 int P, int Q, __nv_bfloat16* out, uint32_t* argmax, cudaStream_t stream) {
   if (argmax != nullptr && k * k > 15) return cudaErrorInvalidValue;
   const long long work = static_cast<long long>(N) * P * Q * (C / 8);
+  if (k == 3 && stride == 2 && fits32(work) && fits32(static_cast<long long>(N) * H * W * C))
+    return launch_pdl(maxpool3s2_nhwc_kernel, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, pad, P,
+                      Q, out, argmax);
   if (fits32(work))
     return launch_pdl(maxpool_nhwc_kernel<int>, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, k,
                       stride, pad, P, Q, out, argmax);
@@ -489,6 +616,9 @@ cudaError_t launch_col2im_nhwc(const __nv_bfloat16* dcol, long long ldc, int N, 
                                int stride, int pad, int P, int Q, const __nv_bfloat16* add,
                                const __nv_bfloat16* mask, __nv_bfloat16* dx, cudaStream_t stream) {
   const long long work = static_cast<long long>(N) * H * W * (C / 8);
+  if (stride == 2 && R <= 4 && S <= 4 && fits32(static_cast<long long>(N) * H * W * C))
+    return launch_pdl(col2im_s2_nhwc_kernel, dim3(grid_for(work)), dim3(256), 0, stream, 1, dcol, ldc, N, H, W, C, R,
+                      S, pad, P, Q, add, mask, dx);
   if (fits32(work))
     return launch_pdl(col2im_nhwc_kernel<int>, dim3(grid_for(work)), dim3(256), 0, stream, 1, dcol, ldc, N, H, W, C,
                       R, S, stride, pad, P, Q, add, mask, dx);
