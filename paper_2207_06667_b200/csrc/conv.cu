@@ -63,11 +63,20 @@ constexpr int kPackQ = 56;
 // (8 consecutive K indices) and walks the block's pixels with it, so its 8
 // patch offsets are computed once; threads ch = 0..chunks-1 of one pixel
 // write one contiguous output row.
+// CU / RR / ST / LDO: compile-time c_used, R = S, stride and ldo (0: the
+// runtime argument); the <3, 7, 2, 160> instance (the RGB stem) unrolls the
+// staging and the gather (the runtime-shaped loops ran ~225 instructions per
+// 16-byte output chunk, ALU-bound at 487 us per batch of 256).
+template <int CU, int RR, int ST, int LDO>
 __global__ void __launch_bounds__(256) im2col_nhwc_packed_kernel(const __nv_bfloat16* __restrict__ x, int N, int H,
-                                                                 int W, int C, int c_used, int R, int S, int stride,
-                                                                 int pad, int P, int Q,
-                                                                 __nv_bfloat16* __restrict__ out, long long ldo) {
+                                                                 int W, int C, int c_used_rt, int R_rt, int S_rt,
+                                                                 int stride_rt, int pad, int P, int Q,
+                                                                 __nv_bfloat16* __restrict__ out, long long ldo_rt) {
   griddep_wait();
+  const int c_used = CU > 0 ? CU : c_used_rt;
+  const int R = RR > 0 ? RR : R_rt, S = RR > 0 ? RR : S_rt;
+  const int stride = ST > 0 ? ST : stride_rt;
+  const long long ldo = LDO > 0 ? LDO : ldo_rt;
   extern __shared__ __align__(16) uint8_t psm[];
   unsigned short* patch = reinterpret_cast<unsigned short*>(psm);   // [R][Wt][c_used]
   const int qblocks = (Q + kPackQ - 1) / kPackQ;
@@ -105,19 +114,22 @@ __global__ void __launch_bounds__(256) im2col_nhwc_packed_kernel(const __nv_bflo
   for (int j = 0; j < 8; ++j) {
     const int k = 8 * ch + j;
     const int r = k / krow;
-    off[j] = k < kreal ? r * rowpitch + (k - r * krow) : -1;
+    off[j] = k < kreal ? r * rowpitch + (k - r * krow) : 0;   // K padding: any in-patch element, masked below
   }
+  uint32_t keep[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    keep[j] = (8 * ch + 2 * j < kreal ? 0xFFFFu : 0u) | (8 * ch + 2 * j + 1 < kreal ? 0xFFFF0000u : 0u);
   __syncthreads();
   if (qg >= groups) return;
   uint4* dst = reinterpret_cast<uint4*>(out + ((static_cast<long long>(n) * P + p) * Q + q0) * ldo) + ch;
   for (int ql = qg; ql < nq; ql += groups) {
-    const unsigned short* pb = patch + ql * stride * c_used;
+    const int base = ql * stride * c_used;
     uint32_t v[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const uint32_t lo = off[2 * j] >= 0 ? pb[off[2 * j]] : 0u;
-      const uint32_t hi = off[2 * j + 1] >= 0 ? pb[off[2 * j + 1]] : 0u;
-      v[j] = lo | (hi << 16);
+      v[j] = (static_cast<uint32_t>(patch[base + off[2 * j]]) | (static_cast<uint32_t>(patch[base + off[2 * j + 1]]) << 16)) &
+             keep[j];
     }
     dst[static_cast<long long>(ql) * chunks] = make_uint4(v[0], v[1], v[2], v[3]);
   }
@@ -206,27 +218,43 @@ __global__ void __launch_bounds__(256) maxpool3s2_nhwc_kernel(const __nv_bfloat1
         v[3 * r + s] = __ldg(reinterpret_cast<const uint4*>(x + ((static_cast<long long>(n) * H + hc) * W + wc) * C) + c8);
       }
     }
-    float best[8];
-    uint32_t arg = 0xFFFFFFFFu;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) best[j] = -INFINITY;
+    // Packed bf16x2 arithmetic (the per-lane float scan was ALU-bound, 362
+    // instructions per output vector): invalid taps become -inf, the max is
+    // four HMNMX2 per tap, and a scan from the last tap to the first writes
+    // each tap's equal-to-max lanes into the output and argmax word, so the
+    // FIRST maximum in scan order wins, value (incl. the sign of a zero) and
+    // position, exactly as the strict '>' scan.
+    uint32_t mx[4] = {0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u};   // -inf
 #pragma unroll
     for (int t = 0; t < 9; ++t) {
-      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v[t]);
+      if (!ok[t]) v[t] = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+      const uint32_t* vt = reinterpret_cast<const uint32_t*>(&v[t]);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float f = ok[t] ? __bfloat162float(b[j]) : -INFINITY;
-        const bool gt = f > best[j];
-        best[j] = gt ? f : best[j];
-        arg = gt ? ((arg & ~(0xFu << (4 * j))) | (static_cast<uint32_t>(t) << (4 * j))) : arg;
+      for (int k = 0; k < 4; ++k) {
+        const __nv_bfloat162 r = __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&mx[k]),
+                                         *reinterpret_cast<const __nv_bfloat162*>(&vt[k]));
+        mx[k] = *reinterpret_cast<const uint32_t*>(&r);
       }
     }
-    uint4 o;
-    o.x = pack_bf16x2(best[0], best[1]);
-    o.y = pack_bf16x2(best[2], best[3]);
-    o.z = pack_bf16x2(best[4], best[5]);
-    o.w = pack_bf16x2(best[6], best[7]);
-    *reinterpret_cast<uint4*>(out + static_cast<long long>(m) * C + 8 * c8) = o;
+    uint32_t o[4] = {mx[0], mx[1], mx[2], mx[3]};
+    uint32_t arg = 0xFFFFFFFFu;
+#pragma unroll
+    for (int t = 8; t >= 0; --t) {
+      const uint32_t* vt = reinterpret_cast<const uint32_t*>(&v[t]);
+      uint32_t e[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        e[k] = __heq2_mask(*reinterpret_cast<const __nv_bfloat162*>(&vt[k]),
+                           *reinterpret_cast<const __nv_bfloat162*>(&mx[k]));
+        o[k] = (vt[k] & e[k]) | (o[k] & ~e[k]);
+      }
+      // lane 2k <- low half of e[k], lane 2k + 1 <- high half: nibble masks
+      const uint32_t p01 = __byte_perm(e[0], e[1], 0x6420), p23 = __byte_perm(e[2], e[3], 0x6420);
+      const uint32_t lo = __byte_perm(p01, p23, 0x6420), hi = __byte_perm(p01, p23, 0x7531);
+      const uint32_t nm = (lo & 0x0F0F0F0Fu) | (hi & 0xF0F0F0F0u);
+      arg = (arg & ~nm) | (nm & (static_cast<uint32_t>(t) * 0x11111111u));
+    }
+    *reinterpret_cast<uint4*>(out + static_cast<long long>(m) * C + 8 * c8) = make_uint4(o[0], o[1], o[2], o[3]);
     if (argmax != nullptr) argmax[i] = arg;
   }
 }
@@ -560,6 +588,80 @@ __global__ void __launch_bounds__(256) maxpool_bwd_argmax_nhwc_kernel(const uint
   }
 }
 
+// 3x3 / stride 2 case of maxpool_bwd_argmax_nhwc_kernel (the stem pool's
+// backward): input row h lies in windows p with 2p - pad + r = h, i.e. taps
+// r = r0, r0 + 2 (r0 = (h + pad) & 1), likewise s: <= 4 windows, whose argmax
+// words, dy vectors and the mask are all loaded up front from clamped
+// addresses (invalid windows masked afterwards). Same (r, s) summation
+// order as the generic kernel, whose branches serialised the loads.
+__global__ void __launch_bounds__(256) maxpool3s2_bwd_nhwc_kernel(const uint32_t* __restrict__ argmax, int N,
+                                                                  int H, int W, int C, int pad, int P, int Q,
+                                                                  const __nv_bfloat16* __restrict__ dy,
+                                                                  const __nv_bfloat16* __restrict__ mask,
+                                                                  __nv_bfloat16* __restrict__ dx) {
+  griddep_wait();
+  const int cv = C / 8;
+  const int n = blockIdx.x / H, h = blockIdx.x - n * H;   // one block per input row (n, h)
+  const int r0 = (h + pad) & 1;
+  bool rok[2];
+  long long prow[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int r = r0 + 2 * u, p = (h + pad - r) >> 1;
+    rok[u] = r < 3 && h + pad - r >= 0 && p < P;
+    prow[u] = rok[u] ? (static_cast<long long>(n) * P + p) * Q : 0;
+  }
+  for (int i = threadIdx.x; i < W * cv; i += blockDim.x) {
+    const int w = i / cv, c8 = i - w * cv;
+    const int s0 = (w + pad) & 1;
+    const long long off = ((static_cast<long long>(n) * H + h) * W + w) * C + 8 * c8;
+    uint4 m4 = make_uint4(0u, 0u, 0u, 0u);
+    if (mask != nullptr) m4 = __ldg(reinterpret_cast<const uint4*>(mask + off));
+    // per window: the lanes whose argmax nibble is this window's tap, as a
+    // zero-nibble test of a ^ (tap * 0x11111111), turned into bf16x2 masks
+    // that zero the other lanes' dy (acc starts at +0 and so is never -0:
+    // adding a masked +0 leaves it bitwise unchanged, as skipping would)
+    uint4 g[4];
+    uint32_t z[4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int r = r0 + 2 * u, s = s0 + 2 * v, q = (w + pad - s) >> 1;
+        const bool valid = rok[u] && s < 3 && w + pad - s >= 0 && q < Q;
+        const long long win = valid ? prow[u] + q : 0;
+        const uint32_t x = __ldg(argmax + win * cv + c8) ^ (static_cast<uint32_t>(r * 3 + s) * 0x11111111u);
+        g[2 * u + v] = __ldg(reinterpret_cast<const uint4*>(dy + win * C) + c8);
+        const uint32_t zz = ~(((x & 0x77777777u) + 0x77777777u) | x | 0x77777777u);   // bit 4j+3: nibble j == 0
+        z[2 * u + v] = valid ? zz : 0u;
+      }
+    }
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const uint32_t* gt = reinterpret_cast<const uint32_t*>(&g[t]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t lo = (z[t] >> (8 * k + 3)) & 1u, hi = (z[t] >> (8 * k + 7)) & 1u;
+        const uint32_t gm = gt[k] & ((lo * 0xFFFFu) | (hi * 0xFFFF0000u));
+        acc[2 * k] += __uint_as_float(gm << 16);
+        acc[2 * k + 1] += __uint_as_float(gm & 0xFFFF0000u);
+      }
+    }
+    if (mask != nullptr) {
+      const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&m4);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = __bfloat162float(mb[j]) > 0.f ? acc[j] : 0.f;
+    }
+    uint4 o;
+    o.x = pack_bf16x2(acc[0], acc[1]);
+    o.y = pack_bf16x2(acc[2], acc[3]);
+    o.z = pack_bf16x2(acc[4], acc[5]);
+    o.w = pack_bf16x2(acc[6], acc[7]);
+    *reinterpret_cast<uint4*>(dx + off) = o;
+  }
+}
+
 bool fits32(long long n) { return n < (1LL << 31) - (1LL << 24); }
 
 int grid_for(long long work) {
@@ -577,13 +679,19 @@ cudaError_t launch_im2col_nhwc(const __nv_bfloat16* x, int N, int H, int W, int 
     const int Wt = (kPackQ - 1) * stride + S;
     const int smem = R * Wt * c_used * 2;
     if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    const bool stem = c_used == 3 && R == 7 && S == 7 && stride == 2 && ldo == 160;
+    const void* kern = stem ? reinterpret_cast<const void*>(im2col_nhwc_packed_kernel<3, 7, 2, 160>)
+                            : reinterpret_cast<const void*>(im2col_nhwc_packed_kernel<0, 0, 0, 0>);
     if (smem > 48 * 1024) {
-      cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(im2col_nhwc_packed_kernel), smem);
+      cudaError_t e = ensure_kernel_attrs(kern, smem);
       if (e != cudaSuccess) return e;
     }
     const long long blocks = static_cast<long long>(N) * P * ((Q + kPackQ - 1) / kPackQ);
-    return launch_pdl(im2col_nhwc_packed_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), smem, stream, 1, x,
-                      N, H, W, C, c_used, R, S, stride, pad, P, Q, out, ldo);
+    if (stem)
+      return launch_pdl(im2col_nhwc_packed_kernel<3, 7, 2, 160>, dim3(static_cast<unsigned>(blocks)), dim3(256), smem,
+                        stream, 1, x, N, H, W, C, c_used, R, S, stride, pad, P, Q, out, ldo);
+    return launch_pdl(im2col_nhwc_packed_kernel<0, 0, 0, 0>, dim3(static_cast<unsigned>(blocks)), dim3(256), smem,
+                      stream, 1, x, N, H, W, C, c_used, R, S, stride, pad, P, Q, out, ldo);
   }
   const long long work = static_cast<long long>(N) * P * Q * R * S * (C / 8);
   if (fits32(work))
@@ -650,8 +758,8 @@ cudaError_t launch_maxpool_bwd_argmax_nhwc(const uint32_t* argmax, int N, int H,
   if (rows > 0x7fffffffLL) return cudaErrorInvalidValue;
   const int threads = W * (C / 8) >= 256 ? 256 : ((W * (C / 8) + 31) / 32) * 32;
   if (k == 3 && stride == 2)
-    return launch_pdl(maxpool_bwd_argmax_nhwc_kernel<3, 2>, dim3(static_cast<unsigned>(rows)), dim3(threads), 0,
-                      stream, 1, argmax, N, H, W, C, k, stride, pad, P, Q, dy, mask, dx);
+    return launch_pdl(maxpool3s2_bwd_nhwc_kernel, dim3(static_cast<unsigned>(rows)), dim3(threads), 0, stream, 1,
+                      argmax, N, H, W, C, pad, P, Q, dy, mask, dx);
   return launch_pdl(maxpool_bwd_argmax_nhwc_kernel<0, 0>, dim3(static_cast<unsigned>(rows)), dim3(threads), 0, stream,
                     1, argmax, N, H, W, C, k, stride, pad, P, Q, dy, mask, dx);
 }

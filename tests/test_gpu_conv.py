@@ -243,38 +243,47 @@ def test_bwd_weight_splitk_vs_torch(M, N, K, ld_pad, ws_scale):
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
 
 
-@pytest.mark.parametrize("k,st,pd", [(3, 2, 1), (2, 2, 0)])
-def test_maxpool_bwd_vs_torch_with_ties(k, st, pd):
+@pytest.mark.parametrize("k,st,pd,H", [(3, 2, 1, 17), (3, 2, 1, 16), (3, 2, 0, 15), (2, 2, 0, 17)])
+def test_maxpool_bwd_vs_torch_with_ties(k, st, pd, H):
     """edl_maxpool_bwd_nhwc (3x3 / 2 / pad 1, the stem pool) against torch
     autograd, on integer-valued inputs so windows have tied maxima: the
-    gradient goes to the first maximum in scan order, as torch's does."""
+    gradient goes to the first maximum in scan order, as torch's does. The
+    3x3 / 2 shapes run the branch-free stem kernels (forward and argmax
+    backward), checked against torch's forward and the generic backward; the
+    masked backward (ReLU mask of the pool input) against dx * (x > 0)."""
     import torch.nn.functional as F
 
     from paper_2207_06667_b200 import _lib
     from paper_2207_06667_b200.resnet import to_nhwc
-    rng = np.random.default_rng(3)
-    x = rng.integers(-3, 4, size=(3, 16, 17, 17)).astype(np.float32)
-    P = (17 + 2 * pd - k) // st + 1
+    rng = np.random.default_rng(3 + H)
+    x = rng.integers(-3, 4, size=(3, 16, H, H)).astype(np.float32)
+    P = (H + 2 * pd - k) // st + 1
     gy = rng.normal(size=(3, 16, P, P)).astype(np.float32)
     xt = torch.from_numpy(x).requires_grad_(True)
-    F.max_pool2d(xt, k, st, pd).backward(ref._bf(torch.from_numpy(gy)))
+    yt = F.max_pool2d(xt, k, st, pd)
+    yt.backward(ref._bf(torch.from_numpy(gy)))
     xd, dyd = to_nhwc(x, "cuda"), to_nhwc(gy, "cuda")
     dx = torch.empty_like(xd)
-    _lib.call("edl_maxpool_bwd_nhwc", xd.data_ptr(), 3, 17, 17, 16, k, st, pd, dyd.data_ptr(), None, dx.data_ptr(), _s())
+    _lib.call("edl_maxpool_bwd_nhwc", xd.data_ptr(), 3, H, H, 16, k, st, pd, dyd.data_ptr(), None, dx.data_ptr(), _s())
     # the training pair: forward records the argmax words, backward gathers from them
     y_plain = torch.empty(3, P, P, 16, dtype=torch.bfloat16, device="cuda")
     y_arg = torch.empty_like(y_plain)
     arg = torch.empty(3 * P * P * 2, dtype=torch.int32, device="cuda")
-    _lib.call("edl_maxpool_nhwc", xd.data_ptr(), 3, 17, 17, 16, k, st, pd, y_plain.data_ptr(), _s())
-    _lib.call("edl_maxpool_argmax_nhwc", xd.data_ptr(), 3, 17, 17, 16, k, st, pd, y_arg.data_ptr(), arg.data_ptr(), _s())
+    _lib.call("edl_maxpool_nhwc", xd.data_ptr(), 3, H, H, 16, k, st, pd, y_plain.data_ptr(), _s())
+    _lib.call("edl_maxpool_argmax_nhwc", xd.data_ptr(), 3, H, H, 16, k, st, pd, y_arg.data_ptr(), arg.data_ptr(), _s())
     dx2 = torch.empty_like(xd)
-    _lib.call("edl_maxpool_bwd_argmax_nhwc", arg.data_ptr(), 3, 17, 17, 16, k, st, pd, dyd.data_ptr(), None,
+    _lib.call("edl_maxpool_bwd_argmax_nhwc", arg.data_ptr(), 3, H, H, 16, k, st, pd, dyd.data_ptr(), None,
               dx2.data_ptr(), _s())
+    dx3 = torch.empty_like(xd)
+    _lib.call("edl_maxpool_bwd_argmax_nhwc", arg.data_ptr(), 3, H, H, 16, k, st, pd, dyd.data_ptr(), xd.data_ptr(),
+              dx3.data_ptr(), _s())
     torch.cuda.synchronize()
     got = dx.float().cpu().permute(0, 3, 1, 2)
     torch.testing.assert_close(got, ref._bf(xt.grad), rtol=1e-2, atol=1e-2)
+    assert torch.equal(y_plain.float().cpu().permute(0, 3, 1, 2), yt.detach())
     assert torch.equal(y_arg, y_plain)
     assert torch.equal(dx2, dx)
+    assert torch.equal(dx3, torch.where(xd > 0, dx, torch.zeros_like(dx)))
 
 
 @pytest.mark.parametrize("N,C,H,K,k,stride,relu,residual", [
@@ -404,3 +413,28 @@ def test_conv_dgrad_implicit_vs_torch(N, C, H, K, k, use_add, use_mask):
     torch.cuda.synchronize()
     got = dx.float().cpu().permute(0, 3, 1, 2)
     assert _rel(got, want) < 1e-2
+
+
+@pytest.mark.parametrize("N,H", [(2, 224), (3, 30)])
+def test_packed_stem_im2col_bitwise(N, H):
+    """edl_im2col_nhwc packed (c_used = 3 of 16 channels, 7x7 / 2 / pad 3,
+    ldo 160: the compile-time stem instance) against torch unfold, bit for
+    bit: K order (r, s, c), zeros outside the image and in the K padding."""
+    import torch.nn.functional as F
+
+    from paper_2207_06667_b200 import _lib
+    from paper_2207_06667_b200.resnet import to_nhwc
+    rng = np.random.default_rng(H)
+    imgs = rng.normal(size=(N, 3, H, H)).astype(np.float32)
+    x = to_nhwc(imgs, "cuda")                                  # [N][H][W][16] bf16
+    assert x.shape[-1] == 16
+    P = (H + 6 - 7) // 2 + 1
+    cols = torch.full((N * P * P, 160), 7.0, dtype=torch.bfloat16, device="cuda")
+    _lib.call("edl_im2col_nhwc", x.data_ptr(), N, H, H, 16, 3, 7, 7, 2, 3, cols.data_ptr(), 160, _s())
+    torch.cuda.synchronize()
+    xb = x[..., :3].permute(0, 3, 1, 2).float().cpu()         # exact bf16 values
+    u = F.unfold(xb, 7, padding=3, stride=2)                   # [N][(c, r, s)][P*P]
+    want = u.view(N, 3, 49, P * P).permute(0, 3, 2, 1).reshape(N * P * P, 147)
+    got = cols.float().cpu()
+    assert torch.equal(got[:, :147], want)
+    assert torch.equal(got[:, 147:], torch.zeros_like(got[:, 147:]))
