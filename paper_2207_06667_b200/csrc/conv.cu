@@ -640,10 +640,17 @@ __global__ void __launch_bounds__(256) maxpool3s2_bwd_nhwc_kernel(const uint32_t
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const uint32_t* gt = reinterpret_cast<const uint32_t*>(&g[t]);
+      // byte k of z carries lane 2k's flag in bit 3 and lane 2k + 1's in bit
+      // 7; prmt's sign-replicate selectors (bit 3 of a selector nibble; the
+      // __byte_perm intrinsic masks it off, hence the asm) broadcast a byte's
+      // msb, so one PRMT builds word k's two lane masks
+      const uint32_t zl = z[t] << 4;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const uint32_t lo = (z[t] >> (8 * k + 3)) & 1u, hi = (z[t] >> (8 * k + 7)) & 1u;
-        const uint32_t gm = gt[k] & ((lo * 0xFFFFu) | (hi * 0xFFFF0000u));
+        uint32_t lm;
+        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(lm) : "r"(zl), "r"(z[t]),
+            "r"((8u | k) | ((8u | k) << 4) | ((12u | k) << 8) | ((12u | k) << 12)));
+        const uint32_t gm = gt[k] & lm;
         acc[2 * k] += __uint_as_float(gm << 16);
         acc[2 * k + 1] += __uint_as_float(gm & 0xFFFF0000u);
       }

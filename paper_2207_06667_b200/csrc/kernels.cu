@@ -556,17 +556,21 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
   }
 }
 
-__global__ void __launch_bounds__(256) splitk_reduce_t_kernel(const float* __restrict__ P, int ksplit,
-                                                              long long sstride, int GM, int GN,
-                                                              float* __restrict__ out, long long ldo) {
+// One thread per output (1024-thread blocks): the swapped-operand weight
+// gradients have few 32 x 32 tiles (36 for a 3x3 64 -> 64 conv, 10 for the
+// stem) and deep split-K stacks (29-75 partials), so 256-thread blocks with
+// four outputs per thread were latency-bound (22-44 us). Same per-output
+// summation order as before.
+__global__ void __launch_bounds__(1024) splitk_reduce_t_kernel(const float* __restrict__ P, int ksplit,
+                                                               long long sstride, int GM, int GN,
+                                                               float* __restrict__ out, long long ldo) {
   griddep_wait();
   __shared__ float tile[32][33];
   const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
   const int r0 = blockIdx.x * 32;       // output rows = GEMM columns (GN)
   const int c0 = blockIdx.y * 32;       // output cols = GEMM rows (GM)
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int c = c0 + ty + 8 * j, r = r0 + tx;
+  {
+    const int c = c0 + ty, r = r0 + tx;
     float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (c < GM && r < GN) {
       const float* src = P + static_cast<long long>(c) * GN + r;
@@ -577,20 +581,17 @@ __global__ void __launch_bounds__(256) splitk_reduce_t_kernel(const float* __res
       }
       for (; s < ksplit; ++s) a[0] += __ldcg(src + s * sstride);
     }
-    tile[ty + 8 * j][tx] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+    tile[ty][tx] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
   }
   __syncthreads();
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int r = r0 + ty + 8 * j, c = c0 + tx;
-    if (r < GN && c < GM) out[r * ldo + c] = tile[tx][ty + 8 * j];
-  }
+  const int r = r0 + ty, c = c0 + tx;
+  if (r < GN && c < GM) out[r * ldo + c] = tile[tx][ty];
 }
 
 cudaError_t launch_splitk_reduce(const float* P, int ksplit, long long sstride, int GM, int GN, bool transposed,
                                  float* out, long long ldo, int sms, cudaStream_t stream) {
   if (transposed)
-    return launch_pdl(splitk_reduce_t_kernel, dim3((GN + 31) / 32, (GM + 31) / 32), dim3(256), 0, stream, 1, P,
+    return launch_pdl(splitk_reduce_t_kernel, dim3((GN + 31) / 32, (GM + 31) / 32), dim3(1024), 0, stream, 1, P,
                       ksplit, sstride, GM, GN, out, ldo);
   const long long total = static_cast<long long>(GM) * GN;
   long long blocks = (total + 255) / 256;
