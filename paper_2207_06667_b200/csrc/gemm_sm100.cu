@@ -34,13 +34,14 @@ __host__ __device__ constexpr uint32_t tmem_cols_for(int cols) {
 template <int BN>
 struct GemmCfg {
   static constexpr int kStages = BN >= 256 ? 4 : BN >= 128 ? 6 : 8;
+  static constexpr int kAcc = BN <= 64 ? 4 : 2;          // TMEM accumulator ring (gemm_kernel)
   static constexpr uint32_t kABytes = kBM * kBK * 2;
   static constexpr uint32_t kBBytes = BN * kBK * 2;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr uint32_t kEpiBytes = BN * 4;          // the tile's bias slice
   static constexpr uint32_t kStoreBytes = 4 * 2 * 4096;  // TMA-store staging: two 32x32 fp32 tiles per epilogue warp
   static constexpr uint32_t kSmem =
-      kStages * kStageBytes + kStoreBytes + kEpiBytes + 1024 /*align*/ + 320 /*barriers*/;
+      kStages * kStageBytes + kStoreBytes + kEpiBytes + 1024 /*align*/ + 352 /*barriers*/;
   static_assert(kSmem <= 227 * 1024, "exceeds the sm_100 per-CTA shared memory limit");
 };
 
@@ -647,7 +648,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   using Cfg = GemmCfg<BN>;
   unsigned* const sched = ep.sched;
   constexpr int S = Cfg::kStages;
-  constexpr uint32_t kTmemCols = tmem_cols_for(2 * BN);
+  // TMEM accumulator ring depth: 4 for BN = 64 (short-K conv tiles: the
+  // epilogue and the TMA latency alternate as the stall; 2 deep left both
+  // the MMA and the producer waiting), 2 otherwise
+  constexpr int kAcc = Cfg::kAcc;
+  constexpr uint32_t kTmemCols = tmem_cols_for(kAcc * BN);
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
@@ -658,8 +663,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(stg + Cfg::kStoreBytes + Cfg::kEpiBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* tile_full = tempty + 2;       // [4] tile-index ring
+  uint64_t* tempty = tfull + kAcc;
+  uint64_t* tile_full = tempty + kAcc;    // [4] tile-index ring
   uint64_t* tile_empty = tile_full + 4;   // [4]
   int* tile_ring = reinterpret_cast<int*>(tile_empty + 4);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + 4);
@@ -673,7 +678,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
+    for (int s = 0; s < kAcc; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
     // tile ring consumers: the MMA thread, the second producer, 4 epilogue warps
     for (int s = 0; s < 4; ++s) { mbar_init(&tile_full[s], 1); mbar_init(&tile_empty[s], 2 + 4); }
     if (tma_res) {
@@ -794,8 +799,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (t >= tiles) break;
       int mt, nt, kb0, kb1;
       decode(t, mt, nt, kb0, kb1);
-      const uint32_t as = i & 1;
-      mbar_wait(&tempty[as], ((i >> 1) & 1) ^ 1);
+      const uint32_t as = i % kAcc;
+      mbar_wait(&tempty[as], ((i / kAcc) & 1) ^ 1);
       tc_fence_after();
       const uint32_t d = tmem_base + as * BN;
       for (int kb = kb0; kb < kb1; ++kb, ++g) {
@@ -838,8 +843,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         epi_bar_sync();
         staged_n0 = n0;
       }
-      const uint32_t as = i & 1;
-      mbar_wait(&tfull[as], (i >> 1) & 1);
+      const uint32_t as = i % kAcc;
+      mbar_wait(&tfull[as], (i / kAcc) & 1);
       tc_fence_after();
       if constexpr (epi_tma_store<EPI>())
         epilogue_tile_tma<BN, EPI>(eps, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e,
