@@ -272,15 +272,18 @@ __global__ void __launch_bounds__(256) col2im_s2_nhwc_kernel(const __nv_bfloat16
                                                              __nv_bfloat16* __restrict__ dx) {
   griddep_wait();
   const int cv = C / 8;
-  const int total = N * H * W * cv;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int c8 = i % cv;
-    const int pix = i / cv;
-    const int w = pix % W;
-    const int nh = pix / W;
-    const int h = nh % H;
-    const int n = nh / H;
-    const int r0 = (h + pad) & 1, s0 = (w + pad) & 1;
+  // one block per input row (n, h): the row's tap parity r0 is block-uniform
+  // and each item needs one division (by cv), not the four of a flat index
+  const int n = blockIdx.x / H, h = blockIdx.x - n * H;
+  const int r0 = (h + pad) & 1;
+  for (int i = threadIdx.x; i < W * cv; i += blockDim.x) {
+    const int w = i / cv, c8 = i - w * cv;
+    const int pix = blockIdx.x * W + w;
+    const int s0 = (w + pad) & 1;
+    const long long off = static_cast<long long>(pix) * C + 8 * c8;
+    // the add / mask vectors are loaded up front with the taps
+    const uint4 a4 = add != nullptr ? __ldg(reinterpret_cast<const uint4*>(add + off)) : make_uint4(0u, 0u, 0u, 0u);
+    const uint4 m4 = mask != nullptr ? __ldg(reinterpret_cast<const uint4*>(mask + off)) : make_uint4(0u, 0u, 0u, 0u);
     uint4 v[4];
     bool ok[4];
 #pragma unroll
@@ -304,15 +307,12 @@ __global__ void __launch_bounds__(256) col2im_s2_nhwc_kernel(const __nv_bfloat16
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(b[j]);
     }
-    const long long off = static_cast<long long>(pix) * C + 8 * c8;
     if (add != nullptr) {
-      const uint4 a4 = __ldg(reinterpret_cast<const uint4*>(add + off));
       const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&a4);
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(b[j]);
     }
     if (mask != nullptr) {
-      const uint4 m4 = __ldg(reinterpret_cast<const uint4*>(mask + off));
       const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&m4);
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j] = __bfloat162float(b[j]) > 0.f ? acc[j] : 0.f;
@@ -731,9 +731,11 @@ cudaError_t launch_col2im_nhwc(const __nv_bfloat16* dcol, long long ldc, int N, 
                                int stride, int pad, int P, int Q, const __nv_bfloat16* add,
                                const __nv_bfloat16* mask, __nv_bfloat16* dx, cudaStream_t stream) {
   const long long work = static_cast<long long>(N) * H * W * (C / 8);
-  if (stride == 2 && R <= 4 && S <= 4 && fits32(static_cast<long long>(N) * H * W * C))
-    return launch_pdl(col2im_s2_nhwc_kernel, dim3(grid_for(work)), dim3(256), 0, stream, 1, dcol, ldc, N, H, W, C, R,
-                      S, pad, P, Q, add, mask, dx);
+  if (stride == 2 && R <= 4 && S <= 4 && fits32(static_cast<long long>(N) * H * W * C)) {
+    const int threads = W * (C / 8) >= 256 ? 256 : ((W * (C / 8) + 31) / 32) * 32;
+    return launch_pdl(col2im_s2_nhwc_kernel, dim3(static_cast<unsigned>(N * H)), dim3(threads), 0, stream, 1, dcol,
+                      ldc, N, H, W, C, R, S, pad, P, Q, add, mask, dx);
+  }
   if (fits32(work))
     return launch_pdl(col2im_nhwc_kernel<int>, dim3(grid_for(work)), dim3(256), 0, stream, 1, dcol, ldc, N, H, W, C,
                       R, S, stride, pad, P, Q, add, mask, dx);

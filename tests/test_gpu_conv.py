@@ -438,3 +438,35 @@ def test_packed_stem_im2col_bitwise(N, H):
     got = cols.float().cpu()
     assert torch.equal(got[:, :147], want)
     assert torch.equal(got[:, 147:], torch.zeros_like(got[:, 147:]))
+
+
+@pytest.mark.parametrize("N,H,C,k,pad", [(2, 15, 64, 3, 1), (3, 16, 64, 3, 1), (2, 14, 128, 1, 0), (2, 9, 16, 4, 1)])
+def test_col2im_stride2_vs_fold(N, H, C, k, pad):
+    """edl_col2im_nhwc at stride 2 (the row-blocked stride-2 kernel: the <= 4
+    contributing taps enumerated directly) against torch fold of the same
+    column gradient, with the shortcut add and the ReLU mask fused: sums of
+    <= 4 bf16 terms + add in fp32, so <= 1 bf16 rounding step apart."""
+    import torch.nn.functional as F
+
+    from paper_2207_06667_b200 import _lib
+    rng = np.random.default_rng(N * 100 + H + k)
+    P = (H + 2 * pad - k) // 2 + 1
+    kd = k * k * C
+    dcol = torch.from_numpy(rng.normal(size=(N * P * P, kd)).astype(np.float32)).to(torch.bfloat16)
+    add = torch.from_numpy(rng.normal(size=(N, H, H, C)).astype(np.float32)).to(torch.bfloat16)
+    mask = torch.from_numpy(rng.normal(size=(N, H, H, C)).astype(np.float32)).to(torch.bfloat16)
+    dx = torch.empty(N, H, H, C, dtype=torch.bfloat16, device="cuda")
+    dd, ad, md = dcol.cuda(), add.cuda(), mask.cuda()
+    _lib.call("edl_col2im_nhwc", dd.data_ptr(), kd, N, H, H, C, k, k, 2, pad, ad.data_ptr(), md.data_ptr(),
+              dx.data_ptr(), _s())
+    dx2 = torch.empty_like(dx)
+    _lib.call("edl_col2im_nhwc", dd.data_ptr(), kd, N, H, H, C, k, k, 2, pad, None, None, dx2.data_ptr(), _s())
+    torch.cuda.synchronize()
+    # columns [(n, p, q)][(r, s, c)] -> fold input [n][(c, r, s)][(p, q)]
+    cols = dcol.double().view(N, P * P, k * k, C).permute(0, 3, 2, 1).reshape(N, C * k * k, P * P)
+    full = F.fold(cols, (H, H), k, padding=pad, stride=2).permute(0, 2, 3, 1)   # NHWC fp64
+    want2 = full.to(torch.bfloat16).float()
+    want = torch.where(mask.double() > 0, full + add.double(), torch.zeros_like(full)).to(torch.bfloat16).float()
+    for got, exp in ((dx, want), (dx2, want2)):
+        g = got.float().cpu()
+        assert torch.allclose(g, exp, rtol=8e-3, atol=1e-6), (g - exp).abs().max()
