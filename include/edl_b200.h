@@ -138,6 +138,12 @@ int edl_maxpool_argmax_nhwc(const void* x, int N, int H, int W, int C, int k, in
                             unsigned* argmax, void* stream);
 int edl_maxpool_bwd_argmax_nhwc(const unsigned* argmax, int N, int H, int W, int C, int k, int stride, int pad,
                                 const void* dy, const void* mask, void* dx, void* stream);
+/* edl_maxpool_argmax_nhwc for a pool whose input is a ReLU output (the
+ * stem): lanes whose window maximum is not > 0 get the no-match position 0xF,
+ * so edl_maxpool_bwd_argmax_nhwc with mask = NULL equals the masked backward
+ * (mask = the pool input) without reading the full-resolution mask. */
+int edl_maxpool_argmax_relu_nhwc(const void* x, int N, int H, int W, int C, int k, int stride, int pad, void* out,
+                                 unsigned* argmax, void* stream);
 
 /* Backprop through one tanh layer, edl/nnkit.py:308:
  *   dX[M][K] = (dY[M][N] @ W[N][K]) * (1 - H[M][K]^2)      (all bf16)

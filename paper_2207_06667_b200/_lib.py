@@ -51,6 +51,8 @@ _SIGNATURES = {
                              c_void_p],
     "edl_maxpool_argmax_nhwc": [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p,
                                 c_void_p],
+    "edl_maxpool_argmax_relu_nhwc": [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p,
+                                     c_void_p],
     "edl_maxpool_bwd_argmax_nhwc": [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p,
                                     c_void_p, c_void_p],
     "edl_linear_bwd_data": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_ll,

@@ -513,20 +513,32 @@ int edl_maxpool_nhwc(const void* x, int N, int H, int W, int C, int k, int strid
   const int P = (H + 2 * pad - k) / stride + 1, Q = (W + 2 * pad - k) / stride + 1;
   if (P < 1 || Q < 1) return fail(EDL_ERR_SHAPE, "maxpool_nhwc: empty output");
   cudaError_t e = launch_maxpool_nhwc(reinterpret_cast<const __nv_bfloat16*>(x), N, H, W, C, k, stride, pad, P, Q,
-                                      reinterpret_cast<__nv_bfloat16*>(out), nullptr, as_stream(stream));
+                                      reinterpret_cast<__nv_bfloat16*>(out), nullptr, false, as_stream(stream));
   return e == cudaSuccess ? 0 : cuda_fail(e, "maxpool_nhwc");
 }
 
-int edl_maxpool_argmax_nhwc(const void* x, int N, int H, int W, int C, int k, int stride, int pad, void* out,
-                            unsigned* argmax, void* stream) {
+namespace {
+int maxpool_argmax_impl(const void* x, int N, int H, int W, int C, int k, int stride, int pad, void* out,
+                        unsigned* argmax, bool relu_mask, void* stream) {
   if (N < 1 || H < 1 || W < 1 || C < 8 || C % 8 || k < 1 || k * k > 15 || stride < 1 || pad < 0 || pad >= k ||
       !argmax)
     return fail(EDL_ERR_SHAPE, "maxpool_argmax_nhwc: bad shape");
   const int P = (H + 2 * pad - k) / stride + 1, Q = (W + 2 * pad - k) / stride + 1;
   if (P < 1 || Q < 1) return fail(EDL_ERR_SHAPE, "maxpool_argmax_nhwc: empty output");
   cudaError_t e = launch_maxpool_nhwc(reinterpret_cast<const __nv_bfloat16*>(x), N, H, W, C, k, stride, pad, P, Q,
-                                      reinterpret_cast<__nv_bfloat16*>(out), argmax, as_stream(stream));
+                                      reinterpret_cast<__nv_bfloat16*>(out), argmax, relu_mask, as_stream(stream));
   return e == cudaSuccess ? 0 : cuda_fail(e, "maxpool_argmax_nhwc");
+}
+}  // namespace
+
+int edl_maxpool_argmax_nhwc(const void* x, int N, int H, int W, int C, int k, int stride, int pad, void* out,
+                            unsigned* argmax, void* stream) {
+  return maxpool_argmax_impl(x, N, H, W, C, k, stride, pad, out, argmax, false, stream);
+}
+
+int edl_maxpool_argmax_relu_nhwc(const void* x, int N, int H, int W, int C, int k, int stride, int pad, void* out,
+                                 unsigned* argmax, void* stream) {
+  return maxpool_argmax_impl(x, N, H, W, C, k, stride, pad, out, argmax, true, stream);
 }
 
 int edl_maxpool_bwd_argmax_nhwc(const unsigned* argmax, int N, int H, int W, int C, int k, int stride, int pad,

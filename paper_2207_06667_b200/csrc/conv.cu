@@ -142,7 +142,7 @@ template <typename I>
 __global__ void __launch_bounds__(256) maxpool_nhwc_kernel(const __nv_bfloat16* __restrict__ x, int N, int H, int W,
                                                            int C, int k, int stride, int pad, int P, int Q,
                                                            __nv_bfloat16* __restrict__ out,
-                                                           uint32_t* __restrict__ argmax) {
+                                                           uint32_t* __restrict__ argmax, bool relu_mask) {
   griddep_wait();
   const int cv = C / 8;
   const I total = static_cast<I>(N) * P * Q * cv;
@@ -182,6 +182,12 @@ __global__ void __launch_bounds__(256) maxpool_nhwc_kernel(const __nv_bfloat16* 
     o.z = pack_bf16x2(best[4], best[5]);
     o.w = pack_bf16x2(best[6], best[7]);
     *reinterpret_cast<uint4*>(out + static_cast<long long>(m) * C + 8 * c8) = o;
+    if (relu_mask) {   // a window whose maximum is not > 0 routes no gradient (see the 3x3 / 2 kernel)
+      const __nv_bfloat16* ob = reinterpret_cast<const __nv_bfloat16*>(&o);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (!(__bfloat162float(ob[j]) > 0.f)) arg |= 0xFu << (4 * j);
+    }
     if (argmax != nullptr) argmax[i] = arg;
   }
 }
@@ -194,7 +200,7 @@ __global__ void __launch_bounds__(256) maxpool_nhwc_kernel(const __nv_bfloat16* 
 __global__ void __launch_bounds__(256) maxpool3s2_nhwc_kernel(const __nv_bfloat16* __restrict__ x, int N, int H,
                                                               int W, int C, int pad, int P, int Q,
                                                               __nv_bfloat16* __restrict__ out,
-                                                              uint32_t* __restrict__ argmax) {
+                                                              uint32_t* __restrict__ argmax, bool relu_mask) {
   griddep_wait();
   const int cv = C / 8;
   const int total = N * P * Q * cv;
@@ -255,6 +261,18 @@ __global__ void __launch_bounds__(256) maxpool3s2_nhwc_kernel(const __nv_bfloat1
       arg = (arg & ~nm) | (nm & (static_cast<uint32_t>(t) * 0x11111111u));
     }
     *reinterpret_cast<uint4*>(out + static_cast<long long>(m) * C + 8 * c8) = make_uint4(o[0], o[1], o[2], o[3]);
+    if (relu_mask) {
+      // training pair behind a ReLU: the pool input's ReLU mask at a window's
+      // argmax is (window max > 0), so lanes whose max is not > 0 get the
+      // no-match nibble 0xF and the backward needs no full-resolution mask
+      uint32_t g[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        g[k] = ~__hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&o[k]), __float2bfloat162_rn(0.f));
+      const uint32_t p01 = __byte_perm(g[0], g[1], 0x6420), p23 = __byte_perm(g[2], g[3], 0x6420);
+      const uint32_t lo = __byte_perm(p01, p23, 0x6420), hi = __byte_perm(p01, p23, 0x7531);
+      arg |= (lo & 0x0F0F0F0Fu) | (hi & 0xF0F0F0F0u);
+    }
     if (argmax != nullptr) argmax[i] = arg;
   }
 }
@@ -709,17 +727,18 @@ cudaError_t launch_im2col_nhwc(const __nv_bfloat16* x, int N, int H, int W, int 
 }
 
 cudaError_t launch_maxpool_nhwc(const __nv_bfloat16* x, int N, int H, int W, int C, int k, int stride, int pad,
-                                int P, int Q, __nv_bfloat16* out, uint32_t* argmax, cudaStream_t stream) {
+                                int P, int Q, __nv_bfloat16* out, uint32_t* argmax, bool relu_mask,
+                                cudaStream_t stream) {
   if (argmax != nullptr && k * k > 15) return cudaErrorInvalidValue;
   const long long work = static_cast<long long>(N) * P * Q * (C / 8);
   if (k == 3 && stride == 2 && fits32(work) && fits32(static_cast<long long>(N) * H * W * C))
     return launch_pdl(maxpool3s2_nhwc_kernel, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, pad, P,
-                      Q, out, argmax);
+                      Q, out, argmax, relu_mask);
   if (fits32(work))
     return launch_pdl(maxpool_nhwc_kernel<int>, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, k,
-                      stride, pad, P, Q, out, argmax);
+                      stride, pad, P, Q, out, argmax, relu_mask);
   return launch_pdl(maxpool_nhwc_kernel<long long>, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, k,
-                    stride, pad, P, Q, out, argmax);
+                    stride, pad, P, Q, out, argmax, relu_mask);
 }
 
 cudaError_t launch_avgpool_nhwc(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* out, long long ldo,

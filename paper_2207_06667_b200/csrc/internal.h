@@ -139,7 +139,8 @@ cudaError_t launch_im2col_nhwc(const __nv_bfloat16* x, int N, int H, int W, int 
                                int stride, int pad, int P, int Q, __nv_bfloat16* out, long long ldo,
                                cudaStream_t stream);
 cudaError_t launch_maxpool_nhwc(const __nv_bfloat16* x, int N, int H, int W, int C, int k, int stride, int pad,
-                                int P, int Q, __nv_bfloat16* out, uint32_t* argmax, cudaStream_t stream);
+                                int P, int Q, __nv_bfloat16* out, uint32_t* argmax, bool relu_mask,
+                                cudaStream_t stream);
 cudaError_t launch_conv_flip_weights(const __nv_bfloat16* w, long long ldw, int K, int C, int R, int S,
                                      __nv_bfloat16* wf, long long ldf, cudaStream_t stream);
 cudaError_t launch_maxpool_bwd_argmax_nhwc(const uint32_t* argmax, int N, int H, int W, int C, int k, int stride,

@@ -475,7 +475,8 @@ class ResNetStudent:
     def forward(self, x, s):
         self._fwd(0, x, (self.cfg.image, self.cfg.image), self.y0, None, s)
         h, w = self.stem_hw
-        _lib.call("edl_maxpool_argmax_nhwc", self.y0.data_ptr(), self.B, h, w, self.y0.shape[-1], 3, 2, 1,
+        # the pool input is the stem's ReLU output: argmax words carry its mask
+        _lib.call("edl_maxpool_argmax_relu_nhwc", self.y0.data_ptr(), self.B, h, w, self.y0.shape[-1], 3, 2, 1,
                   self.x1.data_ptr(), self.pool_arg.data_ptr(), s)
         cur = self.x1
         for (i1, i2, isc), (hw, h1, sc, y) in zip(self.block_idx, self.acts):
@@ -593,7 +594,7 @@ class ResNetStudent:
         h, w = self.stem_hw
         dy0 = self.g[(cur + 1) % 3][:self.y0.numel()].view_as(self.y0)
         _lib.call("edl_maxpool_bwd_argmax_nhwc", self.pool_arg.data_ptr(), B, h, w, self.y0.shape[-1], 3, 2, 1,
-                  dz.data_ptr(), self.y0.data_ptr(), dy0.data_ptr(), s)
+                  dz.data_ptr(), None, dy0.data_ptr(), s)   # ReLU mask folded into the argmax words
         self._wgrad(0, dy0, x, (self.cfg.image, self.cfg.image), s)
         _lib.call("edl_sgd_step", self.flat.data_ptr(), self.flat_bf16.data_ptr(), self.grads.data_ptr(), self.size,
                   float(eta), s)

@@ -284,6 +284,23 @@ def test_maxpool_bwd_vs_torch_with_ties(k, st, pd, H):
     assert torch.equal(y_arg, y_plain)
     assert torch.equal(dx2, dx)
     assert torch.equal(dx3, torch.where(xd > 0, dx, torch.zeros_like(dx)))
+    # pool behind a ReLU (the stem): the relu argmax words fold the mask in,
+    # so the unmasked backward equals the masked one (ties at 0 included)
+    xr = torch.clamp(xd, min=0)
+    arg_p, arg_r = torch.empty_like(arg), torch.empty_like(arg)
+    y_p, y_r = torch.empty_like(y_plain), torch.empty_like(y_plain)
+    _lib.call("edl_maxpool_argmax_nhwc", xr.data_ptr(), 3, H, H, 16, k, st, pd, y_p.data_ptr(), arg_p.data_ptr(), _s())
+    _lib.call("edl_maxpool_argmax_relu_nhwc", xr.data_ptr(), 3, H, H, 16, k, st, pd, y_r.data_ptr(), arg_r.data_ptr(),
+              _s())
+    dx_m, dx_r = torch.empty_like(xd), torch.empty_like(xd)
+    _lib.call("edl_maxpool_bwd_argmax_nhwc", arg_p.data_ptr(), 3, H, H, 16, k, st, pd, dyd.data_ptr(), xr.data_ptr(),
+              dx_m.data_ptr(), _s())
+    _lib.call("edl_maxpool_bwd_argmax_nhwc", arg_r.data_ptr(), 3, H, H, 16, k, st, pd, dyd.data_ptr(), None,
+              dx_r.data_ptr(), _s())
+    torch.cuda.synchronize()
+    assert torch.equal(y_r, y_p)
+    assert torch.equal(dx_r, dx_m)
+    assert (xr == 0).float().mean().item() > 0.3          # many zero (masked, tied) inputs
 
 
 @pytest.mark.parametrize("N,C,H,K,k,stride,relu,residual", [
