@@ -197,6 +197,8 @@ __global__ void __launch_bounds__(256) maxpool_nhwc_kernel(const __nv_bfloat16* 
 // taps masked to -inf afterwards), so each thread has all nine 16-byte loads
 // in flight; the generic kernel's bounds branches serialised them (240 us at
 // batch 256, ~2.2 TB/s). Same first-maximum scan order and argmax words.
+// ARG: record argmax words (training); inference skips the nibble masks.
+template <bool ARG>
 __global__ void __launch_bounds__(256) maxpool3s2_nhwc_kernel(const __nv_bfloat16* __restrict__ x, int N, int H,
                                                               int W, int C, int pad, int P, int Q,
                                                               __nv_bfloat16* __restrict__ out,
@@ -255,13 +257,15 @@ __global__ void __launch_bounds__(256) maxpool3s2_nhwc_kernel(const __nv_bfloat1
         o[k] = (vt[k] & e[k]) | (o[k] & ~e[k]);
       }
       // lane 2k <- low half of e[k], lane 2k + 1 <- high half: nibble masks
-      const uint32_t p01 = __byte_perm(e[0], e[1], 0x6420), p23 = __byte_perm(e[2], e[3], 0x6420);
-      const uint32_t lo = __byte_perm(p01, p23, 0x6420), hi = __byte_perm(p01, p23, 0x7531);
-      const uint32_t nm = (lo & 0x0F0F0F0Fu) | (hi & 0xF0F0F0F0u);
-      arg = (arg & ~nm) | (nm & (static_cast<uint32_t>(t) * 0x11111111u));
+      if constexpr (ARG) {
+        const uint32_t p01 = __byte_perm(e[0], e[1], 0x6420), p23 = __byte_perm(e[2], e[3], 0x6420);
+        const uint32_t lo = __byte_perm(p01, p23, 0x6420), hi = __byte_perm(p01, p23, 0x7531);
+        const uint32_t nm = (lo & 0x0F0F0F0Fu) | (hi & 0xF0F0F0F0u);
+        arg = (arg & ~nm) | (nm & (static_cast<uint32_t>(t) * 0x11111111u));
+      }
     }
     *reinterpret_cast<uint4*>(out + static_cast<long long>(m) * C + 8 * c8) = make_uint4(o[0], o[1], o[2], o[3]);
-    if (relu_mask) {
+    if (ARG && relu_mask) {
       // training pair behind a ReLU: the pool input's ReLU mask at a window's
       // argmax is (window max > 0), so lanes whose max is not > 0 get the
       // no-match nibble 0xF and the backward needs no full-resolution mask
@@ -273,7 +277,7 @@ __global__ void __launch_bounds__(256) maxpool3s2_nhwc_kernel(const __nv_bfloat1
       const uint32_t lo = __byte_perm(p01, p23, 0x6420), hi = __byte_perm(p01, p23, 0x7531);
       arg |= (lo & 0x0F0F0F0Fu) | (hi & 0xF0F0F0F0u);
     }
-    if (argmax != nullptr) argmax[i] = arg;
+    if (ARG) argmax[i] = arg;
   }
 }
 
@@ -732,8 +736,11 @@ cudaError_t launch_maxpool_nhwc(const __nv_bfloat16* x, int N, int H, int W, int
   if (argmax != nullptr && k * k > 15) return cudaErrorInvalidValue;
   const long long work = static_cast<long long>(N) * P * Q * (C / 8);
   if (k == 3 && stride == 2 && fits32(work) && fits32(static_cast<long long>(N) * H * W * C))
-    return launch_pdl(maxpool3s2_nhwc_kernel, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, pad, P,
-                      Q, out, argmax, relu_mask);
+    return argmax != nullptr
+               ? launch_pdl(maxpool3s2_nhwc_kernel<true>, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W,
+                            C, pad, P, Q, out, argmax, relu_mask)
+               : launch_pdl(maxpool3s2_nhwc_kernel<false>, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W,
+                            C, pad, P, Q, out, argmax, relu_mask);
   if (fits32(work))
     return launch_pdl(maxpool_nhwc_kernel<int>, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, k,
                       stride, pad, P, Q, out, argmax, relu_mask);
