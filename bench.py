@@ -402,6 +402,9 @@ def main():
                 "bound": "tensor", "achieved": round(achieved, 1), "peak": peak_sust,
                 "peak_kind": f"{peak_kind} bf16_tflops_sustained", "unit": "TFLOP/s",
                 "frac": round(achieved / peak_sust, 4), "avg_us": round(avg * 1e6, 2),
+                # the sustained peak is cuBLAS under the box's power cap; the burst
+                # figure bounds a kernel that runs at full clock inside the step
+                "frac_of_burst": round(achieved / peak_burst, 4), "peak_burst": peak_burst,
                 "algorithmic_flop_per_launch": flop, "traffic": _traffic_from_profiles()}
 
     online = None
