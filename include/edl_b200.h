@@ -49,6 +49,20 @@ int edl_device_sms(void);
  * otherwise queue behind teacher GEMMs that hold every SM. */
 int edl_set_stream_max_ctas(void* stream, int max_ctas);
 
+/* Hidden-layer tanh of the forward GEMM epilogues on the CURRENT device:
+ * 0 = tanh.approx.f32, one MUFU op with ~2^-11 relative error (default);
+ * 1 = tanhf, <= 2 ulp fp32 (+2.6% teacher batch, +6% student step at cfg3,
+ * gradient error vs the bf16-storage oracle 1.38e-3 instead of 1.65e-3:
+ * profiles/r02_parity_probe.json). Not stream
+ * ordered: call while no forward GEMM is in flight on that device.
+ *
+ * Tile scheduling: every stream that launches the persistent GEMMs gets a
+ * {next tile, CTAs done} counter pair from a static device pool on first
+ * use (nothing is allocated, so the first use may be inside stream capture).
+ * A graph captured on stream S reuses S's pair: do not replay it while eager
+ * GEMMs run on S from another thread, or replay it on two streams at once. */
+int edl_set_tanh_mode(int mode);
+
 /* One dense layer of edl.nnkit.forward (edl/nnkit.py:223-234, `z = h @ w.T + b`
  * at :232, tanh at :233). X: bf16 [M][ldx] (K used), W: bf16 [N][ldw], bias:
  * fp32 [N]. act=EDL_ACT_TANH writes bf16 Y [M][ldy]; EDL_ACT_NONE writes fp32.
@@ -277,6 +291,20 @@ int edl_topk_hits(const float* logits, long long ld, const long long* labels, in
 /* fp32 -> bf16 matrix cast (parameter / input staging). */
 int edl_cast_bf16(const float* src, long long ld_src, void* dst, long long ld_dst, int rows,
                   int cols, void* stream);
+
+/* TeacherConfig.simulated_delay (edl/teacher_node.py:30-44, slept per batch
+ * by TeacherServer._compute_loop :157-170): a single-thread device busy wait
+ * of `ns` nanoseconds on `stream`, so a throttled teacher delays its own
+ * stream and never the host thread. */
+int edl_stream_delay_ns(long long ns, void* stream);
+
+/* Soft-label handoff from a teacher GPU to its student's slot (the reply
+ * leg of edl/student_node.py:407-423): cudaMemcpyPeerAsync on the TEACHER's
+ * stream only. (torch's cross-device copy_ also orders the destination
+ * device's current stream, i.e. the student's training stream, which
+ * serialises teacher and student.) */
+int edl_memcpy_peer_async(void* dst, int dst_device, const void* src, int src_device, long long bytes,
+                          void* stream);
 
 #ifdef __cplusplus
 }

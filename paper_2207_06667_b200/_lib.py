@@ -29,6 +29,7 @@ _SIGNATURES = {
     "edl_last_error": [],
     "edl_device_sms": [],
     "edl_set_stream_max_ctas": [c_void_p, c_int],
+    "edl_set_tanh_mode": [c_int],
     "edl_linear_fwd": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_void_p, c_ll, c_int, c_int,
                        c_int, c_int, c_void_p],
     "edl_linear_fwd_residual": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_void_p, c_ll, c_void_p, c_ll, c_int,
@@ -84,6 +85,8 @@ _SIGNATURES = {
                         c_void_p],
     "edl_topk_hits": [c_void_p, c_ll, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p],
     "edl_cast_bf16": [c_void_p, c_ll, c_void_p, c_ll, c_int, c_int, c_void_p],
+    "edl_stream_delay_ns": [c_ll, c_void_p],
+    "edl_memcpy_peer_async": [c_void_p, c_int, c_void_p, c_int, c_ll, c_void_p],
 }
 _RESTYPES = {"edl_last_error": c_char_p, "edl_colsum_workspace_floats": c_ll,
              "edl_bwd_weight_workspace_floats": c_ll,
@@ -144,7 +147,9 @@ _LAUNCHES = {"edl_linear_bwd_weight": 3,   # GEMM + two column-sum passes when d
              "edl_conv_bwd_weight_nhwc": 4,   # the same plan with an im2col operand
              "edl_kd_loss_fwd_bwd": 2,     # row pass + deterministic batch-mean pass
              "edl_stream_wait_geq": 0,     # stream memory ops, not kernels
-             "edl_stream_write_u32": 0}
+             "edl_stream_write_u32": 0,
+             "edl_set_tanh_mode": 0,
+             "edl_memcpy_peer_async": 0}
 launch_count = 0
 
 

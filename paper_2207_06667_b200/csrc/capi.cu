@@ -297,11 +297,17 @@ cudaError_t edl::ensure_kernel_attrs(const void* kern, int smem_bytes, bool nonp
 namespace {
 
 // Per-(device, stream) tile-scheduler counters for the persistent GEMM
-// ({next tile, CTAs done}, reset by each launch's last CTA). Allocated on a
-// stream's first GEMM only; launches on one stream are ordered (PDL waits),
-// launches on different streams never share a counter.
+// ({next tile, CTAs done}, reset by each launch's last CTA). They come from
+// a static device pool (no allocation on any call, so a stream's first GEMM
+// may be inside graph capture); a stream keeps its pair for the process
+// lifetime. Launches on one stream are ordered (PDL waits); launches on
+// different streams never share a pair. Past kSchedSlots streams per device
+// the GEMMs fall back to the static tile schedule.
+constexpr int kSchedSlots = 256;
+__device__ unsigned g_sched_pool[2 * kSchedSlots];
 std::mutex g_sched_mu;
 std::unordered_map<std::string, unsigned*> g_sched;
+std::unordered_map<int, int> g_sched_used;
 
 // Per-stream cap on the persistent GEMM grid (edl_set_stream_max_ctas): a
 // teacher stream capped below the SM count leaves SMs free, so the student's
@@ -330,9 +336,11 @@ unsigned* stream_sched(cudaStream_t s) {
   std::lock_guard<std::mutex> g(g_sched_mu);
   auto it = g_sched.find(key);
   if (it != g_sched.end()) return it->second;
-  unsigned* p = nullptr;
-  if (cudaMalloc(&p, 2 * sizeof(unsigned)) != cudaSuccess) return nullptr;  // static schedule fallback
-  cudaMemsetAsync(p, 0, 2 * sizeof(unsigned), s);
+  int& used = g_sched_used[dev];
+  if (used >= kSchedSlots) return nullptr;   // static schedule
+  void* base = nullptr;
+  if (cudaGetSymbolAddress(&base, g_sched_pool) != cudaSuccess) return nullptr;
+  unsigned* p = static_cast<unsigned*>(base) + 2 * used++;
   g_sched.emplace(key, p);
   return p;
 }
@@ -346,6 +354,12 @@ int edl_version(void) { return EDL_B200_ABI_VERSION; }
 const char* edl_last_error(void) { return g_err.c_str(); }
 
 int edl_device_sms(void) { return num_sms(); }
+
+int edl_set_tanh_mode(int mode) {
+  if (mode != 0 && mode != 1) return fail(EDL_ERR_PARAM, "set_tanh_mode: mode must be 0 or 1");
+  const cudaError_t e = edl::set_tanh_mode(mode);
+  return e == cudaSuccess ? 0 : cuda_fail(e, "set_tanh_mode");
+}
 
 int edl_set_stream_max_ctas(void* stream, int max_ctas) {
   std::lock_guard<std::mutex> g(g_cap_mu);
@@ -993,6 +1007,22 @@ int edl_cast_bf16(const float* src, long long ld_src, void* dst, long long ld_ds
   cudaError_t e = launch_cast_bf16(src, ld_src, reinterpret_cast<__nv_bfloat16*>(dst), ld_dst, rows,
                                    cols, as_stream(stream));
   return e == cudaSuccess ? 0 : cuda_fail(e, "cast_bf16");
+}
+
+int edl_stream_delay_ns(long long ns, void* stream) {
+  if (ns < 0) return fail(EDL_ERR_PARAM, "stream_delay_ns: negative delay");
+  if (ns == 0) return 0;
+  cudaError_t e = launch_stream_delay(static_cast<unsigned long long>(ns), as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "stream_delay_ns");
+}
+
+int edl_memcpy_peer_async(void* dst, int dst_device, const void* src, int src_device, long long bytes,
+                          void* stream) {
+  if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(EDL_ERR_SHAPE, "memcpy_peer_async: bad arguments");
+  if (bytes == 0) return 0;
+  cudaError_t e = cudaMemcpyPeerAsync(dst, dst_device, src, src_device, static_cast<size_t>(bytes),
+                                      as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "memcpy_peer_async");
 }
 
 }  // extern "C"

@@ -23,6 +23,12 @@
 
 namespace edl {
 
+__device__ int g_tanh_mode = 0;
+
+cudaError_t set_tanh_mode(int mode) {
+  return cudaMemcpyToSymbol(g_tanh_mode, &mode, sizeof(int));
+}
+
 constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr int kThreads = 256;
@@ -230,8 +236,9 @@ __device__ __forceinline__ void epilogue_store(const EpiArgs& ep, int row, int M
     }
   }
   if constexpr (EPI == EPI_TANH_BF16) {
+    const int tm = g_tanh_mode;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = tanh_fast(v[i]);
+    for (int i = 0; i < 32; ++i) v[i] = tanh_act(v[i], tm);
   }
   if constexpr (EPI == EPI_DTANH_BF16) {
     const __nv_bfloat16* h = ep.aux + static_cast<size_t>(row) * ep.ld_aux + col0;
@@ -432,8 +439,9 @@ __device__ __forceinline__ void epi_math(const EpiArgs& ep, int row, int M, int 
     }
   }
   if constexpr (EPI == EPI_TANH_BF16) {
+    const int tm = g_tanh_mode;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = tanh_fast(v[i]);
+    for (int i = 0; i < 32; ++i) v[i] = tanh_act(v[i], tm);
   }
   if constexpr (EPI == EPI_RELU_BF16) {
     // residual (ResNet shortcut, bf16, same shape as the output), then ReLU

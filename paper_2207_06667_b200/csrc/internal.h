@@ -118,6 +118,9 @@ cudaError_t launch_gemm_grouped_pair_bwd_weight(const GroupMaps& maps, const Gro
 cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
                         const CUtensorMap& ty, int M, int N, int K, const EpiArgs& ep, int num_sms,
                         cudaStream_t stream, const CUtensorMap* tr = nullptr);
+// Hidden-layer tanh of the GEMM epilogues on the current device: 1 = tanhf
+// (default), 0 = tanh.approx.f32 (gemm_sm100.cu).
+cudaError_t set_tanh_mode(int mode);
 // Stream-ordered flag fallbacks (exchange.cu).
 cudaError_t launch_flag_wait(const uint32_t* addr, uint32_t value, cudaStream_t stream);
 cudaError_t launch_flag_write(uint32_t* addr, uint32_t value, cudaStream_t stream);
@@ -200,5 +203,6 @@ cudaError_t launch_topk_hits(const float* logits, long long ld, const int64_t* l
                              int K, int k, unsigned* hits, cudaStream_t stream);
 cudaError_t launch_cast_bf16(const float* src, long long ld_src, __nv_bfloat16* dst,
                              long long ld_dst, int rows, int cols, cudaStream_t stream);
+cudaError_t launch_stream_delay(unsigned long long ns, cudaStream_t stream);
 
 }  // namespace edl

@@ -631,26 +631,67 @@ cudaError_t launch_topk_hits(const float* logits, long long ld, const int64_t* l
 }
 
 // ------------------------------------------------------------------ fp32 -> bf16
+// Row-blocked cast (refresh of the bf16 weight copy; host fp32 batches staged
+// on the device, bench e2e): blockIdx.y strides rows, each thread converts 4
+// consecutive columns per iteration (16-byte load, 8-byte store) when the
+// row pitches and bases allow it, so there is no per-element division.
 __global__ void cast_bf16_kernel(const float* __restrict__ src, long long ld_src,
                                  __nv_bfloat16* __restrict__ dst, long long ld_dst, int rows,
-                                 int cols) {
+                                 int cols, int vec) {
   griddep_wait();
-  const long long total = static_cast<long long>(rows) * cols;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long r = i / cols, c = i % cols;
-    dst[r * ld_dst + c] = __float2bfloat16_rn(src[r * ld_src + c]);
+  const long long step = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (int r = blockIdx.y; r < rows; r += gridDim.y) {
+    const float* sr = src + static_cast<size_t>(r) * ld_src;
+    __nv_bfloat16* dr = dst + static_cast<size_t>(r) * ld_dst;
+    if (vec) {
+      const int c4 = cols / 4;
+      for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < c4; i += step) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(sr) + i);
+        uint2 o;
+        o.x = pack_bf16x2(v.x, v.y);
+        o.y = pack_bf16x2(v.z, v.w);
+        reinterpret_cast<uint2*>(dr)[i] = o;
+      }
+    } else {
+      for (long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; c < cols; c += step)
+        dr[c] = __float2bfloat16_rn(sr[c]);
+    }
   }
 }
 
 cudaError_t launch_cast_bf16(const float* src, long long ld_src, __nv_bfloat16* dst,
                              long long ld_dst, int rows, int cols, cudaStream_t stream) {
-  long long total = static_cast<long long>(rows) * cols;
-  long long blocks = (total + 255) / 256;
-  if (blocks > 148 * 32) blocks = 148 * 32;
-  if (blocks < 1) blocks = 1;
-  cast_bf16_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(src, ld_src, dst, ld_dst, rows, cols);
-  return cudaGetLastError();
+  const bool vec = cols % 4 == 0 && ld_src % 4 == 0 && ld_dst % 4 == 0 &&
+                   reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(dst) % 8 == 0;
+  const long long per_row = vec ? cols / 4 : cols;
+  long long bx = (per_row + 255) / 256;
+  int by = rows;
+  // ~16 blocks per SM in total
+  const long long target = 148LL * 16;
+  if (by > target) by = static_cast<int>(target);
+  if (bx * by > target) bx = (target + by - 1) / by;
+  if (bx < 1) bx = 1;
+  if (by < 1) by = 1;
+  return launch_pdl(cast_bf16_kernel, dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)), dim3(256), 0,
+                    stream, 1, src, ld_src, dst, ld_dst, rows, cols, vec ? 1 : 0);
+}
+
+// ------------------------------------------------------------------ stream delay
+// A device-side busy wait of `ns` nanoseconds on one thread (globaltimer):
+// TeacherConfig.simulated_delay (edl/teacher_node.py:30-44) on the teacher's
+// stream, so a throttled teacher slows its stream, not the host.
+__global__ void stream_delay_kernel(unsigned long long ns) {
+  griddep_wait();
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
+cudaError_t launch_stream_delay(unsigned long long ns, cudaStream_t stream) {
+  return launch_pdl(stream_delay_kernel, dim3(1), dim3(32), 0, stream, 1, ns);
 }
 
 }  // namespace edl

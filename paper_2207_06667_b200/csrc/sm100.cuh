@@ -382,6 +382,17 @@ __device__ __forceinline__ float tanh_fast(float x) {
   return y;
 }
 
+// Hidden-layer activation of the tanh epilogues. tanh.approx.f32 (one MUFU
+// op) carries ~2^-11 relative error, 1/8 of a bf16 ulp, so ~5% of the stored
+// bf16 activations round to the other neighbour of the exact value;
+// CUDA's tanhf (<= 2 ulp fp32) leaves only fp32 accumulation-order flips.
+// mode (g_tanh_mode in gemm_sm100.cu, edl_set_tanh_mode): 1 = tanhf, 0 = tanh.approx.
+// Measured at cfg3 (profiles/r02_parity_probe.json): tanhf costs +2.6% per
+// teacher batch and +6% per student step and lowers the gradient error vs
+// the bf16-storage oracle only from 1.65e-3 to 1.38e-3 (the bf16 flips are
+// driven by fp32 accumulation order), so tanh.approx is the default.
+__device__ __forceinline__ float tanh_act(float x, int mode) { return mode ? tanhf(x) : tanh_fast(x); }
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);

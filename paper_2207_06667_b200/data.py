@@ -94,7 +94,11 @@ def gather_batch(data: DeviceDataset, rows: torch.Tensor, out: Batch | None = No
     if out is None:
         out = Batch(torch.empty(B, data.samples.shape[1], dtype=torch.bfloat16, device=data.device),
                     torch.empty(B, dtype=torch.int64, device=data.device), data.dim)
-    s = (stream or torch.cuda.current_stream()).cuda_stream
+    st = stream or torch.cuda.current_stream(data.device)
+    s = st.cuda_stream
+    # the epoch-order tensor `rows` views was allocated on the sampler's copy
+    # stream: keep its block from being recycled while this gather may run
+    rows.record_stream(st)
     _lib.call("edl_gather_rows", data.samples.data_ptr(), data.samples.stride(0), rows.data_ptr(),
               out.inputs.data_ptr(), out.inputs.stride(0), B, data.samples.shape[1],
               data.labels.data_ptr(), out.hard_labels.data_ptr(), s)

@@ -210,6 +210,9 @@ class SoftLabels:
     # reader's slot on the student's device (DistilReader share_batch): the
     # student trains on it instead of gathering the same rows again
     batch: "Batch | None" = None
+    # the producing teacher's class count (its head width); kd_loss raises
+    # ShapeError when it differs from the student's (edl/nnkit.py:272-274)
+    num_classes: int | None = None
 
     @property
     def size(self) -> int:
@@ -228,13 +231,26 @@ class DeviceLoss:
         self.status = status
 
     def __float__(self) -> float:
-        st = int(self.status.item())
         v = float(self.value.item())
-        if st == _lib.EDL_ERR_SHAPE:
-            raise ShapeError("label or soft-label class out of range")
-        if st == _lib.EDL_ERR_NUMERIC or not np.isfinite(v):
+        check_status(self.status)
+        if not np.isfinite(v):
             raise NumericError(f"loss is not finite: {v}")
         return v
+
+
+def check_status(status: torch.Tensor) -> None:
+    """Read a loss workspace's device status word (synchronises) and raise the
+    reference's exception for a device-detected error (bad label / class id
+    -> ShapeError, non-finite loss -> NumericError, edl/nnkit.py:272-297).
+    The word is sticky across launches until read here; raising clears it, so
+    one bad batch does not poison later checks on the same workspace."""
+    st = int(status.item())
+    if st == 0:
+        return
+    status.zero_()
+    if st == _lib.EDL_ERR_SHAPE:
+        raise ShapeError("label or soft-label class out of range")
+    raise NumericError("loss is not finite")
 
 
 def make_batch(inputs, labels, device=None) -> Batch:
@@ -378,6 +394,7 @@ def teacher_soft_labels(model: Model, inputs, temperature: float, k: int, out: S
     if out is None:
         out = SoftLabels(torch.empty(B, k, dtype=torch.float32, device=x.device),
                          torch.empty(B, k, dtype=torch.int32, device=x.device), float(temperature))
+    out.num_classes = K
     l = L.layers - 1
     _lib.call("edl_teacher_head_softmax_topk", h.data_ptr(), h.stride(0), model.w_bf16(l).data_ptr(),
               L.dims_p[l], model.b(l).data_ptr(), B, K, L.dims_p[l], float(temperature), int(k),
@@ -398,8 +415,10 @@ def kd_loss(model: Model, batch: Batch, soft: SoftLabels | None, cfg: TrainConfi
             raise ShapeError(f"soft batch {soft.size} != input batch {batch.size}")
         if soft.temperature != cfg.temperature:
             raise ValueError(f"soft labels tempered at {soft.temperature}, config says {cfg.temperature}")
-        if soft.k > model.num_classes:
-            raise ShapeError("soft-label class count does not match model")
+        if soft.k > model.num_classes or (soft.num_classes is not None
+                                          and soft.num_classes != model.num_classes):
+            raise ShapeError(f"soft labels over {soft.num_classes} classes (k={soft.k}), "
+                             f"student has {model.num_classes}")
     x = batch.inputs
     _check_inputs(model, x)
     B = x.shape[0]

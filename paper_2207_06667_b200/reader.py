@@ -209,7 +209,8 @@ class TeacherPool:
 
 
 class _Slot:
-    __slots__ = ("probs", "classes", "done", "release", "iteration", "teacher", "batch", "batch_filled")
+    __slots__ = ("probs", "classes", "done", "release", "iteration", "teacher", "batch", "batch_filled",
+                 "num_classes")
 
     def __init__(self, B: int, k: int, device, batch=None):
         self.probs = torch.empty(B, k, dtype=torch.float32, device=device)
@@ -220,6 +221,7 @@ class _Slot:
         self.teacher = None
         self.batch = batch              # input buffers a same-device teacher gathers into
         self.batch_filled = False
+        self.num_classes = None         # the producing teacher's head width
 
 
 class _TeacherHandle:
@@ -252,6 +254,10 @@ class DistilReader:
         self._teachers: dict[str, _TeacherHandle] = {}
         self._ready: dict[int, _Slot] = {}
         self._free: list[_Slot] = []
+        # slots a failed teacher may still write (its queued kernels / copies):
+        # (slot, event recorded on that teacher's stream at failure time);
+        # recycled only once the event has completed
+        self._retired: list[tuple[_Slot, torch.cuda.Event | None]] = []
         self._pending: deque[int] = deque()
         self._next_new = start_iteration
         self._end = end_iteration
@@ -304,6 +310,15 @@ class DistilReader:
         return it
 
     def _slot(self) -> _Slot:
+        if self._retired:
+            keep = []
+            for slot, ev in self._retired:
+                if ev is None or ev.query():
+                    slot.done = None
+                    self._free.append(slot)
+                else:
+                    keep.append((slot, ev))
+            self._retired = keep
         if self._free:
             slot = self._free.pop()
         else:
@@ -425,7 +440,7 @@ class DistilReader:
         self._last_consumed = slot
         self.pump()
         return SoftLabels(slot.probs, slot.classes, self.expected_temperature,
-                          slot.batch if slot.batch_filled else None)
+                          slot.batch if slot.batch_filled else None, slot.num_classes)
 
     def _inflight_slot(self, iteration: int):
         for h in self._teachers.values():
@@ -443,8 +458,16 @@ class DistilReader:
         unanswered = sorted(h.outstanding)
         for it in reversed(unanswered):
             self._pending.appendleft(it)
-        # slots of a dead teacher may still be written by its queued kernels:
-        # retire them (never reused) rather than recycle
+        # slots of a dead teacher may still be written by its queued kernels
+        # or peer copies: retire them behind an event on its stream (recycled
+        # once everything it had queued has drained; never, if it is hung)
+        drained = None
+        stream = getattr(h.worker, "stream", None)
+        if isinstance(stream, torch.cuda.Stream):
+            drained = torch.cuda.Event()
+            drained.record(stream)
+        for slot in h.outstanding.values():
+            self._retired.append((slot, drained))
         h.outstanding.clear()
         self.events.append("teacher_failure", node=node_id, context=context, unanswered=unanswered)
         if self._stopped:

@@ -240,6 +240,12 @@ class StudentStep:
             for ev in self._ready:
                 s.wait_event(ev)
 
+    def check_status(self) -> None:
+        """Raise ShapeError / NumericError if any step since the last check
+        saw a bad label, a soft label outside the class range or a
+        non-finite loss (device status word; synchronises)."""
+        nnkit.check_status(self.ws.status)
+
     def loss_values(self) -> list[float]:
         return self.losses[:min(self._n, self.losses.shape[0])].tolist()
 
@@ -365,12 +371,15 @@ class StudentNode:
             done = it + 1
             if cfg.checkpoint_dir and cfg.rank == 0 and done % cfg.checkpoint_interval == 0:
                 engine.settle()
+                engine.check_status()
                 save_checkpoint(cfg.checkpoint_dir, model.to_host(), done, self.host_data.id, cfg.world_size)
                 self.events.append("checkpoint", iteration=done)
             if cfg.metrics_dir and done % self.sampler.batches_per_epoch == 0:
                 engine.settle()
+                engine.check_status()
                 self._record_epoch(done, model)
         engine.settle()
+        engine.check_status()
         t1.record()
         torch.cuda.synchronize()
         span = t0.elapsed_time(t1) / 1e3

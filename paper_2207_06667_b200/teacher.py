@@ -23,7 +23,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import nnkit
+from . import _lib, nnkit
 from .data import DeviceDataset, gather_batch
 from .nnkit import Batch, Model, SoftLabels
 
@@ -35,7 +35,7 @@ class TeacherConfig:
     node_id: str
     temperature: float = 2.0
     k: int = 16
-    simulated_delay: float = 0.0   # accepted for API parity; device time is real
+    simulated_delay: float = 0.0   # seconds per batch, spent on the worker's stream (edl_stream_delay_ns)
 
     def __post_init__(self):
         if self.temperature <= 0:
@@ -90,7 +90,6 @@ class TeacherWorker:
         self.device = model.device
         self.stream = torch.cuda.Stream(device=self.device)
         if sm_reserve > 0:
-            from . import _lib
             with torch.cuda.device(self.device):
                 sms = _lib.load().edl_device_sms()
             _lib.call("edl_set_stream_max_ctas", self.stream.cuda_stream, max(1, sms - sm_reserve))
@@ -127,6 +126,8 @@ class TeacherWorker:
             batch = gather_batch(self.data, rows, target, self.stream)
             if target is not self._batch:
                 slot.batch_filled = True
+                target.inputs.record_stream(self.stream)
+                target.hard_labels.record_stream(self.stream)
             if local:
                 out = SoftLabels(slot.probs, slot.classes, self.cfg.temperature)
             else:
@@ -137,9 +138,23 @@ class TeacherWorker:
                 out = self._staging
             nnkit.teacher_soft_labels(self.model, batch.inputs, self.cfg.temperature, slot.probs.shape[1],
                                       out=out, stream=self.stream, probe=self.probe, ws=self._ws)
-            if not local:   # NVLink peer copy into the student-owned slot, on this side stream
-                slot.probs.copy_(out.probs, non_blocking=True)
-                slot.classes.copy_(out.classes, non_blocking=True)
+            if self.cfg.simulated_delay > 0:
+                _lib.call("edl_stream_delay_ns", int(self.cfg.simulated_delay * 1e9), self.stream.cuda_stream)
+            if not local:
+                # NVLink peer copy into the student-owned slot, ordered on this
+                # stream only (the student's stream never waits on it here;
+                # it waits on slot.done when it consumes the slot)
+                for dst, src in ((slot.probs, out.probs), (slot.classes, out.classes)):
+                    _lib.call("edl_memcpy_peer_async", dst.data_ptr(), dst.device.index, src.data_ptr(),
+                              src.device.index, src.numel() * src.element_size(), self.stream.cuda_stream)
+            if local:
+                # the slot's memory belongs to the student's allocator: keep it
+                # from being recycled while this stream may still write it
+                # (a remote slot is held by the reader until slot.done, or
+                # retired behind this stream if the teacher fails)
+                slot.probs.record_stream(self.stream)
+                slot.classes.record_stream(self.stream)
+            slot.num_classes = self.model.num_classes
             slot.done = torch.cuda.Event()
             slot.done.record(self.stream)
         self.batches_served += 1

@@ -34,8 +34,13 @@ def timeit(fn, iters, warm=5):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=30)
+    ap.add_argument("--tanh-mode", type=int, default=None, help="1 = tanhf, 0 = tanh.approx (edl_set_tanh_mode)")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    if a.tanh_mode is not None:
+        from paper_2207_06667_b200 import _lib
+        _lib.call("edl_set_tanh_mode", a.tanh_mode)
     B = 4096
     data = DeviceDataset(formats.make_blobs(0, 16384, 3072, 1000, 1.0), dev)
     sampler = DeviceShardSampler(data, 1, 0, B, seed=0)
