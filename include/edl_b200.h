@@ -306,6 +306,31 @@ int edl_stream_delay_ns(long long ns, void* stream);
 int edl_memcpy_peer_async(void* dst, int dst_device, const void* src, int src_device, long long bytes,
                           void* stream);
 
+/* Elastic teacher pool across processes (pool.ElasticPool; replaces the
+ * reference's INFER_REQUEST / INFER_REPLY socket path,
+ * edl/student_node.py:369-423 and edl/teacher_node.py:157-170, and the
+ * coordinator's registry, edl/coordinator.py:99-197, for teachers and
+ * students on one box):
+ *   edl_ipc_export / edl_ipc_open / edl_ipc_close: CUDA IPC of the student's
+ *     soft-label slot ring (handle = 64 bytes; the export names the whole
+ *     allocation, `offset` locates `ptr` in it). A teacher process opens it
+ *     and its head kernel writes (prob, class) pairs straight into the slot,
+ *     over NVLink when the student sits on another GPU.
+ *   edl_host_register / edl_host_unregister: map the pool's shared-memory
+ *     control block into the device address space, so a teacher's stream
+ *     writes a slot's READY tag (edl_stream_write_u32) after its kernels and
+ *     the student's host sees it with a plain load — no host waits on the
+ *     teacher's side and no device waits on the student's side, so a dead
+ *     teacher can never leave a student stream blocked.
+ *   edl_memcpy_async: cudaMemcpyAsync(cudaMemcpyDefault) for UVA / IPC
+ *     pointers. */
+int edl_memcpy_async(void* dst, const void* src, long long bytes, void* stream);
+int edl_host_register(void* ptr, long long bytes, void** dev_ptr);
+int edl_host_unregister(void* ptr);
+int edl_ipc_export(const void* ptr, void* handle, long long* offset);
+int edl_ipc_open(const void* handle, void** base);
+int edl_ipc_close(void* base);
+
 #ifdef __cplusplus
 }
 #endif

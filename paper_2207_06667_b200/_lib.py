@@ -87,6 +87,12 @@ _SIGNATURES = {
     "edl_cast_bf16": [c_void_p, c_ll, c_void_p, c_ll, c_int, c_int, c_void_p],
     "edl_stream_delay_ns": [c_ll, c_void_p],
     "edl_memcpy_peer_async": [c_void_p, c_int, c_void_p, c_int, c_ll, c_void_p],
+    "edl_memcpy_async": [c_void_p, c_void_p, c_ll, c_void_p],
+    "edl_host_register": [c_void_p, c_ll, c_void_p],
+    "edl_host_unregister": [c_void_p],
+    "edl_ipc_export": [c_void_p, c_void_p, c_void_p],
+    "edl_ipc_open": [c_void_p, c_void_p],
+    "edl_ipc_close": [c_void_p],
 }
 _RESTYPES = {"edl_last_error": c_char_p, "edl_colsum_workspace_floats": c_ll,
              "edl_bwd_weight_workspace_floats": c_ll,
@@ -149,7 +155,13 @@ _LAUNCHES = {"edl_linear_bwd_weight": 3,   # GEMM + two column-sum passes when d
              "edl_stream_wait_geq": 0,     # stream memory ops, not kernels
              "edl_stream_write_u32": 0,
              "edl_set_tanh_mode": 0,
-             "edl_memcpy_peer_async": 0}
+             "edl_memcpy_peer_async": 0,
+             "edl_memcpy_async": 0,
+             "edl_host_register": 0,
+             "edl_host_unregister": 0,
+             "edl_ipc_export": 0,
+             "edl_ipc_open": 0,
+             "edl_ipc_close": 0}
 launch_count = 0
 
 

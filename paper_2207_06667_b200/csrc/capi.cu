@@ -1009,6 +1009,67 @@ int edl_cast_bf16(const float* src, long long ld_src, void* dst, long long ld_ds
   return e == cudaSuccess ? 0 : cuda_fail(e, "cast_bf16");
 }
 
+int edl_memcpy_async(void* dst, const void* src, long long bytes, void* stream) {
+  if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(EDL_ERR_SHAPE, "memcpy_async: bad arguments");
+  if (bytes == 0) return 0;
+  cudaError_t e = cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDefault, as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "memcpy_async");
+}
+
+int edl_host_register(void* ptr, long long bytes, void** dev_ptr) {
+  if (!ptr || bytes <= 0 || !dev_ptr) return fail(EDL_ERR_SHAPE, "host_register: bad arguments");
+  cudaError_t e = cudaHostRegister(ptr, static_cast<size_t>(bytes), cudaHostRegisterMapped | cudaHostRegisterPortable);
+  if (e != cudaSuccess) return cuda_fail(e, "host_register");
+  e = cudaHostGetDevicePointer(dev_ptr, ptr, 0);
+  if (e != cudaSuccess) {
+    cudaHostUnregister(ptr);
+    return cuda_fail(e, "host_register (device pointer)");
+  }
+  return 0;
+}
+
+int edl_host_unregister(void* ptr) {
+  cudaError_t e = cudaHostUnregister(ptr);
+  return e == cudaSuccess ? 0 : cuda_fail(e, "host_unregister");
+}
+
+int edl_ipc_export(const void* ptr, void* handle, long long* offset) {
+  if (!ptr || !handle || !offset) return fail(EDL_ERR_SHAPE, "ipc_export: bad arguments");
+  // the handle names the whole cudaMalloc allocation (a caching allocator
+  // sub-allocates); the importer adds the offset
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  using PFN_range = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static PFN_range range = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    return (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess) ? reinterpret_cast<PFN_range>(p) : nullptr;
+  }();
+  if (!range) return fail(EDL_ERR_CUDA, "ipc_export: cuMemGetAddressRange unavailable");
+  const CUresult r = range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr));
+  if (r != CUDA_SUCCESS) return fail(EDL_ERR_CUDA, "ipc_export: cuMemGetAddressRange failed (%d)", static_cast<int>(r));
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return cuda_fail(e, "ipc_export");
+  std::memcpy(handle, &h, sizeof(h));
+  *offset = static_cast<long long>(reinterpret_cast<CUdeviceptr>(ptr) - base);
+  return 0;
+}
+
+int edl_ipc_open(const void* handle, void** base) {
+  if (!handle || !base) return fail(EDL_ERR_SHAPE, "ipc_open: bad arguments");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? 0 : cuda_fail(e, "ipc_open");
+}
+
+int edl_ipc_close(void* base) {
+  cudaError_t e = cudaIpcCloseMemHandle(base);
+  return e == cudaSuccess ? 0 : cuda_fail(e, "ipc_close");
+}
+
 int edl_stream_delay_ns(long long ns, void* stream) {
   if (ns < 0) return fail(EDL_ERR_PARAM, "stream_delay_ns: negative delay");
   if (ns == 0) return 0;

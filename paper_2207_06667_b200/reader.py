@@ -210,7 +210,7 @@ class TeacherPool:
 
 class _Slot:
     __slots__ = ("probs", "classes", "done", "release", "iteration", "teacher", "batch", "batch_filled",
-                 "num_classes")
+                 "num_classes", "index")
 
     def __init__(self, B: int, k: int, device, batch=None):
         self.probs = torch.empty(B, k, dtype=torch.float32, device=device)
@@ -222,6 +222,7 @@ class _Slot:
         self.batch = batch              # input buffers a same-device teacher gathers into
         self.batch_filled = False
         self.num_classes = None         # the producing teacher's head width
+        self.index = -1                 # position in a fixed (IPC-exported) ring, elastic.SlotRing
 
 
 class _TeacherHandle:
@@ -254,6 +255,13 @@ class DistilReader:
         self._teachers: dict[str, _TeacherHandle] = {}
         self._ready: dict[int, _Slot] = {}
         self._free: list[_Slot] = []
+        # a pool of teacher PROCESSES (elastic.ElasticPool) hands out slots of
+        # the student's IPC-exported ring; in-process teachers get lazily
+        # allocated slots
+        source = getattr(pool, "slot_source", None)
+        self._ring = source() if source is not None else None
+        if self._ring is not None:
+            self._free = list(self._ring.slots)
         # slots a failed teacher may still write (its queued kernels / copies):
         # (slot, event recorded on that teacher's stream at failure time);
         # recycled only once the event has completed
@@ -309,7 +317,7 @@ class DistilReader:
         self._next_new += 1
         return it
 
-    def _slot(self) -> _Slot:
+    def _slot(self) -> _Slot | None:
         if self._retired:
             keep = []
             for slot, ev in self._retired:
@@ -319,6 +327,16 @@ class DistilReader:
                 else:
                     keep.append((slot, ev))
             self._retired = keep
+        if self._ring is not None:
+            # fixed ring: a slot goes back to a teacher only once the step
+            # that read it has completed (its release event), because a remote
+            # teacher cannot order its stream after ours
+            for i, slot in enumerate(self._free):
+                if slot.release is None or slot.release.query():
+                    slot.release = None
+                    slot.batch_filled = False
+                    return self._free.pop(i)
+            return None
         if self._free:
             slot = self._free.pop()
         else:
@@ -339,13 +357,16 @@ class DistilReader:
             target = pick_teacher(out, self.cfg.pipeline_depth)
             if target is None:
                 return
+            slot = self._slot()
+            if slot is None:
+                return          # every ring slot is in flight or still being read
             it = self._take_next_iteration()
             handle = self._teachers[target]
-            slot = self._slot()
             slot.iteration, slot.teacher = it, target
             self.dispatch_count[it] = self.dispatch_count.get(it, 0) + 1
+            rows = self.sampler.rows_for(it) if getattr(handle.worker, "needs_rows", True) else None
             try:
-                handle.worker.submit(self.sampler.rows_for(it), slot)
+                handle.worker.submit(rows, slot)
             except RuntimeError:
                 self._pending.appendleft(it)
                 self._free.append(slot)
@@ -436,7 +457,9 @@ class DistilReader:
         self._consumed.add(iteration)
         self.consume_count[iteration] = self.consume_count.get(iteration, 0) + 1
         self._apply_tick()
-        stream.wait_event(slot.done)
+        if isinstance(slot.done, torch.cuda.Event):
+            stream.wait_event(slot.done)
+        # (a remote reply, elastic.HostFlag, is complete in memory once seen)
         self._last_consumed = slot
         self.pump()
         return SoftLabels(slot.probs, slot.classes, self.expected_temperature,
@@ -463,13 +486,16 @@ class DistilReader:
         # once everything it had queued has drained; never, if it is hung)
         drained = None
         stream = getattr(h.worker, "stream", None)
-        if isinstance(stream, torch.cuda.Stream):
+        if hasattr(h.worker, "drain_marker"):
+            drained = h.worker.drain_marker()       # a teacher process: until it has exited
+        elif isinstance(stream, torch.cuda.Stream):
             drained = torch.cuda.Event()
             drained.record(stream)
         for slot in h.outstanding.values():
             self._retired.append((slot, drained))
         h.outstanding.clear()
-        self.events.append("teacher_failure", node=node_id, context=context, unanswered=unanswered)
+        self.events.append("teacher_failure", node=node_id, context=context, unanswered=unanswered,
+                           why=getattr(h.worker, "failure", None))
         if self._stopped:
             return
         try:

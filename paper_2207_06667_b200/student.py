@@ -342,6 +342,12 @@ class StudentNode:
         reader = None
         online_out = None
         if cfg.mode == MODE_EDL:
+            if hasattr(self.pool, "open"):
+                # a pool of teacher processes (elastic.ElasticPool): publish our
+                # IPC slot ring and sampler parameters before dispatching
+                n_slots = min(cfg.sched.ut + 2 + cfg.sched.pipeline_depth * 8, self.pool.cb.max_slots)
+                self.pool.open(cfg.world_size, cfg.rank, cfg.train.batch_size, self.k, cfg.train.seed,
+                               cfg.train.temperature, self.classes, n_slots, model.device)
             reader = DistilReader(self.student_id, self.pool, cfg.sched, self.sampler, start, self.total_steps,
                                   1, self.events, cfg.train.temperature, self.k)
             self._initial_acquire(reader)
