@@ -292,6 +292,13 @@ int edl_topk_hits(const float* logits, long long ld, const long long* labels, in
 int edl_cast_bf16(const float* src, long long ld_src, void* dst, long long ld_dst, int rows,
                   int cols, void* stream);
 
+/* A reference caller's float64 batch (edl/nnkit.py:97-110 Batch.inputs,
+ * B x D) uploaded as is and converted on the device: fp64 -> fp32 -> bf16,
+ * the same double rounding as the host path (numpy astype(float32) then
+ * round-to-nearest-even), into the padded bf16 batch layout. */
+int edl_cast_bf16_f64(const double* src, long long ld_src, void* dst, long long ld_dst, int rows, int cols,
+                      void* stream);
+
 /* TeacherConfig.simulated_delay (edl/teacher_node.py:30-44, slept per batch
  * by TeacherServer._compute_loop :157-170): a single-thread device busy wait
  * of `ns` nanoseconds on `stream`, so a throttled teacher delays its own

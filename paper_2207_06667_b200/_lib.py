@@ -85,6 +85,7 @@ _SIGNATURES = {
                         c_void_p],
     "edl_topk_hits": [c_void_p, c_ll, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p],
     "edl_cast_bf16": [c_void_p, c_ll, c_void_p, c_ll, c_int, c_int, c_void_p],
+    "edl_cast_bf16_f64": [c_void_p, c_ll, c_void_p, c_ll, c_int, c_int, c_void_p],
     "edl_stream_delay_ns": [c_ll, c_void_p],
     "edl_memcpy_peer_async": [c_void_p, c_int, c_void_p, c_int, c_ll, c_void_p],
     "edl_memcpy_async": [c_void_p, c_void_p, c_ll, c_void_p],

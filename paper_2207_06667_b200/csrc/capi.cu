@@ -1009,6 +1009,15 @@ int edl_cast_bf16(const float* src, long long ld_src, void* dst, long long ld_ds
   return e == cudaSuccess ? 0 : cuda_fail(e, "cast_bf16");
 }
 
+int edl_cast_bf16_f64(const double* src, long long ld_src, void* dst, long long ld_dst, int rows, int cols,
+                      void* stream) {
+  if (rows < 0 || cols < 0 || ld_src < cols || ld_dst < cols) return fail(EDL_ERR_SHAPE, "cast_bf16_f64: bad shape");
+  if (rows == 0 || cols == 0) return 0;
+  cudaError_t e = launch_cast_bf16_f64(src, ld_src, reinterpret_cast<__nv_bfloat16*>(dst), ld_dst, rows, cols,
+                                       as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "cast_bf16_f64");
+}
+
 int edl_memcpy_async(void* dst, const void* src, long long bytes, void* stream) {
   if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(EDL_ERR_SHAPE, "memcpy_async: bad arguments");
   if (bytes == 0) return 0;

@@ -203,6 +203,8 @@ cudaError_t launch_topk_hits(const float* logits, long long ld, const int64_t* l
                              int K, int k, unsigned* hits, cudaStream_t stream);
 cudaError_t launch_cast_bf16(const float* src, long long ld_src, __nv_bfloat16* dst,
                              long long ld_dst, int rows, int cols, cudaStream_t stream);
+cudaError_t launch_cast_bf16_f64(const double* src, long long ld_src, __nv_bfloat16* dst,
+                                 long long ld_dst, int rows, int cols, cudaStream_t stream);
 cudaError_t launch_stream_delay(unsigned long long ns, cudaStream_t stream);
 
 }  // namespace edl

@@ -635,32 +635,46 @@ cudaError_t launch_topk_hits(const float* logits, long long ld, const int64_t* l
 // on the device, bench e2e): blockIdx.y strides rows, each thread converts 4
 // consecutive columns per iteration (16-byte load, 8-byte store) when the
 // row pitches and bases allow it, so there is no per-element division.
-__global__ void cast_bf16_kernel(const float* __restrict__ src, long long ld_src,
+template <typename T>
+__global__ void cast_bf16_kernel(const T* __restrict__ src, long long ld_src,
                                  __nv_bfloat16* __restrict__ dst, long long ld_dst, int rows,
                                  int cols, int vec) {
   griddep_wait();
   const long long step = static_cast<long long>(gridDim.x) * blockDim.x;
   for (int r = blockIdx.y; r < rows; r += gridDim.y) {
-    const float* sr = src + static_cast<size_t>(r) * ld_src;
+    const T* sr = src + static_cast<size_t>(r) * ld_src;
     __nv_bfloat16* dr = dst + static_cast<size_t>(r) * ld_dst;
     if (vec) {
       const int c4 = cols / 4;
       for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < c4; i += step) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(sr) + i);
+        float v0, v1, v2, v3;
+        if constexpr (sizeof(T) == 4) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(sr) + i);
+          v0 = v.x; v1 = v.y; v2 = v.z; v3 = v.w;
+        } else {
+          // fp64 -> fp32 -> bf16: the reference's float64 batch through the
+          // same double rounding as the host path (numpy astype(float32),
+          // then round-to-nearest-even to bf16)
+          const double2 a = __ldg(reinterpret_cast<const double2*>(sr) + 2 * i);
+          const double2 b = __ldg(reinterpret_cast<const double2*>(sr) + 2 * i + 1);
+          v0 = __double2float_rn(a.x); v1 = __double2float_rn(a.y);
+          v2 = __double2float_rn(b.x); v3 = __double2float_rn(b.y);
+        }
         uint2 o;
-        o.x = pack_bf16x2(v.x, v.y);
-        o.y = pack_bf16x2(v.z, v.w);
+        o.x = pack_bf16x2(v0, v1);
+        o.y = pack_bf16x2(v2, v3);
         reinterpret_cast<uint2*>(dr)[i] = o;
       }
     } else {
       for (long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; c < cols; c += step)
-        dr[c] = __float2bfloat16_rn(sr[c]);
+        dr[c] = __float2bfloat16_rn(static_cast<float>(sr[c]));
     }
   }
 }
 
-cudaError_t launch_cast_bf16(const float* src, long long ld_src, __nv_bfloat16* dst,
-                             long long ld_dst, int rows, int cols, cudaStream_t stream) {
+template <typename T>
+static cudaError_t launch_cast_t(const T* src, long long ld_src, __nv_bfloat16* dst, long long ld_dst, int rows,
+                                 int cols, cudaStream_t stream) {
   const bool vec = cols % 4 == 0 && ld_src % 4 == 0 && ld_dst % 4 == 0 &&
                    reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(dst) % 8 == 0;
   const long long per_row = vec ? cols / 4 : cols;
@@ -672,8 +686,18 @@ cudaError_t launch_cast_bf16(const float* src, long long ld_src, __nv_bfloat16* 
   if (bx * by > target) bx = (target + by - 1) / by;
   if (bx < 1) bx = 1;
   if (by < 1) by = 1;
-  return launch_pdl(cast_bf16_kernel, dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)), dim3(256), 0,
+  return launch_pdl(cast_bf16_kernel<T>, dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)), dim3(256), 0,
                     stream, 1, src, ld_src, dst, ld_dst, rows, cols, vec ? 1 : 0);
+}
+
+cudaError_t launch_cast_bf16(const float* src, long long ld_src, __nv_bfloat16* dst,
+                             long long ld_dst, int rows, int cols, cudaStream_t stream) {
+  return launch_cast_t(src, ld_src, dst, ld_dst, rows, cols, stream);
+}
+
+cudaError_t launch_cast_bf16_f64(const double* src, long long ld_src, __nv_bfloat16* dst,
+                                 long long ld_dst, int rows, int cols, cudaStream_t stream) {
+  return launch_cast_t(src, ld_src, dst, ld_dst, rows, cols, stream);
 }
 
 // ------------------------------------------------------------------ stream delay
