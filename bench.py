@@ -806,13 +806,18 @@ class _StreamedRing:
     """The EDL e2e input path: iteration it's batch is copied from pinned host
     memory (the caller's fp32 or fp64 B x D rows + int64 labels) into a device
     staging buffer and converted to the padded bf16 batch layout in ring slot
-    it % R (edl_cast_bf16 / edl_cast_bf16_f64), all on a copy stream
-    LOOKAHEAD iterations before its first reader; the teacher worker and the
-    student gather it by row index exactly as from a DeviceDataset (same
-    interface: samples / labels / dim / device; rows_for / batch_for /
-    batch_size as a sampler)."""
+    it % R (edl_cast_bf16 / edl_cast_bf16_f64), LOOKAHEAD iterations before
+    its first reader; the teacher worker and the student gather it by row
+    index exactly as from a DeviceDataset (same interface: samples / labels /
+    dim / device; rows_for / batch_for / batch_size as a sampler).
+
+    The copies and the conversions run on two streams over a 3-deep staging
+    ring: a conversion kernel that waits for SMs behind the teacher's GEMMs
+    must not hold up the next host->device copy (the copy engine would idle,
+    measured 44 vs 51 GB/s when both shared one stream)."""
 
     LOOKAHEAD = 4
+    STAGES = 3
 
     def __init__(self, host_x, host_y, dim, dev, ring_slots):
         import torch
@@ -824,10 +829,13 @@ class _StreamedRing:
         self.dim, self.device, self.data = dim, dev, self
         self.samples = torch.zeros(self.R * B, nnkit.pad(dim), dtype=torch.bfloat16, device=dev)
         self.labels = torch.zeros(self.R * B, dtype=torch.int64, device=dev)
-        self.stage = torch.empty(B, host_x.shape[2], dtype=host_x.dtype, device=dev)
+        self.stage = [torch.empty(B, host_x.shape[2], dtype=host_x.dtype, device=dev) for _ in range(self.STAGES)]
+        self.stage_free = [None] * self.STAGES
+        self.n_up = 0
         self.cast = "edl_cast_bf16_f64" if host_x.dtype == torch.float64 else "edl_cast_bf16"
         self.rows = [torch.arange(j * B, (j + 1) * B, device=dev) for j in range(self.R)]
         self.copy = torch.cuda.Stream(dev)
+        self.convert = torch.cuda.Stream(dev, priority=-1)
         self.landed: dict = {}          # iteration -> event (copy + conversion done)
         self.free = [None] * self.R     # slot -> event after the slot's last reader
         self.owner = [None] * self.R    # slot -> iteration it holds
@@ -840,17 +848,26 @@ class _StreamedRing:
         j, B = it % self.R, self.batch_size
         if self.owner[j] is not None and self.free[j] is None:
             raise RuntimeError(f"ring slot {j} still holds unconsumed iteration {self.owner[j]}")
+        st = self.n_up % self.STAGES
+        self.n_up += 1
+        src = it % self.host_x.shape[0]
         with torch.cuda.stream(self.copy):
+            if self.stage_free[st] is not None:
+                self.copy.wait_event(self.stage_free[st])      # its previous conversion has read it
+            self.stage[st].copy_(self.host_x[src], non_blocking=True)
+            copied = torch.cuda.Event()
+            copied.record(self.copy)
+        with torch.cuda.stream(self.convert):
+            self.convert.wait_event(copied)
             if self.free[j] is not None:
-                self.copy.wait_event(self.free[j])
-            src = it % self.host_x.shape[0]
-            self.stage.copy_(self.host_x[src], non_blocking=True)
+                self.convert.wait_event(self.free[j])
             dst = self.samples[j * B:(j + 1) * B]
-            _lib.call(self.cast, self.stage.data_ptr(), self.stage.stride(0), dst.data_ptr(), dst.stride(0), B,
-                      self.dim, self.copy.cuda_stream)
+            _lib.call(self.cast, self.stage[st].data_ptr(), self.stage[st].stride(0), dst.data_ptr(), dst.stride(0),
+                      B, self.dim, self.convert.cuda_stream)
             self.labels[j * B:(j + 1) * B].copy_(self.host_y[src], non_blocking=True)
             ev = torch.cuda.Event()
-            ev.record(self.copy)
+            ev.record(self.convert)
+        self.stage_free[st] = ev
         self.landed[it] = ev
         self.owner[j], self.free[j] = it, None
         self.h2d_bytes += self.host_x[src].numel() * self.host_x.element_size() + self.host_y[src].numel() * 8
@@ -968,7 +985,7 @@ def _e2e(cfg, samples, labels, teacher, student_h, tcfg, B, W, K, world, rank, d
     tws = nnkit.Workspace(teacher, B)
     bufs = [Batch(torch.zeros(B, Dp, dtype=torch.bfloat16, device=dev), torch.empty(B, dtype=torch.int64, device=dev),
                   cfg["dim"]) for _ in range(2)]
-    stage = torch.empty(B, cfg["dim"], dtype=torch.float32, device=dev)
+    stages = [torch.empty(B, cfg["dim"], dtype=torch.float32, device=dev) for _ in range(2)]
     out = SoftLabels(torch.empty(B, cfg["topk"], device=dev),
                      torch.empty(B, cfg["topk"], dtype=torch.int32, device=dev), cfg["T"])
     copy = torch.cuda.Stream(dev)
@@ -977,13 +994,13 @@ def _e2e(cfg, samples, labels, teacher, student_h, tcfg, B, W, K, world, rank, d
     used = [None, None]
 
     def upload(i):
+        # the copy stream only copies (a conversion queued behind GEMMs there
+        # would idle the copy engine); the conversion runs on the main stream
         j = i % 2
         with torch.cuda.stream(copy):
             if used[j] is not None:
                 copy.wait_event(used[j])
-            stage.copy_(host_x[i % nb], non_blocking=True)
-            _lib.call("edl_cast_bf16", stage.data_ptr(), stage.stride(0), bufs[j].inputs.data_ptr(),
-                      bufs[j].inputs.stride(0), B, cfg["dim"], copy.cuda_stream)
+            stages[j].copy_(host_x[i % nb], non_blocking=True)
             bufs[j].hard_labels.copy_(host_y[i % nb], non_blocking=True)
             up[j].record(copy)
 
@@ -997,6 +1014,8 @@ def _e2e(cfg, samples, labels, teacher, student_h, tcfg, B, W, K, world, rank, d
                 upload(i + 1)
             j = i % 2
             main.wait_event(up[j])
+            _lib.call("edl_cast_bf16", stages[j].data_ptr(), stages[j].stride(0), bufs[j].inputs.data_ptr(),
+                      bufs[j].inputs.stride(0), B, cfg["dim"], main.cuda_stream)
             soft = nnkit.teacher_soft_labels(teacher, bufs[j].inputs, cfg["T"], cfg["topk"], out=out, ws=tws)
             eng.step(bufs[j], soft)
             loss_host[i:i + 1].copy_(eng.losses[(eng._n - 1) % eng.losses.shape[0]:][:1], non_blocking=True)
