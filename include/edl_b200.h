@@ -225,6 +225,20 @@ int edl_teacher_head_softmax_topk(const void* H, long long ldh, const void* W, l
 int edl_tempered_softmax(const float* logits, long long ld, float* probs, long long ldp, int B,
                          int K, float T, void* stream);
 
+/* The student's logit layer fused with kd_loss (edl/nnkit.py:232 for the
+ * last layer, :283-299 for the loss and dlogits): one launch computes
+ * z = H W^T + b on the tensor cores, keeps the logit tile in TMEM, and writes
+ * only the per-row loss and bf16 dlogits — the fp32 logits never reach HBM.
+ * H: bf16 [B][ldh] (D used), W: bf16 [K][ldw], bias fp32 [K], labels int64
+ * [B], top-k soft labels as for edl_kd_loss_fwd_bwd; dlogits bf16 [B][lddz]
+ * (columns K .. pad16(K) written as 0). Followed by the same fixed-order
+ * batch mean into loss_out. K <= 2048 and k <= 32 (else EDL_ERR_SHAPE: use
+ * edl_linear_fwd + edl_kd_loss_fwd_bwd). */
+int edl_linear_kd_loss_fwd_bwd(const void* H, long long ldh, const void* W, long long ldw, const float* bias,
+                               const long long* labels, const float* q_vals, const int* q_idx, int B, int K, int D,
+                               int k, float alpha, float beta, float T, float* row_loss, float* loss_out,
+                               void* dlogits, long long lddz, int* status, void* stream);
+
 /* Fused distillation loss forward + backward, edl/nnkit.py:283-295:
  *   loss = mean_rows[ alpha*CE(onehot(y), softmax z) + beta*T^2*CE(q, softmax(z/T)) ]
  *   dz   = alpha/B*(softmax z - onehot y) + beta*T/B*(softmax(z/T) - q)

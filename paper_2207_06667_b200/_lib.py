@@ -76,6 +76,9 @@ _SIGNATURES = {
     "edl_kd_loss_fwd_bwd": [c_void_p, c_ll, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int,
                             c_float, c_float, c_float, c_void_p, c_void_p, c_void_p, c_void_p,
                             c_ll, c_void_p, c_void_p],
+    "edl_linear_kd_loss_fwd_bwd": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
+                                   c_int, c_int, c_int, c_float, c_float, c_float, c_void_p, c_void_p, c_void_p,
+                                   c_ll, c_void_p, c_void_p],
     "edl_sgd_step": [c_void_p, c_void_p, c_void_p, c_ll, c_float, c_void_p],
     "edl_stream_wait_geq": [c_void_p, c_uint, c_void_p],
     "edl_stream_write_u32": [c_void_p, c_uint, c_void_p],
@@ -153,6 +156,7 @@ _LAUNCHES = {"edl_linear_bwd_weight": 3,   # GEMM + two column-sum passes when d
              "edl_linear_bwd_weight_ws": 4,   # split-K GEMM + reduce + two column-sum passes (at most)
              "edl_conv_bwd_weight_nhwc": 4,   # the same plan with an im2col operand
              "edl_kd_loss_fwd_bwd": 2,     # row pass + deterministic batch-mean pass
+             "edl_linear_kd_loss_fwd_bwd": 2,   # fused logit GEMM + loss/dz, batch-mean pass
              "edl_stream_wait_geq": 0,     # stream memory ops, not kernels
              "edl_stream_write_u32": 0,
              "edl_set_tanh_mode": 0,

@@ -877,6 +877,38 @@ int edl_tempered_softmax(const float* logits, long long ld, float* probs, long l
   return e == cudaSuccess ? 0 : cuda_fail(e, "tempered_softmax");
 }
 
+int edl_linear_kd_loss_fwd_bwd(const void* H, long long ldh, const void* W, long long ldw, const float* bias,
+                               const long long* labels, const float* q_vals, const int* q_idx, int B, int K, int D,
+                               int k, float alpha, float beta, float T, float* row_loss, float* loss_out,
+                               void* dlogits, long long lddz, int* status, void* stream) {
+  if (B < 1 || K < 1 || D < 1 || ldh < D || ldw < D || lddz < K)
+    return fail(EDL_ERR_SHAPE, "linear_kd_loss: bad shape B=%d K=%d D=%d", B, K, D);
+  if (!(T > 0.f) || !std::isfinite(T)) return fail(EDL_ERR_PARAM, "linear_kd_loss: temperature %g", T);
+  if (alpha < 0.f || beta < 0.f || !(alpha + beta > 0.f)) return fail(EDL_ERR_PARAM, "linear_kd_loss: alpha/beta");
+  if (beta > 0.f && (k < 1 || k > K || k > 32 || !q_vals || !q_idx))
+    return fail(EDL_ERR_SHAPE, "linear_kd_loss: beta > 0 requires 1..32 soft labels (k=%d)", k);
+  const long long kp16 = (K + 15) / 16 * 16;
+  const int Nw = static_cast<int>(lddz < kp16 ? lddz : kp16);
+  if (Nw > 8 * 256) return fail(EDL_ERR_SHAPE, "linear_kd_loss: %d classes exceed 8 x 256", K);
+  const int ks = beta > 0.f ? k : 0;
+  const int kmax = ks <= 4 ? 4 : ks <= 8 ? 8 : ks <= 16 ? 16 : 32;
+  CUtensorMap ta, tb, ty;
+  int rc;
+  if ((rc = tensor_map(H, B, D, ldh, 64, 128, &ta))) return rc;
+  if ((rc = tensor_map(W, K, D, ldw, 64, 256, &tb))) return rc;
+  if ((rc = tensor_map_out(dlogits, B, Nw, lddz, false, &ty))) return rc;
+  KdArgs kp{bias, reinterpret_cast<const int64_t*>(labels), q_vals, q_idx, ks, alpha, beta, T, 1.0f / T,
+            T == 2.0f ? 1 : 0, row_loss, status};
+  static const int dbg = [] {
+    const char* v = getenv("EDL_KD_DEBUG");
+    return v ? atoi(v) : 0;
+  }();
+  kp.debug = dbg;
+  cudaError_t e = launch_kd_head(kmax, ta, tb, ty, B, K, Nw, D, kp, as_stream(stream));
+  if (e == cudaSuccess) e = launch_loss_mean(row_loss, B, loss_out, status, as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "linear_kd_loss");
+}
+
 int edl_kd_loss_fwd_bwd(const float* logits, long long ldz, const long long* labels,
                         const float* q_vals, const int* q_idx, int B, int K, int k, float alpha,
                         float beta, float T, float* row_loss, float* loss_out, unsigned* ticket,

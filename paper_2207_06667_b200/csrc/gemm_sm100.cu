@@ -1683,6 +1683,369 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---- student KD head: the logit GEMM with the distillation loss and its
+// gradient in the epilogue (edl/nnkit.py:283-299), so the fp32 logits never
+// reach HBM. A cluster of ceil(K / BN) CTAs splits the classes of a 128-row
+// block; each CTA keeps its 128 x BN logit tile in TMEM for two passes:
+//   pass 1: per row, running max m and the sums l1 = sum exp(z - m),
+//           lT = sum exp((z - m) / T), plus z at the label and the q-weighted
+//           sum of z at the soft classes (gathered through a per-thread
+//           shared-memory spill only for the ~1 in 2 chunks that hold one);
+//   merge:  halves through shared memory, then every CTA reads all the
+//           cluster's row states over DSMEM in rank order (identical results
+//           in every CTA); rank 0 writes the row loss
+//           alpha (lse1 - z_y) + beta T^2 (lseT - sum_j q_j z_j / T);
+//   pass 2: dz = alpha/B (softmax(z) - onehot(y)) + beta T/B (softmax(z/T) - q)
+//           from the same TMEM tile, sparse terms applied through the spill,
+//           bf16 through the TMA-store staging tiles (columns >= K are 0).
+// With T == 2 one MUFU per element and pass: exp(d) = exp(d / 2)^2.
+// The batch mean stays a separate fixed-order launch (loss_mean_kernel).
+template <int BN, int KMAX, bool T2>
+__global__ void __launch_bounds__(kThreads, 1)
+    kd_head_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmY, int M, int N, int Nw, int K, KdArgs kp) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int S = Cfg::kStages;
+  // T2: columns BN..2BN-1 keep pass 1's exponentials for pass 2
+  constexpr uint32_t kTmemCols = tmem_cols_for(T2 ? 2 * BN : BN);
+  constexpr int kChunks = BN / 64;            // chunks per thread and pass
+  constexpr float kL2E = 1.4426950408889634f;
+  constexpr int kSt = 5;                      // row state: m, l1, lT, z_y, sum q z
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * Cfg::kABytes;
+  uint8_t* stg = sB + S * Cfg::kBBytes;                              // [8 warps][2][2 KB] bf16 store tiles
+  float* sbias = reinterpret_cast<float*>(stg + Cfg::kStoreBytes);   // [BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + Cfg::kStoreBytes + Cfg::kEpiBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  // epilogue scratch in the drained operand ring (word-interleaved by thread)
+  float* spill = reinterpret_cast<float*>(smem);                    // [32][256]
+  float* hx = spill + 32 * kThreads;                                 // [kSt][128] half handover
+  float* st = hx + kSt * kBM;                                        // [kSt][128] this CTA's row states
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int cs = static_cast<int>(gridDim.x);
+  const int rank = static_cast<int>(blockIdx.x);
+  const int m0 = blockIdx.y * kBM;
+  const int n0 = rank * BN;
+  const int nk = (K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    prefetch_tmap(&tmY);
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(&tfull[0], 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();
+
+  if (warp == 0 && lane == 0) {
+    const uint64_t pa = l2_policy_evict_normal(), pb = l2_policy_evict_normal();
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % S;
+      mbar_wait(&empty[s], ((kb / S) & 1) ^ 1);
+      load_kblock<BN, false, false>(&tmA, &tmB, sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes,
+                                    &full[s], m0, n0, kb * kBK, pa, pb);
+    }
+  } else if (warp == 1 && lane == 0) {
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % S;
+      mbar_wait(&full[s], (kb / S) & 1);
+      tc_fence_after();
+      mma_kblock<BN, false, false>(tmem_base, smem_u32(sA + s * Cfg::kABytes),
+                                   smem_u32(sB + s * Cfg::kBBytes), kb == 0);
+      umma_commit(&empty[s]);
+    }
+    umma_commit(&tfull[0]);
+  }
+  __syncwarp();
+
+  const int q = warp & 3;
+  const int half = warp >> 2;
+  const int rl = 32 * q + lane;
+  const int row = m0 + rl;
+  const int tid = threadIdx.x;
+  const bool row_ok = row < M;
+  const bool soft = kp.beta > 0.f && kp.k > 0;
+  // this row's sparse entries (label, renormalised top-k), loaded while the MMAs run
+  int y = -1;
+  int qc[KMAX];
+  float qn[KMAX];
+  bool bad = false;
+  if (row_ok) {
+    const int64_t yy = __ldg(kp.labels + row);
+    bad = yy < 0 || yy >= N;
+    y = bad ? -1 : static_cast<int>(yy);
+  }
+  float qsum = 0.f;
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j) {
+    qc[j] = -1;
+    qn[j] = 0.f;
+    if (soft && row_ok && j < kp.k) {
+      qn[j] = __ldg(kp.qv + static_cast<size_t>(row) * kp.k + j);
+      const int c = __ldg(kp.qi + static_cast<size_t>(row) * kp.k + j);
+      qsum += qn[j];
+      if (c >= 0 && c < N) qc[j] = c;
+      else bad = true;
+    }
+  }
+  if (soft) {
+    const float inv_q = qsum > 0.f ? 1.0f / qsum : 0.f;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) qn[j] *= inv_q;
+  }
+  if (bad && rank == 0 && half == 0 && kp.status) atomicCAS(kp.status, 0, -1);
+  // Everything below works in base-2 units of the tempered logit:
+  // t = z log2(e) / T = fma(acc, kT, bias kT). Columns >= N get bias -inf,
+  // so their t and every exponential of them vanish without a predicate.
+  const float kT = kL2E * kp.inv_t;
+  const float Tt = kp.T;
+  if (warp >= 2) {
+    for (int j = tid - 64; j < BN; j += kThreads - 64)
+      sbias[j] = (n0 + j < N) ? __ldg(kp.bias + n0 + j) * kT : -INFINITY;
+  }
+  asm volatile("bar.sync 2, 256;" ::: "memory");
+  mbar_wait(&tfull[0], 0);
+  tc_fence_after();
+
+  const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * q) << 16);
+  auto hit_of = [&](int col0) {
+    bool h = static_cast<unsigned>(y - col0) < 32u;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) h |= static_cast<unsigned>(qc[j] - col0) < 32u;
+    return h;
+  };
+  // t for the 32 columns of a chunk (bias pre-scaled, float4 smem broadcast)
+  auto tvals = [&](const uint32_t (&rr)[32], int c, float (&t)[32]) {
+    const float4* b4 = reinterpret_cast<const float4*>(sbias + c);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 b = b4[i];
+      t[4 * i + 0] = fmaf(__uint_as_float(rr[4 * i + 0]), kT, b.x);
+      t[4 * i + 1] = fmaf(__uint_as_float(rr[4 * i + 1]), kT, b.y);
+      t[4 * i + 2] = fmaf(__uint_as_float(rr[4 * i + 2]), kT, b.z);
+      t[4 * i + 3] = fmaf(__uint_as_float(rr[4 * i + 3]), kT, b.w);
+    }
+  };
+  // scale factors of a running state when its max moves from m to nm
+  // (both 0 when the state is empty)
+  auto rescale = [&](float m, float nm, float& sT, float& s1) {
+    const bool live = m != -INFINITY;
+    const float e = live ? exp2f_approx(m - nm) : 0.f;
+    sT = e;
+    if constexpr (T2) s1 = e * e;
+    else s1 = live ? exp2f_approx((m - nm) * Tt) : 0.f;
+  };
+
+  // ---- pass 1: row statistics (tm = max t, lT = sum 2^(t - tm),
+  //      l1 = sum 2^((t - tm) T), ty = t at the label, tq = sum q t)
+  float tm = -INFINITY, l1 = 0.f, lT = 0.f, ty = 0.f, tq = 0.f;
+  float cmv[kChunks];            // T2: each chunk's max (pass 2 rescales its stored exponentials)
+  uint32_t r[32];
+  tmem_ld32_issue(taddr + 32 * half, r);
+  tmem_ld_wait(r);
+#pragma unroll
+  for (int i = 0; i < kChunks; ++i) {
+    const int c = 32 * half + 64 * i;
+    float t[32];
+    tvals(r, c, t);
+    const bool more = i + 1 < kChunks;
+    if (more) tmem_ld32_issue(taddr + c + 64, r);
+    const int col0 = n0 + c;
+    cmv[i] = -INFINITY;
+    if (col0 < N && !(kp.debug & 5)) {
+      // tree max and 4-way partial sums: no 32-long dependency chains
+      float mx[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) mx[j] = fmaxf(t[j], t[j + 16]);
+#pragma unroll
+      for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+        for (int j = 0; j < w; ++j) mx[j] = fmaxf(mx[j], mx[j + w]);
+      const float cm = mx[0];
+      float aT[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
+      if constexpr (T2) {
+        // exponentials relative to the chunk's own max, kept in TMEM
+        float e[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          e[j] = exp2f_approx(t[j] - cm);
+          aT[j & 3] += e[j];
+          a1[j & 3] = fmaf(e[j], e[j], a1[j & 3]);
+        }
+        tmem_st32(taddr + BN + c, e);
+        cmv[i] = cm;
+        const float nm = fmaxf(tm, cm);
+        float sa, sa1;
+        rescale(tm, nm, sa, sa1);
+        const float sb = exp2f_approx(cm - nm);
+        lT = lT * sa + ((aT[0] + aT[1]) + (aT[2] + aT[3])) * sb;
+        l1 = l1 * sa1 + ((a1[0] + a1[1]) + (a1[2] + a1[3])) * (sb * sb);
+        tm = nm;
+      } else {
+        if (cm > tm) {
+          float sT, s1;
+          rescale(tm, cm, sT, s1);
+          lT *= sT;
+          l1 *= s1;
+          tm = cm;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float e = exp2f_approx(t[j] - tm);
+          aT[j & 3] += e;
+          a1[j & 3] += exp2f_approx((t[j] - tm) * Tt);
+        }
+        lT += (aT[0] + aT[1]) + (aT[2] + aT[3]);
+        l1 += (a1[0] + a1[1]) + (a1[2] + a1[3]);
+      }
+      if (hit_of(col0)) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) spill[j * kThreads + tid] = t[j];
+        if (static_cast<unsigned>(y - col0) < 32u) ty += spill[(y - col0) * kThreads + tid];
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j)
+          if (static_cast<unsigned>(qc[j] - col0) < 32u) tq += qn[j] * spill[(qc[j] - col0) * kThreads + tid];
+      }
+    }
+    __syncwarp();
+    if (more) tmem_ld_wait(r);
+  }
+  if constexpr (T2) tmem_st_wait();
+  // ---- merge: halves, then the cluster (every CTA, rank order)
+  auto combine = [&](float om, float ol1, float olT) {
+    const float nm = fmaxf(tm, om);
+    float sa, sa1, sb, sb1;
+    rescale(tm, nm, sa, sa1);
+    rescale(om, nm, sb, sb1);
+    l1 = l1 * sa1 + ol1 * sb1;
+    lT = lT * sa + olT * sb;
+    tm = nm;
+  };
+  if (half == 1) {
+    hx[0 * kBM + rl] = tm;
+    hx[1 * kBM + rl] = l1;
+    hx[2 * kBM + rl] = lT;
+    hx[3 * kBM + rl] = ty;
+    hx[4 * kBM + rl] = tq;
+  }
+  __syncthreads();
+  if (half == 0) {
+    combine(hx[0 * kBM + rl], hx[1 * kBM + rl], hx[2 * kBM + rl]);
+    st[0 * kBM + rl] = tm;
+    st[1 * kBM + rl] = l1;
+    st[2 * kBM + rl] = lT;
+    st[3 * kBM + rl] = ty + hx[3 * kBM + rl];
+    st[4 * kBM + rl] = tq + hx[4 * kBM + rl];
+  }
+  if (cs > 1) cluster_sync(); else __syncthreads();
+  {
+    float rv[kSt];
+#pragma unroll
+    for (int w = 0; w < kSt; ++w) rv[w] = ld_dsmem_f32(mapa(smem_u32(st + w * kBM + rl), 0));
+    tm = rv[0]; l1 = rv[1]; lT = rv[2]; ty = rv[3]; tq = rv[4];
+#pragma unroll 1
+    for (int rr = 1; rr < cs; ++rr) {
+#pragma unroll
+      for (int w = 0; w < kSt; ++w) rv[w] = ld_dsmem_f32(mapa(smem_u32(st + w * kBM + rl), rr));
+      combine(rv[0], rv[1], rv[2]);
+      ty += rv[3];
+      tq += rv[4];
+    }
+  }
+  const float ch = kp.alpha / static_cast<float>(M);
+  const float csoft = soft ? kp.beta * kp.T / static_cast<float>(M) : 0.f;
+  if (rank == 0 && half == 0 && row_ok) {
+    // ln 2 [alpha (T (tm - t_y) + log2 l1) + beta T^2 (tm - sum q t + log2 lT)]
+    constexpr float kLn2 = 0.6931471805599453f;
+    float loss = 0.f;
+    if (kp.alpha > 0.f && y >= 0) loss += kp.alpha * (Tt * (tm - ty) + __log2f(l1));
+    if (soft) loss += kp.beta * Tt * Tt * (tm - tq + __log2f(lT));
+    kp.row_loss[row] = loss * kLn2;
+  }
+  // ---- pass 2: dz = c1 2^((t - tm) T) + cT 2^(t - tm), sparse terms, bf16 TMA store
+  const float c1 = kp.alpha > 0.f ? ch / l1 : 0.f;
+  const float cT = csoft / lT;
+  uint32_t stores = 0;
+  uint8_t* wstg = stg + warp * 4096;
+  const uint32_t src = T2 ? BN : 0;   // T2: the stored exponentials; else the accumulator
+  tmem_ld32_issue(taddr + src + 32 * half, r);
+  tmem_ld_wait(r);
+#pragma unroll
+  for (int i = 0; i < kChunks; ++i) {
+    const int c = 32 * half + 64 * i;
+    float v[32];
+    if constexpr (T2) {
+      // e' = e 2^(cm - tm) = 2^(t - tm); dz = e' (cT + c1 e')
+      const float sg = cmv[i] == -INFINITY ? 0.f : exp2f_approx(cmv[i] - tm);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float e = __uint_as_float(r[j]) * sg;
+        v[j] = e * fmaf(c1, e, cT);
+      }
+    } else {
+      tvals(r, c, v);
+    }
+    const bool more = i + 1 < kChunks;
+    if (more) tmem_ld32_issue(taddr + src + c + 64, r);
+    const int col0 = n0 + c;
+    if (col0 < Nw && !(kp.debug & 6)) {
+      if constexpr (!T2) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float x = v[j] - tm;
+          v[j] = fmaf(c1, exp2f_approx(x * Tt), cT * exp2f_approx(x));
+        }
+      } else if (col0 >= N) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0.f;   // no exponentials were stored for this chunk
+      }
+      if (hit_of(col0)) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) spill[j * kThreads + tid] = v[j];
+        if (kp.alpha > 0.f && static_cast<unsigned>(y - col0) < 32u) spill[(y - col0) * kThreads + tid] -= ch;
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j)
+          if (static_cast<unsigned>(qc[j] - col0) < 32u) spill[(qc[j] - col0) * kThreads + tid] -= csoft * qn[j];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = spill[j * kThreads + tid];
+      }
+      uint8_t* buf = wstg + (stores & 1) * 2048;
+      if (lane == 0) bulk_wait_read1();
+      __syncwarp();
+      stage_chunk<false>(buf, lane, v);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(&tmY, buf, col0, m0 + 32 * q);
+        bulk_commit();
+      }
+      ++stores;
+    }
+    __syncwarp();
+    if (more) tmem_ld_wait(r);
+  }
+  if (lane == 0) bulk_wait0();
+  tc_fence_before();
+  if (cs > 1) cluster_sync(); else __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
 // ------------------------------------------------------------------ launchers
 template <int BN, bool A_MN, bool B_MN, int EPI>
 static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, int M, int N,
@@ -1841,6 +2204,30 @@ static cudaError_t launch_head_k(int kmax, const CUtensorMap& ta, const CUtensor
     case 8: return launch_head_t<BN, 8>(ta, tb, M, N, K, hp, stream);
     case 16: return launch_head_t<BN, 16>(ta, tb, M, N, K, hp, stream);
     case 32: return launch_head_t<BN, 32>(ta, tb, M, N, K, hp, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int KMAX>
+static cudaError_t launch_kd_head_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, int M,
+                                   int N, int Nw, int K, const KdArgs& kp, cudaStream_t stream) {
+  constexpr int BN = 256;
+  auto kern = kp.t2 ? kd_head_kernel<BN, KMAX, true> : kd_head_kernel<BN, KMAX, false>;
+  cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), GemmCfg<BN>::kSmem);
+  if (e != cudaSuccess) return e;
+  const int cs = (Nw + BN - 1) / BN;
+  if (cs > 8) return cudaErrorInvalidValue;
+  return launch_pdl(kern, dim3(cs, (M + kBM - 1) / kBM, 1), dim3(kThreads), GemmCfg<BN>::kSmem, stream, cs,
+                    ta, tb, ty, M, N, Nw, K, kp);
+}
+
+cudaError_t launch_kd_head(int kmax, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, int M,
+                           int N, int Nw, int K, const KdArgs& kp, cudaStream_t stream) {
+  switch (kmax) {
+    case 4: return launch_kd_head_t<4>(ta, tb, ty, M, N, Nw, K, kp, stream);
+    case 8: return launch_kd_head_t<8>(ta, tb, ty, M, N, Nw, K, kp, stream);
+    case 16: return launch_kd_head_t<16>(ta, tb, ty, M, N, Nw, K, kp, stream);
+    case 32: return launch_kd_head_t<32>(ta, tb, ty, M, N, Nw, K, kp, stream);
     default: return cudaErrorInvalidValue;
   }
 }

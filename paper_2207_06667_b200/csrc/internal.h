@@ -91,6 +91,20 @@ struct HeadArgs {
   int* idx;
 };
 
+// student logit layer + KD loss + dlogits (kd_head_kernel)
+struct KdArgs {
+  const float* bias;
+  const int64_t* labels;
+  const float* qv;      // top-k soft labels [B][k] (k = 0 or beta = 0: none)
+  const int* qi;
+  int k;
+  float alpha, beta, T, inv_t;
+  int t2;               // T == 2: exp(d) = exp(d / 2)^2
+  float* row_loss;
+  int* status;
+  int debug = 0;        // timing experiments only (EDL_KD_DEBUG): 1 skip pass 1, 2 skip pass 2, 4 skip both
+};
+
 enum class GemmKind { FwdTanh, FwdLinear, BwdData, BwdWeight, FwdRelu, FwdIdentBf16, BwdDataPlain, ConvDgrad };
 
 constexpr int kMaxGroup = 4;
@@ -134,6 +148,9 @@ cudaError_t launch_nvls_allreduce_sgd(float* mc_grad, float* mc_param, void* mc_
 cudaError_t launch_gemm_pair(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
                              const CUtensorMap& ty, int M, int N, int K, const EpiArgs& ep, int num_sms,
                              cudaStream_t stream, const CUtensorMap* tr = nullptr);
+cudaError_t launch_kd_head(int kmax, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, int M,
+                           int N, int Nw, int K, const KdArgs& kp, cudaStream_t stream);
+cudaError_t launch_loss_mean(const float* row_loss, int B, float* loss_out, int* status, cudaStream_t stream);
 cudaError_t launch_teacher_head(int bn, int kmax, const CUtensorMap& ta, const CUtensorMap& tb,
                                 int M, int N, int K, const HeadArgs& hp, cudaStream_t stream);
 

@@ -176,6 +176,10 @@ __global__ void __launch_bounds__(256) loss_mean_kernel(const float* __restrict_
   }
 }
 
+cudaError_t launch_loss_mean(const float* row_loss, int B, float* loss_out, int* status, cudaStream_t stream) {
+  return launch_pdl(loss_mean_kernel, dim3(1), dim3(256), 0, stream, 1, row_loss, B, loss_out, status);
+}
+
 template <int KPL>
 static cudaError_t launch_kd_t(const float* logits, long long ld_z, const int64_t* labels,
                                const float* q_vals, const int* q_idx, int B, int K, int Kw, int k,

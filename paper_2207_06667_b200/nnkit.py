@@ -19,6 +19,7 @@ deliberate:
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -311,15 +312,18 @@ def workspace_for(model: Model, batch_size: int) -> Workspace:
 # Core math (edl/nnkit.py:193-335)
 
 
-def _forward_into(model: Model, x: torch.Tensor, ws: Workspace, stream=None, layer_ready=None) -> torch.Tensor:
-    """acts[1..L-1] = tanh layers, ws.logits = last layer (fp32). layer_ready[l]
-    (optional CUDA event) gates layer l's GEMM: its parameters are still being
-    updated on another stream (StudentStep's overlapped gradient exchange)."""
+def _forward_into(model: Model, x: torch.Tensor, ws: Workspace, stream=None, layer_ready=None,
+                  layers: int | None = None) -> torch.Tensor:
+    """acts[1..L-1] = tanh layers, ws.logits = last layer (fp32); `layers`
+    stops early (kd_loss runs the logit layer fused with the loss).
+    layer_ready[l] (optional CUDA event) gates layer l's GEMM: its parameters
+    are still being updated on another stream (StudentStep's overlapped
+    gradient exchange)."""
     L = model.layout
     B = x.shape[0]
     s = _stream(stream)
     h = x
-    for l in range(L.layers):
+    for l in range(L.layers if layers is None else layers):
         if layer_ready is not None and layer_ready[l] is not None:
             (stream or torch.cuda.current_stream()).wait_event(layer_ready[l])
         last = l == L.layers - 1
@@ -402,12 +406,19 @@ def teacher_soft_labels(model: Model, inputs, temperature: float, k: int, out: S
     return out
 
 
+_KD_UNFUSED = os.environ.get("EDL_KD_UNFUSED") == "1"   # A/B switch: logits GEMM + separate loss kernel
+
+
 def kd_loss(model: Model, batch: Batch, soft: SoftLabels | None, cfg: TrainConfig,
             stream=None, ws: Workspace | None = None,
             loss_slot: torch.Tensor | None = None,
-            fused_sgd_eta: float | None = None, layer_ready=None) -> tuple[DeviceLoss, Gradients | None]:
+            fused_sgd_eta: float | None = None, layer_ready=None,
+            fused: bool | None = None) -> tuple[DeviceLoss, Gradients | None]:
     """Combined distillation loss and analytic gradients (edl/nnkit.py:254-309):
-    forward GEMMs -> fused loss/dlogits kernel -> backward GEMMs."""
+    hidden forward GEMMs -> the logit GEMM with the loss and dlogits in its
+    epilogue (edl_linear_kd_loss_fwd_bwd; fp32 logits never reach HBM) ->
+    backward GEMMs. fused=False (or K > 2048) runs the logit GEMM and the
+    separate loss kernel instead (ws.logits then holds the logits)."""
     if cfg.beta > 0:
         if soft is None:
             raise ShapeError("beta > 0 requires soft labels")
@@ -425,16 +436,27 @@ def kd_loss(model: Model, batch: Batch, soft: SoftLabels | None, cfg: TrainConfi
     L = model.layout
     ws = ws or workspace_for(model, B)
     s = _stream(stream)
-    _forward_into(model, x, ws, stream, layer_ready)
-    dz = ws.deltas[L.layers]
     q_vals = soft.probs if (soft is not None and cfg.beta > 0) else None
     q_idx = soft.classes if (soft is not None and cfg.beta > 0) else None
     k = soft.k if q_vals is not None else 0
+    use_fused = (not _KD_UNFUSED if fused is None else fused) and pad(model.num_classes) <= 2048 and k <= 32
+    _forward_into(model, x, ws, stream, layer_ready, layers=L.layers - 1 if use_fused else None)
+    dz = ws.deltas[L.layers]
     loss = ws.loss if loss_slot is None else loss_slot
-    _lib.call("edl_kd_loss_fwd_bwd", ws.logits.data_ptr(), ws.logits.stride(0), batch.hard_labels.data_ptr(),
-              _ptr(q_vals), _ptr(q_idx), B, model.num_classes, k, float(cfg.alpha), float(cfg.beta),
-              float(cfg.temperature), ws.row_loss.data_ptr(), loss.data_ptr(), ws.ticket.data_ptr(),
-              dz.data_ptr(), dz.stride(0), ws.status.data_ptr(), s)
+    if use_fused:
+        l = L.layers - 1
+        if layer_ready is not None and layer_ready[l] is not None:
+            (stream or torch.cuda.current_stream()).wait_event(layer_ready[l])
+        h = x if l == 0 else ws.acts[l]
+        _lib.call("edl_linear_kd_loss_fwd_bwd", h.data_ptr(), h.stride(0), model.w_bf16(l).data_ptr(), L.dims_p[l],
+                  model.b(l).data_ptr(), batch.hard_labels.data_ptr(), _ptr(q_vals), _ptr(q_idx), B,
+                  model.num_classes, L.dims_p[l], k, float(cfg.alpha), float(cfg.beta), float(cfg.temperature),
+                  ws.row_loss.data_ptr(), loss.data_ptr(), dz.data_ptr(), dz.stride(0), ws.status.data_ptr(), s)
+    else:
+        _lib.call("edl_kd_loss_fwd_bwd", ws.logits.data_ptr(), ws.logits.stride(0), batch.hard_labels.data_ptr(),
+                  _ptr(q_vals), _ptr(q_idx), B, model.num_classes, k, float(cfg.alpha), float(cfg.beta),
+                  float(cfg.temperature), ws.row_loss.data_ptr(), loss.data_ptr(), ws.ticket.data_ptr(),
+                  dz.data_ptr(), dz.stride(0), ws.status.data_ptr(), s)
     backward_into(model, x, ws, stream, sgd_eta=fused_sgd_eta)
     # fused_sgd_eta: the model was already updated (kd_loss + sgd_step in one
     # pass, single student); there is no gradient to return

@@ -245,28 +245,29 @@ def test_student_kernels_on_device_operands(setup, teacher_run, student_run):
         MEASURED[f"student_fwd{l}_worst_ratio"] = worst
         assert worst <= 1.0, (l, worst)
         acts[l + 1] = dev
+    # the fused logit GEMM + loss + dz kernel (edl_linear_kd_loss_fwd_bwd):
+    # fp64 on the device's bf16 layer-2 activations; the logit error model
+    # eps = acc(D) sum_k |a_k w_k| enters the loss and, through the softmax,
+    # dz (|d softmax_i| <= 2 p_i eps)
     z = acts[2] @ wq[2].T + student_h.biases[2]
-    zdev = ws.logits[:, :K].cpu().numpy().astype(np.float64)
-    MEASURED["student_logits_rel"] = rel(zdev, z)
-    worst = worst_ratio(zdev, z, acc(acts[2].shape[1]) * (np.abs(acts[2]) @ np.abs(wq[2]).T))
-    MEASURED["student_logits_worst_ratio"] = worst
-    assert rel(zdev, z) <= 1e-5 and worst <= 1.0
-    # the loss kernel on the device's fp32 logits
+    eps = acc(acts[2].shape[1]) * (np.abs(acts[2]) @ np.abs(wq[2]).T).max(axis=1, keepdims=True)
     q = ref.topk_dense(soft.probs.cpu().numpy().astype(np.float64), soft.classes.cpu().numpy(), K)
     rows = np.arange(B)
-    logp = ref.log_softmax(zdev)
-    logp_t = ref.log_softmax(zdev / T)
+    logp = ref.log_softmax(z)
+    logp_t = ref.log_softmax(z / T)
     loss = 0.5 * float(-logp[rows, y].mean()) + 0.5 * T * T * float(-(q * logp_t).sum(axis=1).mean())
-    MEASURED["student_loss_rel_on_device_logits"] = abs(lv - loss) / abs(loss)
+    MEASURED["student_loss_rel_fused"] = abs(lv - loss) / abs(loss)
     assert abs(lv - loss) <= 1e-5 * abs(loss)
-    p = np.exp(logp)
+    p1, pT = np.exp(logp), np.exp(logp_t)
+    p = p1.copy()
     p[rows, y] -= 1.0
-    dz = (0.5 / B) * p + (0.5 * T / B) * (np.exp(logp_t) - q)
+    dz = (0.5 / B) * p + (0.5 * T / B) * (pT - q)
     dz_dev = bf16_host(ws.deltas[3][:, :K])
-    # fp32 softmax terms are each <= 1: acc per unit of the two coefficients
-    worst = worst_ratio(dz_dev, dz, ulp_bf16(dz) + acc(K) * (0.5 + 0.5 * T) / B)
+    bound = ulp_bf16(dz) + 2 * eps * (0.5 / B * p1 + 0.5 * T / B * pT / T) + 2.0 ** -20 * (0.5 + 0.5 * T) / B
+    worst = worst_ratio(dz_dev, dz, bound)
     MEASURED["student_dz_worst_ratio"] = worst
     assert worst <= 1.0
+    assert (bf16_host(ws.deltas[3][:, K:]) == 0).all()
     # backprop data: delta_l = bf16((delta_{l+1} W_l) * (1 - a_l^2))
     deltas = {3: dz_dev}
     for l in (2, 1):

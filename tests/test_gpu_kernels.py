@@ -168,6 +168,108 @@ def test_kd_loss(lib, B, K, k, alpha, beta, T):
     assert (dz[:, K:] == 0).all()
 
 
+def _kd_reference(zz, y, qv, qi, alpha, beta, T):
+    """loss and dlogits in fp64 (edl/nnkit.py:283-299) on fp64 logits."""
+    B, K = zz.shape
+    logp = torch.log_softmax(zz, 1)
+    logpt = torch.log_softmax(zz / T, 1)
+    ref = 0.0
+    dref = torch.zeros_like(zz)
+    if alpha > 0:
+        ref += alpha * (-logp[torch.arange(B), y]).mean()
+        dref += alpha / B * (logp.exp() - torch.nn.functional.one_hot(y, K))
+    if beta > 0:
+        qd = torch.zeros(B, K, device="cuda", dtype=torch.float64).scatter_(1, qi.long(), qv.double())
+        qd = qd / qd.sum(1, keepdim=True)
+        ref += beta * T * T * (-(qd * logpt).sum(1)).mean()
+        dref += beta * T / B * (logpt.exp() - qd)
+    return float(ref), dref, logp.exp(), logpt.exp()
+
+
+# (B, hidden D, classes K, k, alpha, beta, T): one CTA / cluster of 2..8 along
+# the classes, ragged B and K, every KMAX instance, T == 2 (one exp per
+# element) and T != 2, hard-only and soft-only
+KD_HEAD_CASES = [(32, 64, 10, 10, 0.5, 0.5, 2.0), (300, 128, 1000, 16, 0.5, 0.5, 2.0),
+                 (4096, 1024, 1000, 16, 0.5, 0.5, 2.0), (129, 64, 300, 8, 1.0, 0.0, 2.0),
+                 (200, 192, 513, 32, 0.0, 1.0, 3.0), (64, 80, 2048, 4, 0.7, 0.3, 0.5),
+                 (1000, 512, 777, 20, 0.5, 0.5, 1.0)]
+
+
+@pytest.mark.parametrize("B,D,K,k,alpha,beta,T", KD_HEAD_CASES)
+def test_linear_kd_loss_fused(lib, B, D, K, k, alpha, beta, T):
+    """edl_linear_kd_loss_fwd_bwd (logit GEMM + KD loss + dlogits in one
+    epilogue) against fp64 over the SAME bf16 operands: logits error model
+    |dz - ref| <= one bf16 ulp + the softmax's sensitivity to an fp32
+    accumulation error of (D / 16) 2^-24 sum|h w| per logit."""
+    Dp, Kp = (D + 15) // 16 * 16, (K + 15) // 16 * 16
+    h = _padded(torch.tanh(_rand(B, D, seed=3)), B, Dp)
+    w = _padded(_rand(K, D, scale=1.0 / D ** 0.5 * 3, seed=4), Kp, Dp)
+    bias = torch.zeros(Kp, device="cuda")
+    bias[:K] = _rand(K, scale=0.1, seed=5)
+    y = torch.randint(0, K, (B,), generator=torch.Generator().manual_seed(6)).cuda()
+    q = torch.rand(B, K, generator=torch.Generator().manual_seed(7)).cuda() + 0.01
+    qv, qi = torch.topk(q, k, dim=1)
+    qv, qi = (qv / q.sum(1, keepdim=True)).contiguous(), qi.int().contiguous()
+    row = torch.empty(B, device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    dz = torch.full((B, Kp), 7.0, dtype=torch.bfloat16, device="cuda")
+    lib.call("edl_linear_kd_loss_fwd_bwd", h.data_ptr(), Dp, w.data_ptr(), Dp, bias.data_ptr(), y.data_ptr(),
+             qv.data_ptr(), qi.data_ptr(), B, K, Dp, k if beta > 0 else 0, alpha, beta, T, row.data_ptr(),
+             loss.data_ptr(), dz.data_ptr(), Kp, status.data_ptr(), _s())
+    torch.cuda.synchronize()
+    assert status.item() == 0
+    hd, wd = h.double(), w[:K].double()
+    zz = hd @ wd.T + bias[:K].double()
+    ref, dref, p1, pT = _kd_reference(zz, y, qv, qi, alpha, beta, T)
+    eps = ((Dp + 15) // 16 * 2.0 ** -24) * (hd.abs() @ wd.abs().T).max(1, keepdim=True).values
+    assert abs(loss.item() - ref) <= 1e-5 * max(1.0, abs(ref))
+    d = dz[:, :K].double()
+    a = dref.abs()
+    ulp = torch.where(a > 0, torch.exp2(torch.floor(torch.log2(torch.where(a > 0, a, torch.ones_like(a)))) - 7),
+                      torch.zeros_like(a))
+    bound = ulp + 2 * eps * (alpha / B * p1 + beta * T / B * pT / T) + 2.0 ** -20 * (alpha + beta * T) / B
+    assert ((d - dref).abs() / bound).max().item() <= 1.0
+    assert (dz[:, K:] == 0).all()
+    assert torch.isfinite(row).all()
+    # the same numbers as the unfused path (logit GEMM + separate loss kernel)
+    z = torch.zeros(B, Kp, device="cuda")
+    lib.call("edl_linear_fwd", h.data_ptr(), Dp, w.data_ptr(), Dp, bias.data_ptr(), z.data_ptr(), Kp, B, Kp, Dp, 0, _s())
+    row2, loss2 = torch.empty(B, device="cuda"), torch.zeros(1, device="cuda")
+    ticket = torch.zeros(1, dtype=torch.int32, device="cuda")
+    dz2 = torch.full((B, Kp), 7.0, dtype=torch.bfloat16, device="cuda")
+    lib.call("edl_kd_loss_fwd_bwd", z.data_ptr(), Kp, y.data_ptr(), qv.data_ptr(), qi.data_ptr(), B, K,
+             k if beta > 0 else 0, alpha, beta, T, row2.data_ptr(), loss2.data_ptr(), ticket.data_ptr(),
+             dz2.data_ptr(), Kp, status.data_ptr(), _s())
+    torch.cuda.synchronize()
+    assert abs(loss.item() - loss2.item()) <= 1e-5 * max(1.0, abs(loss2.item()))
+    assert ((dz[:, :K].double() - dz2[:, :K].double()).abs() <= 2 * bound).all()
+
+
+def test_linear_kd_loss_bad_labels_set_status(lib):
+    B, D, K, k = 64, 64, 100, 4
+    h = _padded(torch.tanh(_rand(B, D, seed=3)), B, D)
+    w = _padded(_rand(K, D, seed=4), 112, D)
+    bias = torch.zeros(112, device="cuda")
+    y = torch.zeros(B, dtype=torch.int64, device="cuda")
+    y[5] = K                                   # out of range
+    qv = torch.full((B, k), 0.25, device="cuda")
+    qi = torch.arange(k, dtype=torch.int32, device="cuda").repeat(B, 1).contiguous()
+    qi[7, 1] = 5000                            # soft class out of range
+    row, loss = torch.empty(B, device="cuda"), torch.zeros(1, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    dz = torch.zeros(B, 112, dtype=torch.bfloat16, device="cuda")
+    lib.call("edl_linear_kd_loss_fwd_bwd", h.data_ptr(), D, w.data_ptr(), D, bias.data_ptr(), y.data_ptr(),
+             qv.data_ptr(), qi.data_ptr(), B, K, D, k, 0.5, 0.5, 2.0, row.data_ptr(), loss.data_ptr(),
+             dz.data_ptr(), 112, status.data_ptr(), _s())
+    torch.cuda.synchronize()
+    assert status.item() == -1
+    with pytest.raises(Exception):
+        lib.call("edl_linear_kd_loss_fwd_bwd", h.data_ptr(), D, w.data_ptr(), D, bias.data_ptr(), y.data_ptr(),
+                 qv.data_ptr(), qi.data_ptr(), B, 4000, D, k, 0.5, 0.5, 2.0, row.data_ptr(), loss.data_ptr(),
+                 dz.data_ptr(), 4000, status.data_ptr(), _s())     # > 2048 classes: the unfused path's job
+
+
 def test_sgd_and_cast(lib):
     n = 1003
     p = _rand(n, seed=13)
