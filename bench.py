@@ -835,7 +835,7 @@ class _StreamedRing:
         self.cast = "edl_cast_bf16_f64" if host_x.dtype == torch.float64 else "edl_cast_bf16"
         self.rows = [torch.arange(j * B, (j + 1) * B, device=dev) for j in range(self.R)]
         self.copy = torch.cuda.Stream(dev)
-        self.convert = torch.cuda.Stream(dev, priority=-1)
+        self.convert = torch.cuda.Stream(dev)
         self.landed: dict = {}          # iteration -> event (copy + conversion done)
         self.free = [None] * self.R     # slot -> event after the slot's last reader
         self.owner = [None] * self.R    # slot -> iteration it holds

@@ -684,8 +684,10 @@ static cudaError_t launch_cast_t(const T* src, long long ld_src, __nv_bfloat16* 
   const long long per_row = vec ? cols / 4 : cols;
   long long bx = (per_row + 255) / 256;
   int by = rows;
-  // ~16 blocks per SM in total
-  const long long target = 148LL * 16;
+  // two 256-thread blocks per SM, each thread looping: the bf16 conversion of a
+  // host batch runs beside the teacher's GEMMs and NCCL's kernels (e2e input
+  // path) and must not flood the SMs with thousands of CTAs
+  const long long target = 148LL * 2;
   if (by > target) by = static_cast<int>(target);
   if (bx * by > target) bx = (target + by - 1) / by;
   if (bx < 1) bx = 1;

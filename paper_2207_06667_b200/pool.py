@@ -135,11 +135,38 @@ class PeerSoftLabelRing:
         torch.cuda.synchronize(device)
         dist.barrier(group)
 
+    @classmethod
+    def local(cls, pl: Placement, batch_size: int, k: int, temperature: float, device, depth: int = 4,
+              view_rank: int = 0) -> "PeerSoftLabelRing":
+        """Every rank's ring slots and signal pad as separate buffers on ONE
+        device, with the same flag protocol: the teacher and student loops run
+        as two streams of one process (tests on a single GPU)."""
+        self = cls.__new__(cls)
+        self.pl, self.rank, self.depth = pl, view_rank, depth
+        self.B, self.k, self.T = batch_size, k, temperature
+        self.words = 2 * batch_size * k
+        self._bufs = [torch.zeros(depth * self.words, dtype=torch.int32, device=device) for _ in range(pl.world)]
+        self._pads = [torch.zeros(cls.CREDIT + pl.n_students, dtype=torch.int32, device=device)
+                      for _ in range(pl.world)]
+        self.buf = self._bufs[view_rank]
+        self.h = None
+        self.pads = [int(p.data_ptr()) for p in self._pads]
+        return self
+
+    def as_rank(self, rank: int) -> "PeerSoftLabelRing":
+        """The same local ring seen from another rank (local rings only)."""
+        other = object.__new__(type(self))
+        other.__dict__.update(self.__dict__)
+        other.rank, other.buf = rank, self._bufs[rank]
+        return other
+
     def slot(self, j: int) -> tuple[torch.Tensor, SoftLabels]:
         buf = self.buf[j * self.words:(j + 1) * self.words].view(2, self.B, self.k)
         return buf, SoftLabels(buf[0].view(torch.float32), buf[1], self.T)
 
     def peer_slot(self, rank: int, j: int) -> torch.Tensor:
+        if self.h is None:
+            return self._bufs[rank][j * self.words:(j + 1) * self.words].view(2, self.B, self.k)
         return self.h.get_buffer(rank, (2, self.B, self.k), torch.int32, j * self.words)
 
     def pad(self, rank: int, word: int) -> int:
@@ -175,6 +202,29 @@ class PeerSoftLabelRing:
             _lib.call("edl_stream_write_u32", self.pad(t, self.CREDIT + s), (it + 1) & 0xFFFFFFFF, self._s(stream))
 
 
+def ring_server(pl: Placement, rank: int, model: Model, data: DeviceDataset, batch_size: int, seed: int,
+                temperature: float, k: int, ring: PeerSoftLabelRing):
+    """A teacher rank's per-iteration step for the peer ring: serve(it) waits
+    (on the stream) for the slot's credit, gathers the batch, runs the fused
+    head into the staging slot and puts it into the student's ring. All
+    buffers are allocated here, up front: with stream-memory waits queued, a
+    later allocation that synchronises the device could deadlock a process
+    that also drives the consumer's stream."""
+    s = pl.student_of(rank)
+    sampler = DeviceShardSampler(data, pl.n_students, s, batch_size, seed)
+    batch = Batch(torch.empty(batch_size, data.samples.shape[1], dtype=torch.bfloat16, device=data.device),
+                  torch.empty(batch_size, dtype=torch.int64, device=data.device), data.dim)
+    ws = nnkit.Workspace(model, batch_size)
+
+    def serve(it: int) -> None:
+        ring.teacher_wait_credit(s, it)            # staging + student slot it % depth are free
+        gather_batch(data, sampler.rows_for(it), batch)
+        staged, out = ring.slot(it % ring.depth)
+        nnkit.teacher_soft_labels(model, batch.inputs, temperature, k, out=out, ws=ws)
+        ring.teacher_put(s, it, staged)
+    return serve
+
+
 def teacher_serve(pl: Placement, rank: int, model: Model, data: DeviceDataset, batch_size: int, seed: int,
                   temperature: float, k: int, start: int, end: int, depth: int = 4,
                   groups: dict | None = None, ring: PeerSoftLabelRing | None = None) -> int:
@@ -184,17 +234,10 @@ def teacher_serve(pl: Placement, rank: int, model: Model, data: DeviceDataset, b
     outstanding; the student's ring bounds how far teachers run ahead)."""
     s = pl.student_of(rank)
     if ring is not None:
-        sampler = DeviceShardSampler(data, pl.n_students, s, batch_size, seed)
-        batch = Batch(torch.empty(batch_size, data.samples.shape[1], dtype=torch.bfloat16, device=data.device),
-                      torch.empty(batch_size, dtype=torch.int64, device=data.device), data.dim)
-        ws = nnkit.Workspace(model, batch_size)
+        serve = ring_server(pl, rank, model, data, batch_size, seed, temperature, k, ring)
         served = 0
         for it in pl.iterations_of(rank, s, start, end):
-            ring.teacher_wait_credit(s, it)            # staging + student slot it % depth are free
-            gather_batch(data, sampler.rows_for(it), batch)
-            staged, out = ring.slot(it % ring.depth)
-            nnkit.teacher_soft_labels(model, batch.inputs, temperature, k, out=out, ws=ws)
-            ring.teacher_put(s, it, staged)
+            serve(it)
             served += 1
         return served
     group = groups.get((s, rank)) if groups else None
