@@ -18,18 +18,35 @@ import numpy as np
 import pytest
 import torch
 
-pytestmark = [pytest.mark.gpu, pytest.mark.timeout(900)]
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(600)]
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 DIMS, TSEED = (8, 32, 6), 11
 DATA = (1, 512, 8, 6, 1.0)
 
 
+LOGS: list = []
+
+
 def spawn_teacher(path, name, device=0, delay=0.0):
     env = dict(os.environ, PYTHONPATH=ROOT + os.pathsep + os.environ.get("PYTHONPATH", ""))
-    cmd = [sys.executable, "-m", "paper_2207_06667_b200.elastic", "--control", path, "--node-id", name,
+    cmd = [sys.executable, "-u", "-m", "paper_2207_06667_b200.elastic", "--control", path, "--node-id", name,
            "--device", str(device), "--teacher-dims", ",".join(map(str, DIMS)), "--teacher-seed", str(TSEED),
            "--data", ",".join(map(str, DATA)), "--simulated-delay", str(delay)]
-    return subprocess.Popen(cmd, cwd=ROOT, env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
+    log = f"{path}.{name}.log"
+    LOGS.append(log)
+    with open(log, "w") as fh:       # a file, not a pipe nobody drains
+        return subprocess.Popen(cmd, cwd=ROOT, env=env, stdout=fh, stderr=subprocess.STDOUT)
+
+
+def teacher_logs() -> str:
+    out = []
+    for log in LOGS:
+        try:
+            with open(log) as fh:
+                out.append(f"--- {os.path.basename(log)}\n{fh.read()[-3000:]}")
+        except OSError:
+            pass
+    return "\n".join(out)
 
 
 def wait_registered(cb, names, procs, timeout=300):
@@ -41,7 +58,7 @@ def wait_registered(cb, names, procs, timeout=300):
             return
         for p in procs:
             if p.poll() is not None:
-                raise RuntimeError(f"teacher process exited early: {p.stdout.read().decode()[-2000:]}")
+                raise RuntimeError(f"teacher process exited early:\n{teacher_logs()}")
         time.sleep(0.1)
     raise TimeoutError(f"teachers {names} did not register")
 
@@ -53,7 +70,8 @@ def student_cfg(teacher_count=2):
     spec = DataSpec(seed=DATA[0], n=DATA[1], dim=DATA[2], classes=DATA[3], spread=DATA[4])
     train = TrainConfig(eta=0.05, alpha=0.5, beta=0.5, temperature=2.0, batch_size=16, seed=2)
     return StudentConfig(mode="edl", data=spec, train=train, epochs=2, k=4, teacher_count=teacher_count,
-                         sched=SchedulerConfig(lt=2, ut=6, probe_interval=0.0, acquire_cooldown=0.0))
+                         sched=SchedulerConfig(lt=2, ut=6, probe_interval=0.0, acquire_cooldown=0.0),
+                         consume_timeout=120.0)
 
 
 def local_run():
@@ -82,6 +100,12 @@ def control(tmp_path):
             p.wait()
     cb.close()
     os.unlink(path)
+    for log in LOGS:
+        if log.startswith(path):
+            try:
+                os.unlink(log)
+            except OSError:
+                pass
 
 
 def remote_run(cb, path, procs, faults=(), device=0):
@@ -107,7 +131,13 @@ def remote_run(cb, path, procs, faults=(), device=0):
                 log.append(("add", name, it))
             elif kind == "await":
                 wait_registered(cb, [name], [named[name]])
-    res = node.run(on_iteration=hook)
+    try:
+        res = node.run(on_iteration=hook)
+    except Exception as exc:
+        ents = [(bytes(e["node_id"]).rstrip(b"\0").decode(), int(e["state"]), int(e["pid"]), int(e["epoch"]),
+                 int(e["head"]), int(e["tail"]), int(e["served"])) for e in cb.teachers if int(e["state"])]
+        raise RuntimeError(f"{exc!r}\nlog={log}\nteachers={ents}\nevents={node.events.entries[-12:]}\n"
+                           f"pool={pool.events[-8:]}\n{teacher_logs()}") from exc
     return res, node, pool, log
 
 
