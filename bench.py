@@ -268,8 +268,10 @@ def main():
                          "student GPUs over NVLink (EDL-Dist teacher pool)")
     ap.add_argument("--teachers", type=int, default=0, help="teacher GPUs for --placement split")
     ap.add_argument("--split-depth", type=int, default=8, help="split placement: soft-label ring slots per student")
-    ap.add_argument("--split-transport", default="peer", choices=["peer", "nccl"],
-                    help="split placement soft-label handoff: NVLink peer copy + stream flags, or NCCL send/recv")
+    ap.add_argument("--split-transport", default="peer", choices=["peer", "nccl", "elastic"],
+                    help="split placement soft-label handoff: NVLink peer copy + stream flags, NCCL send/recv, or "
+                         "the elastic pool (teacher ranks register in a shared-memory registry and write into the "
+                         "students' CUDA-IPC rings; students dispatch by JSQ, elastic.py)")
     ap.add_argument("--student-priority", default="high", choices=["normal", "high"],
                     help="CUDA stream priority of the student in the co-located EDL loop")
     ap.add_argument("--teacher-sm-reserve", type=int, default=-1,
@@ -541,6 +543,9 @@ def _split_main(args, cfg, world, rank, local, dev, ddata, teacher, student_h, t
     students = list(range(pl.n_students))
     sgroup = dist.new_group(students)
     is_student = pl.is_student(rank)
+    if args.split_transport == "elastic":
+        _elastic_split(args, cfg, world, rank, local, dev, ddata, teacher, student_h, tcfg, pl, sgroup)
+        return
     # soft labels cross NVLink by peer copy + stream-ordered flags (default),
     # or as NCCL send/recv (--split-transport nccl)
     ring = (PeerSoftLabelRing(pl, rank, B, cfg["topk"], cfg["T"], dev, depth=args.split_depth)
@@ -598,6 +603,104 @@ def _split_main(args, cfg, world, rank, local, dev, ddata, teacher, student_h, t
                        "mode": "edl (decoupled)", "global_batch": B * pl.n_students, "per_gpu_batch": B,
                        "topk": cfg["topk"], "parallelism": f"dp{pl.n_students}"},
             "gpu_launches": launches, "clocks": clk.summary(), "losses_finite": ok}), flush=True)
+
+
+def _elastic_split(args, cfg, world, rank, local, dev, ddata, teacher, student_h, tcfg, pl, sgroup):
+    """Split placement over the elastic pool (elastic.py): teacher ranks run
+    TeacherServer processes registered in a shared-memory registry; each
+    student acquires its teachers (longest-available-first), dispatches by
+    JSQ through DistilReader and trains on replies its host sees in the
+    READY words (no device waits; a dead teacher cannot hang a student)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2207_06667_b200 import _lib
+    from paper_2207_06667_b200.data import DeviceShardSampler
+    from paper_2207_06667_b200.elastic import ControlBlock, ElasticPool, TeacherServer
+    from paper_2207_06667_b200.nnkit import Model
+    from paper_2207_06667_b200.reader import DistilReader, EventLog, SchedulerConfig
+    from paper_2207_06667_b200.student import StudentStep
+    B, W, K = cfg["batch"], args.warmup, args.steps
+    cgroup = dist.new_group(backend="gloo")         # control-plane barriers, every rank
+    path = f"/dev/shm/edl-bench-{os.environ.get('MASTER_PORT', '0')}"
+    if rank == 0:
+        if os.path.exists(path):
+            os.unlink(path)
+        cb = ControlBlock(path, create=True, max_students=8, max_teachers=16, max_slots=64, ring_len=16)
+    dist.barrier(cgroup)
+    if rank != 0:
+        cb = ControlBlock(path)
+    is_student = pl.is_student(rank)
+    if not is_student:
+        reserve = args.teacher_sm_reserve if args.teacher_sm_reserve >= 0 else 0
+        server = TeacherServer(cb, f"t{rank}", teacher, ddata, cfg["T"], sm_reserve=reserve)
+        dist.barrier(cgroup)                       # registered
+        served = server.serve_forever()
+        print(f"[elastic] rank {rank} teacher served {served}", file=sys.stderr)
+        dist.barrier(cgroup)
+        cb.close()
+        return
+    dist.barrier(cgroup)
+    s = pl.student_index(rank)
+    sampler = DeviceShardSampler(ddata, pl.n_students, s, B, seed=0)
+    engine = StudentStep(Model.from_host(student_h, dev), tcfg, B, pl.n_students, process_group=sgroup,
+                         max_steps=W + K + 8, exchange=args.exchange)
+    pool = ElasticPool(cb, s, ttl=30.0, reply_timeout=60.0)
+    sched = SchedulerConfig(lt=2, ut=16, pipeline_depth=2, acquire_cooldown=1e9)
+    pool.open(pl.n_students, s, B, cfg["topk"], 0, cfg["T"], cfg["classes"], 48, dev)
+    n_mine = len(pl.teacher_ranks_of(s))
+
+    def run(start, count):
+        reader = DistilReader(f"student-{s}", pool, sched, sampler, start, start + count, 1, EventLog(),
+                              cfg["T"], cfg["topk"])
+        got = reader.acquire(n_mine)
+        dist.barrier(sgroup)
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = _lib.launch_count
+        ev0.record()
+        for it in range(start, start + count):
+            soft = reader.consume(it, timeout=120)
+            batch = sampler.batch_for(it, out=engine.batch)
+            engine.step(batch, soft)
+        engine.settle()
+        ev1.record()
+        torch.cuda.synchronize()
+        ok = reader.ledger()["ok"]
+        reader.close()
+        dist.barrier(sgroup)
+        return ev0.elapsed_time(ev1) / 1e3, _lib.launch_count - l0, ok, got
+
+    run(0, W)
+    with ClockSampler(local) as clk:
+        t, launches, ok, got = run(W, K)
+    tt = torch.tensor([t], dtype=torch.float64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX, group=sgroup)
+    tmax = float(tt.item())
+    losses = engine.loss_values()
+    if rank == 0:
+        value = pl.n_students * B * K / tmax
+        print(json.dumps({
+            "metric": "student_train_samples_per_s_teacher_in_loop", "value": round(value, 1), "unit": "samples/s",
+            "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": round(tmax / K * 1e3, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (make_blobs seed 0, random-init teacher seed 1 / student seed 0)",
+            "config": {"workload": cfg["workload"], "placement": f"split {pl.n_teachers}T+{pl.n_students}S elastic "
+                       "pool (teacher ranks register in a shared-memory registry; fused heads write soft labels "
+                       "into the students' CUDA-IPC rings over NVLink; JSQ dispatch, host-polled READY tags; NCCL "
+                       "student all-reduce)",
+                       "mode": "edl (decoupled)", "global_batch": B * pl.n_students, "per_gpu_batch": B,
+                       "topk": cfg["topk"], "parallelism": f"dp{pl.n_students}", "teachers_acquired": got},
+            "gpu_launches": launches, "clocks": clk.summary(), "ledger_ok": ok,
+            "losses_finite": bool(np.isfinite(losses).all())}), flush=True)
+    dist.barrier(sgroup)
+    if rank == 0:
+        cb.request_shutdown()
+    dist.barrier(cgroup)
+    pool.close()
+    cb.close()
+    if rank == 0:
+        os.unlink(path)
 
 
 def _cfg4_teacher_rate(dev, peak_sust, batch=256, iters=6, warmup=2):
