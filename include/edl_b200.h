@@ -221,6 +221,18 @@ int edl_teacher_head_softmax_topk(const void* H, long long ldh, const void* W, l
                                   const float* bias, int M, int N, int K, float T, int k,
                                   float* vals, int* idx, void* stream);
 
+/* edl_teacher_head_softmax_topk on CTA pairs (256-row tiles, cta_group::2):
+ * the class chunks (256 classes each, any number) are merged through
+ * `workspace` (edl_teacher_head_workspace_bytes(M, N, k) bytes, ZEROED once
+ * by the caller at allocation; the kernel leaves its tickets at zero), so no
+ * cluster has to span the class range. One workspace per stream. With
+ * workspace == NULL (or EDL_HEAD_CLUSTER=1) the single-CTA cluster head runs
+ * instead. Same outputs and tie rule. */
+long long edl_teacher_head_workspace_bytes(int M, int N, int k);
+int edl_teacher_head_softmax_topk_ws(const void* H, long long ldh, const void* W, long long ldw, const float* bias,
+                                     int M, int N, int K, float T, int k, float* vals, int* idx, void* workspace,
+                                     long long ws_bytes, void* stream);
+
 /* Dense tempered softmax, edl/nnkit.py:193-208 (fp32 logits -> fp32 probs). */
 int edl_tempered_softmax(const float* logits, long long ld, float* probs, long long ldp, int B,
                          int K, float T, void* stream);

@@ -72,6 +72,9 @@ _SIGNATURES = {
     "edl_colsum_group_workspace_floats": [c_int, c_void_p, c_void_p],
     "edl_teacher_head_softmax_topk": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_int, c_int,
                                       c_int, c_float, c_int, c_void_p, c_void_p, c_void_p],
+    "edl_teacher_head_workspace_bytes": [c_int, c_int, c_int],
+    "edl_teacher_head_softmax_topk_ws": [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_int, c_int, c_int, c_float,
+                                         c_int, c_void_p, c_void_p, c_void_p, c_ll, c_void_p],
     "edl_tempered_softmax": [c_void_p, c_ll, c_void_p, c_ll, c_int, c_int, c_float, c_void_p],
     "edl_kd_loss_fwd_bwd": [c_void_p, c_ll, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int,
                             c_float, c_float, c_float, c_void_p, c_void_p, c_void_p, c_void_p,
@@ -99,6 +102,7 @@ _SIGNATURES = {
     "edl_ipc_close": [c_void_p],
 }
 _RESTYPES = {"edl_last_error": c_char_p, "edl_colsum_workspace_floats": c_ll,
+             "edl_teacher_head_workspace_bytes": c_ll,
              "edl_bwd_weight_workspace_floats": c_ll,
              "edl_colsum_group_workspace_floats": c_ll}
 

@@ -869,6 +869,43 @@ int edl_teacher_head_softmax_topk(const void* H, long long ldh, const void* W, l
   return e == cudaSuccess ? 0 : cuda_fail(e, "teacher_head");
 }
 
+long long edl_teacher_head_workspace_bytes(int M, int N, int k) {
+  if (M < 1 || N < 1 || k < 1 || k > 32) return 0;
+  const int kmax = k <= 4 ? 4 : k <= 8 ? 8 : k <= 16 ? 16 : 32;
+  const long long part = static_cast<long long>((N + 255) / 256) * (2 + 2 * kmax) * M * 4;
+  const long long tickets = static_cast<long long>((M + 127) / 128 + 1) * 4;
+  return (part + 255) / 256 * 256 + tickets;
+}
+
+int edl_teacher_head_softmax_topk_ws(const void* H, long long ldh, const void* W, long long ldw, const float* bias,
+                                     int M, int N, int K, float T, int k, float* vals, int* idx, void* workspace,
+                                     long long ws_bytes, void* stream) {
+  static const bool cluster_head = [] {
+    const char* v = getenv("EDL_HEAD_CLUSTER");   // A/B switch: the single-CTA cluster head
+    return v && v[0] == '1';
+  }();
+  if (cluster_head || workspace == nullptr)
+    return edl_teacher_head_softmax_topk(H, ldh, W, ldw, bias, M, N, K, T, k, vals, idx, stream);
+  if (M < 1 || N < 1 || K < 1 || ldh < K || ldw < K)
+    return fail(EDL_ERR_SHAPE, "teacher_head: bad shape M=%d N=%d K=%d", M, N, K);
+  if (!(T > 0.f) || !std::isfinite(T)) return fail(EDL_ERR_PARAM, "teacher_head: temperature %g", T);
+  if (k < 1 || k > N || k > 32) return fail(EDL_ERR_PARAM, "teacher_head: k=%d (1..min(N,32))", k);
+  if (ws_bytes < edl_teacher_head_workspace_bytes(M, N, k))
+    return fail(EDL_ERR_SHAPE, "teacher_head: workspace of %lld bytes < %lld", ws_bytes,
+                edl_teacher_head_workspace_bytes(M, N, k));
+  const int kmax = k <= 4 ? 4 : k <= 8 ? 8 : k <= 16 ? 16 : 32;
+  CUtensorMap ta, tb;
+  int rc;
+  if ((rc = tensor_map(H, M, K, ldh, 64, 128, &ta))) return rc;
+  if ((rc = tensor_map(W, N, K, ldw, 64, 128, &tb))) return rc;
+  HeadArgs hp{bias, 1.0f / T, k, vals, idx};
+  const long long part = static_cast<long long>((N + 255) / 256) * (2 + 2 * kmax) * M * 4;
+  float* pw = static_cast<float*>(workspace);
+  unsigned* tickets = reinterpret_cast<unsigned*>(static_cast<char*>(workspace) + (part + 255) / 256 * 256);
+  cudaError_t e = launch_teacher_head_pair(kmax, ta, tb, M, N, K, hp, pw, tickets, as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "teacher_head_pair");
+}
+
 int edl_tempered_softmax(const float* logits, long long ld, float* probs, long long ldp, int B,
                          int K, float T, void* stream) {
   if (B < 1 || K < 1 || ld < K || ldp < K) return fail(EDL_ERR_SHAPE, "tempered_softmax: bad shape");

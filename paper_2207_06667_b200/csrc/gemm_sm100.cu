@@ -1468,6 +1468,126 @@ struct TopK {
   }
 };
 
+// The head epilogue's per-row pass over this CTA's 128 x BN logit tile in
+// TMEM (teacher_head_kernel / teacher_head_pair_kernel): bias + 1/T, online
+// max / sum of exp, and the top-KMAX list; the two warp halves (interleaved
+// 32-column chunks) merge through `hx`. On return the half-0 threads hold the
+// row's state; all 256 threads must call it.
+template <int BN, int KMAX>
+__device__ __forceinline__ void head_rows(uint32_t tmem_base, uint64_t* tfull, int n0, int N, const float* bias,
+                                          float inv_t, float* sbias, float* stage, float* hx, float& run_m,
+                                          float& run_l, TopK<KMAX>& top) {
+  constexpr int kState = 2 + 2 * KMAX;
+  (void)kState;
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int q = warp & 3;       // TMEM lane quarter == row block of this warp
+  const int half = warp >> 2;   // which interleaved 32-column chunks this warp takes
+  const int rl = 32 * q + lane; // local row
+  const int tid = threadIdx.x;
+  top.init();
+  run_m = -INFINITY;
+  run_l = 0.f;
+  // the class chunk's bias, staged by warps 2-7 while the MMAs run; warps 0/1
+  // join the barrier when their producer / MMA loops are done
+  if (warp >= 2) {
+    for (int j = tid - 64; j < BN; j += kThreads - 64)
+      sbias[j] = (n0 + j < N) ? __ldg(bias + n0 + j) : 0.f;
+  }
+  asm volatile("bar.sync 2, 256;" ::: "memory");
+  mbar_wait(&tfull[0], 0);
+  tc_fence_after();
+  bool first = true;
+  const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * q) << 16);
+  uint32_t r[32];
+  tmem_ld32_issue(taddr + 32 * half, r);
+  tmem_ld_wait(r);
+#pragma unroll 1
+  for (int c = 32 * half; c < BN; c += 64) {
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+    const bool more = c + 64 < BN;
+    if (more) tmem_ld32_issue(taddr + c + 64, r);   // next chunk's load overlaps this one's work
+    const int col0 = n0 + c;
+    if (col0 >= N) {
+      if (more) tmem_ld_wait(r);
+      continue;
+    }
+    float cmax = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int n = col0 + j;
+      const float s = (n < N) ? (v[j] + sbias[c + j]) * inv_t : -INFINITY;
+      v[j] = s;
+      cmax = fmaxf(cmax, s);
+    }
+    const float nm = fmaxf(run_m, cmax);
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc += __expf(v[j] - nm);
+    run_l = run_l * __expf(run_m - nm) + acc;
+    run_m = nm;
+    if (first) {
+      // the first chunk seeds the list: bitonic-sort all 32, keep the best KMAX
+      first = false;
+      int ix[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) ix[j] = (col0 + j < N) ? col0 + j : 0x7fffffff;
+      bitonic_sort<32>(v, ix);
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j) { top.v[j] = v[j]; top.i[j] = ix[j]; }
+      if (more) tmem_ld_wait(r);
+      continue;
+    }
+    // later chunks: only columns beating the current k-th entry (rare), each
+    // inserted by a branch-free shift; the values are staged in smem so the
+    // rolled loop can address them
+    uint32_t mask = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      mask |= (Key::better(v[j], col0 + j, top.v[KMAX - 1], top.i[KMAX - 1]) ? 1u : 0u) << j;
+    if (mask) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) stage[j * kThreads + tid] = v[j];
+      while (mask) {
+        const int j = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const float x = stage[j * kThreads + tid];
+        if (Key::better(x, col0 + j, top.v[KMAX - 1], top.i[KMAX - 1])) top.insert(x, col0 + j);
+      }
+    }
+    __syncwarp();   // the insertions above diverge; tcgen05.wait::ld is .sync.aligned
+    if (more) tmem_ld_wait(r);
+  }
+  tc_fence_before();
+  // halves -> one state per row (half 1 hands over through shared memory)
+  if (half == 1) {
+    hx[0 * kBM + rl] = run_m;
+    hx[1 * kBM + rl] = run_l;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+      hx[(2 + j) * kBM + rl] = top.v[j];
+      hx[(2 + KMAX + j) * kBM + rl] = __int_as_float(top.i[j]);
+    }
+  }
+  __syncthreads();
+  if (half == 0) {
+    const float om = hx[0 * kBM + rl], ol = hx[1 * kBM + rl];
+    const float nm = fmaxf(run_m, om);
+    run_l = (run_l > 0.f ? run_l * __expf(run_m - nm) : 0.f) + (ol > 0.f ? ol * __expf(om - nm) : 0.f);
+    run_m = nm;
+    float ov[KMAX];
+    int oi[KMAX];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+      ov[j] = hx[(2 + j) * kBM + rl];
+      oi[j] = __float_as_int(hx[(2 + KMAX + j) * kBM + rl]);
+    }
+    top.merge(ov, oi);
+  }
+}
+
 template <int BN, int KMAX>
 __global__ void __launch_bounds__(kThreads, 1)
     teacher_head_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -1537,110 +1657,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncwarp();
 
-  const int q = warp & 3;       // TMEM lane quarter == row block of this warp
-  const int half = warp >> 2;   // which interleaved 32-column chunks this warp takes
-  const int rl = 32 * q + lane; // local row
-  const int tid = threadIdx.x;
+  const int q = warp & 3;
+  const int half = warp >> 2;
+  const int rl = 32 * q + lane;
   TopK<KMAX> top;
-  top.init();
-  float run_m = -INFINITY, run_l = 0.f;
-  // the class chunk's bias, staged by warps 2-7 while the MMAs run; warps 0/1
-  // join the barrier when their producer / MMA loops are done
-  if (warp >= 2) {
-    for (int j = tid - 64; j < BN; j += kThreads - 64)
-      sbias[j] = (n0 + j < N) ? __ldg(hp.bias + n0 + j) : 0.f;
-  }
-  asm volatile("bar.sync 2, 256;" ::: "memory");
-  mbar_wait(&tfull[0], 0);
-  tc_fence_after();
-  bool first = true;
-  const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * q) << 16);
-  uint32_t r[32];
-  tmem_ld32_issue(taddr + 32 * half, r);
-  tmem_ld_wait(r);
-#pragma unroll 1
-  for (int c = 32 * half; c < BN; c += 64) {
-    float v[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-    const bool more = c + 64 < BN;
-    if (more) tmem_ld32_issue(taddr + c + 64, r);   // next chunk's load overlaps this one's work
-    const int col0 = n0 + c;
-    if (col0 >= N) {
-      if (more) tmem_ld_wait(r);
-      continue;
-    }
-    float cmax = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int n = col0 + j;
-      const float s = (n < N) ? (v[j] + sbias[c + j]) * hp.inv_t : -INFINITY;
-      v[j] = s;
-      cmax = fmaxf(cmax, s);
-    }
-    const float nm = fmaxf(run_m, cmax);
-    float acc = 0.f;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) acc += __expf(v[j] - nm);
-    run_l = run_l * __expf(run_m - nm) + acc;
-    run_m = nm;
-    if (first) {
-      // the first chunk seeds the list: bitonic-sort all 32, keep the best KMAX
-      first = false;
-      int ix[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) ix[j] = (col0 + j < N) ? col0 + j : 0x7fffffff;
-      bitonic_sort<32>(v, ix);
-#pragma unroll
-      for (int j = 0; j < KMAX; ++j) { top.v[j] = v[j]; top.i[j] = ix[j]; }
-      if (more) tmem_ld_wait(r);
-      continue;
-    }
-    // later chunks: only columns beating the current k-th entry (rare), each
-    // inserted by a branch-free shift; the values are staged in smem so the
-    // rolled loop can address them
-    uint32_t mask = 0;
-#pragma unroll
-    for (int j = 0; j < 32; ++j)
-      mask |= (Key::better(v[j], col0 + j, top.v[KMAX - 1], top.i[KMAX - 1]) ? 1u : 0u) << j;
-    if (mask) {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) stage[j * kThreads + tid] = v[j];
-      while (mask) {
-        const int j = __ffs(mask) - 1;
-        mask &= mask - 1;
-        const float x = stage[j * kThreads + tid];
-        if (Key::better(x, col0 + j, top.v[KMAX - 1], top.i[KMAX - 1])) top.insert(x, col0 + j);
-      }
-    }
-    __syncwarp();   // the insertions above diverge; tcgen05.wait::ld is .sync.aligned
-    if (more) tmem_ld_wait(r);
-  }
-  tc_fence_before();
-  // halves -> one state per row (half 1 hands over through shared memory)
-  if (half == 1) {
-    hx[0 * kBM + rl] = run_m;
-    hx[1 * kBM + rl] = run_l;
-#pragma unroll
-    for (int j = 0; j < KMAX; ++j) {
-      hx[(2 + j) * kBM + rl] = top.v[j];
-      hx[(2 + KMAX + j) * kBM + rl] = __int_as_float(top.i[j]);
-    }
-  }
-  __syncthreads();
+  float run_m, run_l;
+  head_rows<BN, KMAX>(tmem_base, tfull, n0, N, hp.bias, hp.inv_t, sbias, stage, hx, run_m, run_l, top);
+  (void)q;
   if (half == 0) {
-    const float om = hx[0 * kBM + rl], ol = hx[1 * kBM + rl];
-    const float nm = fmaxf(run_m, om);
-    run_l = (run_l > 0.f ? run_l * __expf(run_m - nm) : 0.f) + (ol > 0.f ? ol * __expf(om - nm) : 0.f);
-    run_m = nm;
-    float ov[KMAX];
-    int oi[KMAX];
-#pragma unroll
-    for (int j = 0; j < KMAX; ++j) {
-      ov[j] = hx[(2 + j) * kBM + rl];
-      oi[j] = __float_as_int(hx[(2 + KMAX + j) * kBM + rl]);
-    }
-    top.merge(ov, oi);
     st[0 * kBM + rl] = run_m;
     st[1 * kBM + rl] = run_l;
 #pragma unroll
@@ -1681,6 +1705,150 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem_base);
   }
+}
+
+// ---- teacher head on CTA pairs (cta_group::2, 256-row tiles) with the
+// class-chunk merge through global memory. The cluster head above needs the
+// whole class range of a row block in one cluster (4 CTAs, 128 x 256 each);
+// on pairs that is 8 CTAs, and clusters of 8 CTAs of ~200 KB do not fit in a
+// GPC often enough (finding 21). Here a cluster is one pair: the pair's two
+// CTAs stage their 128 A rows and half of the 256 B rows per k-block, rank 0
+// issues 256 x 256 x 16 MMAs over both (2/3 of the single-CTA kernel's
+// operand bytes per FLOP — the head's mainloop is operand-delivery bound),
+// and each CTA's epilogue (head_rows) reduces its 128 rows x 256 classes to
+// a per-row state (max, sum, top-KMAX) in global scratch. The last of the
+// ceil(K / 256) class chunks of a 128-row block (atomic ticket) merges the
+// states in chunk order — deterministic — and writes the (prob, class)
+// pairs.
+template <int KMAX>
+__global__ void __launch_bounds__(kThreads, 1)
+    teacher_head_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                             int M, int N, int K, HeadArgs hp, float* part, unsigned* tickets) {
+  constexpr int BN = 256;
+  using Cfg = PairCfg<BN>;
+  constexpr int S = 6;
+  constexpr uint32_t kTmemCols = tmem_cols_for(BN);
+  constexpr int kState = 2 + 2 * KMAX;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * Cfg::kABytes;
+  float* sbias = reinterpret_cast<float*>(sB + S * Cfg::kBBytes);   // [BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sbias + BN);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  int* merger = reinterpret_cast<int*>(tmem_slot + 2);
+  // epilogue scratch in the drained operand ring
+  float* stage = reinterpret_cast<float*>(smem);                     // [32][256]
+  float* hx = stage + 32 * kThreads;                                  // [kState][128]
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();
+  const int num_n = (N + BN - 1) / BN;
+  const int pair = static_cast<int>(blockIdx.x) / 2;
+  const int mt = pair / num_n, nt = pair % num_n;     // class chunks of a row block adjacent: A reuse in L2
+  const int m0 = mt * 2 * kBM + static_cast<int>(rank) * kBM;
+  const int nk = (K + kBK - 1) / kBK;
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(&tfull[0], 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_pair<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();
+  const uint32_t full0 = mapa(smem_u32(full), 0);
+
+  if (warp == 0 && lane == 0) {
+    const int nb0 = nt * BN + static_cast<int>(rank) * Cfg::kHalfN;
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % S;
+      mbar_wait(&empty[s], ((kb / S) & 1) ^ 1);
+      if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * Cfg::kStageBytes);
+      load_kblock_pair<BN, false, false>(&tmA, &tmB, sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes,
+                                         full0 + 8 * s, m0, nb0, kb * kBK);
+    }
+  } else if (warp == 1 && lane == 0 && rank == 0) {
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % S;
+      mbar_wait(&full[s], (kb / S) & 1);
+      tc_fence_after();
+      mma_kblock_pair<BN, false, false>(tmem_base, smem_u32(sA + s * Cfg::kABytes),
+                                        smem_u32(sB + s * Cfg::kBBytes), kb == 0);
+      umma_commit_pair(&empty[s]);
+    }
+    umma_commit_pair(&tfull[0]);
+  }
+  __syncwarp();
+
+  const int half = warp >> 2;
+  const int rl = 32 * (warp & 3) + lane;
+  const int row = m0 + rl;
+  TopK<KMAX> top;
+  float run_m, run_l;
+  head_rows<BN, KMAX>(tmem_base, tfull, nt * BN, N, hp.bias, hp.inv_t, sbias, stage, hx, run_m, run_l, top);
+  if (half == 0 && row < M) {
+    float* pp = part + static_cast<size_t>(nt) * kState * M + row;
+    pp[0] = run_m;
+    pp[static_cast<size_t>(M)] = run_l;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+      pp[static_cast<size_t>(2 + j) * M] = top.v[j];
+      pp[static_cast<size_t>(2 + KMAX + j) * M] = __int_as_float(top.i[j]);
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned* t = tickets + m0 / kBM;
+    const bool last = atomicAdd(t, 1u) == static_cast<unsigned>(num_n - 1);
+    if (last) atomicExch(t, 0u);        // every chunk has arrived: reset for the next launch
+    *merger = last ? 1 : 0;
+  }
+  __syncthreads();
+  if (*merger && half == 0 && row < M) {
+    __threadfence();
+#pragma unroll 1
+    for (int c = 0; c < num_n; ++c) {
+      const float* pp = part + static_cast<size_t>(c) * kState * M + row;
+      float rv[kState];
+#pragma unroll
+      for (int w = 0; w < kState; ++w) rv[w] = __ldcg(pp + static_cast<size_t>(w) * M);
+      float ov[KMAX];
+      int oi[KMAX];
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j) { ov[j] = rv[2 + j]; oi[j] = __float_as_int(rv[2 + KMAX + j]); }
+      if (c == 0) {
+        run_m = rv[0];
+        run_l = rv[1];
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) { top.v[j] = ov[j]; top.i[j] = oi[j]; }
+      } else {
+        const float nm = fmaxf(run_m, rv[0]);
+        run_l = run_l * __expf(run_m - nm) + rv[1] * __expf(rv[0] - nm);
+        run_m = nm;
+        top.merge(ov, oi);
+      }
+    }
+    const float inv_l = 1.0f / run_l;
+    float* ov = hp.vals + static_cast<size_t>(row) * hp.k;
+    int* oi = hp.idx + static_cast<size_t>(row) * hp.k;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j)
+      if (j < hp.k) { ov[j] = __expf(top.v[j] - run_m) * inv_l; oi[j] = top.i[j]; }
+  }
+  tc_fence_before();
+  cluster_sync();      // the peer's TMEM / smem stay live until rank 0's MMAs are done
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair<kTmemCols>(tmem_base);
 }
 
 // ---- student KD head: the logit GEMM with the distillation loss and its
@@ -2228,6 +2396,30 @@ cudaError_t launch_kd_head(int kmax, const CUtensorMap& ta, const CUtensorMap& t
     case 8: return launch_kd_head_t<8>(ta, tb, ty, M, N, Nw, K, kp, stream);
     case 16: return launch_kd_head_t<16>(ta, tb, ty, M, N, Nw, K, kp, stream);
     case 32: return launch_kd_head_t<32>(ta, tb, ty, M, N, Nw, K, kp, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int KMAX>
+static cudaError_t launch_head_pair_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
+                                     const HeadArgs& hp, float* part, unsigned* tickets, cudaStream_t stream) {
+  constexpr int BN = 256, S = 6;
+  constexpr int smem = S * PairCfg<BN>::kStageBytes + BN * 4 + 1024 + 256;
+  static_assert(smem <= 227 * 1024, "head pair smem");
+  auto kern = teacher_head_pair_kernel<KMAX>;
+  cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), smem);
+  if (e != cudaSuccess) return e;
+  const int pairs = ((M + 2 * kBM - 1) / (2 * kBM)) * ((N + BN - 1) / BN);
+  return launch_pdl(kern, dim3(2 * pairs), dim3(kThreads), smem, stream, 2, ta, tb, M, N, K, hp, part, tickets);
+}
+
+cudaError_t launch_teacher_head_pair(int kmax, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
+                                     const HeadArgs& hp, float* part, unsigned* tickets, cudaStream_t stream) {
+  switch (kmax) {
+    case 4: return launch_head_pair_t<4>(ta, tb, M, N, K, hp, part, tickets, stream);
+    case 8: return launch_head_pair_t<8>(ta, tb, M, N, K, hp, part, tickets, stream);
+    case 16: return launch_head_pair_t<16>(ta, tb, M, N, K, hp, part, tickets, stream);
+    case 32: return launch_head_pair_t<32>(ta, tb, M, N, K, hp, part, tickets, stream);
     default: return cudaErrorInvalidValue;
   }
 }

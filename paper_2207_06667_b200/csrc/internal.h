@@ -148,6 +148,10 @@ cudaError_t launch_nvls_allreduce_sgd(float* mc_grad, float* mc_param, void* mc_
 cudaError_t launch_gemm_pair(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
                              const CUtensorMap& ty, int M, int N, int K, const EpiArgs& ep, int num_sms,
                              cudaStream_t stream, const CUtensorMap* tr = nullptr);
+// teacher head on CTA pairs, class chunks merged through `part`
+// ([ceil(N/256)][2 + 2 kmax][M] floats) and `tickets` (ceil(M/128), zeroed once)
+cudaError_t launch_teacher_head_pair(int kmax, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
+                                     const HeadArgs& hp, float* part, unsigned* tickets, cudaStream_t stream);
 cudaError_t launch_kd_head(int kmax, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, int M,
                            int N, int Nw, int K, const KdArgs& kp, cudaStream_t stream);
 cudaError_t launch_loss_mean(const float* row_loss, int B, float* loss_out, int* status, cudaStream_t stream);

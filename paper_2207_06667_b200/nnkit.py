@@ -293,6 +293,16 @@ class Workspace:
         self.colsum = torch.empty(max(ws, 1), dtype=torch.float32, device=dev)
         self.grads = Gradients(torch.zeros(L.size, dtype=torch.float32, device=dev), L)
         self.probs = None
+        self._head_ws: dict = {}
+
+    def head_workspace(self, N: int, k: int) -> torch.Tensor:
+        """Zeroed scratch of the pair head (class-chunk states + tickets)."""
+        key = (N, k)
+        t = self._head_ws.get(key)
+        if t is None:
+            nbytes = int(_lib.load().edl_teacher_head_workspace_bytes(self.batch_size, N, k))
+            t = self._head_ws[key] = torch.zeros(max(nbytes, 1), dtype=torch.uint8, device=self.grads.flat.device)
+        return t
 
 
 _WS: dict = {}
@@ -400,9 +410,10 @@ def teacher_soft_labels(model: Model, inputs, temperature: float, k: int, out: S
                          torch.empty(B, k, dtype=torch.int32, device=x.device), float(temperature))
     out.num_classes = K
     l = L.layers - 1
-    _lib.call("edl_teacher_head_softmax_topk", h.data_ptr(), h.stride(0), model.w_bf16(l).data_ptr(),
+    hws = ws.head_workspace(K, int(k))
+    _lib.call("edl_teacher_head_softmax_topk_ws", h.data_ptr(), h.stride(0), model.w_bf16(l).data_ptr(),
               L.dims_p[l], model.b(l).data_ptr(), B, K, L.dims_p[l], float(temperature), int(k),
-              out.probs.data_ptr(), out.classes.data_ptr(), s)
+              out.probs.data_ptr(), out.classes.data_ptr(), hws.data_ptr(), hws.numel(), s)
     return out
 
 

@@ -102,18 +102,34 @@ def test_linear_bwd_weight(lib, M, N, K):
 
 @pytest.mark.parametrize("B,H,K,k", [(32, 256, 10, 10), (32, 256, 10, 4), (200, 512, 100, 16),
                                      (256, 1024, 1000, 16), (130, 2048, 1000, 32),
-                                     (64, 256, 2000, 8)])
-def test_teacher_head_softmax_topk(lib, B, H, K, k):
+                                     (64, 256, 2000, 8), (4096, 512, 1000, 16), (300, 256, 3000, 16)])
+@pytest.mark.parametrize("pair", [False, True])
+def test_teacher_head_softmax_topk(lib, B, H, K, k, pair):
+    """The fused head (edl/nnkit.py:193-208 + top-k) against fp64 on the same
+    bf16 operands: the single-CTA cluster kernel and the CTA-pair kernel with
+    the class-chunk merge through global memory (any class count)."""
     T = 2.0
     Hp, Kp = (H + 15) // 16 * 16, (K + 15) // 16 * 16
+    if not pair and (Kp + 255) // 256 > 8:
+        pytest.skip("the cluster head spans at most 8 x 256 classes")
     h = _padded(torch.tanh(_rand(B, H, seed=9)), B, Hp)
     w = _padded(_rand(K, H, scale=3 * H ** -0.5, seed=10), Kp, Hp)
     b = torch.zeros(Kp, device="cuda")
     b[:K] = _rand(K, seed=11) * 0.1
     vals = torch.empty(B, k, device="cuda")
     idx = torch.empty(B, k, dtype=torch.int32, device="cuda")
-    lib.call("edl_teacher_head_softmax_topk", h.data_ptr(), Hp, w.data_ptr(), Hp, b.data_ptr(), B, K,
-             Hp, T, k, vals.data_ptr(), idx.data_ptr(), _s())
+    if pair:
+        nb = int(lib.load().edl_teacher_head_workspace_bytes(B, K, k))
+        ws = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+        for _ in range(2):      # the tickets must come back to zero for the next launch
+            lib.call("edl_teacher_head_softmax_topk_ws", h.data_ptr(), Hp, w.data_ptr(), Hp, b.data_ptr(), B, K,
+                     Hp, T, k, vals.data_ptr(), idx.data_ptr(), ws.data_ptr(), nb, _s())
+        torch.cuda.synchronize()
+        tick = ws[-((B + 127) // 128 + 1) * 4:].view(torch.int32)
+        assert (tick == 0).all()
+    else:
+        lib.call("edl_teacher_head_softmax_topk", h.data_ptr(), Hp, w.data_ptr(), Hp, b.data_ptr(), B, K,
+                 Hp, T, k, vals.data_ptr(), idx.data_ptr(), _s())
     torch.cuda.synchronize()
     z = (h.double() @ w.double().T + b.double())[:, :K]
     p = torch.softmax(z / T, dim=1)
@@ -126,6 +142,34 @@ def test_teacher_head_softmax_topk(lib, B, H, K, k):
     assert torch.equal(idx[safe].long(), order[safe])
     pv = torch.gather(p, 1, idx.long())
     assert (vals.double() - pv).abs().max().item() < 1e-5
+
+
+def test_teacher_head_pair_equals_cluster_head(lib):
+    """cfg3's head shape: the pair kernel and the cluster kernel agree (same
+    per-chunk states, same chunk-order merge)."""
+    B, H, K, k, T = 4096, 8192, 1000, 16, 2.0
+    Kp = 1008
+    h = _padded(torch.tanh(_rand(B, H, seed=19)), B, H)
+    w = _padded(_rand(K, H, scale=3 * H ** -0.5, seed=20), Kp, H)
+    b = torch.zeros(Kp, device="cuda")
+    outs = []
+    for pair in (False, True):
+        vals = torch.empty(B, k, device="cuda")
+        idx = torch.empty(B, k, dtype=torch.int32, device="cuda")
+        if pair:
+            nb = int(lib.load().edl_teacher_head_workspace_bytes(B, K, k))
+            ws = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+            lib.call("edl_teacher_head_softmax_topk_ws", h.data_ptr(), H, w.data_ptr(), H, b.data_ptr(), B, K, H, T, k,
+                     vals.data_ptr(), idx.data_ptr(), ws.data_ptr(), nb, _s())
+        else:
+            lib.call("edl_teacher_head_softmax_topk", h.data_ptr(), H, w.data_ptr(), H, b.data_ptr(), B, K, H, T, k,
+                     vals.data_ptr(), idx.data_ptr(), _s())
+        torch.cuda.synchronize()
+        outs.append((vals, idx))
+    (v0, i0), (v1, i1) = outs
+    same = (i0 == i1).all(1)
+    assert same.float().mean() > 0.99
+    assert (v0 - v1).abs().max().item() <= 1e-6 * v0.abs().max().item()
 
 
 @pytest.mark.parametrize("B,K,k,alpha,beta,T", [(32, 10, 10, 0.5, 0.5, 2.0), (32, 10, 4, 1.0, 0.0, 2.0),
