@@ -41,6 +41,8 @@ CONFIGS = {
     "cfg3": dict(workload="cfg3 wide-MLP distillation (teacher 100.5M -> student 9.4M, 1000 classes)",
                  dim=3072, classes=1000, teacher=(3072, 8192, 8192, 1000), student=(3072, 2048, 1024, 1000),
                  topk=16, T=2.0, alpha=0.5, beta=0.5, eta=0.05, batch=4096, n_data=32768, ref_batch=4096),
+    "cfg4": dict(workload="cfg4 ResNet-50-style teacher pool -> ResNet-18-style students (224x224, 1000 classes)",
+                 image=224, classes=1000, topk=16, T=2.0, alpha=0.5, beta=0.5, eta=1e-3, batch=256),
     "cfg2": dict(workload="cfg2 small-MLP distillation (teacher [16,256,256,10] -> student [16,64,10])",
                  dim=16, classes=10, teacher=(16, 256, 256, 10), student=(16, 64, 10),
                  topk=10, T=2.0, alpha=0.5, beta=0.5, eta=0.05, batch=4096, n_data=65536, ref_batch=4096),
@@ -272,6 +274,10 @@ def main():
                     help="split placement soft-label handoff: NVLink peer copy + stream flags, NCCL send/recv, or "
                          "the elastic pool (teacher ranks register in a shared-memory registry and write into the "
                          "students' CUDA-IPC rings; students dispatch by JSQ, elastic.py)")
+    ap.add_argument("--split-depth-per-teacher", type=int, default=4,
+                    help="elastic split: JSQ pipeline depth (batches in flight per teacher)")
+    ap.add_argument("--no-student-graph", action="store_true",
+                    help="split placement: launch the student's step eagerly instead of replaying a CUDA graph")
     ap.add_argument("--student-priority", default="high", choices=["normal", "high"],
                     help="CUDA stream priority of the student in the co-located EDL loop")
     ap.add_argument("--teacher-sm-reserve", type=int, default=-1,
@@ -283,6 +289,9 @@ def main():
         cfg["batch"] = args.batch
     if args.impl == "reference":
         run_reference_arm(args, cfg)
+        return
+    if args.config == "cfg4":
+        _cfg4_pool_main(args, cfg)
         return
 
     import torch
@@ -605,12 +614,16 @@ def _split_main(args, cfg, world, rank, local, dev, ddata, teacher, student_h, t
             "gpu_launches": launches, "clocks": clk.summary(), "losses_finite": ok}), flush=True)
 
 
-def _elastic_split(args, cfg, world, rank, local, dev, ddata, teacher, student_h, tcfg, pl, sgroup):
+def _elastic_split(args, cfg, world, rank, local, dev, ddata, teacher, student_h, tcfg, pl, sgroup,
+                   cfg4: bool = False):
     """Split placement over the elastic pool (elastic.py): teacher ranks run
     TeacherServer processes registered in a shared-memory registry; each
     student acquires its teachers (longest-available-first), dispatches by
     JSQ through DistilReader and trains on replies its host sees in the
-    READY words (no device waits; a dead teacher cannot hang a student)."""
+    READY words (no device waits; a dead teacher cannot hang a student).
+    cfg4: ResNet-50-style teachers and ResNet-18-style students over an
+    HBM-resident synthetic image set (rows = NHWC images); the students
+    all-reduce their gradients over NCCL among themselves."""
     import torch
     import torch.distributed as dist
 
@@ -643,10 +656,34 @@ def _elastic_split(args, cfg, world, rank, local, dev, ddata, teacher, student_h
     dist.barrier(cgroup)
     s = pl.student_index(rank)
     sampler = DeviceShardSampler(ddata, pl.n_students, s, B, seed=0)
-    engine = StudentStep(Model.from_host(student_h, dev), tcfg, B, pl.n_students, process_group=sgroup,
-                         max_steps=W + K + 8, exchange=args.exchange)
-    pool = ElasticPool(cb, s, ttl=30.0, reply_timeout=60.0)
-    sched = SchedulerConfig(lt=2, ut=16, pipeline_depth=2, acquire_cooldown=1e9)
+    if cfg4:
+        from paper_2207_06667_b200.resnet import ResNetStudent, StudentResNetConfig, init_student_resnet
+        st = ResNetStudent(init_student_resnet(StudentResNetConfig(), 0), dev, B)
+        losses_dev = []
+
+        def step(batch, soft):
+            losses_dev.append(st.train_step(ddata.nhwc(batch.inputs), batch.hard_labels, soft, cfg["alpha"],
+                                            cfg["beta"], cfg["T"], cfg["eta"], process_group=sgroup,
+                                            world_size=pl.n_students).clone())
+        batch_buf = None
+    else:
+        # the split student's step is ~0.2 ms on the GPU and about as long to
+        # launch eagerly from Python: replay it as one CUDA graph
+        engine = StudentStep(Model.from_host(student_h, dev), tcfg, B, pl.n_students, process_group=sgroup,
+                             max_steps=W + K + 8, exchange=args.exchange, graph=not args.no_student_graph)
+
+        def step(batch, soft):
+            engine.step(batch, soft)
+        batch_buf = engine.batch
+    pool = ElasticPool(cb, s, ttl=30.0, reply_timeout=120.0)
+    # 4 batches in flight per teacher: a reply's round trip through two
+    # hosts (READY seen -> next request -> teacher enqueue) must stay hidden
+    # behind the batches already queued on the teacher's GPU
+    # Alg. 1's hysteresis (stop sending above ut, resume below lt): with
+    # teachers faster than the student the buffer cycles between the two, and
+    # a low lt lets it drain below one teacher latency before the pipeline
+    # refills (the student stalls every cycle); resume at half of ut instead
+    sched = SchedulerConfig(lt=12, ut=24, pipeline_depth=args.split_depth_per_teacher, acquire_cooldown=1e9)
     pool.open(pl.n_students, s, B, cfg["topk"], 0, cfg["T"], cfg["classes"], 48, dev)
     n_mine = len(pl.teacher_ranks_of(s))
 
@@ -659,32 +696,38 @@ def _elastic_split(args, cfg, world, rank, local, dev, ddata, teacher, student_h
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         l0 = _lib.launch_count
         ev0.record()
+        h0 = time.perf_counter()
+        wait = 0.0
         for it in range(start, start + count):
-            soft = reader.consume(it, timeout=120)
-            batch = sampler.batch_for(it, out=engine.batch)
-            engine.step(batch, soft)
-        engine.settle()
+            w0 = time.perf_counter()
+            soft = reader.consume(it, timeout=300)
+            wait += time.perf_counter() - w0
+            batch = sampler.batch_for(it, out=batch_buf)
+            step(batch, soft)
+        host = (time.perf_counter() - h0) / count
+        if not cfg4:
+            engine.settle()
         ev1.record()
         torch.cuda.synchronize()
         ok = reader.ledger()["ok"]
         reader.close()
         dist.barrier(sgroup)
-        return ev0.elapsed_time(ev1) / 1e3, _lib.launch_count - l0, ok, got
+        return ev0.elapsed_time(ev1) / 1e3, _lib.launch_count - l0, ok, got, (host, wait / count)
 
     run(0, W)
     with ClockSampler(local) as clk:
-        t, launches, ok, got = run(W, K)
+        t, launches, ok, got, host = run(W, K)
     tt = torch.tensor([t], dtype=torch.float64, device=dev)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX, group=sgroup)
     tmax = float(tt.item())
-    losses = engine.loss_values()
+    losses = ([float(x.item()) for x in losses_dev] if cfg4 else engine.loss_values())
     if rank == 0:
         value = pl.n_students * B * K / tmax
-        print(json.dumps({
+        line = {
             "metric": "student_train_samples_per_s_teacher_in_loop", "value": round(value, 1), "unit": "samples/s",
             "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": round(tmax / K * 1e3, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (make_blobs seed 0, random-init teacher seed 1 / student seed 0)",
+            "data": "synthetic (make_blobs seed 0 / random NHWC images, random-init teacher seed 1 / student seed 0)",
             "config": {"workload": cfg["workload"], "placement": f"split {pl.n_teachers}T+{pl.n_students}S elastic "
                        "pool (teacher ranks register in a shared-memory registry; fused heads write soft labels "
                        "into the students' CUDA-IPC rings over NVLink; JSQ dispatch, host-polled READY tags; NCCL "
@@ -692,7 +735,14 @@ def _elastic_split(args, cfg, world, rank, local, dev, ddata, teacher, student_h
                        "mode": "edl (decoupled)", "global_batch": B * pl.n_students, "per_gpu_batch": B,
                        "topk": cfg["topk"], "parallelism": f"dp{pl.n_students}", "teachers_acquired": got},
             "gpu_launches": launches, "clocks": clk.summary(), "ledger_ok": ok,
-            "losses_finite": bool(np.isfinite(losses).all())}), flush=True)
+            "losses_finite": bool(np.isfinite(losses).all()),
+            "student_host_ms_per_step": round(host[0] * 1e3, 4), "student_consume_wait_ms_per_step":
+                round(host[1] * 1e3, 4)}
+        if cfg4:
+            st_flop = st.flops_per_sample()
+            line["algorithmic_gflop_per_sample"] = {"student_train": round(st_flop / 1e9, 3),
+                                                    "teacher_fwd": round(teacher_flop_cfg4() / 1e9, 3)}
+        print(json.dumps(line), flush=True)
     dist.barrier(sgroup)
     if rank == 0:
         cb.request_shutdown()
@@ -701,6 +751,46 @@ def _elastic_split(args, cfg, world, rank, local, dev, ddata, teacher, student_h
     cb.close()
     if rank == 0:
         os.unlink(path)
+
+
+def teacher_flop_cfg4() -> float:
+    """ResNet-50-style teacher forward GEMM FLOPs per 224^2 image (padded
+    channels included; resnet.ResNetTeacher.flops_per_sample without
+    building the model)."""
+    return 8.199e9
+
+
+def _cfg4_pool_main(args, cfg):
+    """cfg4 (BASELINE configs[3]): the ResNet teacher pool feeding ResNet-18
+    students over the elastic pool, N >= 2 GPUs, half teachers / half
+    students unless --teachers says otherwise."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2207_06667_b200 import _lib
+    from paper_2207_06667_b200.data import DeviceImageDataset
+    from paper_2207_06667_b200.pool import Placement
+    from paper_2207_06667_b200.resnet import ResNetConfig, ResNetTeacher, init_resnet
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world < 2:
+        raise SystemExit("--config cfg4 runs the teacher pool: needs >= 2 GPUs (N=1 cfg4 numbers are the "
+                         "cfg4_* fields of the default cfg3 line)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    _lib.load()
+    nt = args.teachers or max(1, world // 2)
+    pl = Placement(world, min(nt, world - 1))
+    sgroup = dist.new_group(list(range(pl.n_students)))
+    B = cfg["batch"]
+    data = DeviceImageDataset(0, B * pl.n_students * 4, cfg["image"], cfg["classes"], device=dev)
+    teacher = None
+    if not pl.is_student(rank):
+        teacher = ResNetTeacher(init_resnet(ResNetConfig(), 1), dev, B)
+    _elastic_split(args, cfg, world, rank, local, dev, data, teacher, None, None, pl, sgroup, cfg4=True)
+    dist.destroy_process_group()
 
 
 def _cfg4_teacher_rate(dev, peak_sust, batch=256, iters=6, warmup=2):

@@ -36,6 +36,35 @@ class DeviceDataset:
         self.labels = torch.from_numpy(np.ascontiguousarray(data.labels, dtype=np.int64)).to(self.device)
 
 
+class DeviceImageDataset:
+    """cfg4's synthetic image set, HBM-resident: n NHWC bf16 images
+    [image][image][pad(channels)] stored as rows of one [n][image*image*pad(c)]
+    matrix (so DeviceShardSampler / gather_rows select batches by row index,
+    as for the MLP datasets) + int64 labels. Deterministic in (seed, n,
+    image, classes): every teacher and student process builds the same set."""
+
+    def __init__(self, seed: int, n: int, image: int = 224, classes: int = 1000, channels: int = 3,
+                 device=None, chunk: int = 64):
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.image, self.channels, self.classes = image, channels, classes
+        self.cp = pad(channels)
+        self.size = n
+        self.dim = image * image * self.cp
+        self.id = f"images-{seed}-{n}-{image}-{classes}"
+        self.samples = torch.zeros(n, self.dim, dtype=torch.bfloat16, device=self.device)
+        rng = np.random.default_rng(seed)
+        view = self.samples.view(n, image, image, self.cp)
+        for lo in range(0, n, chunk):
+            hi = min(lo + chunk, n)
+            imgs = rng.standard_normal(size=(hi - lo, image, image, channels), dtype=np.float32)
+            view[lo:hi, :, :, :channels] = torch.from_numpy(imgs).to(self.device).to(torch.bfloat16)
+        self.labels = torch.from_numpy(rng.integers(0, classes, size=n).astype(np.int64)).to(self.device)
+
+    def nhwc(self, rows_view: torch.Tensor) -> torch.Tensor:
+        """A gathered [B][dim] batch as NHWC [B][image][image][pad(c)]."""
+        return rows_view.view(rows_view.shape[0], self.image, self.image, self.cp)
+
+
 class DeviceShardSampler:
     """batch_for(iteration) -> Batch gathered on the device from the shard."""
 

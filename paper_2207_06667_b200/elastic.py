@@ -298,23 +298,31 @@ class RemoteTeacher:
         self._sent: dict[int, float] = {}        # tag -> dispatch time (watchdog)
         self.failure: str | None = None
         self.batches_served = 0
+        self._next_check = 0.0                    # the process / heartbeat checks run every check_period
 
     def _entry(self):
         return self.cb.teachers[self.j:self.j + 1]
 
     @property
     def alive(self) -> bool:
+        """The watchdog. The reader asks on every pump (several times a step),
+        so the syscall-backed checks (pid, heartbeat, reply deadlines) run at
+        most every pool.check_period seconds; revocation is a shared-memory
+        read and is checked every time."""
         if self.failure is not None:
             return False
         e = self._entry()
+        now = time.monotonic()
         if int(e["epoch"][0]) != self.epoch or int(e["state"][0]) not in (AVAILABLE, ASSIGNED):
             self.failure = "revoked"
+        elif now < self._next_check:
+            return True
         elif not pid_alive(self.pid):
             self.failure = "process exited"
         elif time.monotonic_ns() - int(e["heartbeat_ns"][0]) > self.pool.ttl * 1e9:
             self.failure = "heartbeat expired"
         else:
-            now = time.monotonic()
+            self._next_check = now + self.pool.check_period
             ready = self.pool.ready
             for tag, (t0, slot) in list(self._sent.items()):
                 if int(ready[slot]) == tag:
@@ -356,9 +364,10 @@ class ElasticPool:
     (acquire_teachers / release_teacher / report_failure / status / kill)
     plus `slot_source` for the DistilReader."""
 
-    def __init__(self, cb: ControlBlock, student_index: int, ttl: float = 5.0, reply_timeout: float = 30.0):
+    def __init__(self, cb: ControlBlock, student_index: int, ttl: float = 5.0, reply_timeout: float = 30.0,
+                 check_period: float = 0.005):
         self.cb, self.s = cb, student_index
-        self.ttl, self.reply_timeout = ttl, reply_timeout
+        self.ttl, self.reply_timeout, self.check_period = ttl, reply_timeout, check_period
         self.ring: SlotRing | None = None
         self.ready = cb.students["ready"][student_index]
         self._tag = (os.getpid() & 0xFFFF) << 16
@@ -509,6 +518,9 @@ class TeacherServer:
         self._rings: dict = {}        # student -> (generation, base ptr, sampler, ...)
         self._ws = None
         self._batch = None
+        # an MLP teacher (nnkit.Model) or a cfg4 ResNet teacher (resnet.ResNetTeacher
+        # over a data.DeviceImageDataset: rows are NHWC images)
+        self._resnet = hasattr(model, "soft_labels")
         self.dev_base = cb.device_base()
         self.j, self.epoch = cb.register_teacher(node_id, os.getpid())
         self.served = 0
@@ -533,7 +545,11 @@ class TeacherServer:
         if self._batch is None or self._batch.size != B:
             self._batch = Batch(torch.empty(B, self.data.samples.shape[1], dtype=torch.bfloat16, device=self.device),
                                 torch.empty(B, dtype=torch.int64, device=self.device), self.data.dim)
-            self._ws = self._nk.Workspace(self.model, B)
+            if self._resnet:
+                if self.model.B != B:
+                    raise RuntimeError(f"ResNet teacher built for batch {self.model.B}, student asks {B}")
+            else:
+                self._ws = self._nk.Workspace(self.model, B)
         entry = (gen, int(base.value), sampler, B, k, float(st["temperature"]),
                  int(base.value) + int(st["ring_offset"]), int(st["slot_bytes"]))
         self._rings[s] = entry
@@ -549,9 +565,12 @@ class TeacherServer:
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
             rows = sampler.rows_for(it)
             batch = gather_batch(self.data, rows, self._batch, self.stream)
-            self._nk.teacher_soft_labels(self.model, batch.inputs, self.T or T, k,
-                                         out=SoftLabels(probs, classes, self.T or T), stream=self.stream,
-                                         ws=self._ws)
+            out = SoftLabels(probs, classes, self.T or T)
+            if self._resnet:
+                self.model.soft_labels(self.data.nhwc(batch.inputs), self.T or T, k, out=out, stream=self.stream)
+            else:
+                self._nk.teacher_soft_labels(self.model, batch.inputs, self.T or T, k, out=out, stream=self.stream,
+                                             ws=self._ws)
             if self.delay_ns:
                 _lib.call("edl_stream_delay_ns", self.delay_ns, self.stream.cuda_stream)
             _lib.call("edl_stream_write_u32", self.dev_base + self.cb.ready_offset(s, slot), tag,
@@ -598,7 +617,9 @@ def main(argv=None) -> int:
     ap.add_argument("--teacher-file", help="EDLD model file (edl/nnkit.py:480-487)")
     ap.add_argument("--teacher-dims", help="init_model dims, e.g. 3072,8192,8192,1000")
     ap.add_argument("--teacher-seed", type=int, default=1)
-    ap.add_argument("--data", required=True, help="make_blobs seed,n,dim,classes[,spread]")
+    ap.add_argument("--data", help="make_blobs seed,n,dim,classes[,spread]")
+    ap.add_argument("--images", help="cfg4: DeviceImageDataset seed,n,image,classes (with --resnet)")
+    ap.add_argument("--resnet", help="cfg4: ResNet-50-style teacher seed,batch[,width]")
     ap.add_argument("--temperature", type=float, default=None)
     ap.add_argument("--simulated-delay", type=float, default=0.0)
     ap.add_argument("--sm-reserve", type=int, default=0)
@@ -606,14 +627,24 @@ def main(argv=None) -> int:
     from . import formats, nnkit
     from .data import DeviceDataset
     torch.cuda.set_device(a.device)
-    if a.teacher_file:
-        model, _ = nnkit.load_model(a.teacher_file)
+    if a.resnet:
+        from .data import DeviceImageDataset
+        from .resnet import ResNetConfig, ResNetTeacher, init_resnet
+        iseed, n, image, classes = _parse_ints(a.images)
+        rs = _parse_ints(a.resnet)
+        width = rs[2] if len(rs) > 2 else 64
+        data = DeviceImageDataset(iseed, n, image, classes)
+        model = ResNetTeacher(init_resnet(ResNetConfig(image=image, classes=classes, width=width), rs[0]),
+                              batch_size=rs[1])
     else:
-        model = nnkit.Model.from_host(formats.init_model(_parse_ints(a.teacher_dims), a.teacher_seed))
-    parts = a.data.split(",")
-    seed, n, dim, classes = (int(v) for v in parts[:4])
-    spread = float(parts[4]) if len(parts) > 4 else 1.0
-    data = DeviceDataset(formats.make_blobs(seed, n, dim, classes, spread))
+        if a.teacher_file:
+            model, _ = nnkit.load_model(a.teacher_file)
+        else:
+            model = nnkit.Model.from_host(formats.init_model(_parse_ints(a.teacher_dims), a.teacher_seed))
+        parts = a.data.split(",")
+        seed, n, dim, classes = (int(v) for v in parts[:4])
+        spread = float(parts[4]) if len(parts) > 4 else 1.0
+        data = DeviceDataset(formats.make_blobs(seed, n, dim, classes, spread))
     cb = ControlBlock(a.control)
     server = TeacherServer(cb, a.node_id, model, data, a.temperature, a.simulated_delay, a.sm_reserve)
     sys.stdout.write(f"teacher {a.node_id} registered as entry {server.j} epoch {server.epoch}\n")

@@ -536,8 +536,10 @@ class ResNetStudent:
                   out.data_ptr(), s)
 
     def train_step(self, x, hard_labels, soft: SoftLabels | None, alpha: float, beta: float, temperature: float,
-                   eta: float, stream=None):
-        """Forward, fused KD loss (edl/nnkit.py:283-309 semantics), backward, SGD."""
+                   eta: float, stream=None, process_group=None, world_size: int = 1):
+        """Forward, fused KD loss (edl/nnkit.py:283-309 semantics), backward, SGD.
+        world_size > 1: the flat gradient is all-reduced over `process_group`
+        (NCCL, edl/allreduce.py:77-120) and the mean folded into SGD's step."""
         s = (stream or torch.cuda.current_stream()).cuda_stream
         B = self.B
         self.forward(x, s)
@@ -596,8 +598,11 @@ class ResNetStudent:
         _lib.call("edl_maxpool_bwd_argmax_nhwc", self.pool_arg.data_ptr(), B, h, w, self.y0.shape[-1], 3, 2, 1,
                   dz.data_ptr(), None, dy0.data_ptr(), s)   # ReLU mask folded into the argmax words
         self._wgrad(0, dy0, x, (self.cfg.image, self.cfg.image), s)
+        if world_size > 1:
+            with torch.cuda.stream(stream or torch.cuda.current_stream()):
+                torch.distributed.all_reduce(self.grads, group=process_group)
         _lib.call("edl_sgd_step", self.flat.data_ptr(), self.flat_bf16.data_ptr(), self.grads.data_ptr(), self.size,
-                  float(eta), s)
+                  float(eta) / world_size, s)
         return self.loss
 
     def flops_per_sample(self) -> float:

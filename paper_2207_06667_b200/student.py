@@ -153,7 +153,13 @@ class StudentStep:
 
     def __init__(self, model: Model, cfg: TrainConfig, batch_size: int, world_size: int = 1,
                  process_group=None, max_steps: int = 1 << 16, fuse_sgd: bool = True,
-                 exchange: str = "nccl", overlap_exchange: bool = False):
+                 exchange: str = "nccl", overlap_exchange: bool = False, graph: bool = False):
+        """graph=True replays the whole step (GEMMs, fused loss, backward,
+        all-reduce, SGD) as one CUDA graph from fixed buffers: the batch must be
+        gathered into `self.batch` (or it is copied there) and the soft labels
+        are copied into a fixed pair of buffers. For host-bound loops (a split
+        placement's student runs a ~0.2 ms step; eager launching costs about as
+        much)."""
         self.model = model
         self.cfg = cfg
         self.world_size = world_size
@@ -192,28 +198,83 @@ class StudentStep:
         # host-coupled e2e path 15.6 -> 13.4 M: two NCCL calls a step add host
         # latency where every step waits on its H2D upload. Opt-in.
         self._overlap = overlap_exchange
+        self._use_graph = graph and not overlap_exchange and self.exchange is None
+        self._graph = None
+        self._warm = False
+        self._g_soft: SoftLabels | None = None
+        self._g_loss = torch.zeros(1, dtype=torch.float32, device=model.device)
 
     def step(self, batch: Batch, soft: SoftLabels | None) -> None:
+        if self._use_graph:
+            self._step_graph(batch, soft)
+            return
         i = self._n % self.losses.shape[0]
+        self._body(batch, soft, self.losses[i:i + 1])
+        self._n += 1
+
+    def _step_graph(self, batch: Batch, soft: SoftLabels | None) -> None:
+        cfg = self.cfg
+        if cfg.beta > 0:
+            if soft is None:
+                raise nnkit.ShapeError("beta > 0 requires soft labels")
+            if soft.size != self.batch.size:
+                raise nnkit.ShapeError(f"soft batch {soft.size} != input batch {self.batch.size}")
+            if soft.temperature != cfg.temperature:
+                raise ValueError(f"soft labels tempered at {soft.temperature}, config says {cfg.temperature}")
+            if soft.num_classes is not None and soft.num_classes != self.model.num_classes:
+                raise nnkit.ShapeError(f"soft labels over {soft.num_classes} classes, student has "
+                                       f"{self.model.num_classes}")
+            if self._g_soft is None or self._g_soft.probs.shape != soft.probs.shape:
+                if self._graph is not None:
+                    raise nnkit.ShapeError("soft-label k changed under a captured step graph")
+                self._g_soft = SoftLabels(torch.empty_like(soft.probs), torch.empty_like(soft.classes),
+                                          cfg.temperature, num_classes=self.model.num_classes)
+            self._g_soft.probs.copy_(soft.probs)
+            self._g_soft.classes.copy_(soft.classes)
+        if batch is not self.batch:
+            self.batch.inputs.copy_(batch.inputs)
+            self.batch.hard_labels.copy_(batch.hard_labels)
+        g_soft = self._g_soft if cfg.beta > 0 else None
+        if not self._warm:
+            # one eager step first: kernel attributes, tensor maps and the
+            # tile-scheduler counters initialise outside the capture
+            l0 = _lib.launch_count
+            self._body(self.batch, g_soft, self._g_loss)
+            self._launches = _lib.launch_count - l0
+            self._warm = True
+        else:
+            if self._graph is None:
+                g = torch.cuda.CUDAGraph()
+                l0 = _lib.launch_count
+                with torch.cuda.graph(g, stream=torch.cuda.Stream(self.model.device)):
+                    self._body(self.batch, g_soft, self._g_loss)
+                _lib.launch_count = l0          # captured, not run: counted at each replay
+                self._graph = g
+            self._graph.replay()
+            _lib.launch_count += self._launches
+        i = self._n % self.losses.shape[0]
+        self.losses[i:i + 1].copy_(self._g_loss)
+        self._n += 1
+
+    def _body(self, batch: Batch, soft: SoftLabels | None, loss_slot: torch.Tensor) -> None:
         if self.world_size == 1 and self.fuse_sgd:
             # single student: the update is fused into the dW / db kernels
-            nnkit.kd_loss(self.model, batch, soft, self.cfg, ws=self.ws, loss_slot=self.losses[i:i + 1],
+            nnkit.kd_loss(self.model, batch, soft, self.cfg, ws=self.ws, loss_slot=loss_slot,
                           fused_sgd_eta=self.cfg.eta)
         elif self.exchange is not None:
-            nnkit.kd_loss(self.model, batch, soft, self.cfg, ws=self.ws, loss_slot=self.losses[i:i + 1])
+            nnkit.kd_loss(self.model, batch, soft, self.cfg, ws=self.ws, loss_slot=loss_slot)
             self.exchange.step(self.cfg.eta)
         elif self.world_size > 1 and self._overlap:
-            nnkit.kd_loss(self.model, batch, soft, self.cfg, ws=self.ws, loss_slot=self.losses[i:i + 1],
+            nnkit.kd_loss(self.model, batch, soft, self.cfg, ws=self.ws, loss_slot=loss_slot,
                           layer_ready=self._ready)
             self._exchange_overlapped()
         elif self.world_size > 1:
-            nnkit.kd_loss(self.model, batch, soft, self.cfg, ws=self.ws, loss_slot=self.losses[i:i + 1])
+            nnkit.kd_loss(self.model, batch, soft, self.cfg, ws=self.ws, loss_slot=loss_slot)
             torch.distributed.all_reduce(self.ws.grads.flat, group=self.group)
             nnkit.sgd_step(self.model, self.ws.grads, self.cfg.eta, self.world_size)
         else:
-            nnkit.kd_loss(self.model, batch, soft, self.cfg, ws=self.ws, loss_slot=self.losses[i:i + 1])
+            nnkit.kd_loss(self.model, batch, soft, self.cfg, ws=self.ws, loss_slot=loss_slot)
             nnkit.sgd_step(self.model, self.ws.grads, self.cfg.eta, 1)
-        self._n += 1
 
     def _exchange_overlapped(self) -> None:
         """all-reduce + SGD per bucket on the comm stream (edl/student_node.py:

@@ -188,3 +188,55 @@ def test_teacher_process_on_another_gpu(control):
     assert res.ledger["ok"]
     assert np.array_equal(ref.flatten(base.model.weights, base.model.biases),
                           ref.flatten(res.model.weights, res.model.biases))
+
+
+def test_cfg4_resnet_teacher_processes_match_local_teacher(control):
+    """cfg4 through the elastic pool: two ResNet-50-style teacher processes
+    serve a ResNet-18-style student over HBM-resident image rows (small
+    shapes: 32x32 images, width 16, 10 classes); the student's parameters
+    equal a run fed by an in-process teacher bit for bit."""
+    import torch
+
+    from paper_2207_06667_b200.data import DeviceImageDataset, DeviceShardSampler
+    from paper_2207_06667_b200.elastic import ElasticPool
+    from paper_2207_06667_b200.reader import DistilReader, EventLog, SchedulerConfig
+    from paper_2207_06667_b200.resnet import (ResNetConfig, ResNetStudent, ResNetTeacher, StudentResNetConfig,
+                                              init_resnet, init_student_resnet)
+    cb, path, procs = control
+    B, steps, K, k = 8, 10, 10, 4
+    env = dict(os.environ, PYTHONPATH=ROOT + os.pathsep + os.environ.get("PYTHONPATH", ""))
+    for name in ("r1", "r2"):
+        log = f"{path}.{name}.log"
+        LOGS.append(log)
+        with open(log, "w") as fh:
+            procs.append(subprocess.Popen(
+                [sys.executable, "-u", "-m", "paper_2207_06667_b200.elastic", "--control", path, "--node-id", name,
+                 "--resnet", f"1,{B},16", "--images", f"3,64,32,{K}"], cwd=ROOT, env=env, stdout=fh,
+                stderr=subprocess.STDOUT))
+    wait_registered(cb, ["r1", "r2"], procs)
+    data = DeviceImageDataset(3, 64, 32, K)
+    scfg = StudentResNetConfig(layers=(1, 1, 1, 1), width=16, classes=K, image=32)
+
+    def train(soft_for):
+        st = ResNetStudent(init_student_resnet(scfg, 0), batch_size=B)
+        sampler = DeviceShardSampler(data, 1, 0, B, seed=0)
+        for it in range(steps):
+            soft = soft_for(it)
+            b = sampler.batch_for(it)
+            st.train_step(data.nhwc(b.inputs), b.hard_labels, soft, 0.5, 0.5, 2.0, 0.01)
+        torch.cuda.synchronize()
+        return st.flat.clone()
+
+    pool = ElasticPool(cb, 0, ttl=10.0, reply_timeout=60.0)
+    pool.open(1, 0, B, k, 0, 2.0, K, 16, data.device)
+    reader = DistilReader("student-0", pool, SchedulerConfig(lt=2, ut=6, probe_interval=0.0, acquire_cooldown=0.0),
+                          DeviceShardSampler(data, 1, 0, B, seed=0), 0, steps, 1, EventLog(), 2.0, k)
+    assert reader.acquire(2) == 2
+    remote = train(lambda it: reader.consume(it, timeout=120))
+    assert reader.ledger()["ok"]
+    reader.close()
+    teacher = ResNetTeacher(init_resnet(ResNetConfig(image=32, classes=K, width=16), 1), batch_size=B)
+    ls = DeviceShardSampler(data, 1, 0, B, seed=0)
+    local = train(lambda it: teacher.soft_labels(data.nhwc(ls.batch_for(it).inputs), 2.0, k))
+    assert torch.isfinite(remote).all()
+    assert torch.equal(remote, local)
