@@ -383,6 +383,16 @@ int edl_linear_fwd(const void* X, long long ldx, const void* W, long long ldw, c
   int rc;
   if ((rc = tensor_map(X, M, K, ldx, 64, 128, &ta))) return rc;
   EpiArgs ep{Y, ldy, bias, nullptr, 0, 1.0f, stream_sched(as_stream(stream))};
+  // raster / L2-policy experiments on the pair GEMM (EDL_RASTER = m-tiles per
+  // raster group, EDL_L2HINT = 1: A evict_last + B evict_first)
+  static const int raster_env = [] { const char* v = getenv("EDL_RASTER"); return v ? atoi(v) : 0; }();
+  static const int l2hint_env = [] { const char* v = getenv("EDL_L2HINT"); return v ? atoi(v) : -1; }();
+  ep.raster = raster_env;
+  // default: when A is too big to sit in L2 beside the streaming B (the
+  // grouped-raster case, raster_group), load A evict_last and B evict_first
+  // -- teacher layer 2: DRAM 515 -> 419 MB per launch, 356 -> 351 us alone
+  // (profiles/r02_layer2_raster.txt)
+  ep.l2hint = l2hint_env >= 0 ? l2hint_env : (static_cast<long long>(M) * K * 2 > (32ll << 20) ? 1 : 0);
   CUtensorMap ty;
   if ((rc = tensor_map_out(Y, M, N, ldy, act == EDL_ACT_NONE, &ty))) return rc;
   const int pbn = pick_pair_bn(M, N, cap);

@@ -997,7 +997,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n;
   const int nk = (K + kBK - 1) / kBK;
-  const int rgroup = raster_group(num_m, M, K);
+  const int rgroup = ep.raster > 0 ? (ep.raster < num_m ? ep.raster : num_m) : raster_group(num_m, M, K);
   const int pair = static_cast<int>(blockIdx.x) / 2;
   const int npairs = static_cast<int>(gridDim.x) / 2;
   const uint32_t full0 = mapa(smem_u32(full), 0);           // rank 0's full[0]
@@ -1045,6 +1045,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_im2col_4d_pair(sA + s * Cfg::kABytes, &tmA, full0 + 8 * s, tap.cb * 64, ct.wb, ct.hb, ct.nb,
                                     static_cast<uint16_t>(tap.s), static_cast<uint16_t>(tap.r));
             tma_load_2d_pair(sB + s * Cfg::kBBytes, &tmB, full0 + 8 * s, kb * kBK, n0);
+          }
+          continue;
+        }
+      }
+      if constexpr (!A_MN && !B_MN) {
+        if (ep.l2hint == 1) {   // keep the A panel resident, stream B through L2
+          const uint64_t pa = l2_policy_evict_last(), pb = l2_policy_evict_first();
+          for (int kb = 0; kb < nk; ++kb, ++g) {
+            const int s = g % S;
+            mbar_wait(&empty[s], ((g / S) & 1) ^ 1);
+            if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * Cfg::kStageBytes);
+            tma_load_2d_pair_hint(sA + s * Cfg::kABytes, &tmA, full0 + 8 * s, kb * kBK, m0, pa);
+            tma_load_2d_pair_hint(sB + s * Cfg::kBBytes, &tmB, full0 + 8 * s, kb * kBK, n0, pb);
           }
           continue;
         }

@@ -81,6 +81,8 @@ struct EpiArgs {
   ConvGeom conv;          // A operand from an im2col map (gemm_kernel / gemm_pair_kernel, K-major A)
   const __nv_bfloat16* aux2 = nullptr;   // EPI_DRELU_BF16: the ReLU mask (the layer's output), ld_aux2
   long long ld_aux2 = 0;
+  int raster = 0;         // tile raster group (m-tiles per group); 0: raster_group()'s heuristic
+  int l2hint = 0;         // gemm_pair_kernel, K-major operands: 1 = A evict_last, B evict_first
 };
 
 struct HeadArgs {

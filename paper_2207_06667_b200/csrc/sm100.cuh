@@ -360,6 +360,16 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       : "memory");
 }
 
+// tma_load_2d_pair with an L2 eviction-priority policy (l2_policy_*).
+__device__ __forceinline__ void tma_load_2d_pair_hint(void* dst, const CUtensorMap* m, uint32_t bar,
+                                                      int32_t c0, int32_t c1, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+
 // TMA im2col loads (implicit-GEMM convolution): a 4-D NHWC tensor map in
 // im2col mode; {c, w, h, n} is the first output pixel's window corner in input
 // coordinates (q*stride - pad, p*stride - pad) and {off_w, off_h} the filter
