@@ -282,7 +282,7 @@ def main():
                     help="CUDA stream priority of the student in the co-located EDL loop")
     ap.add_argument("--teacher-sm-reserve", type=int, default=-1,
                     help="SMs the co-located teacher stream leaves free for the student's NCCL "
-                         "all-reduce / single-wave kernels (-1: 32 when N > 1, else 16)")
+                         "all-reduce / single-wave kernels (-1: 40 when N > 1, else 8)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.batch:
@@ -350,7 +350,11 @@ def main():
     # 40/48/56 -> 17.17-17.35 / 17.19-17.23 / 16.3-16.6 M. The reserved SMs
     # let the student's one-wave kernels (and at N>1 NCCL's all-reduce) run
     # beside the teacher's persistent GEMMs.
-    reserve = args.teacher_sm_reserve if args.teacher_sm_reserve >= 0 else (40 if world > 1 else 16)
+    # Round-2 same-box sweep at N=1 (profiles/r02_reserve_sweep.txt): reserve
+    # 0 / 8 / 12 / 16 / 24 -> 5.26 / 5.31 / 5.26 / 5.22-5.26 / 5.16 M samples/s,
+    # teacher layer 2 in-step 363 / 400 / 399 / 428-441 / 446 us: 8 keeps
+    # the throughput with the dominant kernel at ~0.85 of burst in the step.
+    reserve = args.teacher_sm_reserve if args.teacher_sm_reserve >= 0 else (40 if world > 1 else 8)
     worker = TeacherWorker(TeacherConfig("t1", cfg["T"], cfg["topk"]), teacher, ddata, sm_reserve=reserve)
     pool.register(worker)
     sched = SchedulerConfig(lt=2, ut=8, pipeline_depth=2, acquire_cooldown=1e9)

@@ -325,6 +325,25 @@ int edl_cast_bf16(const float* src, long long ld_src, void* dst, long long ld_ds
 int edl_cast_bf16_f64(const double* src, long long ld_src, void* dst, long long ld_dst, int rows, int cols,
                       void* stream);
 
+/* Training-mode BatchNorm for the cfg4 ResNet-18-style student (BASELINE.json
+ * configs[3]; the reference has no convolutions). z / g / y / dz
+ * are NHWC bf16 rows [M = N*H*W][C], C % 8 == 0 and <= 2048; per-channel
+ * fp32 vectors [C]. Batch statistics are biased (nn.BatchNorm2d training
+ * mode); reductions are deterministic (fixed row blocks, fp64 final sums).
+ *   stats:  mean, rstd = 1 / sqrt(var + eps)
+ *   apply:  y = [relu](gamma (z - mean) rstd + beta [+ residual])
+ *   bwd:    dbeta = sum g, dgamma = sum g xhat (written, not accumulated),
+ *           dz = gamma rstd (g - dbeta / M - xhat dgamma / M)
+ * workspace: edl_bn_workspace_floats(M, C) floats. */
+long long edl_bn_workspace_floats(int M, int C);
+int edl_bn_stats_nhwc(const void* z, int M, int C, float* workspace, long long ws_floats, float* mean, float* rstd,
+                      float eps, void* stream);
+int edl_bn_apply_nhwc(const void* z, int M, int C, const float* mean, const float* rstd, const float* gamma,
+                      const float* beta, const void* residual, int relu, void* y, void* stream);
+int edl_bn_bwd_nhwc(const void* g, const void* z, int M, int C, const float* mean, const float* rstd,
+                    const float* gamma, float* workspace, long long ws_floats, float* dgamma, float* dbeta, void* dz,
+                    void* stream);
+
 /* TeacherConfig.simulated_delay (edl/teacher_node.py:30-44, slept per batch
  * by TeacherServer._compute_loop :157-170): a single-thread device busy wait
  * of `ns` nanoseconds on `stream`, so a throttled teacher delays its own

@@ -1097,6 +1097,50 @@ int edl_cast_bf16_f64(const double* src, long long ld_src, void* dst, long long 
   return e == cudaSuccess ? 0 : cuda_fail(e, "cast_bf16_f64");
 }
 
+// ---- training-mode BatchNorm (cfg4 student)
+static int bn_check(int M, int C, const char* what) {
+  if (M < 1 || C < 8 || C % 8 || C > 2048) return fail(EDL_ERR_SHAPE, "%s: M=%d C=%d (C %% 8 == 0, <= 2048)", what, M, C);
+  return 0;
+}
+
+long long edl_bn_workspace_floats(int M, int C) {
+  return 2LL * bn_partial_blocks(M < 1 ? 1 : M, num_sms()) * C;
+}
+
+int edl_bn_stats_nhwc(const void* z, int M, int C, float* workspace, long long ws_floats, float* mean, float* rstd,
+                      float eps, void* stream) {
+  if (int rc = bn_check(M, C, "bn_stats")) return rc;
+  if (ws_floats < edl_bn_workspace_floats(M, C)) return fail(EDL_ERR_SHAPE, "bn_stats: workspace too small");
+  if (!(eps > 0.f)) return fail(EDL_ERR_PARAM, "bn_stats: eps %g", eps);
+  cudaError_t e = launch_bn_stats(static_cast<const __nv_bfloat16*>(z), M, C, workspace, mean, rstd, eps, num_sms(),
+                                  as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "bn_stats");
+}
+
+int edl_bn_apply_nhwc(const void* z, int M, int C, const float* mean, const float* rstd, const float* gamma,
+                      const float* beta, const void* residual, int relu, void* y, void* stream) {
+  if (int rc = bn_check(M, C, "bn_apply")) return rc;
+  cudaError_t e = launch_bn_apply(static_cast<const __nv_bfloat16*>(z), M, C, mean, rstd, gamma, beta,
+                                  static_cast<const __nv_bfloat16*>(residual), relu != 0,
+                                  static_cast<__nv_bfloat16*>(y), num_sms(), as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "bn_apply");
+}
+
+int edl_bn_bwd_nhwc(const void* g, const void* z, int M, int C, const float* mean, const float* rstd,
+                    const float* gamma, float* workspace, long long ws_floats, float* dgamma, float* dbeta, void* dz,
+                    void* stream) {
+  if (int rc = bn_check(M, C, "bn_bwd")) return rc;
+  if (ws_floats < edl_bn_workspace_floats(M, C)) return fail(EDL_ERR_SHAPE, "bn_bwd: workspace too small");
+  const auto* gg = static_cast<const __nv_bfloat16*>(g);
+  const auto* zz = static_cast<const __nv_bfloat16*>(z);
+  cudaError_t e = launch_bn_bwd_reduce(gg, zz, M, C, mean, rstd, workspace, dbeta, dgamma, num_sms(),
+                                       as_stream(stream));
+  if (e == cudaSuccess)
+    e = launch_bn_bwd_apply(gg, zz, M, C, mean, rstd, gamma, dbeta, dgamma, static_cast<__nv_bfloat16*>(dz),
+                            num_sms(), as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "bn_bwd");
+}
+
 int edl_memcpy_async(void* dst, const void* src, long long bytes, void* stream) {
   if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(EDL_ERR_SHAPE, "memcpy_async: bad arguments");
   if (bytes == 0) return 0;
