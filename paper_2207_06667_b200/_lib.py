@@ -133,7 +133,11 @@ def load() -> ctypes.CDLL:
                 "(the B200 path has no CPU fallback)")
         lib = ctypes.CDLL(LIB_PATH)
         for name, args in _SIGNATURES.items():
-            fn = getattr(lib, name)
+            fn = getattr(lib, name, None)
+            if fn is None and os.environ.get("EDL_LIB"):
+                continue      # an older build under A/B (scripts/ab_lib.sh): entry points it predates
+            if fn is None:
+                raise RuntimeError(f"{LIB_PATH} lacks {name}; rebuild")
             fn.argtypes = args
             fn.restype = _RESTYPES.get(name, c_int)
         if lib.edl_version() != ABI_VERSION:

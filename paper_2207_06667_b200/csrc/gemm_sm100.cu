@@ -209,7 +209,7 @@ __host__ __device__ constexpr bool epi_has_bias() {
 template <int EPI>
 __device__ __forceinline__ void epilogue_store(const EpiArgs& ep, int row, int M, int col0,
                                                int N, float (&v)[32], const float* sb = nullptr,
-                                               const uint4* hpre = nullptr) {
+                                               const uint4* hpre = nullptr, float* out_f32 = nullptr) {
   if (row >= M) return;
   const bool full = (col0 + 32 <= N);
   if constexpr (EPI == EPI_TANH_BF16 || EPI == EPI_BIAS_F32) {
@@ -319,7 +319,7 @@ __device__ __forceinline__ void epilogue_store(const EpiArgs& ep, int row, int M
         if (col0 + i < N) o[i] = __float2bfloat16_rn(v[i]);
     }
   } else {
-    float* o = reinterpret_cast<float*>(ep.out) + static_cast<size_t>(row) * ep.ld_out + col0;
+    float* o = (out_f32 != nullptr ? out_f32 : reinterpret_cast<float*>(ep.out)) + static_cast<size_t>(row) * ep.ld_out + col0;
     if (full) {
 #pragma unroll
       for (int i = 0; i < 8; ++i)
@@ -349,7 +349,7 @@ __device__ __forceinline__ void stage_bias(const EpiArgs& ep, float* sb, int n0,
 // epilogue, so its serial load latencies were the kernel's critical path.
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_tile(const EpiArgs& ep, uint32_t taddr, int row, int M, int n0,
-                                              int N, const float* sb) {
+                                              int N, const float* sb, float* out_f32 = nullptr) {
   // EPI_DTANH_BF16 reads the layer's activations: the next chunk's 64 bytes
   // are loaded together with the next TMEM chunk
   constexpr bool kAux = EPI == EPI_DTANH_BF16;
@@ -384,7 +384,7 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& ep, uint32_t taddr,
     if (c + 32 < BN) tmem_ld32_issue(taddr + c + 32, r);
     if (n0 + c < N)
       epilogue_store<EPI>(ep, row, M, n0 + c, N, v, sb != nullptr ? sb + c : nullptr,
-                          (kAux && n0 + c + 32 <= N) ? hc : nullptr);
+                          (kAux && n0 + c + 32 <= N) ? hc : nullptr, out_f32);
     if (c + 32 < BN) tmem_ld_wait(r);
   }
 }
@@ -836,8 +836,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       int mt, nt, kb0, kb1;
       const int split = decode(t, mt, nt, kb0, kb1);
       const int m0 = mt * kBM, n0 = nt * BN;
-      EpiArgs eps = ep;
-      if (split) eps.out = static_cast<float*>(ep.out) + split * ep.split_stride;
+      // split-K partials: split s writes its slice of the fp32 workspace. (A
+      // by-value copy of `ep` with a patched `out` here broke the split-K
+      // results once EpiArgs outgrew 128 bytes; the slice pointer is passed
+      // down instead.)
+      float* const split_out = split ? static_cast<float*>(ep.out) + split * ep.split_stride : nullptr;
       float* sb = sbias;
       if (tma_res) {   // the first two residual chunks load behind this tile's MMAs
         rs.issue(lane, n0, m0 + 32 * e);
@@ -847,7 +850,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // the first barrier keeps a re-stage behind every warp's previous tile
       if (epi_has_bias<EPI>() && n0 != staged_n0) {
         if (staged_n0 >= 0) epi_bar_sync();
-        stage_bias<BN, EPI>(eps, sb, n0, N, static_cast<int>(threadIdx.x) - 128);
+        stage_bias<BN, EPI>(ep, sb, n0, N, static_cast<int>(threadIdx.x) - 128);
         epi_bar_sync();
         staged_n0 = n0;
       }
@@ -855,12 +858,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[as], (i / kAcc) & 1);
       tc_fence_after();
       if constexpr (epi_tma_store<EPI>())
-        epilogue_tile_tma<BN, EPI>(eps, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e,
+        epilogue_tile_tma<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e,
                                    lane, M, n0, N, epi_has_bias<EPI>() ? sb : nullptr, &tmY, stg + e * 8192, stores,
                                    tma_res ? &rs : nullptr);
       else
-        epilogue_tile<BN, EPI>(eps, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e + lane,
-                               M, n0, N, epi_has_bias<EPI>() ? sb : nullptr);
+        epilogue_tile<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e + lane,
+                               M, n0, N, epi_has_bias<EPI>() ? sb : nullptr, split_out);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[as]);

@@ -39,12 +39,15 @@ class ResNetConfig:
 
 @dataclass
 class HostConv:
-    """Folded conv + BN: w fp32 [cout][cin][k][k], b fp32 [cout]."""
+    """Folded conv + BN: w fp32 [cout][cin][k][k], b fp32 [cout]. A student
+    conv followed by training-mode BatchNorm carries gamma (b is then BN's
+    beta and the conv itself has no bias)."""
     w: np.ndarray
     b: np.ndarray
     stride: int
     pad: int
     relu: bool = True
+    gamma: np.ndarray | None = None
 
 
 @dataclass
@@ -60,6 +63,7 @@ class HostResNet:
     blocks: list = field(default_factory=list)
     fc_w: np.ndarray | None = None     # [classes][features]
     fc_b: np.ndarray | None = None
+    bn: bool = False                   # every conv followed by training-mode BatchNorm (student)
 
 
 def _conv(rng, cin, cout, k, stride, relu=True, gain=1.0):
@@ -283,11 +287,12 @@ def to_nhwc(images: np.ndarray, device) -> torch.Tensor:
 
 
 # ---------------------------------------------------------------------------
-# cfg4 student: BN-free ResNet-18-style training step (basic blocks; each
-# residual branch's second conv starts small, Fixup-style, since training-mode
-# BatchNorm is not on this path yet). Parameters live in one flat fp32 master
-# + bf16 copy (Model's layout idea), gradients in one flat fp32 vector, so SGD
-# is one edl_sgd_step.
+# cfg4 student: ResNet-18-style training step (basic blocks). Default: every
+# conv followed by training-mode BatchNorm (batch statistics, bn.cu; conv
+# without bias, BN's beta in the bias slot, gamma in its own slot). bn=False:
+# the BN-free variant (each residual branch's second conv starts small,
+# Fixup-style). Parameters live in one flat fp32 master + bf16 copy (Model's
+# layout idea), gradients in one flat fp32 vector, so SGD is one edl_sgd_step.
 
 @dataclass(frozen=True)
 class StudentResNetConfig:
@@ -296,13 +301,21 @@ class StudentResNetConfig:
     classes: int = 1000
     image: int = 224
     in_channels: int = 3
+    bn: bool = True
+
+
+def _bn_conv(rng, cin, cout, k, stride, relu=True, gain=1.0):
+    """A plain He-normal conv (no bias) followed by BatchNorm: gamma 1, beta 0."""
+    w = rng.normal(0.0, np.sqrt(2.0 / (cin * k * k)), size=(cout, cin, k, k)).astype(np.float32)
+    return HostConv(w, np.zeros(cout, dtype=np.float32), stride, k // 2, relu, np.ones(cout, dtype=np.float32))
 
 
 def init_student_resnet(cfg: StudentResNetConfig, seed: int) -> HostResNet:
     rng = np.random.default_rng(seed)
     rcfg = ResNetConfig(block="basic", layers=cfg.layers, width=cfg.width, classes=cfg.classes, image=cfg.image,
                         in_channels=cfg.in_channels)
-    net = HostResNet(rcfg, _conv(rng, cfg.in_channels, cfg.width, 7, 2))
+    mk = _bn_conv if cfg.bn else _conv
+    net = HostResNet(rcfg, mk(rng, cfg.in_channels, cfg.width, 7, 2), bn=cfg.bn)
     net.stem.pad = 3
     net.stem.b[:] = 0.0
     cin = cfg.width
@@ -310,11 +323,11 @@ def init_student_resnet(cfg: StudentResNetConfig, seed: int) -> HostResNet:
         cout = cfg.width * (2 ** stage)
         for i in range(n):
             stride = 2 if (i == 0 and stage > 0) else 1
-            c1 = _conv(rng, cin, cout, 3, stride)
-            c2 = _conv(rng, cout, cout, 3, 1, relu=True, gain=0.25)
+            c1 = mk(rng, cin, cout, 3, stride)
+            c2 = mk(rng, cout, cout, 3, 1, relu=True, gain=0.25)
             shortcut = None
             if stride != 1 or cin != cout:
-                shortcut = _conv(rng, cin, cout, 1, stride, relu=False)
+                shortcut = mk(rng, cin, cout, 1, stride, relu=False)
                 shortcut.pad = 0
             net.blocks.append(HostBlock([c1, c2], shortcut))
             cin = cout
@@ -324,20 +337,28 @@ def init_student_resnet(cfg: StudentResNetConfig, seed: int) -> HostResNet:
 
 
 class _Param:
-    """A [rows][cols] weight + [rows] bias view pair inside the flat buffers."""
+    """A [rows][cols] weight + [rows] bias (BN's beta) view pair inside the flat
+    buffers, and BN's gamma [rows] when the conv is followed by BatchNorm."""
 
-    def __init__(self, off_w, rows, cols, off_b):
-        self.off_w, self.rows, self.cols, self.off_b = off_w, rows, cols, off_b
+    def __init__(self, off_w, rows, cols, off_b, off_g=None):
+        self.off_w, self.rows, self.cols, self.off_b, self.off_g = off_w, rows, cols, off_b, off_g
 
 
 class ResNetStudent:
-    """Device BN-free ResNet-18-style student: forward, KD loss (the same fused
-    kernel as the MLP students), full backward and SGD, for a fixed batch."""
+    """Device ResNet-18-style student: forward (convs + training-mode
+    BatchNorm, or BN-free), the fused logit-layer KD head (the MLP students'
+    kernel), full backward and SGD, for a fixed batch."""
+
+    BN_EPS = 1e-5
 
     def __init__(self, host: HostResNet, device=None, batch_size: int = 64):
         self.device = dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.B = B = batch_size
         self.cfg = host.cfg
+        self.bn = bool(getattr(host, "bn", False))
+        hosts = [host.stem]
+        for blk in host.blocks:
+            hosts += [blk.convs[0], blk.convs[1]] + ([blk.shortcut] if blk.shortcut is not None else [])
         self.convs = [_DevConv(host.stem, "cpu")]
         self.block_idx = []                                 # (conv1, conv2, shortcut or None) indices
         for blk in host.blocks:
@@ -351,18 +372,24 @@ class ResNetStudent:
         self.feat_p = pad(feat)
         self.classes = host.fc_w.shape[0]
         self.classes_p = pad(self.classes)
-        # flat layout: every conv [cout_p][kdim] + bias [cout_p], then fc [classes_p][feat_p] + [classes_p]
+        # flat layout: every conv [cout_p][kdim] + bias [cout_p] (+ gamma [cout_p]
+        # with BN), then fc [classes_p][feat_p] + [classes_p]
         self.params, off = [], 0
         for c in self.convs:
             p = _Param(off, c.cout_p, c.kdim, off + c.cout_p * c.kdim)
             off = p.off_b + c.cout_p
+            if self.bn:
+                p.off_g = off
+                off += c.cout_p
             self.params.append(p)
         self.fc = _Param(off, self.classes_p, self.feat_p, off + self.classes_p * self.feat_p)
         self.size = self.fc.off_b + self.classes_p
         flat = torch.zeros(self.size, dtype=torch.float32)
-        for c, p in zip(self.convs, self.params):
+        for c, p, hc in zip(self.convs, self.params, hosts):
             flat[p.off_w:p.off_w + p.rows * p.cols] = c.w.float().reshape(-1)
             flat[p.off_b:p.off_b + p.rows] = c.b
+            if self.bn:
+                flat[p.off_g:p.off_g + hc.gamma.shape[0]] = torch.from_numpy(hc.gamma)
         fcw = torch.zeros(self.classes_p, self.feat_p)
         fcw[:self.classes, :feat] = torch.from_numpy(host.fc_w)
         flat[self.fc.off_w:self.fc.off_w + self.classes_p * self.feat_p] = fcw.reshape(-1)
@@ -419,7 +446,21 @@ class ResNetStudent:
         self.col = torch.empty(col, dtype=torch.bfloat16, device=dev)
         # backward buffers: gradient ping-pong at the largest activation size + a shortcut buffer
         big = max(B * h * w * stem.cout_p, max(a[1].numel() for a in self.acts))
-        self.g = [torch.empty(big, dtype=torch.bfloat16, device=dev) for _ in range(3)]
+        self.g = [torch.empty(big, dtype=torch.bfloat16, device=dev) for _ in range(4 if self.bn else 3)]
+        cmax = max(c.cout_p for c in self.convs)
+        self.zero_b = torch.zeros(cmax, dtype=torch.float32, device=dev)
+        if self.bn:
+            # pre-BN conv outputs z (the backward recomputes xhat from them),
+            # per-conv batch mean / rstd, the reductions' workspace
+            self.z0 = torch.empty_like(self.y0)
+            self.zs = [(torch.empty_like(h1), torch.empty_like(y), torch.empty_like(sc) if sc is not None else None)
+                       for (_, h1, sc, y) in self.acts]
+            self.bn_stats = torch.empty(len(self.convs), 2, cmax, dtype=torch.float32, device=dev)
+            wsn = 0
+            for i, c in enumerate(self.convs):
+                oh, ow = c.out_hw(*self.in_hw[i])
+                wsn = max(wsn, int(_lib.load().edl_bn_workspace_floats(B * oh * ow, c.cout_p)))
+            self.bn_ws = torch.empty(max(wsn, 1), dtype=torch.float32, device=dev)
         self.features = torch.empty(B, self.feat_p, dtype=torch.bfloat16, device=dev)
         self.logits = torch.empty(B, self.classes_p, dtype=torch.float32, device=dev)
         self.dlogits = torch.empty(B, self.classes_p, dtype=torch.bfloat16, device=dev)
@@ -438,6 +479,12 @@ class ResNetStudent:
     def _b(self, p):
         return self.flat[p.off_b:p.off_b + p.rows]
 
+    def _g(self, p):
+        return self.flat[p.off_g:p.off_g + p.rows]
+
+    def _gg(self, p):
+        return self.grads[p.off_g:p.off_g + p.rows]
+
     def _gw(self, p):
         return self.grads[p.off_w:p.off_w + p.rows * p.cols]
 
@@ -452,17 +499,24 @@ class ResNetStudent:
                   c.k, c.k, c.stride, c.pad, self.cols[i].data_ptr(), c.kdim, s)
         return self.cols[i], c.kdim
 
-    def _fwd(self, i, x, hw, out, residual, s):
+    def _fwd(self, i, x, hw, out, residual, s, raw=False):
+        """Conv i: out = act(conv(x) + b [+ residual]); raw=True (BN): out = conv(x)."""
         c, p = self.convs[i], self.params[i]
         oh, ow = c.out_hw(*hw)
+        bias = self.zero_b if raw else self._b(p)
         if c.implicit:
-            act = _lib.EDL_ACT_RELU if (c.relu or residual is not None) else _lib.EDL_ACT_IDENT
+            act = _lib.EDL_ACT_IDENT if raw else (
+                _lib.EDL_ACT_RELU if (c.relu or residual is not None) else _lib.EDL_ACT_IDENT)
             _lib.call("edl_conv_fwd_nhwc", x.data_ptr(), self.B, hw[0], hw[1], c.cin_p, self._w16(p).data_ptr(),
-                      c.kdim, self._b(p).data_ptr(), c.cout_p, c.k, c.k, c.stride, c.pad,
+                      c.kdim, bias.data_ptr(), c.cout_p, c.k, c.k, c.stride, c.pad,
                       None if residual is None else residual.data_ptr(), c.cout_p, out.data_ptr(), c.cout_p, act, s)
             return
         a, lda = self._im2col(i, x, hw, s)
         M = self.B * oh * ow
+        if raw:
+            _lib.call("edl_linear_fwd", a.data_ptr(), lda, self._w16(p).data_ptr(), c.kdim, bias.data_ptr(),
+                      out.data_ptr(), c.cout_p, M, c.cout_p, c.kdim, _lib.EDL_ACT_IDENT, s)
+            return
         if residual is not None:
             _lib.call("edl_linear_fwd_residual", a.data_ptr(), lda, self._w16(p).data_ptr(), c.kdim,
                       self._b(p).data_ptr(), residual.data_ptr(), c.cout_p, out.data_ptr(), c.cout_p, M, c.cout_p,
@@ -472,24 +526,65 @@ class ResNetStudent:
                       out.data_ptr(), c.cout_p, M, c.cout_p, c.kdim,
                       _lib.EDL_ACT_RELU if c.relu else _lib.EDL_ACT_IDENT, s)
 
-    def forward(self, x, s):
-        self._fwd(0, x, (self.cfg.image, self.cfg.image), self.y0, None, s)
+    def _bn_fwd(self, i, z, y, residual, relu, s):
+        """Batch statistics of conv i's output z, then y = [relu](gamma xhat + beta [+ residual])."""
+        c, p = self.convs[i], self.params[i]
+        M = z.numel() // c.cout_p
+        mean, rstd = self.bn_stats[i, 0], self.bn_stats[i, 1]
+        _lib.call("edl_bn_stats_nhwc", z.data_ptr(), M, c.cout_p, self.bn_ws.data_ptr(), self.bn_ws.numel(),
+                  mean.data_ptr(), rstd.data_ptr(), self.BN_EPS, s)
+        _lib.call("edl_bn_apply_nhwc", z.data_ptr(), M, c.cout_p, mean.data_ptr(), rstd.data_ptr(),
+                  self._g(p).data_ptr(), self._b(p).data_ptr(), None if residual is None else residual.data_ptr(),
+                  1 if relu else 0, y.data_ptr(), s)
+
+    def _bn_bwd(self, i, g, z, dz, s):
+        """dgamma, dbeta into the flat gradient; dz = BN's input gradient."""
+        c, p = self.convs[i], self.params[i]
+        M = z.numel() // c.cout_p
+        _lib.call("edl_bn_bwd_nhwc", g.data_ptr(), z.data_ptr(), M, c.cout_p, self.bn_stats[i, 0].data_ptr(),
+                  self.bn_stats[i, 1].data_ptr(), self._g(p).data_ptr(), self.bn_ws.data_ptr(), self.bn_ws.numel(),
+                  self._gg(p).data_ptr(), self._gb(p).data_ptr(), dz.data_ptr(), s)
+
+    def _features_into(self, x, s):
+        """Stem, max pool, residual blocks, global average pool -> self.features."""
+        H = self.cfg.image
+        if self.bn:
+            self._fwd(0, x, (H, H), self.z0, None, s, raw=True)
+            self._bn_fwd(0, self.z0, self.y0, None, True, s)
+        else:
+            self._fwd(0, x, (H, H), self.y0, None, s)
         h, w = self.stem_hw
         # the pool input is the stem's ReLU output: argmax words carry its mask
         _lib.call("edl_maxpool_argmax_relu_nhwc", self.y0.data_ptr(), self.B, h, w, self.y0.shape[-1], 3, 2, 1,
                   self.x1.data_ptr(), self.pool_arg.data_ptr(), s)
         cur = self.x1
-        for (i1, i2, isc), (hw, h1, sc, y) in zip(self.block_idx, self.acts):
+        for bi, ((i1, i2, isc), (hw, h1, sc, y)) in enumerate(zip(self.block_idx, self.acts)):
             shortcut = cur
-            if isc is not None:
-                self._fwd(isc, cur, hw, sc, None, s)
-                shortcut = sc
-            self._fwd(i1, cur, hw, h1, None, s)
-            self._fwd(i2, h1, self.convs[i1].out_hw(*hw), y, shortcut, s)
+            c1hw = self.convs[i1].out_hw(*hw)
+            if self.bn:
+                z1, z2, zsc = self.zs[bi]
+                if isc is not None:
+                    self._fwd(isc, cur, hw, zsc, None, s, raw=True)
+                    self._bn_fwd(isc, zsc, sc, None, False, s)
+                    shortcut = sc
+                self._fwd(i1, cur, hw, z1, None, s, raw=True)
+                self._bn_fwd(i1, z1, h1, None, True, s)
+                self._fwd(i2, h1, c1hw, z2, None, s, raw=True)
+                self._bn_fwd(i2, z2, y, shortcut, True, s)
+            else:
+                if isc is not None:
+                    self._fwd(isc, cur, hw, sc, None, s)
+                    shortcut = sc
+                self._fwd(i1, cur, hw, h1, None, s)
+                self._fwd(i2, h1, c1hw, y, shortcut, s)
             cur = y
         fh, fw = self.final_hw
         _lib.call("edl_avgpool_nhwc", cur.data_ptr(), self.B, fh * fw, cur.shape[-1], self.features.data_ptr(),
                   self.feat_p, s)
+
+    def forward(self, x, s):
+        """features + the linear head: fp32 logits in self.logits (dense API)."""
+        self._features_into(x, s)
         _lib.call("edl_linear_fwd", self.features.data_ptr(), self.feat_p, self._w16(self.fc).data_ptr(), self.feat_p,
                   self._b(self.fc).data_ptr(), self.logits.data_ptr(), self.classes_p, self.B, self.classes_p,
                   self.feat_p, _lib.EDL_ACT_NONE, s)
@@ -501,14 +596,15 @@ class ResNetStudent:
         c, p = self.convs[i], self.params[i]
         oh, ow = c.out_hw(*hw)
         M = self.B * oh * ow
+        db = None if self.bn else self._gb(p).data_ptr()   # with BN the conv has no bias (beta's grad: _bn_bwd)
         if c.implicit:
             _lib.call("edl_conv_bwd_weight_nhwc", x.data_ptr(), self.B, hw[0], hw[1], c.cin_p, c.k, c.k, c.stride,
                       c.pad, dz.data_ptr(), c.cout_p, c.cout_p, self._gw(p).data_ptr(), c.kdim,
-                      self._gb(p).data_ptr(), self.wgrad_ws.data_ptr(), self.wgrad_ws.numel(), 1.0, s)
+                      db, self.wgrad_ws.data_ptr(), self.wgrad_ws.numel(), 1.0, s)
             return
         a, lda = (x, c.cin_p) if self.cols[i] is None else (self.cols[i], c.kdim)
         _lib.call("edl_linear_bwd_weight_ws", dz.data_ptr(), c.cout_p, a.data_ptr(), lda, self._gw(p).data_ptr(),
-                  c.kdim, self._gb(p).data_ptr(), self.wgrad_ws.data_ptr(), self.wgrad_ws.numel(), M, c.cout_p,
+                  c.kdim, db, self.wgrad_ws.data_ptr(), self.wgrad_ws.numel(), M, c.cout_p,
                   c.kdim, 1.0, s)
 
     @staticmethod
@@ -542,7 +638,7 @@ class ResNetStudent:
         (NCCL, edl/allreduce.py:77-120) and the mean folded into SGD's step."""
         s = (stream or torch.cuda.current_stream()).cuda_stream
         B = self.B
-        self.forward(x, s)
+        self._features_into(x, s)
         for c, p, wf in zip(self.convs, self.params, self.wflip):
             if wf is not None:
                 _lib.call("edl_conv_flip_weights", self._w16(p).data_ptr(), c.kdim, c.cout_p, c.cin_p, c.k, c.k,
@@ -550,10 +646,13 @@ class ResNetStudent:
         q_vals = soft.probs if (soft is not None and beta > 0) else None
         q_idx = soft.classes if (soft is not None and beta > 0) else None
         k = soft.probs.shape[1] if q_vals is not None else 0
-        _lib.call("edl_kd_loss_fwd_bwd", self.logits.data_ptr(), self.classes_p, hard_labels.data_ptr(),
+        # the logit layer with the KD loss and dlogits in its epilogue (the MLP
+        # students' kd_head_kernel, edl/nnkit.py:283-299): no fp32 logits stored
+        _lib.call("edl_linear_kd_loss_fwd_bwd", self.features.data_ptr(), self.feat_p, self._w16(self.fc).data_ptr(),
+                  self.feat_p, self._b(self.fc).data_ptr(), hard_labels.data_ptr(),
                   None if q_vals is None else q_vals.data_ptr(), None if q_idx is None else q_idx.data_ptr(), B,
-                  self.classes, k, float(alpha), float(beta), float(temperature), self.row_loss.data_ptr(),
-                  self.loss.data_ptr(), self.ticket.data_ptr(), self.dlogits.data_ptr(), self.classes_p,
+                  self.classes, self.feat_p, k, float(alpha), float(beta), float(temperature),
+                  self.row_loss.data_ptr(), self.loss.data_ptr(), self.dlogits.data_ptr(), self.classes_p,
                   self.status.data_ptr(), s)
         # head: dW_fc / db_fc, dfeat = dz W_fc
         _lib.call("edl_linear_bwd_weight", self.dlogits.data_ptr(), self.classes_p, self.features.data_ptr(),
@@ -568,11 +667,38 @@ class ResNetStudent:
         _lib.call("edl_avgpool_bwd_nhwc", self.dfeat.data_ptr(), self.feat_p, B, fh * fw, y_last.shape[-1],
                   y_last.data_ptr(), dz.data_ptr(), s)
         cur = 0                                             # dz lives in self.g[cur]
+        nb = len(self.g)
         for bi in range(len(self.block_idx) - 1, -1, -1):
             i1, i2, isc = self.block_idx[bi]
             hw, h1, sc, y = self.acts[bi]
             xin = self.x1 if bi == 0 else self.acts[bi - 1][3]
             h1_hw = self.convs[i1].out_hw(*hw)
+            if self.bn:
+                # dz is g2: the gradient at bn2's output (+ the shortcut), ReLU-masked
+                z1, z2, zsc = self.zs[bi]
+                b1, b2, b3 = [j for j in range(nb) if j != cur]
+                dz2 = self.g[b1][:y.numel()].view_as(y)
+                self._bn_bwd(i2, dz, z2, dz2, s)
+                self._wgrad(i2, dz2, h1, h1_hw, s)
+                g1 = self.g[b2][:h1.numel()].view_as(h1)
+                self._dgrad(i2, dz2, h1_hw, g1, None, h1, s)
+                dz1 = self.g[b1][:h1.numel()].view_as(h1)     # dz2's readers ran above (stream order)
+                self._bn_bwd(i1, g1, z1, dz1, s)
+                if isc is not None:
+                    dzsc = self.g[b2][:sc.numel()].view_as(sc)  # g1's reader ran above
+                    self._bn_bwd(isc, dz, zsc, dzsc, s)
+                    self._wgrad(isc, dzsc, xin, hw, s)
+                    add = self.g[b3][:xin.numel()].view_as(xin)
+                    self._dgrad(isc, dzsc, hw, add, None, None, s)
+                    out_buf = cur                               # g2's last readers ran above
+                else:
+                    add = dz
+                    out_buf = b2
+                self._wgrad(i1, dz1, xin, hw, s)
+                dx = self.g[out_buf][:xin.numel()].view_as(xin)
+                self._dgrad(i1, dz1, hw, dx, add, xin if bi > 0 else None, s)
+                dz, cur = dx, out_buf
+                continue
             b1, b2 = [j for j in range(3) if j != cur]
             # conv2: dW2, db2; dZ1 = col2im(dZ2 W2) * (h1 > 0)
             self._wgrad(i2, dz, h1, h1_hw, s)
@@ -594,9 +720,13 @@ class ResNetStudent:
             dz, cur = dx, out_buf
         # maxpool + stem ReLU, then the stem's weight gradient (the images need no gradient)
         h, w = self.stem_hw
-        dy0 = self.g[(cur + 1) % 3][:self.y0.numel()].view_as(self.y0)
+        dy0 = self.g[(cur + 1) % nb][:self.y0.numel()].view_as(self.y0)
         _lib.call("edl_maxpool_bwd_argmax_nhwc", self.pool_arg.data_ptr(), B, h, w, self.y0.shape[-1], 3, 2, 1,
                   dz.data_ptr(), None, dy0.data_ptr(), s)   # ReLU mask folded into the argmax words
+        if self.bn:
+            dz0 = self.g[(cur + 2) % nb][:self.y0.numel()].view_as(self.y0)
+            self._bn_bwd(0, dy0, self.z0, dz0, s)
+            dy0 = dz0
         self._wgrad(0, dy0, x, (self.cfg.image, self.cfg.image), s)
         if world_size > 1:
             with torch.cuda.stream(stream or torch.cuda.current_stream()):

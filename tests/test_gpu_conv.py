@@ -158,7 +158,7 @@ def test_resnet_student_grads_vs_torch_autograd(width):
     at width 16 -- storage, not a structural error (cosine >= 0.996)."""
     from paper_2207_06667_b200.nnkit import SoftLabels
     from paper_2207_06667_b200.resnet import ResNetStudent, StudentResNetConfig, init_student_resnet, to_nhwc
-    cfg = StudentResNetConfig(layers=(1, 1, 1, 1), width=width, classes=40, image=32)
+    cfg = StudentResNetConfig(layers=(1, 1, 1, 1), width=width, classes=40, image=32, bn=False)
     net = init_student_resnet(cfg, 4)
     B, k, T = 6, 5, 2.0
     rng = np.random.default_rng(9)
@@ -187,6 +187,157 @@ def test_resnet_student_grads_vs_torch_autograd(width):
     gfc = student._gw(p).view(p.rows, p.cols)[:40, :student.feat_p].float().cpu()
     assert _relnorm(gfc[:, :want["fc"][0].shape[1]], want["fc"][0]) < 3e-2
     assert _relnorm(student._gb(p)[:40].float().cpu(), want["fc"][1]) < 3e-2
+
+
+def _nchw(t, c):
+    """A device NHWC bf16 activation [B][H][W][C_p] as an NCHW float tensor (CPU)."""
+    return t.permute(0, 3, 1, 2)[:, :c].float().cpu().contiguous()
+
+
+@pytest.mark.parametrize("width,B", [(16, 8), (64, 8), (64, 32)])
+def test_resnet_student_bn_grads_vs_torch_autograd(width, B):
+    """The BatchNorm student (training-mode BN after every conv, bn.cu), one
+    KD step: loss, every conv's dW, every BN's dgamma / dbeta and the fc's
+    dW / db against torch autograd (F.batch_norm, training=True) on the CPU
+    (oracle/resnet_ref.student_bn_loss_and_grads), differentiating the
+    device's own forward values (substituted straight-through at the bf16
+    storage points, `forced`). At initialisation this BN net's gradient moves
+    ~24% for a 1e-3 relative perturbation of the images (measured), so an
+    independently computed forward cannot pin the backward; with the forward
+    shared, the remaining difference is the backward's bf16 storage and
+    accumulation: <= 3e-2 relative norm per tensor."""
+    from paper_2207_06667_b200.nnkit import SoftLabels
+    from paper_2207_06667_b200.resnet import ResNetStudent, StudentResNetConfig, init_student_resnet, to_nhwc
+    image = 64
+    cfg = StudentResNetConfig(layers=(1, 1, 1, 1), width=width, classes=40, image=image, bn=True)
+    net = init_student_resnet(cfg, 4)
+    k, T = 5, 2.0
+    rng = np.random.default_rng(9)
+    imgs = rng.normal(size=(B, 3, image, image)).astype(np.float32)
+    labels = rng.integers(0, 40, size=B)
+    cls = np.stack([rng.choice(40, size=k, replace=False) for _ in range(B)]).astype(np.int32)
+    pv = rng.uniform(0.1, 1.0, size=(B, k)).astype(np.float32)
+    pv = -np.sort(-pv, axis=1)
+    q = np.zeros((B, 40), dtype=np.float32)
+    np.put_along_axis(q, cls.astype(np.int64), pv / pv.sum(1, keepdims=True), axis=1)
+    student = ResNetStudent(net, "cuda", B)
+    assert student.bn
+    soft = SoftLabels(torch.from_numpy(pv).cuda(), torch.from_numpy(cls).cuda(), T)
+    loss = student.train_step(to_nhwc(imgs, "cuda"), torch.from_numpy(labels).cuda(), soft, 0.5, 0.5, T, eta=0.0)
+    torch.cuda.synchronize()
+    cw = lambda i: student.convs[i].cout_p if False else net_c(i)  # noqa: E731
+    couts = [net.stem.w.shape[0]] + [c.w.shape[0] for blk in net.blocks
+                                     for c in [blk.convs[0], blk.convs[1]] + ([blk.shortcut] if blk.shortcut else [])]
+
+    def net_c(i):
+        return couts[i]
+    forced = {"stem_z": _nchw(student.z0, cw(0)), "stem_y": _nchw(student.y0, cw(0)),
+              "features": student.features[:, :net.fc_w.shape[1]].float().cpu()}
+    for bi, ((i1, i2, isc), (_, h1, sc, y), (z1, z2, zsc)) in enumerate(zip(student.block_idx, student.acts,
+                                                                          student.zs)):
+        forced.update({f"b{bi}_z1": _nchw(z1, cw(i1)), f"b{bi}_h1": _nchw(h1, cw(i1)),
+                       f"b{bi}_z2": _nchw(z2, cw(i2)), f"b{bi}_y": _nchw(y, cw(i2))})
+        if isc is not None:
+            forced.update({f"b{bi}_zsc": _nchw(zsc, cw(isc)), f"b{bi}_sc": _nchw(sc, cw(isc))})
+    want_loss, want = ref.student_bn_loss_and_grads(net, imgs, labels, q, 0.5, 0.5, T, forced=forced)
+    assert abs(loss.item() - want_loss) <= 1e-3 * abs(want_loss)
+    worst = {}
+
+    def check(idx, gw):
+        p = student.params[idx]
+        dw, _ = _device_grad(student, idx)
+        cout = gw[1].shape[0]
+        worst[idx] = (_relnorm(dw, gw[0]), _relnorm(student._gg(p)[:cout].float().cpu(), gw[1]),
+                      _relnorm(student._gb(p)[:cout].float().cpu(), gw[2]))
+    check(0, want["stem"])
+    for (i1, i2, isc), (g1, g2, gs) in zip(student.block_idx, want["blocks"]):
+        check(i1, g1)
+        check(i2, g2)
+        if isc is not None:
+            check(isc, gs)
+    p = student.fc
+    gfc = student._gw(p).view(p.rows, p.cols)[:40, :student.feat_p].float().cpu()
+    assert _relnorm(gfc[:, :want["fc"][0].shape[1]], want["fc"][0]) < 3e-2
+    assert _relnorm(student._gb(p)[:40].float().cpu(), want["fc"][1]) < 3e-2
+    print("bn grad rel-norms (dW, dgamma, dbeta):", {k: tuple(round(float(x), 5) for x in v) for k, v in worst.items()})
+    assert max(max(v) for v in worst.values()) < 3e-2, worst
+
+
+@pytest.mark.parametrize("M,C", [(2048, 16), (777, 64), (4096, 512), (32, 512), (100352, 64)])
+def test_bn_kernels_vs_torch(M, C):
+    """edl_bn_stats / edl_bn_apply / edl_bn_bwd against torch's training-mode
+    batch_norm (fp64) on the same bf16 z and g: mean / rstd to 1e-5, y and dz
+    within a bf16 rounding, dgamma / dbeta to 1e-5 relative norm."""
+    from paper_2207_06667_b200 import _lib
+    g_ = torch.Generator().manual_seed(M + C)
+    z = (torch.randn(M, C, generator=g_) * 2 + 0.5).to(torch.bfloat16).cuda()
+    g = torch.randn(M, C, generator=g_).to(torch.bfloat16).cuda()
+    res = torch.randn(M, C, generator=g_).to(torch.bfloat16).cuda()
+    gamma = (torch.rand(C, generator=g_) + 0.5).cuda()
+    beta = torch.randn(C, generator=g_).cuda()
+    s = torch.cuda.current_stream().cuda_stream
+    wsn = int(_lib.load().edl_bn_workspace_floats(M, C))
+    ws = torch.empty(wsn, device="cuda")
+    mean, rstd = torch.empty(C, device="cuda"), torch.empty(C, device="cuda")
+    y = torch.empty(M, C, dtype=torch.bfloat16, device="cuda")
+    dgam, dbet = torch.empty(C, device="cuda"), torch.empty(C, device="cuda")
+    dz = torch.empty(M, C, dtype=torch.bfloat16, device="cuda")
+    _lib.call("edl_bn_stats_nhwc", z.data_ptr(), M, C, ws.data_ptr(), wsn, mean.data_ptr(), rstd.data_ptr(), 1e-5, s)
+    _lib.call("edl_bn_apply_nhwc", z.data_ptr(), M, C, mean.data_ptr(), rstd.data_ptr(), gamma.data_ptr(),
+              beta.data_ptr(), res.data_ptr(), 1, y.data_ptr(), s)
+    _lib.call("edl_bn_bwd_nhwc", g.data_ptr(), z.data_ptr(), M, C, mean.data_ptr(), rstd.data_ptr(),
+              gamma.data_ptr(), ws.data_ptr(), wsn, dgam.data_ptr(), dbet.data_ptr(), dz.data_ptr(), s)
+    torch.cuda.synchronize()
+    zd = z.double().cpu().requires_grad_(True)
+    gd, bd = gamma.double().cpu().requires_grad_(True), beta.double().cpu().requires_grad_(True)
+    yn = torch.nn.functional.batch_norm(zd.T.unsqueeze(0), None, None, gd, bd, training=True, eps=1e-5)[0].T
+    yref = torch.relu(yn + res.double().cpu())
+    yn.backward(g.double().cpu())
+    torch.testing.assert_close(mean.double().cpu(), zd.detach().mean(0), rtol=1e-5, atol=1e-5)
+    var = zd.detach().var(0, unbiased=False)
+    torch.testing.assert_close(rstd.double().cpu(), 1 / torch.sqrt(var + 1e-5), rtol=1e-4, atol=1e-5)
+    assert ((y.double().cpu() - yref).abs() <= 2 ** -8 * yref.abs() + 1e-3).all()
+    rel = lambda a, b: ((a - b).norm() / b.norm()).item()  # noqa: E731
+    assert rel(dbet.double().cpu(), bd.grad) < 1e-5 and rel(dgam.double().cpu(), gd.grad) < 1e-4
+    assert rel(dz.double().cpu(), zd.grad) < 1e-2
+
+
+@pytest.mark.parametrize("width,image", [(16, 32), (64, 64)])
+def test_resnet_student_bn_forward_statistics(width, image):
+    """After the forward, each BN layer's batch mean / rstd equal the torch
+    statistics of the device's own conv output z (fp64, biased variance),
+    and its output y = [relu](gamma xhat + beta [+ shortcut]) within a bf16
+    rounding of torch's on the device's own z."""
+    from paper_2207_06667_b200.resnet import ResNetStudent, StudentResNetConfig, init_student_resnet, to_nhwc
+    cfg = StudentResNetConfig(layers=(1, 1, 1, 1), width=width, classes=10, image=image, bn=True)
+    student = ResNetStudent(init_student_resnet(cfg, 2), "cuda", 6)
+    x = to_nhwc(np.random.default_rng(3).normal(size=(6, 3, image, image)).astype(np.float32), "cuda")
+    student.forward(x, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    layers = [(0, student.z0, student.y0, None, True)]
+    prev = student.x1
+    for (i1, i2, isc), (hw, h1, sc, y), (z1, z2, zsc) in zip(student.block_idx, student.acts, student.zs):
+        if isc is not None:
+            layers.append((isc, zsc, sc, None, False))
+        layers.append((i1, z1, h1, None, True))
+        layers.append((i2, z2, y, sc if isc is not None else prev, True))
+        prev = y
+    for i, z, y, res, relu in layers:
+        C = student.convs[i].cout_p
+        p = student.params[i]
+        zz = z.reshape(-1, C).double()
+        mean = zz.mean(0)
+        var = zz.var(0, unbiased=False)
+        torch.testing.assert_close(student.bn_stats[i, 0, :C].double(), mean, rtol=1e-5, atol=1e-5)
+        torch.testing.assert_close(student.bn_stats[i, 1, :C].double(), 1.0 / torch.sqrt(var + 1e-5),
+                                   rtol=1e-4, atol=1e-3)
+        ref_y = (zz - mean) / torch.sqrt(var + 1e-5) * student._g(p).double() + student._b(p).double()
+        if res is not None:
+            ref_y = ref_y + res.reshape(-1, C).double()
+        if relu:
+            ref_y = torch.relu(ref_y)
+        err = (y.reshape(-1, C).double() - ref_y).abs()
+        assert (err <= 2 ** -8 * ref_y.abs() + 1e-3).all(), (i, err.max().item())
 
 
 def test_resnet_student_sgd_updates_flat_master():
