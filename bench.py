@@ -830,8 +830,8 @@ def _cfg4_teacher_rate(dev, peak_sust, batch=256, iters=6, warmup=2):
 
 
 def _cfg4_student_rate(dev, peak_sust, batch=256, iters=6, warmup=2):
-    """cfg4 (BASELINE configs[3]) student: the BN-free ResNet-18-style KD
-    training step (forward, fused KD loss, implicit-GEMM weight / data
+    """cfg4 (BASELINE configs[3]) student: the ResNet-18-style KD training
+    step with training-mode BatchNorm after every conv (forward, fused KD loss, implicit-GEMM weight / data
     gradients, SGD) alone, and co-located with the ResNet-50-style teacher
     (online: the teacher's top-16 soft labels for the same batch, then the
     student step, one stream), 224^2 synthetic images, 1000 classes, random
@@ -846,7 +846,8 @@ def _cfg4_student_rate(dev, peak_sust, batch=256, iters=6, warmup=2):
     rng = np.random.default_rng(0)
     xs = [to_nhwc(rng.normal(size=(batch, 3, 224, 224)).astype(np.float32), dev) for _ in range(2)]
     ys = [torch.from_numpy(rng.integers(0, 1000, size=batch)).to(dev) for _ in range(2)]
-    out = {"model": "resnet18-style student (basic [2,2,2,2], width 64, BN-free) <- resnet50-style teacher, 224x224, "
+    out = {"model": "resnet18-style student (basic [2,2,2,2], width 64, training-mode BatchNorm) <- resnet50-style teacher, "
+                    "224x224, "
                     "1000 classes, top-16 soft labels, alpha = beta = 0.5, T = 2", "batch": batch}
     for name, with_teacher in (("student_only", False), ("online_colocated", True)):
         def step(i):

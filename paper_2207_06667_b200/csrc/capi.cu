@@ -345,6 +345,30 @@ unsigned* stream_sched(cudaStream_t s) {
   return p;
 }
 
+// Per-(device, stream) arrival tickets for the one-launch BatchNorm
+// reductions (bn.cu): zero at rest, reset by each launch's last cluster.
+__device__ unsigned g_ticket_pool[kSchedSlots];
+std::mutex g_ticket_mu;
+std::unordered_map<std::string, unsigned*> g_ticket;
+std::unordered_map<int, int> g_ticket_used;
+
+unsigned* stream_ticket(cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  char key[64];
+  snprintf(key, sizeof(key), "%d:%p", dev, static_cast<void*>(s));
+  std::lock_guard<std::mutex> g(g_ticket_mu);
+  auto it = g_ticket.find(key);
+  if (it != g_ticket.end()) return it->second;
+  int& used = g_ticket_used[dev];
+  if (used >= kSchedSlots) return nullptr;   // a separate finishing launch
+  void* base = nullptr;
+  if (cudaGetSymbolAddress(&base, g_ticket_pool) != cudaSuccess) return nullptr;
+  unsigned* p = static_cast<unsigned*>(base) + used++;
+  g_ticket.emplace(key, p);
+  return p;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1104,7 +1128,7 @@ static int bn_check(int M, int C, const char* what) {
 }
 
 long long edl_bn_workspace_floats(int M, int C) {
-  return 2LL * bn_partial_blocks(M < 1 ? 1 : M, num_sms()) * C;
+  return bn_partial_floats(M < 1 ? 1 : M, C < 8 ? 8 : C, num_sms());
 }
 
 int edl_bn_stats_nhwc(const void* z, int M, int C, float* workspace, long long ws_floats, float* mean, float* rstd,
@@ -1112,8 +1136,8 @@ int edl_bn_stats_nhwc(const void* z, int M, int C, float* workspace, long long w
   if (int rc = bn_check(M, C, "bn_stats")) return rc;
   if (ws_floats < edl_bn_workspace_floats(M, C)) return fail(EDL_ERR_SHAPE, "bn_stats: workspace too small");
   if (!(eps > 0.f)) return fail(EDL_ERR_PARAM, "bn_stats: eps %g", eps);
-  cudaError_t e = launch_bn_stats(static_cast<const __nv_bfloat16*>(z), M, C, workspace, mean, rstd, eps, num_sms(),
-                                  as_stream(stream));
+  cudaError_t e = launch_bn_stats(static_cast<const __nv_bfloat16*>(z), M, C, workspace,
+                                  stream_ticket(as_stream(stream)), mean, rstd, eps, num_sms(), as_stream(stream));
   return e == cudaSuccess ? 0 : cuda_fail(e, "bn_stats");
 }
 
@@ -1133,8 +1157,8 @@ int edl_bn_bwd_nhwc(const void* g, const void* z, int M, int C, const float* mea
   if (ws_floats < edl_bn_workspace_floats(M, C)) return fail(EDL_ERR_SHAPE, "bn_bwd: workspace too small");
   const auto* gg = static_cast<const __nv_bfloat16*>(g);
   const auto* zz = static_cast<const __nv_bfloat16*>(z);
-  cudaError_t e = launch_bn_bwd_reduce(gg, zz, M, C, mean, rstd, workspace, dbeta, dgamma, num_sms(),
-                                       as_stream(stream));
+  cudaError_t e = launch_bn_bwd_reduce(gg, zz, M, C, mean, rstd, workspace, stream_ticket(as_stream(stream)), dbeta,
+                                       dgamma, num_sms(), as_stream(stream));
   if (e == cudaSuccess)
     e = launch_bn_bwd_apply(gg, zz, M, C, mean, rstd, gamma, dbeta, dgamma, static_cast<__nv_bfloat16*>(dz),
                             num_sms(), as_stream(stream));

@@ -184,13 +184,15 @@ cudaError_t launch_maxpool_bwd_nhwc(const __nv_bfloat16* x, int N, int H, int W,
                                     __nv_bfloat16* dx, cudaStream_t stream);
 
 // training-mode BatchNorm (bn.cu): z / g NHWC bf16 rows [M][C], C % 8 == 0, C <= 2048;
-// partial: 2 * bn_partial_blocks(M, sms) * C floats
-int bn_partial_blocks(int M, int sms);
-cudaError_t launch_bn_stats(const __nv_bfloat16* z, int M, int C, float* partial, float* mean, float* rstd,
-                            float eps, int sms, cudaStream_t stream);
+// partial: bn_partial_floats(M, C, sms) floats (fp64 per-cluster partials);
+// ticket: a zeroed per-stream counter (left zeroed), or nullptr for a
+// separate finishing launch
+long long bn_partial_floats(int M, int C, int sms);
+cudaError_t launch_bn_stats(const __nv_bfloat16* z, int M, int C, float* partial, unsigned* ticket, float* mean,
+                            float* rstd, float eps, int sms, cudaStream_t stream);
 cudaError_t launch_bn_bwd_reduce(const __nv_bfloat16* g, const __nv_bfloat16* z, int M, int C, const float* mean,
-                                 const float* rstd, float* partial, float* dbeta, float* dgamma, int sms,
-                                 cudaStream_t stream);
+                                 const float* rstd, float* partial, unsigned* ticket, float* dbeta, float* dgamma,
+                                 int sms, cudaStream_t stream);
 cudaError_t launch_bn_apply(const __nv_bfloat16* z, int M, int C, const float* mean, const float* rstd,
                             const float* gamma, const float* beta, const __nv_bfloat16* res, bool relu,
                             __nv_bfloat16* y, int sms, cudaStream_t stream);

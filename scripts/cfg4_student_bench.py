@@ -1,4 +1,5 @@
-"""cfg4 student timing: the BN-free ResNet-18-style KD step alone and the
+"""cfg4 student timing: the ResNet-18-style KD step (training-mode BN;
+CFG4_BN=0 for the BN-free variant) alone and the
 co-located (online) teacher ResNet-50 -> student step, at a few batch sizes.
 
     python scripts/cfg4_student_bench.py                 # timings
@@ -17,7 +18,8 @@ from paper_2207_06667_b200.resnet import (ResNetConfig, ResNetStudent, ResNetTea
 
 
 def run(B, iters=6, warmup=2, with_teacher=False, profile=False):
-    st = ResNetStudent(init_student_resnet(StudentResNetConfig(), 0), "cuda", B)
+    bn = os.environ.get("CFG4_BN", "1") != "0"
+    st = ResNetStudent(init_student_resnet(StudentResNetConfig(bn=bn), 0), "cuda", B)
     te = ResNetTeacher(init_resnet(ResNetConfig(), 1), "cuda", B) if with_teacher else None
     rng = np.random.default_rng(0)
     xs = [to_nhwc(rng.normal(size=(B, 3, 224, 224)).astype(np.float32), "cuda") for _ in range(2)]
@@ -42,7 +44,7 @@ def run(B, iters=6, warmup=2, with_teacher=False, profile=False):
     torch.cuda.synchronize()
     t = s.elapsed_time(e) / 1e3 / iters
     flop = st.flops_per_sample() + (te.flops_per_sample() if te is not None else 0.0)
-    return {"B": B, "teacher": with_teacher, "samples_per_s": round(B / t, 1), "ms": round(t * 1e3, 3),
+    return {"B": B, "bn": bn, "teacher": with_teacher, "samples_per_s": round(B / t, 1), "ms": round(t * 1e3, 3),
             "tflops": round(B * flop / t / 1e12, 1), "gflop_per_sample": round(flop / 1e9, 3),
             "loss": round(float(loss.item()), 4)}
 

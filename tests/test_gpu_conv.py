@@ -263,11 +263,14 @@ def test_resnet_student_bn_grads_vs_torch_autograd(width, B):
     assert max(max(v) for v in worst.values()) < 3e-2, worst
 
 
-@pytest.mark.parametrize("M,C", [(2048, 16), (777, 64), (4096, 512), (32, 512), (100352, 64)])
+@pytest.mark.parametrize("M,C", [(2048, 16), (777, 64), (4096, 512), (32, 512), (100352, 64), (300, 24),
+                                 (1000, 264), (64, 2048), (802816, 64)])
 def test_bn_kernels_vs_torch(M, C):
     """edl_bn_stats / edl_bn_apply / edl_bn_bwd against torch's training-mode
     batch_norm (fp64) on the same bf16 z and g: mean / rstd to 1e-5, y and dz
-    within a bf16 rounding, dgamma / dbeta to 1e-5 relative norm."""
+    within a bf16 rounding, dgamma / dbeta to 1e-5 relative norm. The
+    one-launch cluster reductions are deterministic: a second run on another
+    stream (its own ticket counter) is bitwise equal."""
     from paper_2207_06667_b200 import _lib
     g_ = torch.Generator().manual_seed(M + C)
     z = (torch.randn(M, C, generator=g_) * 2 + 0.5).to(torch.bfloat16).cuda()
@@ -288,6 +291,21 @@ def test_bn_kernels_vs_torch(M, C):
     _lib.call("edl_bn_bwd_nhwc", g.data_ptr(), z.data_ptr(), M, C, mean.data_ptr(), rstd.data_ptr(),
               gamma.data_ptr(), ws.data_ptr(), wsn, dgam.data_ptr(), dbet.data_ptr(), dz.data_ptr(), s)
     torch.cuda.synchronize()
+    first = [t.clone() for t in (mean, rstd, y, dgam, dbet, dz)]
+    other = torch.cuda.Stream()
+    with torch.cuda.stream(other):
+        so = other.cuda_stream
+        for t in (mean, rstd, y, dgam, dbet, dz):
+            t.zero_()
+        _lib.call("edl_bn_stats_nhwc", z.data_ptr(), M, C, ws.data_ptr(), wsn, mean.data_ptr(), rstd.data_ptr(), 1e-5,
+                  so)
+        _lib.call("edl_bn_apply_nhwc", z.data_ptr(), M, C, mean.data_ptr(), rstd.data_ptr(), gamma.data_ptr(),
+                  beta.data_ptr(), res.data_ptr(), 1, y.data_ptr(), so)
+        _lib.call("edl_bn_bwd_nhwc", g.data_ptr(), z.data_ptr(), M, C, mean.data_ptr(), rstd.data_ptr(),
+                  gamma.data_ptr(), ws.data_ptr(), wsn, dgam.data_ptr(), dbet.data_ptr(), dz.data_ptr(), so)
+    torch.cuda.synchronize()
+    for a, b in zip(first, (mean, rstd, y, dgam, dbet, dz)):
+        assert torch.equal(a, b)
     zd = z.double().cpu().requires_grad_(True)
     gd, bd = gamma.double().cpu().requires_grad_(True), beta.double().cpu().requires_grad_(True)
     yn = torch.nn.functional.batch_norm(zd.T.unsqueeze(0), None, None, gd, bd, training=True, eps=1e-5)[0].T
