@@ -93,6 +93,8 @@ _SIGNATURES = {
     "edl_cast_bf16": [c_void_p, c_ll, c_void_p, c_ll, c_int, c_int, c_void_p],
     "edl_cast_bf16_f64": [c_void_p, c_ll, c_void_p, c_ll, c_int, c_int, c_void_p],
     "edl_stream_delay_ns": [c_ll, c_void_p],
+    "edl_halo_probe": [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_int, c_int, c_int,
+                       c_void_p, c_void_p],
     "edl_bn_workspace_floats": [c_int, c_int],
     "edl_bn_stats_nhwc": [c_void_p, c_int, c_int, c_void_p, c_ll, c_void_p, c_void_p, c_float, c_void_p],
     "edl_bn_apply_nhwc": [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p,
@@ -170,7 +172,7 @@ _LAUNCHES = {"edl_linear_bwd_weight": 3,   # GEMM + two column-sum passes when d
              "edl_linear_bwd_weight_ws": 4,   # split-K GEMM + reduce + two column-sum passes (at most)
              "edl_conv_bwd_weight_nhwc": 4,   # the same plan with an im2col operand
              "edl_kd_loss_fwd_bwd": 2,     # row pass + deterministic batch-mean pass
-             "edl_bn_stats_nhwc": 2, "edl_bn_bwd_nhwc": 3,
+             "edl_bn_stats_nhwc": 1, "edl_bn_bwd_nhwc": 2,
              "edl_linear_kd_loss_fwd_bwd": 2,   # fused logit GEMM + loss/dz, batch-mean pass
              "edl_stream_wait_geq": 0,     # stream memory ops, not kernels
              "edl_stream_write_u32": 0,

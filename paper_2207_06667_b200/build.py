@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libedl_b200.so")
-SOURCES = ["gemm_sm100.cu", "kernels.cu", "exchange.cu", "conv.cu", "bn.cu", "capi.cu"]
+SOURCES = ["gemm_sm100.cu", "kernels.cu", "exchange.cu", "conv.cu", "bn.cu", "halo.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

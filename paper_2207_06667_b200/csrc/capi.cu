@@ -150,6 +150,50 @@ int conv_map(const void* x, int N, int H, int W, int C, int R, int S, int stride
   return 0;
 }
 
+// 5-D tiled map of an NHWC bf16 tensor with C = 64 for the halo conv
+// (halo.cu): dims {8 channels, W, H, N, C/8 chunks}, the chunk dimension at a
+// 16-byte stride, so a box {8, W + 2, rows, 1, 8} lands in shared memory as
+// [chunk][row][pixel][8 channels] — the no-swizzle K-major core-matrix layout.
+// Boxes starting at w = -1 / h = -1 read the TMA's zero fill.
+int halo_map(const void* x, int N, int H, int W, int C, int box_rows, CUtensorMap* out) {
+  auto fn = encode_fn();
+  if (!fn) return fail(EDL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || C != 64 || W + 2 > 256 || box_rows > 256)
+    return fail(EDL_ERR_SHAPE, "halo map: C must be 64 and W + 2 <= 256 (C=%d W=%d)", C, W);
+  cuuint64_t dims[5] = {8, static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H), static_cast<cuuint64_t>(N),
+                        static_cast<cuuint64_t>(C / 8)};
+  cuuint64_t strides[4] = {static_cast<cuuint64_t>(C) * 2, static_cast<cuuint64_t>(W) * C * 2,
+                           static_cast<cuuint64_t>(H) * W * C * 2, 16};
+  cuuint32_t box[5] = {8, static_cast<cuuint32_t>(W + 2), static_cast<cuuint32_t>(box_rows), 1,
+                       static_cast<cuuint32_t>(C / 8)};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(x), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(EDL_ERR_CUDA, "halo map: cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+  return 0;
+}
+
+// 4-D tiled map of an NHWC bf16 tensor with C = 64: box {64, box_w, rows, 1},
+// SWIZZLE_128B — pixel rows of 128 B in the K-major operand layout.
+int halo_map_sw128(const void* x, int N, int H, int W, int C, int box_w, int box_rows, CUtensorMap* out) {
+  auto fn = encode_fn();
+  if (!fn) return fail(EDL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || C != 64 || W + 2 > 256 || box_rows > 256)
+    return fail(EDL_ERR_SHAPE, "halo map: C must be 64 and W + 2 <= 256 (C=%d W=%d)", C, W);
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+                        static_cast<cuuint64_t>(N)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(C) * 2, static_cast<cuuint64_t>(W) * C * 2,
+                           static_cast<cuuint64_t>(H) * W * C * 2};
+  cuuint32_t box[4] = {static_cast<cuuint32_t>(C), static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_rows), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(EDL_ERR_CUDA, "halo map: cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+  return 0;
+}
+
 int tensor_map(const void* ptr, long long rows, long long cols, long long ld, int box0, int box1,
                CUtensorMap* out) {
   return tensor_map_ex(ptr, rows, cols, ld, box0, box1, kOperandBf16, out);
@@ -432,6 +476,67 @@ int edl_linear_fwd(const void* X, long long ldx, const void* W, long long ldw, c
   return e == cudaSuccess ? 0 : cuda_fail(e, "linear_fwd");
 }
 
+// The halo-tiled conv (halo.cu) for 3x3 / stride 1 / pad 1 convolutions with
+// 64 input and 64 output channels and W <= 62 (>= 2 output rows per tile; the
+// cfg4 stage-1 layers and their data gradients); EDL_HALO=0 keeps them on the
+// TMA im2col GEMM (A/B runs).
+bool halo_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("EDL_HALO");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+int halo_conv(const void* x, int N, int H, int W, const void* w, long long ldw, const float* bias, const void* res,
+              const void* mask, bool relu, void* out, cudaStream_t st) {
+  CUtensorMap mx, mw, my, mr{}, mm{};
+  const int R = halo_rows_per_tile(W);
+  if (int rc = halo_map_sw128(x, N, H, W, 64, W + 2, R + 2, &mx)) return rc;
+  if (int rc = halo_map_sw128(out, N, H, W, 64, W, R, &my)) return rc;
+  if (res != nullptr)
+    if (int rc = halo_map_sw128(res, N, H, W, 64, W, R, &mr)) return rc;
+  if (mask != nullptr)
+    if (int rc = halo_map_sw128(mask, N, H, W, 64, W, R, &mm)) return rc;
+  if (int rc = tensor_map(w, 64, 9 * 64, ldw, 64, 64, &mw)) return rc;
+  HaloArgs a{};
+  a.N = N; a.H = H; a.W = W; a.R = R;
+  a.tiles_per_image = (H + R - 1) / R;
+  a.tiles = N * a.tiles_per_image;
+  a.bias = bias;
+  a.res = static_cast<const __nv_bfloat16*>(res);
+  a.mask = static_cast<const __nv_bfloat16*>(mask);
+  a.relu = relu ? 1 : 0;
+  a.out = static_cast<__nv_bfloat16*>(out);
+  static const int dbg = [] {
+    const char* v = getenv("EDL_HALO_DEBUG");
+    return v ? atoi(v) : 0;
+  }();
+  a.debug = dbg;
+  const int cap = grid_cap(st);
+  const int grid = a.tiles < cap ? a.tiles : cap;
+  cudaError_t e = launch_halo_conv(mx, mw, my, mr, mm, a, grid, st);
+  return e == cudaSuccess ? 0 : cuda_fail(e, "halo_conv");
+}
+
+// Layout probe for the halo conv (tests only): one tap's 128 x 64 product
+// from the staged patch of image n, rows h0-1 .. h0+2, shifted by `off` rows.
+int edl_halo_probe(const void* x, int N, int H, int W, int n, int h0, int off, const void* w, int mode, int reps,
+                   int smem_kb, float* out, void* stream) {
+  if (off < 0 || off + 128 > 256 || n < 0 || n >= N || mode < 0 || mode > 3 || reps < 0)
+    return fail(EDL_ERR_SHAPE, "halo_probe: bad arguments");
+  CUtensorMap mx, mw;
+  if (mode == 0) {
+    if (int rc = halo_map(x, N, H, W, 64, 4, &mx)) return rc;
+  } else {
+    if (int rc = halo_map_sw128(x, N, H, W, 64, W + 2, 4, &mx)) return rc;
+  }
+  if (int rc = tensor_map(w, 64, mode == 3 ? 576 : 64, mode == 3 ? 576 : 64, 64, 64, &mw)) return rc;
+  if (smem_kb < 0 || smem_kb > 227) return fail(EDL_ERR_SHAPE, "halo_probe: smem_kb");
+  cudaError_t e = launch_halo_probe(mx, mw, n, h0, W, off, mode, reps, smem_kb, out, as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "halo_probe");
+}
+
 int edl_conv_fwd_nhwc(const void* x, int N, int H, int W, int C, const void* w, long long ldw, const float* bias,
                       int K, int R, int S, int stride, int pad, const void* residual, long long ldr, void* y,
                       long long ldy, int act, void* stream) {
@@ -448,6 +553,9 @@ int edl_conv_fwd_nhwc(const void* x, int N, int H, int W, int C, const void* w, 
     return fail(EDL_ERR_SHAPE, "conv_fwd_nhwc: bad leading dimension");
   const int M = static_cast<int>(Ml);
   cudaStream_t st = as_stream(stream);
+  if (C == 64 && K == 64 && R == 3 && S == 3 && stride == 1 && pad == 1 && W + 2 <= 64 && ldy == 64 &&
+      (!residual || ldr == 64) && halo_enabled())
+    return halo_conv(x, N, H, W, w, ldw, bias, residual, nullptr, act == EDL_ACT_RELU, y, st);
   const int cap = grid_cap(st);
   CUtensorMap ta, tb, ty;
   int rc;
@@ -494,6 +602,8 @@ int edl_conv_dgrad_nhwc(const void* dz, int N, int P, int Q, int K, const void* 
   if (Ml > (1LL << 31) - 256) return fail(EDL_ERR_SHAPE, "conv_dgrad_nhwc: too many pixels");
   const int M = static_cast<int>(Ml), Kd = R * S * K;
   cudaStream_t st = as_stream(stream);
+  if (C == 64 && K == 64 && R == 3 && S == 3 && pd == 1 && Q + 2 <= 64 && halo_enabled())
+    return halo_conv(dz, N, P, Q, wf, ldf, nullptr, add, mask, false, dx, st);
   const int cap = grid_cap(st);
   CUtensorMap ta, tb, ty;
   int rc;

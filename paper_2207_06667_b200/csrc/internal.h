@@ -183,6 +183,25 @@ cudaError_t launch_maxpool_bwd_nhwc(const __nv_bfloat16* x, int N, int H, int W,
                                     int P, int Q, const __nv_bfloat16* dy, const __nv_bfloat16* mask,
                                     __nv_bfloat16* dx, cudaStream_t stream);
 
+// halo-tiled 3x3 convolution (halo.cu): C = K = 64, stride 1, pad 1, W + 2 <= 128;
+// out = [relu](conv + bias [+ res]), then * (mask > 0) when mask is given
+struct HaloArgs {
+  int N, H, W, R;                   // R output rows per 128-row tile (128 / (W + 2))
+  int tiles_per_image, tiles;
+  const float* bias;
+  const __nv_bfloat16* res;
+  const __nv_bfloat16* mask;
+  int relu;
+  __nv_bfloat16* out;
+  int debug;                        // timing experiments (EDL_HALO_DEBUG): 1 no epilogue math / stores, 2 one patch load
+};
+int halo_rows_per_tile(int W);
+cudaError_t launch_halo_conv(const CUtensorMap& tmX, const CUtensorMap& tmW, const CUtensorMap& tmY,
+                             const CUtensorMap& tmR, const CUtensorMap& tmM, const HaloArgs& a, int grid,
+                             cudaStream_t stream);
+cudaError_t launch_halo_probe(const CUtensorMap& tmX, const CUtensorMap& tmW, int n, int h0, int W, int off, int mode,
+                              int reps, int smem_kb, float* out, cudaStream_t stream);
+
 // training-mode BatchNorm (bn.cu): z / g NHWC bf16 rows [M][C], C % 8 == 0, C <= 2048;
 // partial: bn_partial_floats(M, C, sms) floats (fp64 per-cluster partials);
 // ticket: a zeroed per-stream counter (left zeroed), or nullptr for a
