@@ -102,7 +102,10 @@ int edl_avgpool_nhwc(const void* x, int N, int HW, int C, void* out, long long l
  * (+ residual[(n,p,q)][k])). The tcgen05 GEMM's producer loads its A tiles
  * straight from x with TMA im2col loads (one filter tap x 64 channels per
  * k-block): no column matrix in HBM. act: EDL_ACT_RELU or EDL_ACT_IDENT;
- * residual (optional) needs EDL_ACT_RELU. y: [N*P*Q][ldy], TMA-stored. */
+ * residual (optional) needs EDL_ACT_RELU. y: [N*P*Q][ldy], TMA-stored.
+ * C == K == 64, 3x3, stride 1, pad 1, W <= 62 (the stage-1 layers) runs the
+ * halo-tiled conv instead: one TMA patch per two output rows, the nine taps
+ * as row-shifted views of it (bitwise equal; EDL_HALO=0 disables). */
 int edl_conv_fwd_nhwc(const void* x, int N, int H, int W, int C, const void* w, long long ldw, const float* bias,
                       int K, int R, int S, int stride, int pad, const void* residual, long long ldr, void* y,
                       long long ldy, int act, void* stream);
@@ -124,6 +127,16 @@ int edl_conv_bwd_weight_nhwc(const void* x, int N, int H, int W, int C, int R, i
  * output. Replaces edl_linear_bwd_data + edl_col2im_nhwc for stride 1. */
 int edl_conv_flip_weights(const void* w, long long ldw, int K, int C, int R, int S, void* wf, long long ldf,
                           void* stream);
+/* Layout probe for the halo conv (diagnostics and tests only): the 128 x 64
+ * product of one tap's row-shifted view of the staged patch of image n (rows
+ * h0-1 .. h0+2) with w [64][64] (mode 3: [64][576], nine taps), into out
+ * [128][64] fp32; mode 0: no-swizzle chunk-plane layout, 1: SWIZZLE_128B with
+ * the descriptor base offset (wrong by design), 2: SWIZZLE_128B. reps > 0:
+ * issue the 9-tap sequence reps % 1000 times (odd thousands digit: on 148
+ * CTAs) and store the cycle count in out[128 * 64]; smem_kb > 0 sets the
+ * dynamic shared memory. x: NHWC bf16 with C = 64. */
+int edl_halo_probe(const void* x, int N, int H, int W, int n, int h0, int off, const void* w, int mode, int reps,
+                   int smem_kb, float* out, void* stream);
 int edl_conv_dgrad_nhwc(const void* dz, int N, int P, int Q, int K, const void* wf, long long ldf, int C, int R,
                         int S, int pad, const void* add, const void* mask, void* dx, void* stream);
 

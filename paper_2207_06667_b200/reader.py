@@ -267,6 +267,7 @@ class DistilReader:
         # recycled only once the event has completed
         self._retired: list[tuple[_Slot, torch.cuda.Event | None]] = []
         self._pending: deque[int] = deque()
+        self._waiting_for: int | None = None    # the iteration consume() is blocked on
         self._next_new = start_iteration
         self._end = end_iteration
         self._consumed: set[int] = set()
@@ -351,8 +352,18 @@ class DistilReader:
         slot.batch_filled = False
         return slot
 
+    def _demanded(self) -> bool:
+        """The consumer is blocked on an iteration that nobody is computing: a
+        failed teacher's unanswered batch, re-queued at the head of _pending.
+        Alg. 1's hysteresis may have stopped sending (the buffer holds the
+        LATER iterations that did arrive), and the buffer cannot drain past the
+        missing one, so that one batch is dispatched regardless (the reference,
+        edl/student_node.py:351-376, waits for the volume to drain and hangs in
+        this case; the iteration ledger is unchanged)."""
+        return self._waiting_for is not None and bool(self._pending) and self._pending[0] == self._waiting_for
+
     def _dispatch(self) -> None:
-        while not self._stopped and self.sending_enabled and self._have_work():
+        while not self._stopped and self._have_work() and (self.sending_enabled or self._demanded()):
             out = {nid: len(h.outstanding) for nid, h in self._teachers.items() if not h.dead}
             target = pick_teacher(out, self.cfg.pipeline_depth)
             if target is None:
@@ -442,17 +453,21 @@ class DistilReader:
             self._free.append(self._last_consumed)
             self._last_consumed = None
         self.pump()
-        while iteration not in self._ready:
-            if self._stopped:
-                raise RuntimeError("reader stopped while waiting for soft labels")
-            if deadline is not None and time.monotonic() > deadline:
-                raise TimeoutError(f"no soft labels for iteration {iteration}")
-            slot = self._inflight_slot(iteration)
-            if slot is not None and slot.done is not None:
-                slot.done.synchronize()     # blocking wait only when the buffer is empty
-            else:
-                time.sleep(0.0002)
-            self.pump()
+        self._waiting_for = iteration
+        try:
+            while iteration not in self._ready:
+                if self._stopped:
+                    raise RuntimeError("reader stopped while waiting for soft labels")
+                if deadline is not None and time.monotonic() > deadline:
+                    raise TimeoutError(f"no soft labels for iteration {iteration}")
+                slot = self._inflight_slot(iteration)
+                if slot is not None and slot.done is not None:
+                    slot.done.synchronize()     # blocking wait only when the buffer is empty
+                else:
+                    time.sleep(0.0002)
+                self.pump()
+        finally:
+            self._waiting_for = None
         slot = self._ready.pop(iteration)
         self._consumed.add(iteration)
         self.consume_count[iteration] = self.consume_count.get(iteration, 0) + 1

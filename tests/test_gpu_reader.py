@@ -97,6 +97,38 @@ def test_kill_teacher_with_inflight_redispatches_exactly_unanswered(cluster):
     reader.close()
 
 
+def test_head_of_line_unanswered_is_dispatched_while_sending_is_stopped(cluster):
+    """A slow teacher holds the lowest iterations while a fast one fills the
+    buffer past ut (sending stops); the slow one dies with no replacement.
+    The buffer cannot drain past the missing head-of-line batch, so the
+    reader dispatches exactly that batch to the survivor despite the stop
+    (the reference would wait forever here: edl/student_node.py:351-376)."""
+    import time
+
+    from paper_2207_06667_b200.reader import SchedulerConfig
+    from paper_2207_06667_b200.teacher import TeacherConfig, TeacherWorker
+    pool, spawn, make_reader, _ = cluster
+    fast = spawn("t2")
+    slow = TeacherWorker(TeacherConfig("t1", 2.0, 4, simulated_delay=0.5), cluster[3], fast.data)
+    pool.register(slow)
+    sched = SchedulerConfig(lt=2, ut=5, probe_interval=0.0, acquire_cooldown=1e9, pipeline_depth=2)
+    reader, events, _ = make_reader(end=16, sched=sched)
+    assert reader.acquire(2) == 2
+    t0 = time.monotonic()
+    while reader.sending_enabled and time.monotonic() - t0 < 10:
+        reader.pump()
+        time.sleep(0.001)
+    assert not reader.sending_enabled
+    assert 0 not in reader._ready and 0 in reader._teachers["t1"].outstanding
+    slow.stop()
+    for i in range(16):
+        reader.consume(i, timeout=10)
+    kinds = [e["event"] for e in events.entries]
+    assert "teacher_failure" in kinds and "no_replacement" in kinds
+    assert reader.ledger()["ok"]
+    reader.close()
+
+
 def test_kill_idle_teacher_acquires_exactly_one_replacement(cluster):
     pool, spawn, make_reader, _ = cluster
     idle = spawn("t1")
