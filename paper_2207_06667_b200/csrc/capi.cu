@@ -436,6 +436,18 @@ int edl_set_stream_max_ctas(void* stream, int max_ctas) {
   return 0;
 }
 
+// bf16 conv-layer epilogues on 256-wide pair tiles store (and read their
+// residual) in 64 x 32 SWIZZLE_128B boxes: 128-byte box rows, half the TMA
+// row walk of 32 x 32 boxes (profiles/README.md finding 41). EDL_W128=0
+// keeps the 32 x 32 path for A/B runs.
+static bool w128_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("EDL_W128");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 int edl_linear_fwd(const void* X, long long ldx, const void* W, long long ldw, const float* bias,
                    void* Y, long long ldy, int M, int N, int K, int act, void* stream) {
   if (M < 1 || N < 1 || K < 1 || ldx < K || ldw < K || ldy < N)
@@ -462,12 +474,14 @@ int edl_linear_fwd(const void* X, long long ldx, const void* W, long long ldw, c
   // (profiles/r02_layer2_raster.txt)
   ep.l2hint = l2hint_env >= 0 ? l2hint_env : (static_cast<long long>(M) * K * 2 > (32ll << 20) ? 1 : 0);
   CUtensorMap ty;
-  if ((rc = tensor_map_out(Y, M, N, ldy, act == EDL_ACT_NONE, &ty))) return rc;
   const int pbn = pick_pair_bn(M, N, cap);
+  const bool w128 = pbn == 256 && (act == EDL_ACT_RELU || act == EDL_ACT_IDENT) && w128_enabled();
+  if ((rc = w128 ? tensor_map(Y, M, N, ldy, 64, 32, &ty) : tensor_map_out(Y, M, N, ldy, act == EDL_ACT_NONE, &ty)))
+    return rc;
   cudaError_t e;
   if (pbn > 0) {
     if ((rc = tensor_map(W, N, K, ldw, 64, pbn / 2, &tb))) return rc;
-    e = launch_gemm_pair(kind, pbn, ta, tb, ty, M, N, K, ep, cap, as_stream(stream));
+    e = launch_gemm_pair(kind, pbn, ta, tb, ty, M, N, K, ep, cap, as_stream(stream), nullptr, w128);
   } else {
     const int bn = pick_bn_cap(M, N, cap);
     if ((rc = tensor_map(W, N, K, ldw, 64, bn, &tb))) return rc;
@@ -569,7 +583,13 @@ int edl_conv_fwd_nhwc(const void* x, int N, int H, int W, int C, const void* w, 
   if (residual && (rc = tensor_map_out(residual, M, K, ldr, false, &tr))) return rc;
   const int pbn = pick_pair_bn(M, K, cap);
   cudaError_t e;
-  if (pbn > 0) {
+  if (pbn == 256 && w128_enabled()) {
+    CUtensorMap ty2, tr2;
+    if ((rc = tensor_map(y, M, K, ldy, 64, 32, &ty2))) return rc;
+    if (residual && (rc = tensor_map(residual, M, K, ldr, 64, 32, &tr2))) return rc;
+    if ((rc = tensor_map(w, K, Kd, ldw, 64, pbn / 2, &tb))) return rc;
+    e = launch_gemm_pair(kind, pbn, ta, tb, ty2, M, K, Kd, ep, cap, st, residual ? &tr2 : nullptr, true);
+  } else if (pbn > 0) {
     if ((rc = tensor_map(w, K, Kd, ldw, 64, pbn / 2, &tb))) return rc;
     e = launch_gemm_pair(kind, pbn, ta, tb, ty, M, K, Kd, ep, cap, st, residual ? &tr : nullptr);
   } else {
@@ -635,15 +655,16 @@ int edl_linear_fwd_residual(const void* X, long long ldx, const void* W, long lo
   CUtensorMap ta, tb, ty;
   int rc;
   if ((rc = tensor_map(X, M, K, ldx, 64, 128, &ta))) return rc;
-  if ((rc = tensor_map_out(Y, M, N, ldy, false, &ty))) return rc;
+  const int pbn = pick_pair_bn(M, N, cap);
+  const bool w128 = pbn == 256 && w128_enabled();
+  if ((rc = w128 ? tensor_map(Y, M, N, ldy, 64, 32, &ty) : tensor_map_out(Y, M, N, ldy, false, &ty))) return rc;
   EpiArgs ep{Y, ldy, bias, reinterpret_cast<const __nv_bfloat16*>(R), ldr, 1.0f, stream_sched(as_stream(stream))};
   CUtensorMap tr;
-  if ((rc = tensor_map_out(R, M, N, ldr, false, &tr))) return rc;
-  const int pbn = pick_pair_bn(M, N, cap);
+  if ((rc = w128 ? tensor_map(R, M, N, ldr, 64, 32, &tr) : tensor_map_out(R, M, N, ldr, false, &tr))) return rc;
   cudaError_t e;
   if (pbn > 0) {
     if ((rc = tensor_map(W, N, K, ldw, 64, pbn / 2, &tb))) return rc;
-    e = launch_gemm_pair(GemmKind::FwdRelu, pbn, ta, tb, ty, M, N, K, ep, cap, as_stream(stream), &tr);
+    e = launch_gemm_pair(GemmKind::FwdRelu, pbn, ta, tb, ty, M, N, K, ep, cap, as_stream(stream), &tr, w128);
   } else {
     const int bn = pick_bn_cap(M, N, cap);
     if ((rc = tensor_map(W, N, K, ldw, 64, bn, &tb))) return rc;

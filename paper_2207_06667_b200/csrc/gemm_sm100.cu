@@ -541,28 +541,118 @@ __device__ __forceinline__ void stage_chunk(uint8_t* stg, int lane, const float 
 // (count & 1), phase (count >> 1) & 1.
 struct ResStream {
   const CUtensorMap* map;
-  uint8_t* stg;
-  uint64_t* bar;      // this warp's two barriers
+  uint8_t* rbuf;      // slot b at rbuf + b * stride
+  uint32_t stride;
+  uint64_t* bar;      // this warp's `depth` barriers
+  uint32_t depth;     // boxes in flight
+  uint32_t bytes;     // box bytes: 2048 (32 x 32, SWIZZLE_64B) or 4096 (64 x 32, SWIZZLE_128B)
   uint32_t ri, rc;
   __device__ __forceinline__ void issue(int lane, int col, int row0) {
-    const uint32_t b = ri & 1;
+    const uint32_t b = ri % depth;
     if (lane == 0) {
-      mbar_arrive_expect_tx(&bar[b], 2048);
-      tma_load_2d(stg + b * 4096 + 2048, map, &bar[b], col, row0);
+      mbar_arrive_expect_tx(&bar[b], bytes);
+      tma_load_2d(rbuf + b * stride, map, &bar[b], col, row0);
     }
     ++ri;
   }
-  // this lane's row of the next chunk (bf16 SWIZZLE_64B: 16-byte unit i at i ^ ((row / 2) % 4))
+  // the first `depth` boxes of a tile (cols = the box width)
+  __device__ __forceinline__ void prime(int lane, int n0, int N, int BN, int cols, int row0) {
+    for (uint32_t j = 0; j < depth; ++j)
+      if (static_cast<int>(cols * j) < BN && n0 + static_cast<int>(cols * j) < N) issue(lane, n0 + cols * j, row0);
+  }
+  // this lane's row of the next 32 x 32 box (bf16 SWIZZLE_64B: 16-byte unit i at i ^ ((row / 2) % 4))
   __device__ __forceinline__ void take(int lane, uint4 (&h)[4]) {
-    const uint32_t b = rc & 1;
-    mbar_wait(&bar[b], (rc >> 1) & 1);
-    const uint4* src = reinterpret_cast<const uint4*>(stg + b * 4096 + 2048 + lane * 64);
+    const uint32_t b = rc % depth;
+    mbar_wait(&bar[b], (rc / depth) & 1);
+    const uint4* src = reinterpret_cast<const uint4*>(rbuf + b * stride + lane * 64);
 #pragma unroll
     for (int i = 0; i < 4; ++i) h[i] = src[i ^ ((lane >> 1) & 3)];
     ++rc;
     __syncwarp();   // every lane has read the buffer before it is refilled
   }
+  // this lane's row of the next 64 x 32 box (bf16 SWIZZLE_128B: unit i at i ^ (row % 8))
+  __device__ __forceinline__ void take8(int lane, uint4 (&h)[8]) {
+    const uint32_t b = rc % depth;
+    mbar_wait(&bar[b], (rc / depth) & 1);
+    const uint4* src = reinterpret_cast<const uint4*>(rbuf + b * stride + lane * 128);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) h[i] = src[i ^ (lane & 7)];
+    ++rc;
+    __syncwarp();
+  }
 };
+
+// bf16 epilogue on 64-column steps with 128-byte TMA boxes (64 x 32,
+// SWIZZLE_128B) for the output stores and the residual loads: half the box
+// rows of the 32-column path per byte. The TMA walks a box row by row, and
+// with 64-byte rows its row rate bounded the K = 64 residual convs (the
+// teacher's 1x1 expansions; profiles/README.md finding 41). stg: 2 x 4 KB.
+template <int BN, int EPI>
+__device__ __forceinline__ void epilogue_tile_tma128(const EpiArgs& ep, uint32_t taddr, int row0, int lane, int M,
+                                                     int n0, int N, const float* sb, const CUtensorMap* tmY,
+                                                     uint8_t* stg, uint32_t& stores, ResStream* rs) {
+  static_assert(EPI == EPI_RELU_BF16 || EPI == EPI_BIAS_BF16, "bf16 conv epilogues only");
+  const int row = row0 + lane;
+  uint32_t ra[32], rb[32];
+  tmem_ld32_issue(taddr, ra);
+  tmem_ld32_issue(taddr + 32, rb);
+  tmem_ld_wait(ra);
+  tmem_ld_wait(rb);
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 64) {
+    float v0[32], v1[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) { v0[i] = __uint_as_float(ra[i]); v1[i] = __uint_as_float(rb[i]); }
+    if (c + 64 < BN) {
+      tmem_ld32_issue(taddr + c + 64, ra);
+      tmem_ld32_issue(taddr + c + 96, rb);
+    }
+    const bool live = n0 + c < N;   // warp-uniform
+    if (live) {
+      if (EPI == EPI_RELU_BF16 && rs != nullptr) {
+        uint4 h[8];
+        rs->take8(lane, h);
+        const int cn = c + 64 * static_cast<int>(rs->depth);
+        if (cn < BN && n0 + cn < N) rs->issue(lane, n0 + cn, row0);
+        uint4 h0[4] = {h[0], h[1], h[2], h[3]}, h1[4] = {h[4], h[5], h[6], h[7]};
+        epi_math<EPI>(ep, row, M, n0 + c, N, v0, sb != nullptr ? sb + c : nullptr, h0);
+        epi_math<EPI>(ep, row, M, n0 + c + 32, N, v1, sb != nullptr ? sb + c + 32 : nullptr, h1);
+      } else {
+        epi_math<EPI>(ep, row, M, n0 + c, N, v0, sb != nullptr ? sb + c : nullptr, nullptr);
+        epi_math<EPI>(ep, row, M, n0 + c + 32, N, v1, sb != nullptr ? sb + c + 32 : nullptr, nullptr);
+      }
+      uint8_t* buf = stg + (stores & 1) * 4096;
+      if (lane == 0) bulk_wait_read1();        // only the newest store may still be reading
+      __syncwarp();
+      uint4* dst = reinterpret_cast<uint4*>(buf + lane * 128);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint4 q;
+        q.x = pack_bf16x2(v0[8 * i + 0], v0[8 * i + 1]);
+        q.y = pack_bf16x2(v0[8 * i + 2], v0[8 * i + 3]);
+        q.z = pack_bf16x2(v0[8 * i + 4], v0[8 * i + 5]);
+        q.w = pack_bf16x2(v0[8 * i + 6], v0[8 * i + 7]);
+        dst[i ^ (lane & 7)] = q;
+        q.x = pack_bf16x2(v1[8 * i + 0], v1[8 * i + 1]);
+        q.y = pack_bf16x2(v1[8 * i + 2], v1[8 * i + 3]);
+        q.z = pack_bf16x2(v1[8 * i + 4], v1[8 * i + 5]);
+        q.w = pack_bf16x2(v1[8 * i + 6], v1[8 * i + 7]);
+        dst[(4 + i) ^ (lane & 7)] = q;
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(tmY, buf, n0 + c, row0);
+        bulk_commit();
+      }
+      ++stores;
+    }
+    if (c + 64 < BN) {
+      tmem_ld_wait(ra);
+      tmem_ld_wait(rb);
+    }
+  }
+}
 
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_tile_tma(const EpiArgs& ep, uint32_t taddr, int row0, int lane, int M,
@@ -603,7 +693,8 @@ __device__ __forceinline__ void epilogue_tile_tma(const EpiArgs& ep, uint32_t ta
     const bool live = n0 + c < N;   // warp-uniform
     if (EPI == EPI_RELU_BF16 && rs != nullptr && live) {
       rs->take(lane, hc);
-      if (c + 64 < BN && n0 + c + 64 < N) rs->issue(lane, n0 + c + 64, row0);
+      const int cn = c + 32 * static_cast<int>(rs->depth);
+      if (cn < BN && n0 + cn < N) rs->issue(lane, n0 + cn, row0);
       epi_math<EPI>(ep, row, M, n0 + c, N, v, sb != nullptr ? sb + c : nullptr, hc);
     } else if (live) {
       epi_math<EPI>(ep, row, M, n0 + c, N, v, sb != nullptr ? sb + c : nullptr,
@@ -661,6 +752,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // the MMA and the producer waiting), 2 otherwise
   constexpr int kAcc = Cfg::kAcc;
   constexpr uint32_t kTmemCols = tmem_cols_for(kAcc * BN);
+  constexpr bool kW128 = false;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
@@ -824,7 +916,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     const int e = warp - 4;
     uint32_t stores = 0;
-    ResStream rs{&tmR, stg + e * 8192, rbar + 2 * e, 0u, 0u};
+    ResStream rs{&tmR, stg + e * 8192 + 2048, 4096u, rbar + 2 * e, 2u, 2048u, 0u, 0u};
     int staged_n0 = -1;
     for (uint32_t i = 0;; ++i) {
       const int slot = i & 3;
@@ -842,10 +934,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // down instead.)
       float* const split_out = split ? static_cast<float*>(ep.out) + split * ep.split_stride : nullptr;
       float* sb = sbias;
-      if (tma_res) {   // the first two residual chunks load behind this tile's MMAs
-        rs.issue(lane, n0, m0 + 32 * e);
-        if (n0 + 32 < N) rs.issue(lane, n0 + 32, m0 + 32 * e);
-      }
+      if (tma_res) rs.prime(lane, n0, N, BN, kW128 ? 64 : 32, m0 + 32 * e);   // behind this tile's MMAs
       // the bias slice only changes with n0 (one n-tile: staged once per CTA);
       // the first barrier keeps a re-stage behind every warp's previous tile
       if (epi_has_bias<EPI>() && n0 != staged_n0) {
@@ -945,21 +1034,30 @@ __device__ __forceinline__ void mma_kblock_pair(uint32_t d_tmem, uint32_t a_base
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+// W128 (bf16 conv epilogues, edl_conv_fwd_nhwc): outputs and residual in
+// 64 x 32 SWIZZLE_128B boxes (epilogue_tile_tma128). With a residual
+// (EPI_RELU_BF16) the operand ring gives up two stages for a 4-deep 4 KB
+// residual ring per epilogue warp.
+template <int BN, bool A_MN, bool B_MN, int EPI, bool W128 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmR, int M, int N,
                      int K, EpiArgs ep) {
   using Cfg = PairCfg<BN>;
   unsigned* const sched = ep.sched;
-  constexpr int S = Cfg::kStages;
+  constexpr bool kW128 = W128;
+  constexpr bool kResRing = W128 && EPI == EPI_RELU_BF16;
+  constexpr int kRD = 4;                                   // residual boxes in flight (kResRing)
+  constexpr int S = Cfg::kStages - (kResRing ? 2 : 0);
+  static_assert(!kResRing || (2 * kRD * 4096 <= 2 * Cfg::kABytes && 2 * kRD * 4096 <= 2 * Cfg::kBBytes),
+                "the residual ring must fit the two freed stages");
   constexpr uint32_t kTmemCols = tmem_cols_for(2 * BN);
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + S * Cfg::kABytes;
-  uint8_t* stg = sB + S * Cfg::kBBytes;                              // [4 warps][2][4 KB] TMA-store staging
+  uint8_t* sB = smem + Cfg::kStages * Cfg::kABytes;
+  uint8_t* stg = sB + Cfg::kStages * Cfg::kBBytes;                   // [4 warps][2][4 KB] TMA-store staging
   float* sbias = reinterpret_cast<float*>(stg + Cfg::kStoreBytes);   // [BN]
   uint64_t* full = reinterpret_cast<uint64_t*>(stg + Cfg::kStoreBytes + Cfg::kEpiBytes);
   uint64_t* empty = full + S;
@@ -969,7 +1067,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tile_empty = tile_full + 4;   // [4] (rank 0's is the one used)
   int* tile_ring = reinterpret_cast<int*>(tile_empty + 4);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + 4);
-  uint64_t* rbar = reinterpret_cast<uint64_t*>(tmem_slot + 2);   // [4 warps][2] residual stream
+  uint64_t* rbar = reinterpret_cast<uint64_t*>(tmem_slot + 2);   // [4 warps][2 or kRD] residual stream
   // the residual of EPI_RELU_BF16 arrives by TMA (ResStream)
   const bool tma_res = EPI == EPI_RELU_BF16 && ep.aux != nullptr;
 
@@ -985,7 +1083,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < 4; ++s) { mbar_init(&tile_full[s], 1); mbar_init(&tile_empty[s], 10); }
     if (tma_res) {
       prefetch_tmap(&tmR);
-      for (int s = 0; s < 8; ++s) mbar_init(&rbar[s], 1);
+      for (int s = 0; s < 4 * (kResRing ? kRD : 2); ++s) mbar_init(&rbar[s], 1);
     }
     fence_mbar_init();
   }
@@ -1096,7 +1194,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     const int e = warp - 4;
     uint32_t stores = 0;
-    ResStream rs{&tmR, stg + e * 8192, rbar + 2 * e, 0u, 0u};
+    uint8_t* const rring = !kResRing ? stg + e * 8192 + 2048
+                                     : (e < 2 ? sA + S * Cfg::kABytes + e * kRD * 4096
+                                              : sB + S * Cfg::kBBytes + (e - 2) * kRD * 4096);
+    ResStream rs{&tmR, rring, kResRing ? 4096u : 4096u, rbar + (kResRing ? kRD : 2) * e,
+                 kResRing ? static_cast<uint32_t>(kRD) : 2u, kW128 ? 4096u : 2048u, 0u, 0u};
     int staged_n0 = -1;
     for (uint32_t i = 0;; ++i) {
       const int t = take_tile(i);
@@ -1108,10 +1210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m0 = mt * 2 * kBM + static_cast<int>(rank) * kBM;
       const int n0 = nt * BN;
       float* sb = sbias;
-      if (tma_res) {   // the first two residual chunks load behind this tile's MMAs
-        rs.issue(lane, n0, m0 + 32 * e);
-        if (n0 + 32 < N) rs.issue(lane, n0 + 32, m0 + 32 * e);
-      }
+      if (tma_res) rs.prime(lane, n0, N, BN, kW128 ? 64 : 32, m0 + 32 * e);   // behind this tile's MMAs
       // the bias slice only changes with n0 (one n-tile: staged once per CTA);
       // the first barrier keeps a re-stage behind every warp's previous tile
       if (epi_has_bias<EPI>() && n0 != staged_n0) {
@@ -1123,7 +1222,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t as = i & 1;
       mbar_wait(&tfull[as], (i >> 1) & 1);
       tc_fence_after();
-      if constexpr (epi_tma_store<EPI>())
+      if constexpr (kW128)
+        epilogue_tile_tma128<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e,
+                                      lane, M, n0, N, epi_has_bias<EPI>() ? sb : nullptr, &tmY, stg + e * 8192, stores,
+                                      tma_res ? &rs : nullptr);
+      else if constexpr (epi_tma_store<EPI>())
         epilogue_tile_tma<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e,
                                    lane, M, n0, N, epi_has_bias<EPI>() ? sb : nullptr, &tmY, stg + e * 8192, stores,
                                    tma_res ? &rs : nullptr);
@@ -2284,9 +2387,11 @@ cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUte
 template <int BN, bool A_MN, bool B_MN, int EPI>
 static cudaError_t launch_pair_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, int M, int N,
                                  int K, const EpiArgs& ep, int num_sms, cudaStream_t stream,
-                                 const CUtensorMap* tr) {
+                                 const CUtensorMap* tr, bool w128 = false) {
   if (EPI == EPI_RELU_BF16 && ep.aux != nullptr && tr == nullptr) return cudaErrorInvalidValue;
-  auto kern = gemm_pair_kernel<BN, A_MN, B_MN, EPI>;
+  constexpr bool kCanW128 = BN == 256 && !A_MN && !B_MN && (EPI == EPI_RELU_BF16 || EPI == EPI_BIAS_BF16);
+  auto kern = (kCanW128 && w128) ? gemm_pair_kernel<BN, A_MN, B_MN, EPI, kCanW128>
+                                 : gemm_pair_kernel<BN, A_MN, B_MN, EPI>;
   cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), PairCfg<BN>::kSmem);
   if (e != cudaSuccess) return e;
   const int tiles = ((M + 2 * kBM - 1) / (2 * kBM)) * ((N + BN - 1) / BN);
@@ -2299,17 +2404,25 @@ static cudaError_t launch_pair_t(const CUtensorMap& ta, const CUtensorMap& tb, c
 template <bool A_MN, bool B_MN, int EPI>
 static cudaError_t launch_pair_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, int M,
                                   int N, int K, const EpiArgs& ep, int num_sms, cudaStream_t stream,
-                                  const CUtensorMap* tr = nullptr) {
+                                  const CUtensorMap* tr = nullptr, bool w128 = false) {
   switch (bn) {
     case 128: return launch_pair_t<128, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream, tr);
-    case 256: return launch_pair_t<256, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream, tr);
+    case 256: return launch_pair_t<256, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream, tr, w128);
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_gemm_pair(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
                              const CUtensorMap& ty, int M, int N, int K, const EpiArgs& ep, int num_sms,
-                             cudaStream_t stream, const CUtensorMap* tr) {
+                             cudaStream_t stream, const CUtensorMap* tr, bool w128) {
+  if (w128) {   // 64 x 32 SWIZZLE_128B output / residual maps (edl_conv_fwd_nhwc, bn == 256)
+    if (bn != 256) return cudaErrorInvalidValue;
+    if (kind == GemmKind::FwdRelu)
+      return launch_pair_bn<false, false, EPI_RELU_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream, tr, true);
+    if (kind == GemmKind::FwdIdentBf16)
+      return launch_pair_bn<false, false, EPI_BIAS_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream, nullptr, true);
+    return cudaErrorInvalidValue;
+  }
   switch (kind) {
     case GemmKind::FwdTanh:
       return launch_pair_bn<false, false, EPI_TANH_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);

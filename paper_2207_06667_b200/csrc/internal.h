@@ -149,7 +149,7 @@ cudaError_t launch_nvls_allreduce_sgd(float* mc_grad, float* mc_param, void* mc_
 // map box covers bn/2 rows (K-major) or bn/2 columns (MN-major).
 cudaError_t launch_gemm_pair(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
                              const CUtensorMap& ty, int M, int N, int K, const EpiArgs& ep, int num_sms,
-                             cudaStream_t stream, const CUtensorMap* tr = nullptr);
+                             cudaStream_t stream, const CUtensorMap* tr = nullptr, bool w128 = false);
 // teacher head on CTA pairs, class chunks merged through `part`
 // ([ceil(N/256)][2 + 2 kmax][M] floats) and `tickets` (ceil(M/128), zeroed once)
 cudaError_t launch_teacher_head_pair(int kmax, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
