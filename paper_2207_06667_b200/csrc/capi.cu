@@ -475,7 +475,13 @@ int edl_linear_fwd(const void* X, long long ldx, const void* W, long long ldw, c
   ep.l2hint = l2hint_env >= 0 ? l2hint_env : (static_cast<long long>(M) * K * 2 > (32ll << 20) ? 1 : 0);
   CUtensorMap ty;
   const int pbn = pick_pair_bn(M, N, cap);
-  const bool w128 = pbn == 256 && (act == EDL_ACT_RELU || act == EDL_ACT_IDENT) && w128_enabled();
+  const int bn = pbn > 0 ? pbn : pick_bn_cap(M, N, cap);
+  static const bool w128_tanh = [] {   // the MLP layers' tanh epilogue too (EDL_W128_TANH=0: not)
+    const char* v = getenv("EDL_W128_TANH");
+    return !(v && v[0] == '0');
+  }();
+  const bool w128 = (pbn > 0 ? pbn == 256 : bn % 64 == 0) && w128_enabled() &&
+                    (act == EDL_ACT_RELU || act == EDL_ACT_IDENT || (act == EDL_ACT_TANH && w128_tanh));
   if ((rc = w128 ? tensor_map(Y, M, N, ldy, 64, 32, &ty) : tensor_map_out(Y, M, N, ldy, act == EDL_ACT_NONE, &ty)))
     return rc;
   cudaError_t e;
@@ -483,9 +489,8 @@ int edl_linear_fwd(const void* X, long long ldx, const void* W, long long ldw, c
     if ((rc = tensor_map(W, N, K, ldw, 64, pbn / 2, &tb))) return rc;
     e = launch_gemm_pair(kind, pbn, ta, tb, ty, M, N, K, ep, cap, as_stream(stream), nullptr, w128);
   } else {
-    const int bn = pick_bn_cap(M, N, cap);
     if ((rc = tensor_map(W, N, K, ldw, 64, bn, &tb))) return rc;
-    e = launch_gemm(kind, bn, ta, tb, ty, M, N, K, ep, cap, as_stream(stream));
+    e = launch_gemm(kind, bn, ta, tb, ty, M, N, K, ep, cap, as_stream(stream), nullptr, w128);
   }
   return e == cudaSuccess ? 0 : cuda_fail(e, "linear_fwd");
 }
@@ -595,7 +600,13 @@ int edl_conv_fwd_nhwc(const void* x, int N, int H, int W, int C, const void* w, 
   } else {
     const int bn = pick_bn_cap(M, K, cap);
     if ((rc = tensor_map(w, K, Kd, ldw, 64, bn, &tb))) return rc;
-    e = launch_gemm(kind, bn, ta, tb, ty, M, K, Kd, ep, cap, st, residual ? &tr : nullptr);
+    if (!residual && bn % 64 == 0 && w128_enabled()) {   // 64 x 32 SWIZZLE_128B output boxes
+      CUtensorMap ty2;
+      if ((rc = tensor_map(y, M, K, ldy, 64, 32, &ty2))) return rc;
+      e = launch_gemm(kind, bn, ta, tb, ty2, M, K, Kd, ep, cap, st, nullptr, true);
+    } else {
+      e = launch_gemm(kind, bn, ta, tb, ty, M, K, Kd, ep, cap, st, residual ? &tr : nullptr);
+    }
   }
   return e == cudaSuccess ? 0 : cuda_fail(e, "conv_fwd_nhwc");
 }

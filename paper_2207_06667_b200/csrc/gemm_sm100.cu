@@ -591,7 +591,7 @@ template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_tile_tma128(const EpiArgs& ep, uint32_t taddr, int row0, int lane, int M,
                                                      int n0, int N, const float* sb, const CUtensorMap* tmY,
                                                      uint8_t* stg, uint32_t& stores, ResStream* rs) {
-  static_assert(EPI == EPI_RELU_BF16 || EPI == EPI_BIAS_BF16, "bf16 conv epilogues only");
+  static_assert(EPI == EPI_RELU_BF16 || EPI == EPI_BIAS_BF16 || EPI == EPI_TANH_BF16, "bf16 epilogues only");
   const int row = row0 + lane;
   uint32_t ra[32], rb[32];
   tmem_ld32_issue(taddr, ra);
@@ -739,7 +739,9 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int gro
 }
 
 // ------------------------------------------------------------------ GEMM
-template <int BN, bool A_MN, bool B_MN, int EPI>
+// W128: bf16 outputs without a residual in 64 x 32 SWIZZLE_128B boxes
+// (epilogue_tile_tma128), as in the pair kernel.
+template <int BN, bool A_MN, bool B_MN, int EPI, bool W128 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmR, int M, int N,
@@ -752,7 +754,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // the MMA and the producer waiting), 2 otherwise
   constexpr int kAcc = Cfg::kAcc;
   constexpr uint32_t kTmemCols = tmem_cols_for(kAcc * BN);
-  constexpr bool kW128 = false;
+  constexpr bool kW128 = W128;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
@@ -946,7 +948,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t as = i % kAcc;
       mbar_wait(&tfull[as], (i / kAcc) & 1);
       tc_fence_after();
-      if constexpr (epi_tma_store<EPI>())
+      if constexpr (kW128)
+        epilogue_tile_tma128<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e,
+                                      lane, M, n0, N, epi_has_bias<EPI>() ? sb : nullptr, &tmY, stg + e * 8192, stores,
+                                      nullptr);
+      else if constexpr (epi_tma_store<EPI>())
         epilogue_tile_tma<BN, EPI>(ep, tmem_base + (static_cast<uint32_t>(32 * e) << 16) + as * BN, m0 + 32 * e,
                                    lane, M, n0, N, epi_has_bias<EPI>() ? sb : nullptr, &tmY, stg + e * 8192, stores,
                                    tma_res ? &rs : nullptr);
@@ -2337,9 +2343,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int BN, bool A_MN, bool B_MN, int EPI>
 static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, int M, int N,
                                  int K, const EpiArgs& ep, int num_sms, cudaStream_t stream,
-                                 const CUtensorMap* tr) {
+                                 const CUtensorMap* tr, bool w128 = false) {
   if (EPI == EPI_RELU_BF16 && ep.aux != nullptr && tr == nullptr) return cudaErrorInvalidValue;
-  auto kern = gemm_kernel<BN, A_MN, B_MN, EPI>;
+  constexpr bool kCanW128 = BN % 64 == 0 && !A_MN && !B_MN &&
+                            (EPI == EPI_RELU_BF16 || EPI == EPI_BIAS_BF16 || EPI == EPI_TANH_BF16);
+  if (w128 && (!kCanW128 || tr != nullptr || ep.ksplit > 1)) return cudaErrorInvalidValue;
+  auto kern = (kCanW128 && w128) ? gemm_kernel<BN, A_MN, B_MN, EPI, kCanW128> : gemm_kernel<BN, A_MN, B_MN, EPI>;
   cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), GemmCfg<BN>::kSmem);
   if (e != cudaSuccess) return e;
   const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN) * ep.ksplit;
@@ -2351,18 +2360,28 @@ static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, c
 template <bool A_MN, bool B_MN, int EPI>
 static cudaError_t launch_gemm_bn(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty,
                                   int M, int N, int K, const EpiArgs& ep, int num_sms, cudaStream_t stream,
-                                  const CUtensorMap* tr = nullptr) {
+                                  const CUtensorMap* tr = nullptr, bool w128 = false) {
   switch (bn) {
-    case 64: return launch_gemm_t<64, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream, tr);
-    case 128: return launch_gemm_t<128, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream, tr);
-    case 256: return launch_gemm_t<256, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream, tr);
+    case 64: return launch_gemm_t<64, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream, tr, w128);
+    case 128: return launch_gemm_t<128, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream, tr, w128);
+    case 256: return launch_gemm_t<256, A_MN, B_MN, EPI>(ta, tb, ty, M, N, K, ep, num_sms, stream, tr, w128);
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
                         const CUtensorMap& ty, int M, int N, int K, const EpiArgs& ep, int num_sms,
-                        cudaStream_t stream, const CUtensorMap* tr) {
+                        cudaStream_t stream, const CUtensorMap* tr, bool w128) {
+  if (w128) {   // 64 x 32 SWIZZLE_128B output maps, no residual
+    if (tr != nullptr) return cudaErrorInvalidValue;
+    if (kind == GemmKind::FwdRelu)
+      return launch_gemm_bn<false, false, EPI_RELU_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream, nullptr, true);
+    if (kind == GemmKind::FwdIdentBf16)
+      return launch_gemm_bn<false, false, EPI_BIAS_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream, nullptr, true);
+    if (kind == GemmKind::FwdTanh)
+      return launch_gemm_bn<false, false, EPI_TANH_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream, nullptr, true);
+    return cudaErrorInvalidValue;
+  }
   switch (kind) {
     case GemmKind::FwdTanh:
       return launch_gemm_bn<false, false, EPI_TANH_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream);
@@ -2389,7 +2408,8 @@ static cudaError_t launch_pair_t(const CUtensorMap& ta, const CUtensorMap& tb, c
                                  int K, const EpiArgs& ep, int num_sms, cudaStream_t stream,
                                  const CUtensorMap* tr, bool w128 = false) {
   if (EPI == EPI_RELU_BF16 && ep.aux != nullptr && tr == nullptr) return cudaErrorInvalidValue;
-  constexpr bool kCanW128 = BN == 256 && !A_MN && !B_MN && (EPI == EPI_RELU_BF16 || EPI == EPI_BIAS_BF16);
+  constexpr bool kCanW128 =
+      BN == 256 && !A_MN && !B_MN && (EPI == EPI_RELU_BF16 || EPI == EPI_BIAS_BF16 || EPI == EPI_TANH_BF16);
   auto kern = (kCanW128 && w128) ? gemm_pair_kernel<BN, A_MN, B_MN, EPI, kCanW128>
                                  : gemm_pair_kernel<BN, A_MN, B_MN, EPI>;
   cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), PairCfg<BN>::kSmem);
@@ -2421,6 +2441,8 @@ cudaError_t launch_gemm_pair(GemmKind kind, int bn, const CUtensorMap& ta, const
       return launch_pair_bn<false, false, EPI_RELU_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream, tr, true);
     if (kind == GemmKind::FwdIdentBf16)
       return launch_pair_bn<false, false, EPI_BIAS_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream, nullptr, true);
+    if (kind == GemmKind::FwdTanh)
+      return launch_pair_bn<false, false, EPI_TANH_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream, nullptr, true);
     return cudaErrorInvalidValue;
   }
   switch (kind) {

@@ -133,7 +133,7 @@ cudaError_t launch_gemm_grouped_pair_bwd_weight(const GroupMaps& maps, const Gro
 // (tensor_map_out on ep.aux), streamed into shared memory by TMA.
 cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUtensorMap& tb,
                         const CUtensorMap& ty, int M, int N, int K, const EpiArgs& ep, int num_sms,
-                        cudaStream_t stream, const CUtensorMap* tr = nullptr);
+                        cudaStream_t stream, const CUtensorMap* tr = nullptr, bool w128 = false);
 // Hidden-layer tanh of the GEMM epilogues on the current device: 1 = tanhf
 // (default), 0 = tanh.approx.f32 (gemm_sm100.cu).
 cudaError_t set_tanh_mode(int mode);
