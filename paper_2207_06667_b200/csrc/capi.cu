@@ -448,6 +448,15 @@ static bool w128_enabled() {
   return on;
 }
 
+// the MLP layers' tanh / dtanh epilogues too (EDL_W128_TANH=0: not)
+static bool w128_tanh() {
+  static const bool on = [] {
+    const char* v = getenv("EDL_W128_TANH");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 int edl_linear_fwd(const void* X, long long ldx, const void* W, long long ldw, const float* bias,
                    void* Y, long long ldy, int M, int N, int K, int act, void* stream) {
   if (M < 1 || N < 1 || K < 1 || ldx < K || ldw < K || ldy < N)
@@ -476,12 +485,8 @@ int edl_linear_fwd(const void* X, long long ldx, const void* W, long long ldw, c
   CUtensorMap ty;
   const int pbn = pick_pair_bn(M, N, cap);
   const int bn = pbn > 0 ? pbn : pick_bn_cap(M, N, cap);
-  static const bool w128_tanh = [] {   // the MLP layers' tanh epilogue too (EDL_W128_TANH=0: not)
-    const char* v = getenv("EDL_W128_TANH");
-    return !(v && v[0] == '0');
-  }();
   const bool w128 = (pbn > 0 ? pbn == 256 : bn % 64 == 0) && w128_enabled() &&
-                    (act == EDL_ACT_RELU || act == EDL_ACT_IDENT || (act == EDL_ACT_TANH && w128_tanh));
+                    (act == EDL_ACT_RELU || act == EDL_ACT_IDENT || (act == EDL_ACT_TANH && w128_tanh()));
   if ((rc = w128 ? tensor_map(Y, M, N, ldy, 64, 32, &ty) : tensor_map_out(Y, M, N, ldy, act == EDL_ACT_NONE, &ty)))
     return rc;
   cudaError_t e;
@@ -639,20 +644,22 @@ int edl_conv_dgrad_nhwc(const void* dz, int N, int P, int Q, int K, const void* 
   CUtensorMap ta, tb, ty;
   int rc;
   if ((rc = conv_map(dz, N, P, Q, K, R, S, 1, pd, 128, &ta))) return rc;
-  if ((rc = tensor_map_out(dx, M, C, C, false, &ty))) return rc;
+  const int pbn_d = pick_pair_bn(M, C, cap);
+  const bool w128 = (pbn_d > 0 ? pbn_d == 256 : pick_bn_cap(M, C, cap) % 64 == 0) && w128_enabled();
+  if ((rc = w128 ? tensor_map(dx, M, C, C, 64, 32, &ty) : tensor_map_out(dx, M, C, C, false, &ty))) return rc;
   EpiArgs ep{dx, C, nullptr, reinterpret_cast<const __nv_bfloat16*>(add), add ? C : 0, 1.0f, stream_sched(st)};
   ep.aux2 = reinterpret_cast<const __nv_bfloat16*>(mask);
   ep.ld_aux2 = mask ? C : 0;
   ep.conv = ConvGeom{H, W, 1, pd, S, K / 64};
-  const int pbn = pick_pair_bn(M, C, cap);
+  const int pbn = pbn_d;
   cudaError_t e;
   if (pbn > 0) {
     if ((rc = tensor_map(wf, C, Kd, ldf, 64, pbn / 2, &tb))) return rc;
-    e = launch_gemm_pair(GemmKind::ConvDgrad, pbn, ta, tb, ty, M, C, Kd, ep, cap, st);
+    e = launch_gemm_pair(GemmKind::ConvDgrad, pbn, ta, tb, ty, M, C, Kd, ep, cap, st, nullptr, w128);
   } else {
     const int bn = pick_bn_cap(M, C, cap);
     if ((rc = tensor_map(wf, C, Kd, ldf, 64, bn, &tb))) return rc;
-    e = launch_gemm(GemmKind::ConvDgrad, bn, ta, tb, ty, M, C, Kd, ep, cap, st);
+    e = launch_gemm(GemmKind::ConvDgrad, bn, ta, tb, ty, M, C, Kd, ep, cap, st, nullptr, w128);
   }
   return e == cudaSuccess ? 0 : cuda_fail(e, "conv_dgrad_nhwc");
 }
@@ -766,11 +773,14 @@ int edl_linear_bwd_data(const void* dY, long long lddy, const void* W, long long
   EpiArgs ep{dX, lddx, nullptr, reinterpret_cast<const __nv_bfloat16*>(H), ldh, 1.0f,
              stream_sched(as_stream(stream))};
   CUtensorMap ty;
-  if ((rc = tensor_map_out(dX, M, K, lddx, false, &ty))) return rc;
   const int pbn = pick_pair_bn(M, K, cap);
-  cudaError_t e = pbn > 0 ? launch_gemm_pair(kind, pbn, ta, tb, ty, M, K, N, ep, cap, as_stream(stream))
-                          : launch_gemm(kind, pick_bn_cap(M, K, cap), ta, tb, ty, M, K, N, ep, cap,
-                                        as_stream(stream));
+  const int bn = pbn > 0 ? pbn : pick_bn_cap(M, K, cap);
+  // not with H (the (1 - a^2) epilogue): its per-element row reads of H made
+  // the cfg3 student step 208 -> 256 us on 128-byte boxes
+  const bool w128 = (pbn > 0 ? pbn == 256 : bn % 64 == 0) && w128_enabled() && H == nullptr;
+  if ((rc = w128 ? tensor_map(dX, M, K, lddx, 64, 32, &ty) : tensor_map_out(dX, M, K, lddx, false, &ty))) return rc;
+  cudaError_t e = pbn > 0 ? launch_gemm_pair(kind, pbn, ta, tb, ty, M, K, N, ep, cap, as_stream(stream), nullptr, w128)
+                          : launch_gemm(kind, bn, ta, tb, ty, M, K, N, ep, cap, as_stream(stream), nullptr, w128);
   return e == cudaSuccess ? 0 : cuda_fail(e, "linear_bwd_data");
 }
 

@@ -591,7 +591,9 @@ template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_tile_tma128(const EpiArgs& ep, uint32_t taddr, int row0, int lane, int M,
                                                      int n0, int N, const float* sb, const CUtensorMap* tmY,
                                                      uint8_t* stg, uint32_t& stores, ResStream* rs) {
-  static_assert(EPI == EPI_RELU_BF16 || EPI == EPI_BIAS_BF16 || EPI == EPI_TANH_BF16, "bf16 epilogues only");
+  static_assert(EPI == EPI_RELU_BF16 || EPI == EPI_BIAS_BF16 || EPI == EPI_TANH_BF16 || EPI == EPI_DRELU_BF16 ||
+                    EPI == EPI_DTANH_BF16,
+                "bf16 epilogues only");
   const int row = row0 + lane;
   uint32_t ra[32], rb[32];
   tmem_ld32_issue(taddr, ra);
@@ -2345,8 +2347,9 @@ static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, c
                                  int K, const EpiArgs& ep, int num_sms, cudaStream_t stream,
                                  const CUtensorMap* tr, bool w128 = false) {
   if (EPI == EPI_RELU_BF16 && ep.aux != nullptr && tr == nullptr) return cudaErrorInvalidValue;
-  constexpr bool kCanW128 = BN % 64 == 0 && !A_MN && !B_MN &&
-                            (EPI == EPI_RELU_BF16 || EPI == EPI_BIAS_BF16 || EPI == EPI_TANH_BF16);
+  constexpr bool kCanW128 = BN % 64 == 0 && !A_MN &&
+                            (EPI == EPI_RELU_BF16 || EPI == EPI_BIAS_BF16 || EPI == EPI_TANH_BF16 ||
+                             EPI == EPI_DRELU_BF16 || EPI == EPI_DTANH_BF16);
   if (w128 && (!kCanW128 || tr != nullptr || ep.ksplit > 1)) return cudaErrorInvalidValue;
   auto kern = (kCanW128 && w128) ? gemm_kernel<BN, A_MN, B_MN, EPI, kCanW128> : gemm_kernel<BN, A_MN, B_MN, EPI>;
   cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), GemmCfg<BN>::kSmem);
@@ -2380,6 +2383,13 @@ cudaError_t launch_gemm(GemmKind kind, int bn, const CUtensorMap& ta, const CUte
       return launch_gemm_bn<false, false, EPI_BIAS_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream, nullptr, true);
     if (kind == GemmKind::FwdTanh)
       return launch_gemm_bn<false, false, EPI_TANH_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream, nullptr, true);
+    if (kind == GemmKind::BwdData)
+      return launch_gemm_bn<false, true, EPI_DTANH_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream, nullptr, true);
+    if (kind == GemmKind::BwdDataPlain)
+      return launch_gemm_bn<false, true, EPI_BIAS_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream, nullptr, true);
+    if (kind == GemmKind::ConvDgrad)
+      return launch_gemm_bn<false, false, EPI_DRELU_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream, nullptr,
+                                                          true);
     return cudaErrorInvalidValue;
   }
   switch (kind) {
@@ -2408,8 +2418,9 @@ static cudaError_t launch_pair_t(const CUtensorMap& ta, const CUtensorMap& tb, c
                                  int K, const EpiArgs& ep, int num_sms, cudaStream_t stream,
                                  const CUtensorMap* tr, bool w128 = false) {
   if (EPI == EPI_RELU_BF16 && ep.aux != nullptr && tr == nullptr) return cudaErrorInvalidValue;
-  constexpr bool kCanW128 =
-      BN == 256 && !A_MN && !B_MN && (EPI == EPI_RELU_BF16 || EPI == EPI_BIAS_BF16 || EPI == EPI_TANH_BF16);
+  constexpr bool kCanW128 = BN == 256 && !A_MN &&
+                            (EPI == EPI_RELU_BF16 || EPI == EPI_BIAS_BF16 || EPI == EPI_TANH_BF16 ||
+                             EPI == EPI_DRELU_BF16 || EPI == EPI_DTANH_BF16);
   auto kern = (kCanW128 && w128) ? gemm_pair_kernel<BN, A_MN, B_MN, EPI, kCanW128>
                                  : gemm_pair_kernel<BN, A_MN, B_MN, EPI>;
   cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), PairCfg<BN>::kSmem);
@@ -2443,6 +2454,13 @@ cudaError_t launch_gemm_pair(GemmKind kind, int bn, const CUtensorMap& ta, const
       return launch_pair_bn<false, false, EPI_BIAS_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream, nullptr, true);
     if (kind == GemmKind::FwdTanh)
       return launch_pair_bn<false, false, EPI_TANH_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream, nullptr, true);
+    if (kind == GemmKind::BwdData)
+      return launch_pair_bn<false, true, EPI_DTANH_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream, nullptr, true);
+    if (kind == GemmKind::BwdDataPlain)
+      return launch_pair_bn<false, true, EPI_BIAS_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream, nullptr, true);
+    if (kind == GemmKind::ConvDgrad)
+      return launch_pair_bn<false, false, EPI_DRELU_BF16>(bn, ta, tb, ty, M, N, K, ep, num_sms, stream, nullptr,
+                                                          true);
     return cudaErrorInvalidValue;
   }
   switch (kind) {
