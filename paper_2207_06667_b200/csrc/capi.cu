@@ -547,7 +547,7 @@ int halo_conv(const void* x, int N, int H, int W, const void* w, long long ldw, 
 // from the staged patch of image n, rows h0-1 .. h0+2, shifted by `off` rows.
 int edl_halo_probe(const void* x, int N, int H, int W, int n, int h0, int off, const void* w, int mode, int reps,
                    int smem_kb, float* out, void* stream) {
-  if (off < 0 || off + 128 > 256 || n < 0 || n >= N || mode < 0 || mode > 3 || reps < 0)
+  if (off < 0 || off + 128 > 256 || n < 0 || n >= N || mode < 0 || mode > 4 || reps < 0)
     return fail(EDL_ERR_SHAPE, "halo_probe: bad arguments");
   CUtensorMap mx, mw;
   if (mode == 0) {
@@ -943,7 +943,10 @@ long long edl_colsum_workspace_floats(int M, int N) { return colsum_workspace_fl
 
 long long edl_bwd_weight_workspace_floats(int M, int N, int K) {
   if (M < 1 || N < 1 || K < 1) return -1;
-  return wgrad_workspace_floats(M, N, K, num_sms());
+  const long long ws = wgrad_workspace_floats(M, N, K, num_sms());
+  // a 64 -> 64 3x3 conv may run the halo weight gradient: its per-CTA partials
+  const long long halo = (N == 64 && K == 576) ? halo_wgrad_partial_floats(num_sms()) : 0;
+  return ws > halo ? ws : halo;
 }
 
 }  // extern "C"
@@ -1025,6 +1028,25 @@ int edl_conv_bwd_weight_nhwc(const void* x, int N, int H, int W, int C, int R, i
     return fail(EDL_ERR_SHAPE, "conv_bwd_weight_nhwc: bad leading dimension");
   CUtensorMap xm;
   int rc;
+  if (C == 64 && K == 64 && R == 3 && S == 3 && stride == 1 && pad == 1 && W + 2 <= 64 && lddy == 64 &&
+      db == nullptr && halo_enabled()) {
+    // the halo weight gradient (halo.cu): patch views as MN-major operands
+    cudaStream_t st = as_stream(stream);
+    const int Rt = halo_rows_per_tile(W);
+    HaloArgs a{};
+    a.N = N; a.H = H; a.W = W; a.R = Rt;
+    a.tiles_per_image = (H + Rt - 1) / Rt;
+    a.tiles = N * a.tiles_per_image;
+    const int cap = grid_cap(st);
+    const int grid = a.tiles < cap ? a.tiles : cap;
+    if (workspace_floats >= halo_wgrad_partial_floats(grid)) {
+      CUtensorMap mx, md;
+      if ((rc = halo_map_sw128(x, N, H, W, 64, W + 2, Rt + 2, &mx))) return rc;
+      if ((rc = halo_map_sw128(dY, N, H, W, 64, W + 2, Rt, &md))) return rc;
+      cudaError_t e = launch_halo_wgrad(mx, md, a, grid, workspace, scale, dW, lddw, st);
+      return e == cudaSuccess ? 0 : cuda_fail(e, "halo_wgrad");
+    }
+  }
   if ((rc = conv_map(x, N, H, W, C, R, S, stride, pad, 64, &xm))) return rc;
   const ConvGeom g{P, Q, stride, pad, S, C / 64};
   return bwd_weight_ws_impl(dY, lddy, nullptr, 0, &xm, &g, dW, lddw, db, workspace, workspace_floats,

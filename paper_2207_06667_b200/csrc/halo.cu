@@ -119,7 +119,17 @@ __global__ void __launch_bounds__(128, 1) halo_probe_kernel(const __grid_constan
       }
     };
     long long t0 = clock64();
-    if (reps == 0) {
+    if (mode == 4) {
+      // MN-major A of two stacked 64-wide views (rows off and off + reps) via
+      // LBO = reps rows; B = the weight tile read MN-major (K = its rows)
+      constexpr uint32_t idesc_mn = idesc_bf16_f32(128, 64, true, true);
+      for (int k = 0; k < 4; ++k) {
+        const uint64_t ad = smem_desc_sw128(smem_u32(sp) + static_cast<uint32_t>(off) * 128u + 2048u * k,
+                                            static_cast<uint32_t>(reps) * 128u, 1024);
+        const uint64_t bd = smem_desc_sw128(smem_u32(sw) + 2048u * k, 8192, 1024);
+        umma_bf16(tmem, ad, bd, idesc_mn, k ? 1u : 0u);
+      }
+    } else if (reps == 0) {
       issue(off, true, 0, tmem);
     } else {
       for (int r = 0; r < reps % 1000; ++r) {  // NOLINT
@@ -130,8 +140,8 @@ __global__ void __launch_bounds__(128, 1) halo_probe_kernel(const __grid_constan
     }
     umma_commit(&done);
     mbar_wait(&done, 0);
-    if (reps > 0 && blockIdx.x == 0) out[128 * 64] = static_cast<float>(clock64() - t0);
-    if (reps > 0 && blockIdx.x == 0) out[128 * 64 + 1] = static_cast<float>(smem_u32(sp));
+    if (mode != 4 && reps > 0 && blockIdx.x == 0) out[128 * 64] = static_cast<float>(clock64() - t0);
+    if (mode != 4 && reps > 0 && blockIdx.x == 0) out[128 * 64 + 1] = static_cast<float>(smem_u32(sp));
   }
   __syncwarp();
   mbar_wait(&done, 0);
@@ -376,6 +386,139 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
   }
 }
 
+// ---- halo weight gradient: dW[cout][tap][cin] = sum over pixels of
+// dz[p][cout] x[p + off(tap)][cin], for the same 64 -> 64 3x3 stride-1 layers.
+// Per tile (two output rows): the zero-padded x patch (as in the forward) and
+// the dz tile in the same padded row space (a {64, W + 2, R, 1} box: the two
+// columns past the image are the TMA's zero fill, rows 116..127 stay zero).
+// The UMMA's M = 128 rows are two taps' 64 input channels: an MN-major A
+// whose two 64-wide halves are the patch viewed at both taps' row offsets
+// (LBO = the offset difference; `edl_halo_probe` mode 4), K = 16 pixel rows
+// per instruction, B = dz MN-major (N = cout 64). Five tap pairs (the ninth
+// tap pairs with itself) accumulate in five TMEM accumulators over all of a
+// CTA's tiles; the CTA writes its partial [tap][cin][cout] once and
+// halo_wgrad_reduce_kernel adds the CTAs' partials in CTA order
+// (deterministic). Two warps issue the MMAs (pairs 0-2 / 3-4).
+constexpr int kWgStages = 3;
+constexpr int kWgThreads = 256;
+
+struct WgGeom {
+  uint32_t patch_bytes, dz_bytes, stage_bytes, dz_off;   // per stage: patch (padded), then dz tile
+};
+
+__global__ void __launch_bounds__(kWgThreads, 1)
+    halo_wgrad_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmD, HaloArgs a,
+                      WgGeom g, float* __restrict__ partial) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
+  uint8_t* sS = smem;                                        // stages: [patch | dz]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sS + kWgStages * g.stage_bytes);
+  uint64_t* full = bars;
+  uint64_t* empty = full + kWgStages;
+  uint64_t* done = empty + kWgStages;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int Wp = a.W + 2;
+  // zero the stages once: dz rows past R (W + 2) and patch rows past (R + 2) (W + 2)
+  // are never written by the TMA and must read as 0 (0 x garbage could be NaN)
+  for (uint32_t i = threadIdx.x; i < kWgStages * g.stage_bytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(sS)[i] = make_uint4(0u, 0u, 0u, 0u);
+  fence_proxy_async_smem();
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmX);
+    prefetch_tmap(&tmD);
+    for (int i = 0; i < kWgStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 2); }
+    mbar_init(done, 2);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  griddep_wait();
+
+  if (warp == 0 && lane == 0) {
+    int it = 0;
+    for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++it) {
+      const int s = it % kWgStages, u = it / kWgStages;
+      mbar_wait(&empty[s], (u & 1) ^ 1);
+      mbar_arrive_expect_tx(&full[s], g.patch_bytes + g.dz_bytes);
+      const int n = tile / a.tiles_per_image, h0 = (tile % a.tiles_per_image) * a.R;
+      uint8_t* st = sS + s * g.stage_bytes;
+      tma_load_4d(&tmX, smem_u32(st), smem_u32(&full[s]), 0, -1, h0 - 1, n);
+      tma_load_4d(&tmD, smem_u32(st + g.dz_off), smem_u32(&full[s]), 0, 0, h0, n);
+    }
+  } else if ((warp == 1 || warp == 3) && lane == 0) {
+    constexpr uint32_t idesc = idesc_bf16_f32(128, 64, true, true);
+    const int p_lo = warp == 1 ? 0 : 3, p_hi = warp == 1 ? 3 : 5;
+    const uint64_t a0 = smem_desc_sw128(smem_u32(sS), 16, 1024);
+    const uint64_t b0 = smem_desc_sw128(smem_u32(sS + g.dz_off), 8192, 1024);
+    int it = 0;
+    for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++it) {
+      const int s = it % kWgStages, u = it / kWgStages;
+      mbar_wait(&full[s], u & 1);
+      tc_fence_after();
+      const uint64_t so = static_cast<uint64_t>((s * g.stage_bytes) >> 4);
+      for (int pr = p_lo; pr < p_hi; ++pr) {
+        const int ta = 2 * pr, tb = pr == 4 ? 8 : 2 * pr + 1;
+        const int oa = (ta / 3) * Wp + ta % 3, ob = (tb / 3) * Wp + tb % 3;
+        // LBO (bits 16-29) = the second tap's view, (ob - oa) rows of 128 B further
+        const uint64_t ad = (a0 & ~(static_cast<uint64_t>(0x3FFF) << 16)) |
+                            (static_cast<uint64_t>(((ob - oa) * 128) >> 4) << 16);
+        const uint32_t d = tmem + 64u * pr;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)          // 16 pixel rows per UMMA
+          umma_bf16(d, ad + so + static_cast<uint64_t>(oa * 8 + kk * 128), b0 + so + static_cast<uint64_t>(kk * 128),
+                    idesc, (it == 0 && kk == 0) ? 0u : 1u);
+      }
+      umma_commit(&empty[s]);
+    }
+    umma_commit(done);
+  }
+  __syncwarp();
+  if (warp >= 4) {
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const int q = warp - 4;
+    const int lane_row = 32 * q + lane;                 // M row: tap half, input channel
+    const int half = lane_row / 64, cin = lane_row % 64;
+    float* dst = partial + static_cast<long long>(blockIdx.x) * 9 * 64 * 64;
+    for (int pr = 0; pr < 5; ++pr) {
+      const int tap = pr == 4 ? 8 : 2 * pr + half;
+      const bool keep = !(pr == 4 && half == 1);
+      for (int c = 0; c < 64; c += 32) {
+        float v[32];
+        tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + 64u * pr + c, v);
+        if (keep) {
+          float4* o = reinterpret_cast<float4*>(dst + (static_cast<long long>(tap) * 64 + cin) * 64 + c);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) __stcg(o + j, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// dW[cout][tap * 64 + cin] = scale * sum over CTAs (in order) of partial[cta][tap][cin][cout]
+__global__ void __launch_bounds__(256) halo_wgrad_reduce_kernel(const float* __restrict__ partial, int ctas,
+                                                                 float scale, float* __restrict__ dW, long long lddw) {
+  griddep_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;   // (tap, cin, cout), cout fastest
+  if (i >= 9 * 64 * 64) return;
+  float acc = 0.f;
+  for (int c = 0; c < ctas; ++c) acc += __ldg(partial + static_cast<long long>(c) * 9 * 64 * 64 + i);
+  const int cout = i % 64, tc = i / 64;                  // tc = tap * 64 + cin
+  dW[static_cast<long long>(cout) * lddw + tc] = scale * acc;
+}
+
 }  // namespace
 
 cudaError_t launch_halo_probe(const CUtensorMap& tmX, const CUtensorMap& tmW, int n, int h0, int W, int off, int mode,
@@ -384,7 +527,7 @@ cudaError_t launch_halo_probe(const CUtensorMap& tmX, const CUtensorMap& tmW, in
   const int smem = smem_kb > 0 ? smem_kb * 1024 : (mode == 3 ? 1024 + 9 * 8192 + 96 * 1024 : 1024 + 8192 + 96 * 1024);
   cudaError_t e = cudaFuncSetAttribute(halo_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  halo_probe_kernel<<<((reps / 1000) & 1) ? 148 : 1, 128, smem, stream>>>(tmX, tmW, n, h0, W, off, mode, reps, out);
+  halo_probe_kernel<<<(mode != 4 && ((reps / 1000) & 1)) ? 148 : 1, 128, smem, stream>>>(tmX, tmW, n, h0, W, off, mode, reps, out);
   return cudaGetLastError();
 }
 
@@ -416,6 +559,32 @@ cudaError_t launch_halo_conv(const CUtensorMap& tmX, const CUtensorMap& tmW, con
   cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(halo_conv_kernel), 232448);
   if (e != cudaSuccess) return e;
   return launch_pdl(halo_conv_kernel, dim3(grid), dim3(kHaloThreads), smem, stream, 1, tmX, tmW, tmY, tmR, tmM, a, g);
+}
+
+}  // namespace edl
+
+namespace edl {
+
+long long halo_wgrad_partial_floats(int sms) { return static_cast<long long>(sms) * 9 * 64 * 64; }
+
+cudaError_t launch_halo_wgrad(const CUtensorMap& tmX, const CUtensorMap& tmD, const HaloArgs& a, int grid,
+                              float* partial, float scale, float* dW, long long lddw, cudaStream_t stream) {
+  WgGeom g{};
+  g.patch_bytes = static_cast<uint32_t>((a.R + 2) * (a.W + 2)) * 128u;
+  // A views reach 2 (W + 2) + 2 + 127 rows into the patch (the rows past it read the zeroed tail)
+  const uint32_t view = static_cast<uint32_t>(2 * (a.W + 2) + 2 + 128) * 128u;
+  const uint32_t pbytes = ((g.patch_bytes > view ? g.patch_bytes : view) + 1023) & ~1023u;
+  g.dz_bytes = static_cast<uint32_t>(a.R * (a.W + 2)) * 128u;
+  g.dz_off = pbytes;
+  g.stage_bytes = pbytes + 128u * 128u;                  // dz: 128 pixel rows of 128 B (tail zero)
+  const int smem = 1024 + kWgStages * static_cast<int>(g.stage_bytes) + 256;
+  if (smem > 232448 || a.R * (a.W + 2) > 128) return cudaErrorInvalidValue;
+  cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(halo_wgrad_kernel), 232448);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(halo_wgrad_kernel, dim3(grid), dim3(kWgThreads), smem, stream, 1, tmX, tmD, a, g, partial);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(halo_wgrad_reduce_kernel, dim3((9 * 64 * 64 + 255) / 256), dim3(256), 0, stream, 1,
+                    static_cast<const float*>(partial), grid, scale, dW, lddw);
 }
 
 }  // namespace edl

@@ -196,6 +196,11 @@ struct HaloArgs {
   int debug;                        // timing experiments (EDL_HALO_DEBUG): 1 no epilogue math / stores, 2 one patch load
 };
 int halo_rows_per_tile(int W);
+// halo weight gradient (same layers): dW[cout][(r, s, c)] = scale * sum dz x;
+// partial: halo_wgrad_partial_floats(grid) floats
+long long halo_wgrad_partial_floats(int sms);
+cudaError_t launch_halo_wgrad(const CUtensorMap& tmX, const CUtensorMap& tmD, const HaloArgs& a, int grid,
+                              float* partial, float scale, float* dW, long long lddw, cudaStream_t stream);
 cudaError_t launch_halo_conv(const CUtensorMap& tmX, const CUtensorMap& tmW, const CUtensorMap& tmY,
                              const CUtensorMap& tmR, const CUtensorMap& tmM, const HaloArgs& a, int grid,
                              cudaStream_t stream);

@@ -1,5 +1,5 @@
-"""One 64 -> 64 3x3 stride-1 conv (cfg4 stage 1: 256 x 56 x 56) forward and
-data gradient through the C-ABI, CUDA-event timed (or once under ncu with
+"""One 64 -> 64 3x3 stride-1 conv (cfg4 stage 1: 256 x 56 x 56) forward,
+data gradient and weight gradient through the C-ABI, CUDA-event timed (or once under ncu with
 NCU=1). EDL_HALO=0 selects the TMA-im2col GEMM path instead of the halo conv.
     python scripts/conv64_bench.py [--N 256] [--H 56]"""
 import argparse
@@ -37,14 +37,22 @@ def main():
     def dgrad():
         _lib.call("edl_conv_dgrad_nhwc", x.data_ptr(), N, H, H, 64, wf.data_ptr(), 576, 64, 3, 3, 1, None,
                   y.data_ptr(), dx.data_ptr(), s)
+
+    ws = torch.empty(int(_lib.load().edl_bwd_weight_workspace_floats(N * H * H, 64, 576)), device="cuda")
+    dw = torch.empty(64, 576, device="cuda")
+
+    def wgrad():
+        _lib.call("edl_conv_bwd_weight_nhwc", x.data_ptr(), N, H, H, 64, 3, 3, 1, 1, y.data_ptr(), 64, 64,
+                  dw.data_ptr(), 576, None, ws.data_ptr(), ws.numel(), 1.0, s)
     if os.environ.get("NCU"):
         fwd()
         dgrad()
+        wgrad()
         torch.cuda.synchronize()
         return
     flop = 2.0 * N * H * H * 64 * 576
     res = {"halo": os.environ.get("EDL_HALO", "1")}
-    for name, fn in (("fwd", fwd), ("dgrad", dgrad)):
+    for name, fn in (("fwd", fwd), ("dgrad", dgrad), ("wgrad", wgrad)):
         for _ in range(3):
             fn()
         torch.cuda.synchronize()

@@ -43,6 +43,29 @@ def test_halo_probe_row_shifted_operand(h0, off):
     assert res[0] < 1e-2 and res[2] < 1e-2, res     # the base-offset field must stay 0 (mode 1 is wrong)
 
 
+@pytest.mark.parametrize("off,delta", [(0, 1), (3, 56), (10, 59), (2, 118)])
+def test_halo_probe_mn_major_stacked_views(off, delta):
+    """Mode 4: an MN-major A operand whose two 64-wide M halves are the patch
+    viewed at rows off and off + delta (LBO = delta rows of 128 B), B the
+    weight tile read MN-major: the halo weight-gradient layout (two filter
+    taps per 128-row UMMA)."""
+    from paper_2207_06667_b200 import _lib
+    N, H, W = 1, 56, 56
+    g = torch.Generator().manual_seed(off * 131 + delta)
+    x = torch.randn(N, H, W, 64, generator=g).to(torch.bfloat16)
+    w = torch.randn(64, 64, generator=g).to(torch.bfloat16)
+    p = torch.cat([_patch(x, 0, 20, W), torch.zeros(256, 64)])
+    out = torch.zeros(128 * 64 + 2, device="cuda")
+    _lib.call("edl_halo_probe", x.cuda().data_ptr(), N, H, W, 0, 20, off, w.cuda().data_ptr(), 4, delta, 0,
+              out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    got = out[:128 * 64].view(128, 64).cpu()
+    want = torch.cat([p[off:off + 64].T @ w.float(), p[off + delta:off + delta + 64].T @ w.float()])
+    err = (got - want).abs().max().item()
+    print("mn-stacked", off, delta, err)
+    assert err < 1e-2, err
+
+
 def test_halo_probe_mma_throughput():
     """Cycles for 9 taps x 4 UMMAs (128 x 64 x 16) x reps from the staged
     patch: the no-swizzle chunk-plane layout vs SWIZZLE_128B rows."""
@@ -143,3 +166,52 @@ def test_halo_conv_bitwise_vs_im2col_gemm_and_torch(case, tmp_path):
         want = torch.relu(want)
     got = y.float().permute(0, 3, 1, 2)
     assert ((got - want).norm() / want.norm()).item() < 1e-2
+
+
+def _run_wgrad(case, seed, out_path=None):
+    from paper_2207_06667_b200 import _lib
+    N, H, W = case
+    g = torch.Generator().manual_seed(seed)
+    x = torch.randn(N, H, W, 64, generator=g).to(torch.bfloat16).cuda()
+    dz = (torch.randn(N, H, W, 64, generator=g) * 0.1).to(torch.bfloat16).cuda()
+    s = torch.cuda.current_stream().cuda_stream
+    ws = torch.empty(int(_lib.load().edl_bwd_weight_workspace_floats(N * H * W, 64, 576)), device="cuda")
+    outs = []
+    for _ in range(2):   # determinism: two runs
+        dw = torch.full((64, 576), float("nan"), device="cuda")
+        _lib.call("edl_conv_bwd_weight_nhwc", x.data_ptr(), N, H, W, 64, 3, 3, 1, 1, dz.data_ptr(), 64, 64,
+                  dw.data_ptr(), 576, None, ws.data_ptr(), ws.numel(), 0.5, s)
+        torch.cuda.synchronize()
+        outs.append(dw.cpu())
+    if out_path:
+        torch.save(outs[0], out_path)
+    return outs, x.cpu(), dz.cpu()
+
+
+@pytest.mark.parametrize("case", [(2, 14, 14), (3, 17, 17), (1, 9, 62), (8, 56, 56), (2, 7, 30)])
+def test_halo_wgrad_vs_im2col_and_torch(case, tmp_path):
+    """The halo weight gradient (edl_conv_bwd_weight_nhwc for 64 -> 64 3x3
+    stride-1 layers without db) against the im2col split-K path (EDL_HALO=0 in
+    a subprocess; fp32 sums in another order: <= 1e-5 relative) and torch's
+    fp32 dz^T im2col(x) (<= 1e-3); deterministic (two runs bitwise equal)."""
+    import subprocess
+    import sys
+
+    import torch.nn.functional as F
+    seed = sum(case) * 7
+    (a, b), x, dz = _run_wgrad(case, seed)
+    assert torch.equal(a, b)
+    assert torch.isfinite(a).all()
+    ref_path = str(tmp_path / "ref.pt")
+    code = ("import sys, torch; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+            "import test_gpu_halo as t;"
+            f"t._run_wgrad({case!r}, {seed}, {ref_path!r})")
+    env = dict(__import__("os").environ, EDL_HALO="0")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=300)
+    ref = torch.load(ref_path)
+    assert ((a - ref).norm() / ref.norm()).item() < 1e-5
+    N, H, W = case
+    cols = F.unfold(x.float().permute(0, 3, 1, 2), 3, padding=1)          # [N][C*9][HW], (c, r, s) order
+    cols = cols.view(N, 64, 9, H * W).permute(0, 3, 2, 1).reshape(N * H * W, 576)   # -> (r, s, c)
+    want = 0.5 * dz.float().reshape(-1, 64).T @ cols
+    assert ((a - want).norm() / want.norm()).item() < 1e-3
