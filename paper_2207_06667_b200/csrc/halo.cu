@@ -398,7 +398,8 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
 // tap pairs with itself) accumulate in five TMEM accumulators over all of a
 // CTA's tiles; the CTA writes its partial [tap][cin][cout] once and
 // halo_wgrad_reduce_kernel adds the CTAs' partials in CTA order
-// (deterministic). Two warps issue the MMAs (pairs 0-2 / 3-4).
+// (deterministic). Three warps issue the MMAs (an N = 64 UMMA retires about
+// as fast as one thread issues it).
 constexpr int kWgStages = 3;
 constexpr int kWgThreads = 256;
 
@@ -428,8 +429,8 @@ __global__ void __launch_bounds__(kWgThreads, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmX);
     prefetch_tmap(&tmD);
-    for (int i = 0; i < kWgStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 2); }
-    mbar_init(done, 2);
+    for (int i = 0; i < kWgStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 3); }
+    mbar_init(done, 3);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(tslot);
@@ -450,9 +451,10 @@ __global__ void __launch_bounds__(kWgThreads, 1)
       tma_load_4d(&tmX, smem_u32(st), smem_u32(&full[s]), 0, -1, h0 - 1, n);
       tma_load_4d(&tmD, smem_u32(st + g.dz_off), smem_u32(&full[s]), 0, 0, h0, n);
     }
-  } else if ((warp == 1 || warp == 3) && lane == 0) {
+  } else if (warp >= 1 && warp <= 3 && lane == 0) {
+    // three issuers: tap pairs {0, 1}, {2, 3}, {4} (16 / 16 / 8 UMMAs per tile)
     constexpr uint32_t idesc = idesc_bf16_f32(128, 64, true, true);
-    const int p_lo = warp == 1 ? 0 : 3, p_hi = warp == 1 ? 3 : 5;
+    const int p_lo = warp == 1 ? 0 : warp == 2 ? 2 : 4, p_hi = warp == 1 ? 2 : warp == 2 ? 4 : 5;
     const uint64_t a0 = smem_desc_sw128(smem_u32(sS), 16, 1024);
     const uint64_t b0 = smem_desc_sw128(smem_u32(sS + g.dz_off), 8192, 1024);
     int it = 0;
@@ -502,6 +504,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
+    __syncwarp();   // lane 0 ran an MMA role: dealloc is .sync.aligned
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
