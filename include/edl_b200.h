@@ -342,7 +342,11 @@ int edl_cast_bf16_f64(const double* src, long long ld_src, void* dst, long long 
  * configs[3]; the reference has no convolutions). z / g / y / dz
  * are NHWC bf16 rows [M = N*H*W][C], C % 8 == 0 and <= 2048; per-channel
  * fp32 vectors [C]. Batch statistics are biased (nn.BatchNorm2d training
- * mode); reductions are deterministic (fixed row blocks, fp64 final sums).
+ * mode); reductions are deterministic (fixed row blocks, cluster partials
+ * combined in rank order, fp64 final sums) and take one launch each: the last
+ * block to arrive finishes, counted on a per-(device, stream) ticket from a
+ * static pool (as the GEMM tile counters: a graph captured on stream S uses
+ * S's ticket, so do not replay it while eager BN calls run on S).
  *   stats:  mean, rstd = 1 / sqrt(var + eps)
  *   apply:  y = [relu](gamma (z - mean) rstd + beta [+ residual])
  *   bwd:    dbeta = sum g, dgamma = sum g xhat (written, not accumulated),
