@@ -127,6 +127,10 @@ int edl_conv_bwd_weight_nhwc(const void* x, int N, int H, int W, int C, int R, i
  * output. Replaces edl_linear_bwd_data + edl_col2im_nhwc for stride 1. */
 int edl_conv_flip_weights(const void* w, long long ldw, int K, int C, int R, int S, void* wf, long long ldf,
                           void* stream);
+/* The same for `count` (<= 24) layers in one launch: arrays of the
+ * per-layer arguments above (host memory). */
+int edl_conv_flip_weights_many(int count, const void* const* w, const long long* ldw, const int* K, const int* C,
+                               const int* R, const int* S, void* const* wf, const long long* ldf, void* stream);
 /* Layout probe for the halo conv (diagnostics and tests only): the 128 x 64
  * product of one tap's row-shifted view of the staged patch of image n (rows
  * h0-1 .. h0+2) with w [64][64] (mode 3: [64][576], nine taps), into out

@@ -616,6 +616,33 @@ int edl_conv_fwd_nhwc(const void* x, int N, int H, int W, int C, const void* w, 
   return e == cudaSuccess ? 0 : cuda_fail(e, "conv_fwd_nhwc");
 }
 
+int edl_conv_flip_weights_many(int count, const void* const* w, const long long* ldw, const int* K, const int* C,
+                               const int* R, const int* S, void* const* wf, const long long* ldf, void* stream) {
+  if (count < 0 || count > kMaxFlips) return fail(EDL_ERR_SHAPE, "conv_flip_weights_many: count %d (0..%d)", count,
+                                                  kMaxFlips);
+  FlipGroup g{};
+  g.count = count;
+  long long total = 0;
+  for (int l = 0; l < count; ++l) {
+    if (K[l] < 1 || C[l] < 1 || R[l] < 1 || S[l] < 1 || ldw[l] < static_cast<long long>(R[l]) * S[l] * C[l] ||
+        ldf[l] < static_cast<long long>(R[l]) * S[l] * K[l] || !w[l] || !wf[l])
+      return fail(EDL_ERR_SHAPE, "conv_flip_weights_many: bad layer %d", l);
+    g.start[l] = static_cast<int>(total);
+    g.K[l] = K[l];
+    g.C[l] = C[l];
+    g.RS[l] = R[l] * S[l];
+    g.ldw[l] = ldw[l];
+    g.ldf[l] = ldf[l];
+    g.w[l] = static_cast<const __nv_bfloat16*>(w[l]);
+    g.wf[l] = static_cast<__nv_bfloat16*>(wf[l]);
+    total += static_cast<long long>(C[l]) * R[l] * S[l] * K[l];
+    if (total > (1LL << 31) - 1) return fail(EDL_ERR_SHAPE, "conv_flip_weights_many: too many elements");
+  }
+  g.start[count] = static_cast<int>(total);
+  cudaError_t e = launch_conv_flip_weights_many(g, as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "conv_flip_weights_many");
+}
+
 int edl_conv_flip_weights(const void* w, long long ldw, int K, int C, int R, int S, void* wf, long long ldf,
                           void* stream) {
   if (K < 1 || C < 1 || R < 1 || S < 1 || ldw < static_cast<long long>(R) * S * C ||

@@ -817,6 +817,30 @@ __global__ void __launch_bounds__(256) conv_flip_weights_kernel(const __nv_bfloa
   }
 }
 
+// Every layer's flip in one launch (the student's 13 stride-1 layers cost 13
+// small launches, ~106 us): a grid-stride walk over the concatenated element
+// ranges, each element finding its layer by the prefix offsets.
+__global__ void __launch_bounds__(256) conv_flip_weights_many_kernel(FlipGroup g) {
+  griddep_wait();
+  const int total = g.start[g.count];
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < total; o += gridDim.x * blockDim.x) {
+    int l = 0;
+    while (o >= g.start[l + 1]) ++l;
+    const int r = o - g.start[l];
+    const int K = g.K[l], C = g.C[l], RS = g.RS[l];
+    const int k = r % K, t = r / K;
+    const int rs = t % RS, c = t / RS;
+    g.wf[l][c * g.ldf[l] + static_cast<long long>(rs) * K + k] =
+        g.w[l][k * g.ldw[l] + static_cast<long long>(RS - 1 - rs) * C + c];
+  }
+}
+
+cudaError_t launch_conv_flip_weights_many(const FlipGroup& g, cudaStream_t stream) {
+  const int total = g.start[g.count];
+  if (total <= 0) return cudaSuccess;
+  return launch_pdl(conv_flip_weights_many_kernel, dim3(grid_for(total)), dim3(256), 0, stream, 1, g);
+}
+
 cudaError_t launch_conv_flip_weights(const __nv_bfloat16* w, long long ldw, int K, int C, int R, int S,
                                      __nv_bfloat16* wf, long long ldf, cudaStream_t stream) {
   const long long work = static_cast<long long>(C) * R * S * K;

@@ -183,6 +183,18 @@ cudaError_t launch_maxpool_bwd_nhwc(const __nv_bfloat16* x, int N, int H, int W,
                                     int P, int Q, const __nv_bfloat16* dy, const __nv_bfloat16* mask,
                                     __nv_bfloat16* dx, cudaStream_t stream);
 
+// many layers' weight flips (conv.cu) in one launch
+constexpr int kMaxFlips = 24;
+struct FlipGroup {
+  int count;
+  int start[kMaxFlips + 1];                 // element offsets, start[count] = total
+  int K[kMaxFlips], C[kMaxFlips], RS[kMaxFlips];
+  long long ldw[kMaxFlips], ldf[kMaxFlips];
+  const __nv_bfloat16* w[kMaxFlips];
+  __nv_bfloat16* wf[kMaxFlips];
+};
+cudaError_t launch_conv_flip_weights_many(const FlipGroup& g, cudaStream_t stream);
+
 // halo-tiled 3x3 convolution (halo.cu): C = K = 64, stride 1, pad 1, W + 2 <= 128;
 // out = [relu](conv + bias [+ res]), then * (mask > 0) when mask is given
 struct HaloArgs {

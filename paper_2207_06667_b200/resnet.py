@@ -443,6 +443,19 @@ class ResNetStudent:
         # the flipped filter (refreshed from the forward's bf16 weights each step)
         self.wflip = [torch.empty(c.cin_p, c.k * c.k * c.cout_p, dtype=torch.bfloat16, device=dev)
                       if i > 0 and self._dgrad_implicit(c) else None for i, c in enumerate(self.convs)]
+        import ctypes
+        fl = [(c, p, wf) for c, p, wf in zip(self.convs, self.params, self.wflip) if wf is not None]
+        n = len(fl)
+        self._flip_keep = (
+            (ctypes.c_void_p * n)(*[self._w16(p).data_ptr() for _, p, _ in fl]),
+            (ctypes.c_longlong * n)(*[c.kdim for c, _, _ in fl]),
+            (ctypes.c_int * n)(*[c.cout_p for c, _, _ in fl]),
+            (ctypes.c_int * n)(*[c.cin_p for c, _, _ in fl]),
+            (ctypes.c_int * n)(*[c.k for c, _, _ in fl]),
+            (ctypes.c_int * n)(*[c.k for c, _, _ in fl]),
+            (ctypes.c_void_p * n)(*[wf.data_ptr() for _, _, wf in fl]),
+            (ctypes.c_longlong * n)(*[wf.stride(0) for _, _, wf in fl]))
+        self._flip_args = (n, *[ctypes.cast(a, ctypes.c_void_p) for a in self._flip_keep])
         self.col = torch.empty(col, dtype=torch.bfloat16, device=dev)
         # backward buffers: gradient ping-pong at the largest activation size + a shortcut buffer
         big = max(B * h * w * stem.cout_p, max(a[1].numel() for a in self.acts))
@@ -639,10 +652,8 @@ class ResNetStudent:
         s = (stream or torch.cuda.current_stream()).cuda_stream
         B = self.B
         self._features_into(x, s)
-        for c, p, wf in zip(self.convs, self.params, self.wflip):
-            if wf is not None:
-                _lib.call("edl_conv_flip_weights", self._w16(p).data_ptr(), c.kdim, c.cout_p, c.cin_p, c.k, c.k,
-                          wf.data_ptr(), wf.stride(0), s)
+        # every stride-1 layer's flipped filter, in one launch
+        _lib.call("edl_conv_flip_weights_many", *self._flip_args, s)
         q_vals = soft.probs if (soft is not None and beta > 0) else None
         q_idx = soft.classes if (soft is not None and beta > 0) else None
         k = soft.probs.shape[1] if q_vals is not None else 0

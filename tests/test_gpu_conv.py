@@ -656,3 +656,30 @@ def test_col2im_stride2_vs_fold(N, H, C, k, pad):
     for got, exp in ((dx, want), (dx2, want2)):
         g = got.float().cpu()
         assert torch.allclose(g, exp, rtol=8e-3, atol=1e-6), (g - exp).abs().max()
+
+
+def test_conv_flip_weights_many_equals_per_layer():
+    """edl_conv_flip_weights_many (one launch) writes exactly what one
+    edl_conv_flip_weights call per layer writes, for mixed shapes."""
+    import ctypes
+
+    from paper_2207_06667_b200 import _lib
+    g = torch.Generator().manual_seed(5)
+    shapes = [(64, 64, 3), (128, 64, 3), (24, 40, 1), (512, 256, 3)]   # (K, C, k)
+    ws, wfs, ref = [], [], []
+    for K, C, k in shapes:
+        w = torch.randn(K, k * k * C + 8, generator=g).to(torch.bfloat16).cuda()    # padded ldw
+        ws.append(w)
+        wfs.append(torch.zeros(C, k * k * K + 16, dtype=torch.bfloat16, device="cuda"))
+        r = torch.zeros_like(wfs[-1])
+        _lib.call("edl_conv_flip_weights", w.data_ptr(), w.stride(0), K, C, k, k, r.data_ptr(), r.stride(0), _s())
+        ref.append(r)
+    n = len(shapes)
+    arrs = ((ctypes.c_void_p * n)(*[w.data_ptr() for w in ws]), (ctypes.c_longlong * n)(*[w.stride(0) for w in ws]),
+            (ctypes.c_int * n)(*[K for K, _, _ in shapes]), (ctypes.c_int * n)(*[C for _, C, _ in shapes]),
+            (ctypes.c_int * n)(*[k for _, _, k in shapes]), (ctypes.c_int * n)(*[k for _, _, k in shapes]),
+            (ctypes.c_void_p * n)(*[f.data_ptr() for f in wfs]), (ctypes.c_longlong * n)(*[f.stride(0) for f in wfs]))
+    _lib.call("edl_conv_flip_weights_many", n, *[ctypes.cast(a, ctypes.c_void_p) for a in arrs], _s())
+    torch.cuda.synchronize()
+    for a, b in zip(wfs, ref):
+        assert torch.equal(a, b)
