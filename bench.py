@@ -364,7 +364,7 @@ def main():
     student_stream = (torch.cuda.Stream(dev, priority=-1) if args.student_priority == "high"
                       else torch.cuda.current_stream(dev))
 
-    host_s = [0.0]
+    host_s = [0.0, 0.0]
 
     def edl_run(start, count, timed):
         reader = DistilReader(f"student-{rank}", pool, sched, sampler, start, start + count, 1, EventLog(),
@@ -380,12 +380,16 @@ def main():
         with torch.cuda.stream(student_stream):
             s.record()
             h0 = time.perf_counter()
+            wait = 0.0
             for it in range(start, start + count):
+                c0 = time.perf_counter()
                 soft = reader.consume(it)
+                wait += time.perf_counter() - c0
                 # the teacher worker gathered this iteration's rows into the slot
                 batch = soft.batch if soft.batch is not None else sampler.batch_for(it, out=engine.batch)
                 engine.step(batch, soft)
-            host_s[0] = (time.perf_counter() - h0) / count   # host enqueue time per step (incl. waits)
+            host_s[0] = (time.perf_counter() - h0) / count   # host time per step (incl. waits)
+            host_s[1] = wait / count                           # of which in reader.consume (soft-label waits)
             engine.settle()   # N>1: the last step's exchange + SGD run on a comm stream
             e.record()
         if timed:
@@ -513,6 +517,8 @@ def main():
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "online": online,
             "gpu_launches": launches, "clocks": clocks, "ledger_ok": ledger["ok"],
             "host_ms_per_step": round(host_s[0] * 1e3, 4),
+            "host_consume_wait_ms_per_step": round(host_s[1] * 1e3, 4),
+            "host_enqueue_ms_per_step": round((host_s[0] - host_s[1]) * 1e3, 4),
             "algorithmic_flop_per_sample": {"teacher_fwd": tflop_t, "student_train": tflop_s},
         }
         line["tensor_roofline_samples_per_s"] = round(world * peak_sust * 1e12 / (tflop_t + tflop_s), 1)
