@@ -11,8 +11,8 @@
 // row-range blocks (8 channels per thread, 16 loads in flight per thread, row
 // lanes combined in a fixed order through shared memory), the cluster's 8
 // block sums added in rank order over DSMEM into one fp64 partial per
-// cluster (each rank one eighth of the channels), and the last block to
-// arrive (a per-stream ticket) adds the
+// cluster (each rank one eighth of the channels), and the last cluster to
+// arrive (a per-stream ticket; its 8 CTAs one eighth of the channels each) adds the
 // cluster partials in cluster order: deterministic, independent of timing.
 // The elementwise passes keep each thread on one 8-channel group (its
 // per-channel constants in registers) and walk the rows back to front, so
@@ -34,7 +34,7 @@ int bn_stats_blocks(int M, int C, int sms) {
   int g = 4 * sms;
   const int min_rows = 64;
   if (g > (M + min_rows - 1) / min_rows) g = (M + min_rows - 1) / min_rows;
-  const int max_clusters = 8192 / C > 1 ? 8192 / C : 1;
+  const int max_clusters = 65536 / C > 1 ? 65536 / C : 1;   // finish: clusters x C / 8 per CTA
   if (g > max_clusters * kBnCluster) g = max_clusters * kBnCluster;
   g = (g + kBnCluster - 1) / kBnCluster * kBnCluster;
   return g < kBnCluster ? kBnCluster : g;
@@ -76,10 +76,11 @@ __device__ __forceinline__ uint4 pack8(const float* v) {
 // MODE 0: out1 = mean, out2 = rstd = 1 / sqrt(var + eps); MODE 1: out1 = dbeta, out2 = dgamma
 template <int MODE>
 __device__ void bn_finish(const double* partial, int Gc, int C, int M, float eps, float* out1, float* out2,
-                          double* scratch) {
-  const int L = C < kBnThreads ? kBnThreads / C : 1;
-  for (int c0 = 0; c0 < C; c0 += kBnThreads) {
-    const int nc = C - c0 < kBnThreads ? C - c0 : kBnThreads;
+                          double* scratch, int cb, int ce) {
+  const int span = ce - cb;
+  const int L = span < kBnThreads ? kBnThreads / span : 1;
+  for (int c0 = cb; c0 < ce; c0 += kBnThreads) {
+    const int nc = ce - c0 < kBnThreads ? ce - c0 : kBnThreads;
     const int t = threadIdx.x;
     const int c = t % nc, lane = t / nc;
     double t1 = 0.0, t2 = 0.0;
@@ -230,16 +231,21 @@ __global__ void __launch_bounds__(kBnThreads) bn_reduce_kernel(const __nv_bfloat
   cluster_sync();                            // every rank's csum stays alive until the cluster has read it
   if (ticket == nullptr) return;
   __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  cluster_sync();                            // the cluster's partial is written before it is counted
+  if (rank == 0 && threadIdx.x == 0) {
     const unsigned t = atomicAdd(ticket, 1u);
-    s_last = t == gridDim.x - 1;
-    if (s_last) *ticket = 0u;               // every block has arrived: leave the counter zeroed
+    const int last = t == static_cast<unsigned>(gridDim.x / kBnCluster - 1);
+    if (last) *ticket = 0u;                  // every cluster has arrived: leave the counter zeroed
+#pragma unroll
+    for (int k = 0; k < kBnCluster; ++k) st_dsmem_s32(mapa(smem_u32(&s_last), k), last);
   }
-  __syncthreads();
+  cluster_sync();
   if (!s_last) return;
   __threadfence();
-  bn_finish<MODE>(partial, gridDim.x / kBnCluster, C, M, eps, out1, out2, reinterpret_cast<double*>(red));
+  // the last cluster finishes: each rank one eighth of the channels
+  const int per = C / kBnCluster;
+  bn_finish<MODE>(partial, gridDim.x / kBnCluster, C, M, eps, out1, out2, reinterpret_cast<double*>(red),
+                  static_cast<int>(rank) * per, static_cast<int>(rank + 1) * per);
 }
 
 // Without a ticket counter: the finishing pass as its own launch.
@@ -249,7 +255,7 @@ __global__ void __launch_bounds__(kBnThreads) bn_finish_kernel(const double* __r
                                                                float* __restrict__ out2) {
   griddep_wait();
   __shared__ double scratch[2 * kBnThreads];
-  bn_finish<MODE>(partial, Gc, C, M, eps, out1, out2, scratch);
+  bn_finish<MODE>(partial, Gc, C, M, eps, out1, out2, scratch, 0, C);
 }
 
 // y = act(gamma (z - mean) rstd + beta [+ res])
