@@ -18,7 +18,7 @@ import torch
 
 from . import _lib
 from .formats import Dataset, epoch_order
-from .nnkit import Batch, pad
+from .nnkit import Batch, img_pad, pad
 
 
 class DeviceDataset:
@@ -38,7 +38,7 @@ class DeviceDataset:
 
 class DeviceImageDataset:
     """cfg4's synthetic image set, HBM-resident: n NHWC bf16 images
-    [image][image][pad(channels)] stored as rows of one [n][image*image*pad(c)]
+    [image][image][img_pad(channels)] stored as rows of one [n][image*image*img_pad(c)]
     matrix (so DeviceShardSampler / gather_rows select batches by row index,
     as for the MLP datasets) + int64 labels. Deterministic in (seed, n,
     image, classes): every teacher and student process builds the same set."""
@@ -47,7 +47,7 @@ class DeviceImageDataset:
                  device=None, chunk: int = 64):
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.image, self.channels, self.classes = image, channels, classes
-        self.cp = pad(channels)
+        self.cp = img_pad(channels)
         self.size = n
         self.dim = image * image * self.cp
         self.id = f"images-{seed}-{n}-{image}-{classes}"
@@ -61,7 +61,7 @@ class DeviceImageDataset:
         self.labels = torch.from_numpy(rng.integers(0, classes, size=n).astype(np.int64)).to(self.device)
 
     def nhwc(self, rows_view: torch.Tensor) -> torch.Tensor:
-        """A gathered [B][dim] batch as NHWC [B][image][image][pad(c)]."""
+        """A gathered [B][dim] batch as NHWC [B][image][image][img_pad(c)]."""
         return rows_view.view(rows_view.shape[0], self.image, self.image, self.cp)
 
 

@@ -44,6 +44,13 @@ def pad(n: int) -> int:
     return (int(n) + PAD - 1) // PAD * PAD
 
 
+def img_pad(c: int) -> int:
+    """Channel pitch of NHWC image inputs: 8 for the RGB stems' packed im2col
+    (< 8 channels: one 16-byte load per pixel, half the bytes of a 16-pitch),
+    else pad(c)."""
+    return 8 if int(c) < 8 else pad(c)
+
+
 def _stream(stream=None) -> int:
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream

@@ -20,7 +20,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .nnkit import SoftLabels, pad
+from .nnkit import SoftLabels, img_pad, pad
 
 
 @dataclass(frozen=True)
@@ -109,7 +109,7 @@ class _DevConv:
     def __init__(self, c: HostConv, dev):
         cout, cin, k, _ = c.w.shape
         self.k, self.stride, self.pad, self.relu = k, c.stride, c.pad, c.relu
-        self.cin, self.cin_p, self.cout_p = cin, pad(cin), pad(cout)
+        self.cin, self.cin_p, self.cout_p = cin, img_pad(cin), pad(cout)
         self.packed = cin < 8
         wt = c.w.transpose(0, 2, 3, 1)                      # [cout][k][k][cin]
         if self.packed:
@@ -166,7 +166,7 @@ class ResNetTeacher:
         self.classes = host.fc_w.shape[0]
         # shapes + buffers
         H = W = self.cfg.image
-        self.in_c = pad(self.cfg.in_channels)
+        self.in_c = img_pad(self.cfg.in_channels)
         h, w = self.stem.out_hw(H, W)
         col = B * h * w * self.stem.kdim
         self.x0 = torch.empty(B, h, w, self.stem.cout_p, dtype=torch.bfloat16, device=dev)
@@ -218,7 +218,7 @@ class ResNetTeacher:
         return oh, ow
 
     def features(self, x: torch.Tensor, stream=None) -> torch.Tensor:
-        """x: NHWC bf16 [B][image][image][pad(in_channels)] -> pooled features bf16 [B][feat_p]."""
+        """x: NHWC bf16 [B][image][image][img_pad(in_channels)] -> pooled features bf16 [B][feat_p]."""
         if tuple(x.shape) != (self.B, self.cfg.image, self.cfg.image, self.in_c) or x.dtype != torch.bfloat16:
             raise ValueError(f"expected NHWC bf16 {(self.B, self.cfg.image, self.cfg.image, self.in_c)}")
         s = (stream or torch.cuda.current_stream()).cuda_stream
@@ -279,9 +279,10 @@ class ResNetTeacher:
 
 
 def to_nhwc(images: np.ndarray, device) -> torch.Tensor:
-    """NCHW float images -> NHWC bf16 with channels padded to 16."""
+    """NCHW float images -> NHWC bf16 with channels padded to img_pad(c)
+    (8 for RGB, the packed stems' input pitch)."""
     n, c, h, w = images.shape
-    x = torch.zeros(n, h, w, pad(c), dtype=torch.bfloat16, device=device)
+    x = torch.zeros(n, h, w, img_pad(c), dtype=torch.bfloat16, device=device)
     x[..., :c] = torch.from_numpy(np.ascontiguousarray(images.transpose(0, 2, 3, 1), dtype=np.float32)).to(device).to(torch.bfloat16)
     return x
 

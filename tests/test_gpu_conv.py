@@ -601,22 +601,25 @@ def test_conv_dgrad_implicit_vs_torch(N, C, H, K, k, use_add, use_mask):
     assert _rel(got, want) < 1e-2
 
 
-@pytest.mark.parametrize("N,H", [(2, 224), (3, 30)])
-def test_packed_stem_im2col_bitwise(N, H):
-    """edl_im2col_nhwc packed (c_used = 3 of 16 channels, 7x7 / 2 / pad 3,
-    ldo 160: the compile-time stem instance) against torch unfold, bit for
-    bit: K order (r, s, c), zeros outside the image and in the K padding."""
+@pytest.mark.parametrize("N,H,C", [(2, 224, 8), (3, 30, 8), (2, 30, 16)])
+def test_packed_stem_im2col_bitwise(N, H, C):
+    """edl_im2col_nhwc packed (c_used = 3 of C = 8 (to_nhwc's RGB pitch) or
+    16 channels, 7x7 / 2 / pad 3, ldo 160: the compile-time stem instance)
+    against torch unfold, bit for bit: K order (r, s, c), zeros outside the
+    image and in the K padding."""
     import torch.nn.functional as F
 
     from paper_2207_06667_b200 import _lib
     from paper_2207_06667_b200.resnet import to_nhwc
     rng = np.random.default_rng(H)
     imgs = rng.normal(size=(N, 3, H, H)).astype(np.float32)
-    x = to_nhwc(imgs, "cuda")                                  # [N][H][W][16] bf16
-    assert x.shape[-1] == 16
+    x = to_nhwc(imgs, "cuda")                                  # [N][H][W][8] bf16
+    assert x.shape[-1] == 8
+    if C != 8:
+        x = torch.nn.functional.pad(x, (0, C - 8)).contiguous()
     P = (H + 6 - 7) // 2 + 1
     cols = torch.full((N * P * P, 160), 7.0, dtype=torch.bfloat16, device="cuda")
-    _lib.call("edl_im2col_nhwc", x.data_ptr(), N, H, H, 16, 3, 7, 7, 2, 3, cols.data_ptr(), 160, _s())
+    _lib.call("edl_im2col_nhwc", x.data_ptr(), N, H, H, C, 3, 7, 7, 2, 3, cols.data_ptr(), 160, _s())
     torch.cuda.synchronize()
     xb = x[..., :3].permute(0, 3, 1, 2).float().cpu()         # exact bf16 values
     u = F.unfold(xb, 7, padding=3, stride=2)                   # [N][(c, r, s)][P*P]
