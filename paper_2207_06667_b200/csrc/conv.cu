@@ -616,13 +616,17 @@ __global__ void __launch_bounds__(256) maxpool_bwd_argmax_nhwc_kernel(const uint
 // words, dy vectors and the mask are all loaded up front from clamped
 // addresses (invalid windows masked afterwards). Same (r, s) summation
 // order as the generic kernel, whose branches serialised the loads.
+// CV > 0: the channel vectors per pixel at compile time (8 for the 64-channel
+// stem): the per-item (w, c8) split becomes a shift and a mask (ncu: the
+// runtime divisions kept the issue slots 84% busy at 1.8 TB/s).
+template <int CV>
 __global__ void __launch_bounds__(256) maxpool3s2_bwd_nhwc_kernel(const uint32_t* __restrict__ argmax, int N,
                                                                   int H, int W, int C, int pad, int P, int Q,
                                                                   const __nv_bfloat16* __restrict__ dy,
                                                                   const __nv_bfloat16* __restrict__ mask,
                                                                   __nv_bfloat16* __restrict__ dx) {
   griddep_wait();
-  const int cv = C / 8;
+  const int cv = CV > 0 ? CV : C / 8;
   const int n = blockIdx.x / H, h = blockIdx.x - n * H;   // one block per input row (n, h)
   const int r0 = (h + pad) & 1;
   bool rok[2];
@@ -793,8 +797,10 @@ cudaError_t launch_maxpool_bwd_argmax_nhwc(const uint32_t* argmax, int N, int H,
   if (rows > 0x7fffffffLL) return cudaErrorInvalidValue;
   const int threads = W * (C / 8) >= 256 ? 256 : ((W * (C / 8) + 31) / 32) * 32;
   if (k == 3 && stride == 2)
-    return launch_pdl(maxpool3s2_bwd_nhwc_kernel, dim3(static_cast<unsigned>(rows)), dim3(threads), 0, stream, 1,
-                      argmax, N, H, W, C, pad, P, Q, dy, mask, dx);
+    return C == 64 ? launch_pdl(maxpool3s2_bwd_nhwc_kernel<8>, dim3(static_cast<unsigned>(rows)), dim3(threads), 0,
+                                stream, 1, argmax, N, H, W, C, pad, P, Q, dy, mask, dx)
+                   : launch_pdl(maxpool3s2_bwd_nhwc_kernel<0>, dim3(static_cast<unsigned>(rows)), dim3(threads), 0,
+                                stream, 1, argmax, N, H, W, C, pad, P, Q, dy, mask, dx);
   return launch_pdl(maxpool_bwd_argmax_nhwc_kernel<0, 0>, dim3(static_cast<unsigned>(rows)), dim3(threads), 0, stream,
                     1, argmax, N, H, W, C, k, stride, pad, P, Q, dy, mask, dx);
 }
