@@ -274,6 +274,8 @@ def main():
                     help="split placement soft-label handoff: NVLink peer copy + stream flags, NCCL send/recv, or "
                          "the elastic pool (teacher ranks register in a shared-memory registry and write into the "
                          "students' CUDA-IPC rings; students dispatch by JSQ, elastic.py)")
+    ap.add_argument("--split-lt", type=int, default=12, help="elastic split: Alg. 1 resume threshold")
+    ap.add_argument("--split-ut", type=int, default=24, help="elastic split: Alg. 1 stop threshold")
     ap.add_argument("--split-depth-per-teacher", type=int, default=4,
                     help="elastic split: JSQ pipeline depth (batches in flight per teacher)")
     ap.add_argument("--no-student-graph", action="store_true",
@@ -693,7 +695,8 @@ def _elastic_split(args, cfg, world, rank, local, dev, ddata, teacher, student_h
     # teachers faster than the student the buffer cycles between the two, and
     # a low lt lets it drain below one teacher latency before the pipeline
     # refills (the student stalls every cycle); resume at half of ut instead
-    sched = SchedulerConfig(lt=12, ut=24, pipeline_depth=args.split_depth_per_teacher, acquire_cooldown=1e9)
+    sched = SchedulerConfig(lt=args.split_lt, ut=args.split_ut, pipeline_depth=args.split_depth_per_teacher,
+                            acquire_cooldown=1e9)
     pool.open(pl.n_students, s, B, cfg["topk"], 0, cfg["T"], cfg["classes"], 48, dev)
     n_mine = len(pl.teacher_ranks_of(s))
 
