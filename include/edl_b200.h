@@ -167,6 +167,13 @@ int edl_maxpool_bwd_nhwc(const void* x, int N, int H, int W, int C, int k, int s
  * edl_maxpool_nhwc / edl_maxpool_bwd_nhwc. */
 int edl_maxpool_argmax_nhwc(const void* x, int N, int H, int W, int C, int k, int stride, int pad, void* out,
                             unsigned* argmax, void* stream);
+/* Training-mode BN + ReLU fused into the 3x3 / 2 max pool with argmax (the
+ * BN student's stem): out / argmax as edl_maxpool_argmax_relu_nhwc applied to
+ * y = bf16(relu(gamma (z - mean) rstd + beta)) (edl_bn_apply_nhwc's
+ * arithmetic), computed per tap from the raw conv output z; y is not stored. */
+int edl_bn_relu_maxpool_argmax_nhwc(const void* z, int N, int H, int W, int C, const float* mean, const float* rstd,
+                                    const float* gamma, const float* beta, int k, int stride, int pad, void* out,
+                                    unsigned* argmax, void* stream);
 int edl_maxpool_bwd_argmax_nhwc(const unsigned* argmax, int N, int H, int W, int C, int k, int stride, int pad,
                                 const void* dy, const void* mask, void* dx, void* stream);
 /* edl_maxpool_argmax_nhwc for a pool whose input is a ReLU output (the

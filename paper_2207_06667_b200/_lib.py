@@ -93,6 +93,8 @@ _SIGNATURES = {
     "edl_cast_bf16": [c_void_p, c_ll, c_void_p, c_ll, c_int, c_int, c_void_p],
     "edl_cast_bf16_f64": [c_void_p, c_ll, c_void_p, c_ll, c_int, c_int, c_void_p],
     "edl_stream_delay_ns": [c_ll, c_void_p],
+    "edl_bn_relu_maxpool_argmax_nhwc": [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p,
+                                        c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p],
     "edl_conv_flip_weights_many": [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                    c_void_p, c_void_p],
     "edl_halo_probe": [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_int, c_int, c_int,

@@ -765,6 +765,20 @@ int edl_maxpool_argmax_relu_nhwc(const void* x, int N, int H, int W, int C, int 
   return maxpool_argmax_impl(x, N, H, W, C, k, stride, pad, out, argmax, true, stream);
 }
 
+int edl_bn_relu_maxpool_argmax_nhwc(const void* z, int N, int H, int W, int C, const float* mean, const float* rstd,
+                                    const float* gamma, const float* beta, int k, int stride, int pad, void* out,
+                                    unsigned* argmax, void* stream) {
+  if (N < 1 || H < 1 || W < 1 || C < 8 || C % 8 || k != 3 || stride != 2 || pad < 0 || pad >= k || !argmax || !mean ||
+      !rstd || !gamma || !beta)
+    return fail(EDL_ERR_SHAPE, "bn_relu_maxpool_argmax_nhwc: 3x3 / 2 pools with C %% 8 == 0 only");
+  const int P = (H + 2 * pad - k) / stride + 1, Q = (W + 2 * pad - k) / stride + 1;
+  if (P < 1 || Q < 1) return fail(EDL_ERR_SHAPE, "bn_relu_maxpool_argmax_nhwc: empty output");
+  cudaError_t e = launch_bn_relu_maxpool3s2_nhwc(static_cast<const __nv_bfloat16*>(z), N, H, W, C, pad, P, Q, mean,
+                                                 rstd, gamma, beta, static_cast<__nv_bfloat16*>(out),
+                                                 reinterpret_cast<uint32_t*>(argmax), as_stream(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "bn_relu_maxpool_argmax_nhwc");
+}
+
 int edl_maxpool_bwd_argmax_nhwc(const unsigned* argmax, int N, int H, int W, int C, int k, int stride, int pad,
                                 const void* dy, const void* mask, void* dx, void* stream) {
   if (N < 1 || H < 1 || W < 1 || C < 8 || C % 8 || k < 1 || k * k > 15 || stride < 1 || pad < 0 || pad >= k ||

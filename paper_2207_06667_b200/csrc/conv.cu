@@ -198,11 +198,23 @@ __global__ void __launch_bounds__(256) maxpool_nhwc_kernel(const __nv_bfloat16* 
 // in flight; the generic kernel's bounds branches serialised them (240 us at
 // batch 256, ~2.2 TB/s). Same first-maximum scan order and argmax words.
 // ARG: record argmax words (training); inference skips the nibble masks.
-template <bool ARG>
+// BN: x is the stem conv's raw output z and every tap is first taken through
+// training-mode BatchNorm + ReLU, y = bf16(relu(fma(z, gamma rstd, beta -
+// mean gamma rstd))), the exact arithmetic of bn_apply_kernel: the stem's y
+// (411 MB at batch 256) is never written nor re-read.
+struct BnPoolArgs {
+  const float* mean;
+  const float* rstd;
+  const float* gamma;
+  const float* beta;
+};
+
+template <bool ARG, bool BN = false>
 __global__ void __launch_bounds__(256) maxpool3s2_nhwc_kernel(const __nv_bfloat16* __restrict__ x, int N, int H,
                                                               int W, int C, int pad, int P, int Q,
                                                               __nv_bfloat16* __restrict__ out,
-                                                              uint32_t* __restrict__ argmax, bool relu_mask) {
+                                                              uint32_t* __restrict__ argmax, bool relu_mask,
+                                                              BnPoolArgs bn = BnPoolArgs{}) {
   griddep_wait();
   const int cv = C / 8;
   const int total = N * P * Q * cv;
@@ -224,6 +236,26 @@ __global__ void __launch_bounds__(256) maxpool3s2_nhwc_kernel(const __nv_bfloat1
         ok[3 * r + s] = h >= 0 && h < H && w >= 0 && w < W;
         const int hc = h < 0 ? 0 : (h >= H ? H - 1 : h), wc = w < 0 ? 0 : (w >= W ? W - 1 : w);
         v[3 * r + s] = __ldg(reinterpret_cast<const uint4*>(x + ((static_cast<long long>(n) * H + hc) * W + wc) * C) + c8);
+      }
+    }
+    if constexpr (BN) {
+      float sc[8], sh[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int c = 8 * c8 + j;
+        sc[j] = __ldg(bn.gamma + c) * __ldg(bn.rstd + c);
+        sh[j] = __ldg(bn.beta + c) - __ldg(bn.mean + c) * sc[j];
+      }
+#pragma unroll
+      for (int t = 0; t < 9; ++t) {
+        const __nv_bfloat16* hz = reinterpret_cast<const __nv_bfloat16*>(&v[t]);
+        float f[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) f[j] = fmaxf(fmaf(__bfloat162float(hz[j]), sc[j], sh[j]), 0.f);
+        v[t].x = pack_bf16x2(f[0], f[1]);
+        v[t].y = pack_bf16x2(f[2], f[3]);
+        v[t].z = pack_bf16x2(f[4], f[5]);
+        v[t].w = pack_bf16x2(f[6], f[7]);
       }
     }
     // Packed bf16x2 arithmetic (the per-lane float scan was ALU-bound, 362
@@ -742,14 +774,24 @@ cudaError_t launch_maxpool_nhwc(const __nv_bfloat16* x, int N, int H, int W, int
   if (k == 3 && stride == 2 && fits32(work) && fits32(static_cast<long long>(N) * H * W * C))
     return argmax != nullptr
                ? launch_pdl(maxpool3s2_nhwc_kernel<true>, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W,
-                            C, pad, P, Q, out, argmax, relu_mask)
+                            C, pad, P, Q, out, argmax, relu_mask, BnPoolArgs{})
                : launch_pdl(maxpool3s2_nhwc_kernel<false>, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W,
-                            C, pad, P, Q, out, argmax, relu_mask);
+                            C, pad, P, Q, out, argmax, relu_mask, BnPoolArgs{});
   if (fits32(work))
     return launch_pdl(maxpool_nhwc_kernel<int>, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, k,
                       stride, pad, P, Q, out, argmax, relu_mask);
   return launch_pdl(maxpool_nhwc_kernel<long long>, dim3(grid_for(work)), dim3(256), 0, stream, 1, x, N, H, W, C, k,
                     stride, pad, P, Q, out, argmax, relu_mask);
+}
+
+cudaError_t launch_bn_relu_maxpool3s2_nhwc(const __nv_bfloat16* z, int N, int H, int W, int C, int pad, int P, int Q,
+                                           const float* mean, const float* rstd, const float* gamma,
+                                           const float* beta, __nv_bfloat16* out, uint32_t* argmax,
+                                           cudaStream_t stream) {
+  const long long work = static_cast<long long>(N) * P * Q * (C / 8);
+  if (!fits32(work) || !fits32(static_cast<long long>(N) * H * W * C)) return cudaErrorInvalidValue;
+  return launch_pdl(maxpool3s2_nhwc_kernel<true, true>, dim3(grid_for(work)), dim3(256), 0, stream, 1, z, N, H, W, C,
+                    pad, P, Q, out, argmax, true, BnPoolArgs{mean, rstd, gamma, beta});
 }
 
 cudaError_t launch_avgpool_nhwc(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* out, long long ldo,

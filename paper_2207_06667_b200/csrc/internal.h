@@ -169,6 +169,12 @@ cudaError_t launch_maxpool_nhwc(const __nv_bfloat16* x, int N, int H, int W, int
                                 cudaStream_t stream);
 cudaError_t launch_conv_flip_weights(const __nv_bfloat16* w, long long ldw, int K, int C, int R, int S,
                                      __nv_bfloat16* wf, long long ldf, cudaStream_t stream);
+// training-mode BN + ReLU of the stem's raw conv output z fused into its 3x3 /
+// 2 max pool with argmax (+ ReLU mask nibbles): y itself is never stored
+cudaError_t launch_bn_relu_maxpool3s2_nhwc(const __nv_bfloat16* z, int N, int H, int W, int C, int pad, int P, int Q,
+                                           const float* mean, const float* rstd, const float* gamma,
+                                           const float* beta, __nv_bfloat16* out, uint32_t* argmax,
+                                           cudaStream_t stream);
 cudaError_t launch_maxpool_bwd_argmax_nhwc(const uint32_t* argmax, int N, int H, int W, int C, int k, int stride,
                                            int pad, int P, int Q, const __nv_bfloat16* dy, const __nv_bfloat16* mask,
                                            __nv_bfloat16* dx, cudaStream_t stream);

@@ -540,13 +540,19 @@ class ResNetStudent:
                       out.data_ptr(), c.cout_p, M, c.cout_p, c.kdim,
                       _lib.EDL_ACT_RELU if c.relu else _lib.EDL_ACT_IDENT, s)
 
+    def _bn_stats(self, i, z, s):
+        """Batch mean / rstd of conv i's output z into bn_stats[i]."""
+        c = self.convs[i]
+        M = z.numel() // c.cout_p
+        _lib.call("edl_bn_stats_nhwc", z.data_ptr(), M, c.cout_p, self.bn_ws.data_ptr(), self.bn_ws.numel(),
+                  self.bn_stats[i, 0].data_ptr(), self.bn_stats[i, 1].data_ptr(), self.BN_EPS, s)
+
     def _bn_fwd(self, i, z, y, residual, relu, s):
         """Batch statistics of conv i's output z, then y = [relu](gamma xhat + beta [+ residual])."""
         c, p = self.convs[i], self.params[i]
         M = z.numel() // c.cout_p
         mean, rstd = self.bn_stats[i, 0], self.bn_stats[i, 1]
-        _lib.call("edl_bn_stats_nhwc", z.data_ptr(), M, c.cout_p, self.bn_ws.data_ptr(), self.bn_ws.numel(),
-                  mean.data_ptr(), rstd.data_ptr(), self.BN_EPS, s)
+        self._bn_stats(i, z, s)
         _lib.call("edl_bn_apply_nhwc", z.data_ptr(), M, c.cout_p, mean.data_ptr(), rstd.data_ptr(),
                   self._g(p).data_ptr(), self._b(p).data_ptr(), None if residual is None else residual.data_ptr(),
                   1 if relu else 0, y.data_ptr(), s)
@@ -562,15 +568,21 @@ class ResNetStudent:
     def _features_into(self, x, s):
         """Stem, max pool, residual blocks, global average pool -> self.features."""
         H = self.cfg.image
+        h, w = self.stem_hw
         if self.bn:
+            # the stem's BN + ReLU run inside its max pool (the 411 MB y0 is
+            # never written); argmax words carry the ReLU mask
             self._fwd(0, x, (H, H), self.z0, None, s, raw=True)
-            self._bn_fwd(0, self.z0, self.y0, None, True, s)
+            c, p = self.convs[0], self.params[0]
+            self._bn_stats(0, self.z0, s)
+            _lib.call("edl_bn_relu_maxpool_argmax_nhwc", self.z0.data_ptr(), self.B, h, w, c.cout_p,
+                      self.bn_stats[0, 0].data_ptr(), self.bn_stats[0, 1].data_ptr(), self._g(p).data_ptr(),
+                      self._b(p).data_ptr(), 3, 2, 1, self.x1.data_ptr(), self.pool_arg.data_ptr(), s)
         else:
             self._fwd(0, x, (H, H), self.y0, None, s)
-        h, w = self.stem_hw
-        # the pool input is the stem's ReLU output: argmax words carry its mask
-        _lib.call("edl_maxpool_argmax_relu_nhwc", self.y0.data_ptr(), self.B, h, w, self.y0.shape[-1], 3, 2, 1,
-                  self.x1.data_ptr(), self.pool_arg.data_ptr(), s)
+            # the pool input is the stem's ReLU output: argmax words carry its mask
+            _lib.call("edl_maxpool_argmax_relu_nhwc", self.y0.data_ptr(), self.B, h, w, self.y0.shape[-1], 3, 2, 1,
+                      self.x1.data_ptr(), self.pool_arg.data_ptr(), s)
         cur = self.x1
         for bi, ((i1, i2, isc), (hw, h1, sc, y)) in enumerate(zip(self.block_idx, self.acts)):
             shortcut = cur
