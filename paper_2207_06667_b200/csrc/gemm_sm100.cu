@@ -1847,7 +1847,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ceil(K / 256) class chunks of a 128-row block (atomic ticket) merges the
 // states in chunk order — deterministic — and writes the (prob, class)
 // pairs.
-template <int KMAX>
+//
+// CL == 4: a cluster is two pairs on the same class chunk and adjacent row
+// blocks. Pair 0's CTAs multicast the chunk's B halves into both pairs
+// (tma_load_2d_pair_mc), so L2 delivers each B tile once per cluster (3/4 of
+// the pair kernel's operand bytes); each stage's empty barrier then waits for
+// both pairs' MMA commits (count 2, commits multicast to all four CTAs).
+template <int KMAX, int CL>
 __global__ void __launch_bounds__(kThreads, 1)
     teacher_head_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                              int M, int N, int K, HeadArgs hp, float* part, unsigned* tickets) {
@@ -1873,16 +1879,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const uint32_t rank = cluster_ctarank();
+  static_assert(CL == 2 || CL == 4, "head pair cluster");
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t rank = crank & 1;                    // rank within the pair
+  const int pr = static_cast<int>(crank >> 1);        // pair within the cluster
   const int num_n = (N + BN - 1) / BN;
-  const int pair = static_cast<int>(blockIdx.x) / 2;
-  const int mt = pair / num_n, nt = pair % num_n;     // class chunks of a row block adjacent: A reuse in L2
+  const int cl = static_cast<int>(blockIdx.x) / CL;
+  // class chunks of a row block adjacent: A reuse in L2
+  const int mt = (cl / num_n) * (CL / 2) + pr, nt = cl % num_n;
   const int m0 = mt * 2 * kBM + static_cast<int>(rank) * kBM;
   const int nk = (K + kBK - 1) / kBK;
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
-    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], CL / 2); }
     mbar_init(&tfull[0], 1);
     fence_mbar_init();
   }
@@ -1892,27 +1902,34 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   griddep_wait();
-  const uint32_t full0 = mapa(smem_u32(full), 0);
+  const uint32_t full0 = mapa(smem_u32(full), crank & ~1u);   // this pair's leader
 
   if (warp == 0 && lane == 0) {
     const int nb0 = nt * BN + static_cast<int>(rank) * Cfg::kHalfN;
+    const uint16_t bmask = static_cast<uint16_t>((1u << rank) | (1u << (rank + 2)));
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % S;
       mbar_wait(&empty[s], ((kb / S) & 1) ^ 1);
       if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * Cfg::kStageBytes);
-      load_kblock_pair<BN, false, false>(&tmA, &tmB, sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes,
-                                         full0 + 8 * s, m0, nb0, kb * kBK);
+      if constexpr (CL == 2) {
+        load_kblock_pair<BN, false, false>(&tmA, &tmB, sA + s * Cfg::kABytes, sB + s * Cfg::kBBytes,
+                                           full0 + 8 * s, m0, nb0, kb * kBK);
+      } else {
+        tma_load_2d_pair(sA + s * Cfg::kABytes, &tmA, full0 + 8 * s, kb * kBK, m0);
+        if (pr == 0) tma_load_2d_pair_mc(sB + s * Cfg::kBBytes, &tmB, full0 + 8 * s, kb * kBK, nb0, bmask);
+      }
     }
   } else if (warp == 1 && lane == 0 && rank == 0) {
+    const uint16_t all = CL == 2 ? 3 : 15, own = static_cast<uint16_t>(3u << (crank & 2));
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % S;
       mbar_wait(&full[s], (kb / S) & 1);
       tc_fence_after();
       mma_kblock_pair<BN, false, false>(tmem_base, smem_u32(sA + s * Cfg::kABytes),
                                         smem_u32(sB + s * Cfg::kBBytes), kb == 0);
-      umma_commit_pair(&empty[s]);
+      umma_commit_pair_mask(&empty[s], all);
     }
-    umma_commit_pair(&tfull[0]);
+    umma_commit_pair_mask(&tfull[0], own);
   }
   __syncwarp();
 
@@ -2575,11 +2592,18 @@ static cudaError_t launch_head_pair_t(const CUtensorMap& ta, const CUtensorMap& 
   constexpr int BN = 256, S = 6;
   constexpr int smem = S * PairCfg<BN>::kStageBytes + BN * 4 + 1024 + 256;
   static_assert(smem <= 227 * 1024, "head pair smem");
-  auto kern = teacher_head_pair_kernel<KMAX>;
+  static const bool mc = [] {
+    const char* v = getenv("EDL_HEAD_MC");       // A/B switch: 0 = pairs without the B multicast
+    return !(v && v[0] == '0');
+  }();
+  const int mpairs = (M + 2 * kBM - 1) / (2 * kBM);
+  const int pairs = mpairs * ((N + BN - 1) / BN);
+  const bool cl4 = mc && mpairs % 2 == 0;
+  auto kern = cl4 ? teacher_head_pair_kernel<KMAX, 4> : teacher_head_pair_kernel<KMAX, 2>;
   cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
-  const int pairs = ((M + 2 * kBM - 1) / (2 * kBM)) * ((N + BN - 1) / BN);
-  return launch_pdl(kern, dim3(2 * pairs), dim3(kThreads), smem, stream, 2, ta, tb, M, N, K, hp, part, tickets);
+  return launch_pdl(kern, dim3(2 * pairs), dim3(kThreads), smem, stream, cl4 ? 4 : 2, ta, tb, M, N, K, hp, part,
+                    tickets);
 }
 
 cudaError_t launch_teacher_head_pair(int kmax, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
