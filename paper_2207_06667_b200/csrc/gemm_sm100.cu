@@ -1578,11 +1578,13 @@ struct TopK {
     }
     bitonic_clean<KMAX>(v, i);
   }
-  // insert one candidate that beats the current last entry (branch-free shift)
-  __device__ __forceinline__ void insert(float x, int ix) {
+  // insert a candidate that beats the current last entry (branch-free shift);
+  // its index exceeds every listed one (columns scanned in increasing order),
+  // so a tie keeps the listed entry and the order test is a plain v[j] >= x
+  __device__ __forceinline__ void insert_later(float x, int ix) {
     bool b[KMAX];
 #pragma unroll
-    for (int j = 0; j < KMAX; ++j) b[j] = Key::better(v[j], i[j], x, ix);
+    for (int j = 0; j < KMAX; ++j) b[j] = v[j] >= x;
 #pragma unroll
     for (int j = KMAX - 1; j > 0; --j) {
       const float nv = sel(b[j - 1], x, v[j - 1]);
@@ -1669,11 +1671,12 @@ __device__ __forceinline__ void head_rows(uint32_t tmem_base, uint64_t* tfull, i
     }
     // later chunks: only columns beating the current k-th entry (rare), each
     // inserted by a branch-free shift; the values are staged in smem so the
-    // rolled loop can address them
+    // rolled loop can address them. Every listed index is below col0 (the
+    // chunks are scanned in increasing column order), so a tie never beats a
+    // listed entry and the tests are plain float compares.
     uint32_t mask = 0;
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      mask |= (Key::better(v[j], col0 + j, top.v[KMAX - 1], top.i[KMAX - 1]) ? 1u : 0u) << j;
+    for (int j = 0; j < 32; ++j) mask |= (v[j] > top.v[KMAX - 1] ? 1u : 0u) << j;
     if (mask) {
 #pragma unroll
       for (int j = 0; j < 32; ++j) stage[j * kThreads + tid] = v[j];
@@ -1681,7 +1684,7 @@ __device__ __forceinline__ void head_rows(uint32_t tmem_base, uint64_t* tfull, i
         const int j = __ffs(mask) - 1;
         mask &= mask - 1;
         const float x = stage[j * kThreads + tid];
-        if (Key::better(x, col0 + j, top.v[KMAX - 1], top.i[KMAX - 1])) top.insert(x, col0 + j);
+        if (x > top.v[KMAX - 1]) top.insert_later(x, col0 + j);
       }
     }
     __syncwarp();   // the insertions above diverge; tcgen05.wait::ld is .sync.aligned
