@@ -1963,12 +1963,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (*merger && half == 0 && row < M) {
     __threadfence();
+    // chunk c + 1's state is loaded while chunk c merges (one L2 round trip
+    // per chunk otherwise sits on the critical path)
+    float nx[kState];
+#pragma unroll
+    for (int w = 0; w < kState; ++w) nx[w] = __ldcg(part + static_cast<size_t>(w) * M + row);
 #pragma unroll 1
     for (int c = 0; c < num_n; ++c) {
-      const float* pp = part + static_cast<size_t>(c) * kState * M + row;
       float rv[kState];
 #pragma unroll
-      for (int w = 0; w < kState; ++w) rv[w] = __ldcg(pp + static_cast<size_t>(w) * M);
+      for (int w = 0; w < kState; ++w) rv[w] = nx[w];
+      if (c + 1 < num_n) {
+        const float* pn = part + static_cast<size_t>(c + 1) * kState * M + row;
+#pragma unroll
+        for (int w = 0; w < kState; ++w) nx[w] = __ldcg(pn + static_cast<size_t>(w) * M);
+      }
       float ov[KMAX];
       int oi[KMAX];
 #pragma unroll
