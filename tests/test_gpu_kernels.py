@@ -172,6 +172,48 @@ def test_teacher_head_pair_equals_cluster_head(lib):
     assert (v0 - v1).abs().max().item() <= 1e-6 * v0.abs().max().item()
 
 
+def _run_head_pair(B, H, K, k, seed, out_path=None):
+    from paper_2207_06667_b200 import _lib
+    Hp, Kp = (H + 15) // 16 * 16, (K + 15) // 16 * 16
+    h = _padded(torch.tanh(_rand(B, H, seed=seed)), B, Hp)
+    w = _padded(_rand(K, H, scale=3 * H ** -0.5, seed=seed + 1), Kp, Hp)
+    b = torch.zeros(Kp, device="cuda")
+    b[:K] = _rand(K, seed=seed + 2) * 0.1
+    vals = torch.empty(B, k, device="cuda")
+    idx = torch.empty(B, k, dtype=torch.int32, device="cuda")
+    nb = int(_lib.load().edl_teacher_head_workspace_bytes(B, K, k))
+    ws = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+    _lib.call("edl_teacher_head_softmax_topk_ws", h.data_ptr(), Hp, w.data_ptr(), Hp, b.data_ptr(), B, K, Hp, 2.0,
+              k, vals.data_ptr(), idx.data_ptr(), ws.data_ptr(), nb, _s())
+    torch.cuda.synchronize()
+    out = (vals.cpu(), idx.cpu())
+    if out_path:
+        torch.save(out, out_path)
+    return out
+
+
+@pytest.mark.parametrize("B,H,K,k", [(1024, 2048, 1000, 16), (512, 512, 3000, 32), (4096, 1024, 1000, 16),
+                                     (900, 256, 100, 8)])
+def test_teacher_head_multicast_bitwise(lib, B, H, K, k, tmp_path):
+    """With an even number of 256-row blocks the pair head runs in 4-CTA
+    clusters sharing each B tile through a 2-SM TMA multicast: bitwise equal
+    to the 2-CTA pair head (EDL_HEAD_MC=0 in a subprocess; same MMAs per tile,
+    same chunk-order merge)."""
+    import os
+    import subprocess
+    import sys
+    got = _run_head_pair(B, H, K, k, seed=B + K)
+    ref_path = str(tmp_path / "head.pt")
+    code = ("import sys, torch; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+            "import test_gpu_kernels as t;"
+            f"t._run_head_pair({B}, {H}, {K}, {k}, {B + K}, {ref_path!r})")
+    env = dict(os.environ, EDL_HEAD_MC="0")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=300)
+    want = torch.load(ref_path)
+    assert torch.equal(got[1], want[1])
+    assert torch.equal(got[0], want[0])
+
+
 @pytest.mark.parametrize("B,K,k,alpha,beta,T", [(32, 10, 10, 0.5, 0.5, 2.0), (32, 10, 4, 1.0, 0.0, 2.0),
                                                 (300, 1000, 16, 0.5, 0.5, 2.0), (64, 100, 100, 0.0, 1.0, 3.0),
                                                 (4096, 1000, 16, 0.7, 0.3, 0.5)])
