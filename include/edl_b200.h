@@ -251,7 +251,9 @@ int edl_teacher_head_softmax_topk(const void* H, long long ldh, const void* W, l
  * by the caller at allocation; the kernel leaves its tickets at zero), so no
  * cluster has to span the class range. One workspace per stream. With
  * workspace == NULL (or EDL_HEAD_CLUSTER=1) the single-CTA cluster head runs
- * instead. Same outputs and tie rule. */
+ * instead. Same outputs and tie rule. With an even number of 256-row blocks
+ * two pairs share each weight tile through a 2-SM TMA multicast (4-CTA
+ * clusters; bitwise equal, EDL_HEAD_MC=0 disables). */
 long long edl_teacher_head_workspace_bytes(int M, int N, int k);
 int edl_teacher_head_softmax_topk_ws(const void* H, long long ldh, const void* W, long long ldw, const float* bias,
                                      int M, int N, int K, float T, int k, float* vals, int* idx, void* workspace,
